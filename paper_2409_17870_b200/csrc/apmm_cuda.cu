@@ -1,0 +1,487 @@
+// apmm_cuda.cu -- the C ABI (include/apmm_cuda.h): validation with the reference's error
+// semantics, workspace management, and dispatch onto the sm_100a kernels.
+//
+// Validation order follows the reference so the same inputs fail with the same error
+// class: BitWidth (bipolar.hpp:17-19) -> positive dimensions (bitplane.cpp:14-16) ->
+// buffer contents (bitplane.cpp:22-32) -> K agreement / overflow_bound (kernel.cpp:189-199).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "../../include/apmm_cuda.h"
+#include "internal.h"
+
+using namespace apmm_b200;
+
+struct apmm_ctx {
+  int device = 0;
+  int num_sms = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  void* ws = nullptr;  // matmul workspace (u8 codes + rowsums + scratch)
+  size_t ws_bytes = 0;
+  void* io = nullptr;  // device staging for the synchronous host entry points
+  size_t io_bytes = 0;
+  uint64_t launches = 0;
+};
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int status, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  std::vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return status;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+  return fail(APMM_E_CUDA, "%s: %s", where, cudaGetErrorString(e));
+}
+
+#define CU(expr)                                        \
+  do {                                                  \
+    cudaError_t e_ = (expr);                            \
+    if (e_ != cudaSuccess) return cuda_fail(e_, #expr); \
+  } while (0)
+
+constexpr size_t kAlign = 1024;
+size_t align_up(size_t v) { return (v + kAlign - 1) / kAlign * kAlign; }
+
+int check_width(int n) {
+  if (n < 1 || n > 8) return fail(APMM_E_OUT_OF_RANGE, "bit width must be in [1, 8], got %d", n);
+  return APMM_OK;
+}
+
+int check_dims(uint64_t rows, uint64_t cols, const char* what) {
+  if (rows == 0 || cols == 0) {
+    return fail(APMM_E_DIMENSION_MISMATCH, "%s dimensions must be positive", what);
+  }
+  if (rows >= (1ull << 31) || cols >= (1ull << 31)) {
+    return fail(APMM_E_INVALID_ARGUMENT, "%s dimensions exceed 2^31-1", what);
+  }
+  return APMM_OK;
+}
+
+int64_t bound_of(int n_w, int n_x, uint64_t k) {
+  return static_cast<int64_t>(k) * ((1 << n_w) - 1) * ((1 << n_x) - 1);
+}
+
+int check_matmul(int n_w, int n_x, uint64_t rows_w, uint64_t rows_x, uint64_t k) {
+  int st;
+  if ((st = check_width(n_w)) || (st = check_width(n_x))) return st;
+  if ((st = check_dims(rows_w, k, "weights")) || (st = check_dims(rows_x, k, "features"))) {
+    return st;
+  }
+  const int64_t b = bound_of(n_w, n_x, k);
+  if (b > INT32_MAX) {
+    return fail(APMM_E_OVERFLOW_BOUND,
+                "output bound %lld exceeds 32-bit range; K=%llu n_w=%d n_x=%d",
+                static_cast<long long>(b), static_cast<unsigned long long>(k), n_w, n_x);
+  }
+  return APMM_OK;
+}
+
+int ensure(void** buf, size_t* have, size_t need, int device) {
+  if (need <= *have) return APMM_OK;
+  CU(cudaSetDevice(device));
+  if (*buf) {
+    CU(cudaDeviceSynchronize());  // growth only: previous users of the buffer must finish
+    CU(cudaFree(*buf));
+    *buf = nullptr;
+    *have = 0;
+  }
+  const size_t sz = need + need / 4;
+  CU(cudaMalloc(buf, sz));
+  *have = sz;
+  return APMM_OK;
+}
+
+// Workspace carve-up for one matmul.
+struct MatmulWs {
+  uint8_t* codes_w;
+  uint8_t* codes_x;
+  int32_t* rowsum_w;
+  int32_t* rowsum_x;
+  uint64_t kpad;
+};
+
+size_t matmul_ws_bytes(uint64_t rows_w, uint64_t rows_x, uint64_t k) {
+  const uint64_t kpad = round_up(k, kKAlign);
+  return align_up(rows_w * kpad) + align_up(rows_x * kpad) + align_up(rows_w * 4) +
+         align_up(round_up(rows_x, kRowsumPad) * 4);
+}
+
+MatmulWs carve(void* ws, uint64_t rows_w, uint64_t rows_x, uint64_t k) {
+  MatmulWs m;
+  m.kpad = round_up(k, kKAlign);
+  uint8_t* p = static_cast<uint8_t*>(ws);
+  m.codes_w = p;
+  p += align_up(rows_w * m.kpad);
+  m.codes_x = p;
+  p += align_up(rows_x * m.kpad);
+  m.rowsum_w = reinterpret_cast<int32_t*>(p);
+  p += align_up(rows_w * 4);
+  m.rowsum_x = reinterpret_cast<int32_t*>(p);
+  return m;
+}
+
+int run_matmul(apmm_ctx* ctx, const uint32_t* w, uint64_t rows_w, int n_w, const double* s_w,
+               int gran_w, const uint32_t* x, uint64_t rows_x, int n_x, const double* s_x,
+               int gran_x, uint64_t k, int32_t* y, float* yf, cudaStream_t stream) {
+  int st = ensure(&ctx->ws, &ctx->ws_bytes, matmul_ws_bytes(rows_w, rows_x, k), ctx->device);
+  if (st) return st;
+  CU(cudaSetDevice(ctx->device));
+  const MatmulWs m = carve(ctx->ws, rows_w, rows_x, k);
+  const uint64_t rsx_pad = round_up(rows_x, kRowsumPad);
+  if (rsx_pad > rows_x) {
+    CU(cudaMemsetAsync(m.rowsum_x + rows_x, 0, (rsx_pad - rows_x) * 4, stream));
+  }
+  CU(launch_expand(w, rows_w, k, n_w, m.codes_w, m.kpad, m.rowsum_w, stream));
+  CU(launch_expand(x, rows_x, k, n_x, m.codes_x, m.kpad, m.rowsum_x, stream));
+  ctx->launches += 2;
+  GemmArgs a{};
+  a.codes_w = m.codes_w;
+  a.codes_x = m.codes_x;
+  a.rowsum_w = m.rowsum_w;
+  a.rowsum_x = m.rowsum_x;
+  a.rows_w = rows_w;
+  a.rows_x = rows_x;
+  a.kpad = m.kpad;
+  a.k_logical = k;
+  a.n_w = n_w;
+  a.n_x = n_x;
+  a.y = y;
+  a.yf = yf;
+  a.s_w = s_w;
+  a.gran_w = gran_w;
+  a.s_x = s_x;
+  a.gran_x = gran_x;
+  a.num_sms = ctx->num_sms;
+  int launches = 0;
+  CU(launch_gemm_tc(a, stream, &launches));
+  ctx->launches += static_cast<uint64_t>(launches);
+  return APMM_OK;
+}
+
+cudaStream_t pick(apmm_ctx* ctx, apmm_stream_t s) {
+  return s ? reinterpret_cast<cudaStream_t>(s) : ctx->stream;
+}
+
+// Host-side PackedBitPlanes invariants (bitplane.cpp:17-32).
+int check_padding(const uint32_t* planes, uint64_t rows, uint64_t cols, int n) {
+  const uint32_t tail = static_cast<uint32_t>(cols & 31);
+  if (tail == 0) return APMM_OK;
+  const uint32_t pad = ~((1u << tail) - 1u);
+  const uint64_t wpr = (cols + 31) / 32;
+  for (uint64_t pr = 0; pr < uint64_t(n) * rows; ++pr) {
+    if (planes[(pr + 1) * wpr - 1] & pad) {
+      return fail(APMM_E_OUT_OF_RANGE, "packed buffer has nonzero padding bits");
+    }
+  }
+  return APMM_OK;
+}
+
+bool valid_gran(int g) { return g == APMM_PER_TENSOR || g == APMM_PER_ROW; }
+
+}  // namespace
+
+extern "C" {
+
+const char* apmm_last_error(void) { return g_last_error.c_str(); }
+
+const char* apmm_status_name(int s) {
+  switch (s) {
+    case APMM_OK: return "OK";
+    case APMM_E_EVEN_VALUE: return "EvenValue";
+    case APMM_E_OUT_OF_RANGE: return "OutOfRange";
+    case APMM_E_NON_FINITE: return "NonFinite";
+    case APMM_E_LENGTH_MISMATCH: return "LengthMismatch";
+    case APMM_E_DIMENSION_MISMATCH: return "DimensionMismatch";
+    case APMM_E_INDEX_OUT_OF_BOUNDS: return "IndexOutOfBounds";
+    case APMM_E_OVERFLOW: return "Overflow";
+    case APMM_E_OVERFLOW_BOUND: return "OverflowBound";
+    case APMM_E_INVALID_ARGUMENT: return "InvalidArgument";
+    case APMM_E_CUDA: return "CudaError";
+    case APMM_E_NO_DEVICE: return "NoDevice";
+    case APMM_E_UNSUPPORTED_DEVICE: return "UnsupportedDevice";
+    default: return "Unknown";
+  }
+}
+
+const char* apmm_version(void) {
+  return "apmm_b200 0.1 (sm_100a; tcgen05 kind::i8 u8-code GEMM, rank-1 recovery epilogue)";
+}
+
+int apmm_ctx_create(apmm_ctx** out, int device) {
+  if (!out) return fail(APMM_E_INVALID_ARGUMENT, "null context pointer");
+  *out = nullptr;
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
+    cudaGetLastError();
+    return fail(APMM_E_NO_DEVICE, "no CUDA device visible");
+  }
+  if (device < 0 || device >= count) return fail(APMM_E_NO_DEVICE, "device %d out of range", device);
+  cudaDeviceProp prop;
+  CU(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10 || prop.minor != 0) {
+    return fail(APMM_E_UNSUPPORTED_DEVICE, "device %d is sm_%d%d; this library is built for sm_100a",
+                device, prop.major, prop.minor);
+  }
+  CU(cudaSetDevice(device));
+  auto* ctx = new apmm_ctx();
+  ctx->device = device;
+  ctx->num_sms = prop.multiProcessorCount;
+  cudaError_t e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    delete ctx;
+    return cuda_fail(e, "cudaStreamCreate");
+  }
+  ctx->own_stream = true;
+  *out = ctx;
+  return APMM_OK;
+}
+
+int apmm_ctx_destroy(apmm_ctx* ctx) {
+  if (!ctx) return APMM_OK;
+  cudaSetDevice(ctx->device);
+  cudaDeviceSynchronize();
+  if (ctx->ws) cudaFree(ctx->ws);
+  if (ctx->io) cudaFree(ctx->io);
+  if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+  return APMM_OK;
+}
+
+int apmm_ctx_set_stream(apmm_ctx* ctx, apmm_stream_t stream) {
+  if (!ctx) return fail(APMM_E_INVALID_ARGUMENT, "null context");
+  if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+  ctx->stream = reinterpret_cast<cudaStream_t>(stream);
+  ctx->own_stream = false;
+  return APMM_OK;
+}
+
+uint64_t apmm_ctx_launch_count(const apmm_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int apmm_overflow_bound(int n_w, int n_x, uint64_t k, int64_t* bound) {
+  int st;
+  if ((st = check_width(n_w)) || (st = check_width(n_x))) return st;
+  if (!bound) return fail(APMM_E_INVALID_ARGUMENT, "null output");
+  *bound = bound_of(n_w, n_x, k);
+  return APMM_OK;
+}
+
+uint64_t apmm_packed_words(int n, uint64_t rows, uint64_t cols) {
+  return static_cast<uint64_t>(n) * rows * ((cols + 31) / 32);
+}
+
+// ---- device entry points ----------------------------------------------------------------
+int apmm_cu_pack(apmm_ctx* ctx, const uint8_t* codes, uint64_t rows, uint64_t cols, int n,
+                 uint32_t* planes, apmm_stream_t stream) {
+  int st;
+  if (!ctx || !codes || !planes) return fail(APMM_E_INVALID_ARGUMENT, "null argument");
+  if ((st = check_width(n)) || (st = check_dims(rows, cols, "CodeMatrix"))) return st;
+  CU(cudaSetDevice(ctx->device));
+  CU(launch_pack(codes, rows, cols, n, planes, pick(ctx, stream)));
+  ctx->launches += 1;
+  return APMM_OK;
+}
+
+int apmm_cu_unpack(apmm_ctx* ctx, const uint32_t* planes, uint64_t rows, uint64_t cols, int n,
+                   uint8_t* codes, apmm_stream_t stream) {
+  int st;
+  if (!ctx || !codes || !planes) return fail(APMM_E_INVALID_ARGUMENT, "null argument");
+  if ((st = check_width(n)) || (st = check_dims(rows, cols, "PackedBitPlanes"))) return st;
+  CU(cudaSetDevice(ctx->device));
+  CU(launch_unpack(planes, rows, cols, n, codes, pick(ctx, stream)));
+  ctx->launches += 1;
+  return APMM_OK;
+}
+
+int apmm_cu_quantize_pack(apmm_ctx* ctx, const double* values, uint64_t rows, uint64_t cols,
+                          int n, int granularity, uint32_t* planes, double* scales,
+                          uint8_t* codes, apmm_stream_t stream) {
+  int st;
+  if (!ctx || !values || !planes || !scales) return fail(APMM_E_INVALID_ARGUMENT, "null argument");
+  if (!valid_gran(granularity)) return fail(APMM_E_INVALID_ARGUMENT, "bad granularity");
+  if ((st = check_width(n)) || (st = check_dims(rows, cols, "RealMatrix"))) return st;
+  // scratch: amax bits + flag live past the matmul region of the workspace
+  if ((st = ensure(&ctx->ws, &ctx->ws_bytes, 64, ctx->device))) return st;
+  CU(cudaSetDevice(ctx->device));
+  auto* amax = static_cast<unsigned long long*>(ctx->ws);
+  int* flag = reinterpret_cast<int*>(static_cast<uint8_t*>(ctx->ws) + 16);
+  const cudaStream_t s = pick(ctx, stream);
+  CU(launch_quantize_pack(values, rows, cols, n, granularity, planes, scales, codes, amax, flag, s));
+  ctx->launches += granularity == APMM_PER_ROW ? 1 : 2;
+  int h_flag = 0;
+  CU(cudaMemcpyAsync(&h_flag, flag, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  if (h_flag) return fail(APMM_E_NON_FINITE, "input contains NaN or infinity");
+  return APMM_OK;
+}
+
+int apmm_cu_matmul_ap(apmm_ctx* ctx, const uint32_t* w_planes, uint64_t rows_w, int n_w,
+                      const uint32_t* x_planes, uint64_t rows_x, int n_x, uint64_t k,
+                      int32_t* y, apmm_stream_t stream) {
+  if (!ctx || !w_planes || !x_planes || !y) return fail(APMM_E_INVALID_ARGUMENT, "null argument");
+  int st = check_matmul(n_w, n_x, rows_w, rows_x, k);
+  if (st) return st;
+  return run_matmul(ctx, w_planes, rows_w, n_w, nullptr, 0, x_planes, rows_x, n_x, nullptr, 0, k,
+                    y, nullptr, pick(ctx, stream));
+}
+
+int apmm_cu_matmul_ap_dequant(apmm_ctx* ctx, const uint32_t* w_planes, uint64_t rows_w,
+                              int n_w, const double* w_scales, int w_granularity,
+                              const uint32_t* x_planes, uint64_t rows_x, int n_x,
+                              const double* x_scales, int x_granularity, uint64_t k,
+                              float* out, apmm_stream_t stream) {
+  if (!ctx || !w_planes || !x_planes || !out || !w_scales || !x_scales) {
+    return fail(APMM_E_INVALID_ARGUMENT, "null argument");
+  }
+  if (!valid_gran(w_granularity) || !valid_gran(x_granularity)) {
+    return fail(APMM_E_INVALID_ARGUMENT, "bad granularity");
+  }
+  int st = check_matmul(n_w, n_x, rows_w, rows_x, k);
+  if (st) return st;
+  return run_matmul(ctx, w_planes, rows_w, n_w, w_scales, w_granularity, x_planes, rows_x, n_x,
+                    x_scales, x_granularity, k, nullptr, out, pick(ctx, stream));
+}
+
+// ---- host entry points ------------------------------------------------------------------
+int apmm_decompose_and_pack(apmm_ctx* ctx, const uint8_t* codes, uint64_t rows, uint64_t cols,
+                            int n, uint32_t* planes) {
+  int st;
+  if (!ctx || !codes || !planes) return fail(APMM_E_INVALID_ARGUMENT, "null argument");
+  if ((st = check_width(n)) || (st = check_dims(rows, cols, "CodeMatrix"))) return st;
+  const uint32_t limit = 1u << n;
+  for (uint64_t e = 0; e < rows * cols; ++e) {  // CodeMatrix ctor (bipolar.cpp:33-36)
+    if (codes[e] >= limit) return fail(APMM_E_OUT_OF_RANGE, "code has bits above position n-1");
+  }
+  const size_t in_b = align_up(rows * cols), out_b = apmm_packed_words(n, rows, cols) * 4;
+  if ((st = ensure(&ctx->io, &ctx->io_bytes, in_b + out_b, ctx->device))) return st;
+  uint8_t* d_codes = static_cast<uint8_t*>(ctx->io);
+  uint32_t* d_planes = reinterpret_cast<uint32_t*>(d_codes + in_b);
+  CU(cudaMemcpyAsync(d_codes, codes, rows * cols, cudaMemcpyHostToDevice, ctx->stream));
+  if ((st = apmm_cu_pack(ctx, d_codes, rows, cols, n, d_planes, nullptr))) return st;
+  CU(cudaMemcpyAsync(planes, d_planes, out_b, cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  return APMM_OK;
+}
+
+int apmm_unpack(apmm_ctx* ctx, const uint32_t* planes, uint64_t rows, uint64_t cols, int n,
+                uint8_t* codes) {
+  int st;
+  if (!ctx || !codes || !planes) return fail(APMM_E_INVALID_ARGUMENT, "null argument");
+  if ((st = check_width(n)) || (st = check_dims(rows, cols, "PackedBitPlanes"))) return st;
+  if ((st = check_padding(planes, rows, cols, n))) return st;
+  const size_t in_b = align_up(apmm_packed_words(n, rows, cols) * 4), out_b = rows * cols;
+  if ((st = ensure(&ctx->io, &ctx->io_bytes, in_b + out_b, ctx->device))) return st;
+  uint32_t* d_planes = static_cast<uint32_t*>(ctx->io);
+  uint8_t* d_codes = static_cast<uint8_t*>(ctx->io) + in_b;
+  CU(cudaMemcpyAsync(d_planes, planes, apmm_packed_words(n, rows, cols) * 4,
+                     cudaMemcpyHostToDevice, ctx->stream));
+  if ((st = apmm_cu_unpack(ctx, d_planes, rows, cols, n, d_codes, nullptr))) return st;
+  CU(cudaMemcpyAsync(codes, d_codes, out_b, cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  return APMM_OK;
+}
+
+int apmm_quantize_pack(apmm_ctx* ctx, const double* values, uint64_t rows, uint64_t cols, int n,
+                       int granularity, uint8_t* codes, uint32_t* planes, double* scales) {
+  int st;
+  if (!ctx || !values || !planes || !scales) return fail(APMM_E_INVALID_ARGUMENT, "null argument");
+  if (!valid_gran(granularity)) return fail(APMM_E_INVALID_ARGUMENT, "bad granularity");
+  if ((st = check_width(n)) || (st = check_dims(rows, cols, "RealMatrix"))) return st;
+  const uint64_t n_scales = granularity == APMM_PER_ROW ? rows : 1;
+  const size_t x_b = align_up(rows * cols * 8), p_b = align_up(apmm_packed_words(n, rows, cols) * 4);
+  const size_t s_b = align_up(n_scales * 8), c_b = align_up(rows * cols);
+  if ((st = ensure(&ctx->io, &ctx->io_bytes, x_b + p_b + s_b + c_b, ctx->device))) return st;
+  uint8_t* base = static_cast<uint8_t*>(ctx->io);
+  double* d_x = reinterpret_cast<double*>(base);
+  uint32_t* d_p = reinterpret_cast<uint32_t*>(base + x_b);
+  double* d_s = reinterpret_cast<double*>(base + x_b + p_b);
+  uint8_t* d_c = codes ? base + x_b + p_b + s_b : nullptr;
+  CU(cudaMemcpyAsync(d_x, values, rows * cols * 8, cudaMemcpyHostToDevice, ctx->stream));
+  if ((st = apmm_cu_quantize_pack(ctx, d_x, rows, cols, n, granularity, d_p, d_s, d_c, nullptr))) {
+    return st;
+  }
+  CU(cudaMemcpyAsync(planes, d_p, apmm_packed_words(n, rows, cols) * 4, cudaMemcpyDeviceToHost,
+                     ctx->stream));
+  CU(cudaMemcpyAsync(scales, d_s, n_scales * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  if (codes) CU(cudaMemcpyAsync(codes, d_c, rows * cols, cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  return APMM_OK;
+}
+
+static int host_matmul(apmm_ctx* ctx, const uint32_t* w, uint64_t rows_w, int n_w,
+                       const double* s_w, int gran_w, const uint32_t* x, uint64_t rows_x,
+                       int n_x, const double* s_x, int gran_x, uint64_t k, int32_t* y,
+                       float* yf) {
+  int st;
+  if ((st = check_width(n_w)) || (st = check_width(n_x))) return st;
+  if ((st = check_dims(rows_w, k, "weights")) || (st = check_dims(rows_x, k, "features"))) {
+    return st;
+  }
+  if ((st = check_padding(w, rows_w, k, n_w)) || (st = check_padding(x, rows_x, k, n_x))) {
+    return st;
+  }
+  if ((st = check_matmul(n_w, n_x, rows_w, rows_x, k))) return st;
+  const size_t w_words = apmm_packed_words(n_w, rows_w, k), x_words = apmm_packed_words(n_x, rows_x, k);
+  const size_t w_b = align_up(w_words * 4), x_b = align_up(x_words * 4);
+  const size_t y_b = align_up(rows_w * rows_x * 4);
+  const size_t sw_n = gran_w == APMM_PER_ROW ? rows_w : 1, sx_n = gran_x == APMM_PER_ROW ? rows_x : 1;
+  const size_t sw_b = yf ? align_up(sw_n * 8) : 0, sx_b = yf ? align_up(sx_n * 8) : 0;
+  if ((st = ensure(&ctx->io, &ctx->io_bytes, w_b + x_b + y_b + sw_b + sx_b, ctx->device))) return st;
+  CU(cudaSetDevice(ctx->device));
+  uint8_t* base = static_cast<uint8_t*>(ctx->io);
+  uint32_t* d_w = reinterpret_cast<uint32_t*>(base);
+  uint32_t* d_x = reinterpret_cast<uint32_t*>(base + w_b);
+  void* d_y = base + w_b + x_b;
+  double* d_sw = reinterpret_cast<double*>(base + w_b + x_b + y_b);
+  double* d_sx = reinterpret_cast<double*>(base + w_b + x_b + y_b + sw_b);
+  CU(cudaMemcpyAsync(d_w, w, w_words * 4, cudaMemcpyHostToDevice, ctx->stream));
+  CU(cudaMemcpyAsync(d_x, x, x_words * 4, cudaMemcpyHostToDevice, ctx->stream));
+  if (yf) {
+    CU(cudaMemcpyAsync(d_sw, s_w, sw_n * 8, cudaMemcpyHostToDevice, ctx->stream));
+    CU(cudaMemcpyAsync(d_sx, s_x, sx_n * 8, cudaMemcpyHostToDevice, ctx->stream));
+  }
+  st = run_matmul(ctx, d_w, rows_w, n_w, d_sw, gran_w, d_x, rows_x, n_x, d_sx, gran_x, k,
+                  yf ? nullptr : static_cast<int32_t*>(d_y), yf ? static_cast<float*>(d_y) : nullptr,
+                  ctx->stream);
+  if (st) return st;
+  CU(cudaMemcpyAsync(yf ? static_cast<void*>(yf) : static_cast<void*>(y), d_y, rows_w * rows_x * 4,
+                     cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  return APMM_OK;
+}
+
+int apmm_matmul_ap(apmm_ctx* ctx, const uint32_t* w_planes, uint64_t rows_w, int n_w,
+                   const uint32_t* x_planes, uint64_t rows_x, int n_x, uint64_t k, int32_t* y) {
+  if (!ctx || !w_planes || !x_planes || !y) return fail(APMM_E_INVALID_ARGUMENT, "null argument");
+  return host_matmul(ctx, w_planes, rows_w, n_w, nullptr, 0, x_planes, rows_x, n_x, nullptr, 0, k,
+                     y, nullptr);
+}
+
+int apmm_matmul_ap_dequant(apmm_ctx* ctx, const uint32_t* w_planes, uint64_t rows_w, int n_w,
+                           const double* w_scales, int w_granularity, const uint32_t* x_planes,
+                           uint64_t rows_x, int n_x, const double* x_scales, int x_granularity,
+                           uint64_t k, float* out) {
+  if (!ctx || !w_planes || !x_planes || !out || !w_scales || !x_scales) {
+    return fail(APMM_E_INVALID_ARGUMENT, "null argument");
+  }
+  if (!valid_gran(w_granularity) || !valid_gran(x_granularity)) {
+    return fail(APMM_E_INVALID_ARGUMENT, "bad granularity");
+  }
+  return host_matmul(ctx, w_planes, rows_w, n_w, w_scales, w_granularity, x_planes, rows_x, n_x,
+                     x_scales, x_granularity, k, nullptr, out);
+}
+
+}  // extern "C"

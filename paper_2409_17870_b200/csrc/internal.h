@@ -1,0 +1,57 @@
+// internal.h -- declarations shared by the .cu translation units of libapmm_b200.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace apmm_b200 {
+
+// Geometry of the tensor-core GEMM (gemm_tc.cu).
+constexpr int kBM = 128;        // weight rows per CTA tile (MMA M, TMEM lanes)
+constexpr int kBN = 256;        // feature rows per CTA tile (MMA N)
+constexpr int kBK = 128;        // K bytes per pipeline stage (one 128-B swizzle row)
+constexpr int kKAlign = kBK;    // device code rows are padded to a multiple of this
+constexpr int kRowsumPad = kBN; // rowsum_x is zero-padded to a multiple of this
+
+inline uint64_t round_up(uint64_t v, uint64_t m) { return (v + m - 1) / m * m; }
+
+// ---- prep.cu -------------------------------------------------------------------------
+// planes (reference layout) -> u8 codes [rows x kpad] (zero K padding) + rowsum[rows].
+cudaError_t launch_expand(const uint32_t* planes, uint64_t rows, uint64_t cols, int n,
+                          uint8_t* codes, uint64_t kpad, int32_t* rowsum, cudaStream_t s);
+cudaError_t launch_pack(const uint8_t* codes, uint64_t rows, uint64_t cols, int n,
+                        uint32_t* planes, cudaStream_t s);
+cudaError_t launch_unpack(const uint32_t* planes, uint64_t rows, uint64_t cols, int n,
+                          uint8_t* codes, cudaStream_t s);
+// fp64 quantize + pack. flag[0] receives 1 if any input is non-finite. `amax_bits` is a
+// scratch u64 (per-tensor absmax as ordered bits).
+cudaError_t launch_quantize_pack(const double* x, uint64_t rows, uint64_t cols, int n,
+                                 int granularity, uint32_t* planes, double* scales,
+                                 uint8_t* codes, unsigned long long* amax_bits, int* flag,
+                                 cudaStream_t s);
+
+// ---- gemm_tc.cu ----------------------------------------------------------------------
+struct GemmArgs {
+  const uint8_t* codes_w;   // [rows_w x kpad]
+  const uint8_t* codes_x;   // [rows_x x kpad]
+  const int32_t* rowsum_w;  // [rows_w]
+  const int32_t* rowsum_x;  // [round_up(rows_x, kRowsumPad)], zero padded
+  uint64_t rows_w, rows_x, kpad, k_logical;
+  int n_w, n_x;
+  int32_t* y;               // int32 output [rows_w x rows_x] (or null)
+  float* yf;                // dequant output (or null)
+  const double* s_w;
+  int gran_w;
+  const double* s_x;
+  int gran_x;
+  int num_sms;
+};
+// Returns the number of kernel launches it enqueued via *launches.
+cudaError_t launch_gemm_tc(const GemmArgs& a, cudaStream_t s, int* launches);
+
+// Tensor-map encoder obtained from the driver through the runtime (no -lcuda).
+CUresult encode_tmap_u8_2d(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer,
+                           uint32_t box_inner, uint32_t box_outer);
+
+}  // namespace apmm_b200
