@@ -17,7 +17,8 @@
  *     ceil(cols/32) little-endian u32 words, column k at word k>>5 bit k&31, padding
  *     bits zero. Device entry points take that layout in device memory unchanged.
  *   - apmm_cu_* entry points take DEVICE pointers and are stream-ordered: they enqueue
- *     work on `stream` and return without synchronising. Scratch comes from the
+ *     work on `stream` (NULL = the legacy default stream) and return without
+ *     synchronising. Scratch comes from the
  *     context's workspace, grown on first use for a shape and reused afterwards.
  *   - apmm_* entry points without the cu_ prefix take HOST pointers and are
  *     synchronous (H2D, kernels, D2H on the context's stream). They are what a
@@ -74,6 +75,14 @@ APMM_API const char* apmm_status_name(int status);
 APMM_API const char* apmm_version(void);
 /* Number of kernel launches this context has enqueued (launch accounting for bench). */
 APMM_API uint64_t apmm_ctx_launch_count(const apmm_ctx* ctx);
+
+/* Kernel timing for measurement: when enabled, every launch of the given kernel class is
+ * bracketed by CUDA events on the stream it is launched on. apmm_ctx_kernel_time
+ * synchronises on those events and returns the summed device time (ms) and the number of
+ * launches since the last reset, then resets. kernel: 0 = tensor-core GEMM (K3),
+ * 1 = operand expansion (K1). */
+APMM_API int apmm_ctx_enable_timing(apmm_ctx* ctx, int enable);
+APMM_API int apmm_ctx_kernel_time(apmm_ctx* ctx, int kernel, double* total_ms, uint64_t* launches);
 
 /* ---- scalar helpers (no device work) --------------------------------------------- */
 /* overflow_bound (kernel.hpp:78-79, kernel.cpp:183-185): K*(2^n_w-1)*(2^n_x-1). */

@@ -21,6 +21,8 @@ _SIGNATURES = {
     "apmm_status_name": (C.c_char_p, [i32]),
     "apmm_version": (C.c_char_p, []),
     "apmm_ctx_launch_count": (u64, [vp]),
+    "apmm_ctx_enable_timing": (i32, [vp, i32]),
+    "apmm_ctx_kernel_time": (i32, [vp, i32, C.POINTER(C.c_double), C.POINTER(u64)]),
     "apmm_overflow_bound": (i32, [i32, i32, u64, C.POINTER(i64)]),
     "apmm_packed_words": (u64, [i32, u64, u64]),
     "apmm_cu_pack": (i32, [vp, vp, u64, u64, i32, vp, vp]),

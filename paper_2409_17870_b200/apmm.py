@@ -210,6 +210,15 @@ class Context:
     def launch_count(self) -> int:
         return int(self.lib.apmm_ctx_launch_count(self.h))
 
+    def enable_timing(self, enable: bool = True) -> None:
+        _check(self.lib.apmm_ctx_enable_timing(self.h, int(bool(enable))))
+
+    def kernel_time(self, kernel: int = 0):
+        """(total device ms, launches) of kernel class 0=GEMM / 1=expand since last call."""
+        ms, n = C.c_double(), C.c_uint64()
+        _check(self.lib.apmm_ctx_kernel_time(self.h, int(kernel), C.byref(ms), C.byref(n)))
+        return ms.value, int(n.value)
+
 
 _tls = threading.local()
 

@@ -11,6 +11,8 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <utility>
+#include <vector>
 
 #include "../../include/apmm_cuda.h"
 #include "internal.h"
@@ -27,6 +29,10 @@ struct apmm_ctx {
   void* io = nullptr;  // device staging for the synchronous host entry points
   size_t io_bytes = 0;
   uint64_t launches = 0;
+  // measurement: event pairs around launches of kernel class 0 (GEMM) / 1 (expand)
+  bool timing = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pending[2];
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> spare;
 };
 
 namespace {
@@ -134,6 +140,30 @@ MatmulWs carve(void* ws, uint64_t rows_w, uint64_t rows_x, uint64_t k) {
   return m;
 }
 
+// Event bracket around one launch when timing is enabled.
+struct TimedLaunch {
+  apmm_ctx* ctx;
+  int kind;
+  cudaStream_t s;
+  std::pair<cudaEvent_t, cudaEvent_t> ev{nullptr, nullptr};
+  TimedLaunch(apmm_ctx* c, int k, cudaStream_t st) : ctx(c), kind(k), s(st) {
+    if (!ctx->timing) return;
+    if (!ctx->spare.empty()) {
+      ev = ctx->spare.back();
+      ctx->spare.pop_back();
+    } else {
+      cudaEventCreate(&ev.first);
+      cudaEventCreate(&ev.second);
+    }
+    cudaEventRecord(ev.first, s);
+  }
+  ~TimedLaunch() {
+    if (!ctx->timing) return;
+    cudaEventRecord(ev.second, s);
+    ctx->pending[kind].push_back(ev);
+  }
+};
+
 int run_matmul(apmm_ctx* ctx, const uint32_t* w, uint64_t rows_w, int n_w, const double* s_w,
                int gran_w, const uint32_t* x, uint64_t rows_x, int n_x, const double* s_x,
                int gran_x, uint64_t k, int32_t* y, float* yf, cudaStream_t stream) {
@@ -145,8 +175,11 @@ int run_matmul(apmm_ctx* ctx, const uint32_t* w, uint64_t rows_w, int n_w, const
   if (rsx_pad > rows_x) {
     CU(cudaMemsetAsync(m.rowsum_x + rows_x, 0, (rsx_pad - rows_x) * 4, stream));
   }
-  CU(launch_expand(w, rows_w, k, n_w, m.codes_w, m.kpad, m.rowsum_w, stream));
-  CU(launch_expand(x, rows_x, k, n_x, m.codes_x, m.kpad, m.rowsum_x, stream));
+  {
+    TimedLaunch t(ctx, 1, stream);
+    CU(launch_expand(w, rows_w, k, n_w, m.codes_w, m.kpad, m.rowsum_w, stream));
+    CU(launch_expand(x, rows_x, k, n_x, m.codes_x, m.kpad, m.rowsum_x, stream));
+  }
   ctx->launches += 2;
   GemmArgs a{};
   a.codes_w = m.codes_w;
@@ -167,14 +200,17 @@ int run_matmul(apmm_ctx* ctx, const uint32_t* w, uint64_t rows_w, int n_w, const
   a.gran_x = gran_x;
   a.num_sms = ctx->num_sms;
   int launches = 0;
-  CU(launch_gemm_tc(a, stream, &launches));
+  {
+    TimedLaunch t(ctx, 0, stream);
+    CU(launch_gemm_tc(a, stream, &launches));
+  }
   ctx->launches += static_cast<uint64_t>(launches);
   return APMM_OK;
 }
 
-cudaStream_t pick(apmm_ctx* ctx, apmm_stream_t s) {
-  return s ? reinterpret_cast<cudaStream_t>(s) : ctx->stream;
-}
+// Device entry points run on exactly the stream they are given (NULL = the legacy default
+// stream, as everywhere in CUDA); only the host entry points use the context's stream.
+cudaStream_t pick(apmm_ctx* /*ctx*/, apmm_stream_t s) { return reinterpret_cast<cudaStream_t>(s); }
 
 // Host-side PackedBitPlanes invariants (bitplane.cpp:17-32).
 int check_padding(const uint32_t* planes, uint64_t rows, uint64_t cols, int n) {
@@ -257,6 +293,12 @@ int apmm_ctx_destroy(apmm_ctx* ctx) {
   if (ctx->ws) cudaFree(ctx->ws);
   if (ctx->io) cudaFree(ctx->io);
   if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+  for (auto* v : {&ctx->pending[0], &ctx->pending[1], &ctx->spare}) {
+    for (auto& ev : *v) {
+      cudaEventDestroy(ev.first);
+      cudaEventDestroy(ev.second);
+    }
+  }
   delete ctx;
   return APMM_OK;
 }
@@ -270,6 +312,31 @@ int apmm_ctx_set_stream(apmm_ctx* ctx, apmm_stream_t stream) {
 }
 
 uint64_t apmm_ctx_launch_count(const apmm_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int apmm_ctx_enable_timing(apmm_ctx* ctx, int enable) {
+  if (!ctx) return fail(APMM_E_INVALID_ARGUMENT, "null context");
+  ctx->timing = enable != 0;
+  return APMM_OK;
+}
+
+int apmm_ctx_kernel_time(apmm_ctx* ctx, int kernel, double* total_ms, uint64_t* launches) {
+  if (!ctx || !total_ms || !launches || kernel < 0 || kernel > 1) {
+    return fail(APMM_E_INVALID_ARGUMENT, "bad argument");
+  }
+  CU(cudaSetDevice(ctx->device));
+  double sum = 0.0;
+  for (auto& ev : ctx->pending[kernel]) {
+    CU(cudaEventSynchronize(ev.second));
+    float ms = 0.f;
+    CU(cudaEventElapsedTime(&ms, ev.first, ev.second));
+    sum += ms;
+    ctx->spare.push_back(ev);
+  }
+  *launches = ctx->pending[kernel].size();
+  *total_ms = sum;
+  ctx->pending[kernel].clear();
+  return APMM_OK;
+}
 
 int apmm_overflow_bound(int n_w, int n_x, uint64_t k, int64_t* bound) {
   int st;
@@ -370,7 +437,7 @@ int apmm_decompose_and_pack(apmm_ctx* ctx, const uint8_t* codes, uint64_t rows, 
   uint8_t* d_codes = static_cast<uint8_t*>(ctx->io);
   uint32_t* d_planes = reinterpret_cast<uint32_t*>(d_codes + in_b);
   CU(cudaMemcpyAsync(d_codes, codes, rows * cols, cudaMemcpyHostToDevice, ctx->stream));
-  if ((st = apmm_cu_pack(ctx, d_codes, rows, cols, n, d_planes, nullptr))) return st;
+  if ((st = apmm_cu_pack(ctx, d_codes, rows, cols, n, d_planes, reinterpret_cast<apmm_stream_t>(ctx->stream)))) return st;
   CU(cudaMemcpyAsync(planes, d_planes, out_b, cudaMemcpyDeviceToHost, ctx->stream));
   CU(cudaStreamSynchronize(ctx->stream));
   return APMM_OK;
@@ -388,7 +455,7 @@ int apmm_unpack(apmm_ctx* ctx, const uint32_t* planes, uint64_t rows, uint64_t c
   uint8_t* d_codes = static_cast<uint8_t*>(ctx->io) + in_b;
   CU(cudaMemcpyAsync(d_planes, planes, apmm_packed_words(n, rows, cols) * 4,
                      cudaMemcpyHostToDevice, ctx->stream));
-  if ((st = apmm_cu_unpack(ctx, d_planes, rows, cols, n, d_codes, nullptr))) return st;
+  if ((st = apmm_cu_unpack(ctx, d_planes, rows, cols, n, d_codes, reinterpret_cast<apmm_stream_t>(ctx->stream)))) return st;
   CU(cudaMemcpyAsync(codes, d_codes, out_b, cudaMemcpyDeviceToHost, ctx->stream));
   CU(cudaStreamSynchronize(ctx->stream));
   return APMM_OK;
@@ -410,7 +477,8 @@ int apmm_quantize_pack(apmm_ctx* ctx, const double* values, uint64_t rows, uint6
   double* d_s = reinterpret_cast<double*>(base + x_b + p_b);
   uint8_t* d_c = codes ? base + x_b + p_b + s_b : nullptr;
   CU(cudaMemcpyAsync(d_x, values, rows * cols * 8, cudaMemcpyHostToDevice, ctx->stream));
-  if ((st = apmm_cu_quantize_pack(ctx, d_x, rows, cols, n, granularity, d_p, d_s, d_c, nullptr))) {
+  if ((st = apmm_cu_quantize_pack(ctx, d_x, rows, cols, n, granularity, d_p, d_s, d_c,
+                                   reinterpret_cast<apmm_stream_t>(ctx->stream)))) {
     return st;
   }
   CU(cudaMemcpyAsync(planes, d_p, apmm_packed_words(n, rows, cols) * 4, cudaMemcpyDeviceToHost,

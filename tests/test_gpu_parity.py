@@ -1,0 +1,305 @@
+"""GPU parity: the B200 path (through the C ABI) against the oracle / reference, bit for
+bit on integers, on the same seeded inputs. Mirrors the reference's own tests
+(proj/tests/test_kernel.cpp, test_bitplane.cpp, test_bipolar.cpp, acceptance.cpp) and
+extends them to BASELINE.json's full sizes via exact row-sampled checks."""
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+from oracle import PER_ROW, PER_TENSOR
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def planes(ap, oracle, codes, n):
+    rows, cols = codes.shape
+    return ap.PackedBitPlanes(rows, cols, ap.BitWidth(n), oracle.pack(codes, n))
+
+
+def gpu_matmul(ap, ctx, oracle, wc, nw, xc, nx, cfg=None):
+    w, x = planes(ap, oracle, wc, nw), planes(ap, oracle, xc, nx)
+    return ap.matmul_ap(w, x, cfg or ap.TileConfig(), ctx)
+
+
+# ---------------------------------------------------------------- known answers
+def test_worked_two_bit_example(gpu, oracle):
+    ap, ctx = gpu
+    # test_kernel.cpp:125-136: W=[3,1], X=[-1,3] -> 0
+    wc = np.array([[0b11, 0b10]], np.uint8)
+    xc = np.array([[0b01, 0b11]], np.uint8)
+    assert gpu_matmul(ap, ctx, oracle, wc, 2, xc, 2).tolist() == [[0]]
+    # 1-bit worked row (test_kernel.cpp:58-66): [+1,+1].[-1,+1] = 0
+    assert gpu_matmul(ap, ctx, oracle, np.array([[1, 1]], np.uint8), 1,
+                      np.array([[0, 1]], np.uint8), 1).tolist() == [[0]]
+
+
+def test_k1_plane_products_are_signs(gpu, oracle):
+    ap, ctx = gpu
+    rng = oracle.rng(3)
+    for _ in range(20):
+        wc, xc = rng.random_codes(3, 1, 2), rng.random_codes(4, 1, 2)
+        assert np.array_equal(gpu_matmul(ap, ctx, oracle, wc, 2, xc, 2),
+                              oracle.decoded_matmul(wc, 2, xc, 2))
+
+
+def test_ragged_k40(gpu, oracle):
+    ap, ctx = gpu
+    rng = oracle.rng(27)  # test_kernel.cpp:226-231
+    wc, xc = rng.random_codes(6, 40, 3), rng.random_codes(5, 40, 2)
+    assert np.array_equal(gpu_matmul(ap, ctx, oracle, wc, 3, xc, 2),
+                          oracle.decoded_matmul(wc, 3, xc, 2))
+
+
+def test_golden_vectors_from_reference(gpu, golden):
+    ap, ctx = gpu
+    for c in golden["matmul"]:
+        w = ap.PackedBitPlanes(c["rows_w"], c["k"], ap.BitWidth(c["n_w"]),
+                               np.array(c["w_words"], np.uint32))
+        x = ap.PackedBitPlanes(c["rows_x"], c["k"], ap.BitWidth(c["n_x"]),
+                               np.array(c["x_words"], np.uint32))
+        assert ap.matmul_ap(w, x, ctx=ctx).reshape(-1).tolist() == c["y"]
+
+
+# ---------------------------------------------------------------- randomized corpora
+def test_randomized_corpus_200(gpu, oracle):
+    ap, ctx = gpu
+    rng = oracle.rng(31)  # test_kernel.cpp:233-245
+    for _ in range(200):
+        m, n, k = rng.range(1, 32), rng.range(1, 32), rng.range(1, 200)
+        nw, nx = rng.range(1, 8), rng.range(1, 8)
+        wc, xc = rng.random_codes(m, k, nw), rng.random_codes(n, k, nx)
+        assert np.array_equal(gpu_matmul(ap, ctx, oracle, wc, nw, xc, nx),
+                              oracle.decoded_matmul(wc, nw, xc, nx)), (m, n, k, nw, nx)
+
+
+def test_acceptance_oracle_equivalence_1000(gpu, oracle):
+    ap, ctx = gpu
+    rng = oracle.rng(101)  # acceptance.cpp:56-77
+    for _ in range(1000):
+        m, n, k = rng.range(1, 32), rng.range(1, 32), rng.range(1, 200)
+        nw, nx = rng.range(1, 8), rng.range(1, 8)
+        wc, xc = rng.random_codes(m, k, nw), rng.random_codes(n, k, nx)
+        assert np.array_equal(gpu_matmul(ap, ctx, oracle, wc, nw, xc, nx),
+                              oracle.decoded_matmul(wc, nw, xc, nx))
+
+
+def test_tile_shapes_and_edges(gpu, oracle):
+    """Shapes straddling the 128x256x128 tile grid, ragged in every dimension."""
+    ap, ctx = gpu
+    rng = oracle.rng(77)
+    for (m, n, k) in [(127, 255, 127), (128, 256, 128), (129, 257, 129), (300, 513, 1000),
+                      (1, 600, 300), (700, 1, 300), (257, 3, 4097), (5, 260, 33)]:
+        nw, nx = rng.range(1, 8), rng.range(1, 8)
+        while oracle.overflow_bound(nw, nx, k) > 2**31 - 1:
+            nx -= 1
+        wc, xc = rng.random_codes(m, k, nw), rng.random_codes(n, k, nx)
+        wp, xp = oracle.pack(wc, nw), oracle.pack(xc, nx)
+        want = oracle.matmul_ap_mt(wp, m, nw, xp, n, nx, k, 8)
+        assert np.array_equal(gpu_matmul(ap, ctx, oracle, wc, nw, xc, nx), want), (m, n, k)
+
+
+def test_schedule_independence(gpu, oracle):
+    ap, ctx = gpu
+    rng = oracle.rng(707)  # acceptance.cpp:268-294: 100x100x300 W3A4, 9 configs
+    wc, xc = rng.random_codes(100, 300, 3), rng.random_codes(100, 300, 4)
+    ref = gpu_matmul(ap, ctx, oracle, wc, 3, xc, 4)
+    assert np.array_equal(ref, oracle.decoded_matmul(wc, 3, xc, 4))
+    for cfg in [(1, 1, 32), (1, 100, 32), (100, 1, 96), (100, 100, 320), (128, 128, 4096),
+                (7, 13, 64), (33, 17, 160), (3, 97, 2048), (64, 64, 512)]:
+        assert np.array_equal(gpu_matmul(ap, ctx, oracle, wc, 3, xc, 4, ap.TileConfig(*cfg)), ref)
+
+
+def test_determinism(gpu, oracle):
+    ap, ctx = gpu
+    rng = oracle.rng(5)
+    wc, xc = rng.random_codes(333, 777, 4), rng.random_codes(444, 777, 8)
+    a = gpu_matmul(ap, ctx, oracle, wc, 4, xc, 8)
+    b = gpu_matmul(ap, ctx, oracle, wc, 4, xc, 8)
+    assert np.array_equal(a, b)
+
+
+# ---------------------------------------------------------------- overflow contract
+def test_overflow_guard(gpu, oracle):
+    ap, ctx = gpu
+    rng = oracle.rng(99)  # verify.cpp:373-409
+    wc, xc = rng.random_codes(1, 33026, 8), rng.random_codes(1, 33026, 8)
+    with pytest.raises(ap.OverflowBound):
+        gpu_matmul(ap, ctx, oracle, wc, 8, xc, 8)
+    wc, xc = rng.random_codes(3, 33025, 8), rng.random_codes(2, 33025, 8)
+    assert np.array_equal(gpu_matmul(ap, ctx, oracle, wc, 8, xc, 8),
+                          oracle.decoded_matmul(wc, 8, xc, 8))
+    # extreme codes: all-max and all-min at the admissible edge (|Y| = bound)
+    for cw, cx in [(255, 255), (0, 255), (0, 0)]:
+        wc = np.full((2, 33025), cw, np.uint8)
+        xc = np.full((3, 33025), cx, np.uint8)
+        got = gpu_matmul(ap, ctx, oracle, wc, 8, xc, 8)
+        assert np.array_equal(got, oracle.decoded_matmul(wc, 8, xc, 8))
+        assert abs(int(got[0, 0])) == 33025 * 255 * 255
+
+
+def test_dimension_mismatch(gpu, oracle):
+    ap, ctx = gpu
+    w = planes(ap, oracle, np.ones((1, 2), np.uint8), 1)
+    x = planes(ap, oracle, np.ones((1, 3), np.uint8), 1)
+    with pytest.raises(ap.DimensionMismatch):
+        ap.matmul_ap(w, x, ctx=ctx)
+
+
+# ---------------------------------------------------------------- full BASELINE sizes
+def _row_sample_check(ap, ctx, oracle, n_out, m_tok, k, nw, nx, seed, sample=48):
+    """Exact check of a random subset of output rows (every tile row-block and all
+    columns), oracle computed on just those weight rows."""
+    import torch
+    dev = torch.device("cuda", 0)
+    g = torch.Generator(device=dev)
+    g.manual_seed(seed)
+    wc = torch.randint(0, 1 << nw, (n_out, k), generator=g, device=dev, dtype=torch.uint8)
+    xc = torch.randint(0, 1 << nx, (m_tok, k), generator=g, device=dev, dtype=torch.uint8)
+    wpr = (k + 31) // 32
+    wp = torch.empty(nw * n_out * wpr, dtype=torch.int32, device=dev)
+    xp = torch.empty(nx * m_tok * wpr, dtype=torch.int32, device=dev)
+    ap.cu_pack(wc, n_out, k, nw, wp, ctx)
+    ap.cu_pack(xc, m_tok, k, nx, xp, ctx)
+    y = torch.empty((n_out, m_tok), dtype=torch.int32, device=dev)
+    ap.cu_matmul_ap(wp, n_out, nw, xp, m_tok, nx, k, y, ctx)
+    torch.cuda.synchronize()
+    rows = np.unique(np.concatenate([
+        np.array([0, n_out - 1]),
+        np.random.default_rng(seed).integers(0, n_out, size=sample)]))
+    wc_h = wc.cpu().numpy()[rows]
+    xc_h = xc.cpu().numpy()
+    # the GPU pack is itself checked against the oracle pack here
+    assert np.array_equal(xp.cpu().numpy().view(np.uint32), oracle.pack(xc_h, nx))
+    want = oracle.matmul_ap_mt(oracle.pack(wc_h, nw), len(rows), nw, oracle.pack(xc_h, nx),
+                               m_tok, nx, k, os.cpu_count() or 4)
+    got = y.cpu().numpy()[rows]
+    assert np.array_equal(got, want), (n_out, m_tok, k, nw, nx)
+    return y
+
+
+@pytest.mark.parametrize("nw,nx", [(1, 2), (2, 4), (3, 8), (4, 8)])
+def test_config2_4096_cubed_row_sampled(gpu, oracle, nw, nx):
+    ap, ctx = gpu
+    _row_sample_check(ap, ctx, oracle, 4096, 4096, 4096, nw, nx, seed=nw * 10 + nx)
+
+
+def test_config1_1024_cubed_full_bit_exact(gpu, oracle):
+    ap, ctx = gpu
+    rng = oracle.rng(1)  # apmm.cpp:150,161-162: seed 1, W then X
+    wc, xc = rng.random_codes(1024, 1024, 2), rng.random_codes(1024, 1024, 2)
+    wp, xp = oracle.pack(wc, 2), oracle.pack(xc, 2)
+    want = oracle.matmul_ap_mt(wp, 1024, 2, xp, 1024, 2, 1024, os.cpu_count() or 4)
+    assert np.array_equal(gpu_matmul(ap, ctx, oracle, wc, 2, xc, 2), want)
+
+
+@pytest.mark.parametrize("n_out,k,m_tok", [(4096, 4096, 2048), (11008, 4096, 512),
+                                           (4096, 11008, 128), (4096, 4096, 1)])
+def test_config3_llama7b_row_sampled(gpu, oracle, n_out, k, m_tok):
+    ap, ctx = gpu
+    _row_sample_check(ap, ctx, oracle, n_out, m_tok, k, 2, 4, seed=n_out + k + m_tok)
+
+
+@pytest.mark.parametrize("m_tok", [1, 8, 16])
+def test_config4_decode_w3a8(gpu, oracle, m_tok):
+    ap, ctx = gpu
+    _row_sample_check(ap, ctx, oracle, 8192, m_tok, 8192, 3, 8, seed=m_tok, sample=256)
+
+
+# ---------------------------------------------------------------- pack / unpack / quantize
+def test_pack_unpack_match_oracle(gpu, oracle, golden):
+    ap, ctx = gpu
+    for case in golden["pack"]:
+        codes = np.array(case["codes"], np.uint8).reshape(case["rows"], case["cols"])
+        p = ap.decompose_and_pack(codes, ap.BitWidth(case["n"]), ctx)
+        assert p.words().tolist() == case["words"]
+        assert np.array_equal(ap.unpack(p, ctx), codes)
+    rng = oracle.rng(7)  # test_bitplane.cpp:68-78: 500 round trips
+    for _ in range(100):
+        rows, cols, n = rng.range(1, 70), rng.range(1, 70), rng.range(1, 8)
+        codes = rng.random_codes(rows, cols, n)
+        p = ap.decompose_and_pack(codes, ap.BitWidth(n), ctx)
+        assert np.array_equal(p.words(), oracle.pack(codes, n))
+        assert np.array_equal(ap.unpack(p, ctx), codes)
+    with pytest.raises(ap.OutOfRange):  # CodeMatrix ctor (bipolar.cpp:33-36)
+        ap.decompose_and_pack(np.array([[4]], np.uint8), ap.BitWidth(2), ctx)
+
+
+def test_quantize_bit_exact(gpu, oracle, golden):
+    ap, ctx = gpu
+    for case in golden["quantize"]:
+        x = np.array([float.fromhex(h) for h in case["x"]]).reshape(case["rows"], case["cols"])
+        q = ap.quantize(x, ap.BitWidth(case["n"]), ap.Granularity(case["gran"]), ctx)
+        assert q.codes.reshape(-1).tolist() == case["codes"]
+        assert [float(v).hex() for v in q.scales] == case["scales"]
+        assert np.array_equal(q.packed.words(), oracle.pack(q.codes, case["n"]))
+    rng = np.random.default_rng(606)  # acceptance.cpp:236-263 style inputs
+    for t in range(40):
+        rows, cols, n = int(rng.integers(1, 80)), int(rng.integers(1, 300)), int(rng.integers(1, 9))
+        x = rng.uniform(-100, 100, size=(rows, cols))
+        x[rng.random(size=x.shape) < 0.1] = 0.0
+        if t % 5 == 0:
+            x[0] = 0.0
+        for gran in (PER_TENSOR, PER_ROW):
+            q = ap.quantize(x, ap.BitWidth(n), ap.Granularity(gran), ctx)
+            c, s = oracle.quantize(x, n, gran)
+            assert np.array_equal(q.codes, c) and np.array_equal(q.scales, s)
+    with pytest.raises(ap.NonFinite):
+        ap.quantize(np.array([[1.0, np.nan]]), ap.BitWidth(2), ap.Granularity.PerTensor, ctx)
+    with pytest.raises(ap.NonFinite):
+        ap.quantize(np.array([[1.0], [np.inf]]), ap.BitWidth(2), ap.Granularity.PerRow, ctx)
+
+
+def test_dequant_epilogue(gpu, oracle):
+    """Fused dequant vs the CLI epilogue (apmm.cpp:329-340) computed by the oracle in fp64:
+    north-star tolerance 1e-3 relative; the device does the same fp64 ops, so it is exact."""
+    ap, ctx = gpu
+    rng = np.random.default_rng(11)
+    for (m, n, k, nw, nx, gw, gx) in [(1, 1, 2, 2, 2, 0, 0), (64, 48, 300, 2, 4, 1, 1),
+                                      (300, 257, 1000, 3, 8, 1, 0), (129, 1, 4096, 4, 8, 0, 1)]:
+        wv, xv = rng.uniform(-1, 1, (m, k)), rng.uniform(-1, 1, (n, k))
+        wc, ws = oracle.quantize(wv, nw, gw)
+        xc, xs = oracle.quantize(xv, nx, gx)
+        w, x = planes(ap, oracle, wc, nw), planes(ap, oracle, xc, nx)
+        got = ap.matmul_ap_dequant(w, ws, ap.Granularity(gw), x, xs, ap.Granularity(gx), ctx)
+        y = oracle.matmul_ap(w.words(), m, nw, x.words(), n, nx, k)
+        want = oracle.dequant_epilogue(y, ws, gw, xs, gx)
+        np.testing.assert_allclose(got, want, rtol=1e-3, atol=0)
+        assert np.array_equal(got, want)
+    # CLI worked example (test_cli.cpp:147-181) -> 0
+    wc, ws = oracle.quantize(np.array([[3.0, 1.0]]), 2, 0)
+    xc, xs = oracle.quantize(np.array([[-1.0, 3.0]]), 2, 0)
+    out = ap.matmul_ap_dequant(planes(ap, oracle, wc, 2), ws, ap.Granularity.PerTensor,
+                               planes(ap, oracle, xc, 2), xs, ap.Granularity.PerTensor, ctx)
+    assert out.tolist() == [[0.0]]
+
+
+def test_end_to_end_quantize_pack_matmul_dequant(gpu, oracle):
+    """The whole north-star path on device: fp64 activations -> quantize+pack (K2) ->
+    GEMM (K3) -> dequant, vs the oracle chain."""
+    ap, ctx = gpu
+    rng = np.random.default_rng(2409)
+    wv, xv = rng.uniform(-1, 1, (256, 512)), rng.uniform(-1, 1, (130, 512))
+    qw = ap.quantize(wv, ap.BitWidth(2), ap.Granularity.PerRow, ctx)
+    qx = ap.quantize(xv, ap.BitWidth(4), ap.Granularity.PerRow, ctx)
+    got = ap.matmul_ap_dequant(qw.packed, qw.scales, qw.granularity, qx.packed, qx.scales,
+                               qx.granularity, ctx)
+    wc, ws = oracle.quantize(wv, 2, PER_ROW)
+    xc, xs = oracle.quantize(xv, 4, PER_ROW)
+    y = oracle.decoded_matmul(wc, 2, xc, 4)
+    assert np.array_equal(got, oracle.dequant_epilogue(y, ws, PER_ROW, xs, PER_ROW))
+
+
+# ---------------------------------------------------------------- the reference's own suite
+def test_reference_run_verify_with_gpu_kernel():
+    """apmm::run_verify (verify.cpp:413-463) with the B200 kernel in its KernelFn seam,
+    via include/apmm_b200.hpp; plus the mutation check (test_verify.cpp:47-86)."""
+    exe = os.path.join(ROOT, "oracle", "_ref", "verify_gpu")
+    if not os.path.exists(exe):
+        pytest.skip("oracle/_ref/verify_gpu not built")
+    for seed in ("1", "2"):
+        r = subprocess.run([exe, seed, "1000"], capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stdout + r.stderr
+        assert r.stdout.count("PASS") == 9 and "mutant kernel caught" in r.stdout
