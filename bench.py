@@ -296,7 +296,7 @@ def run_ours(args, rank, world, local_rank):
     # heat: ~1 s of untimed steps so clocks settle and the sampler sees the load
     clocks = ClockSampler(local_rank)
     clocks.start()
-    t_end = time.time() + 1.0
+    t_end = time.time() + (0.0 if args.profile else 1.0)
     while time.time() < t_end:
         step()
         torch.cuda.synchronize()
@@ -328,6 +328,9 @@ def run_ours(args, rank, world, local_rank):
     value = world * args.steps * ops_step / (ms_max * 1e-3) / 1e12
 
     # -- e2e through the public host API: pinned host planes -> H2D -> GEMM -> D2H int32
+    if args.profile:
+        print(json.dumps({"profile_run": True, "ms_per_step": ms_max / args.steps}), flush=True)
+        return
     e2e_steps = max(1, min(args.steps, 3))
     host = []
     h2d = d2h = 0
@@ -419,6 +422,8 @@ def main():
     ap_.add_argument("--workload", default="sweep4096",
                      choices=["sweep4096", "w2a4_4096", "llama7b", "decode", "ffn70b"])
     ap_.add_argument("--no-cpu-baseline", action="store_true")
+    ap_.add_argument("--profile", action="store_true",
+                     help="for ncu: no heat phase, no e2e, no CPU baseline (numbers invalid)")
     args = ap_.parse_args()
     args.warmup = max(3, args.warmup)
 

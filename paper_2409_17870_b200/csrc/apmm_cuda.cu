@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <utility>
@@ -31,6 +32,7 @@ struct apmm_ctx {
   uint64_t launches = 0;
   // measurement: event pairs around launches of kernel class 0 (GEMM) / 1 (expand)
   bool timing = false;
+  bool force_single_sm = false;  // APMM_FORCE_1SM=1: always use the 1-SM kernel (testing)
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pending[2];
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> spare;
 };
@@ -177,10 +179,10 @@ int run_matmul(apmm_ctx* ctx, const uint32_t* w, uint64_t rows_w, int n_w, const
   }
   {
     TimedLaunch t(ctx, 1, stream);
-    CU(launch_expand(w, rows_w, k, n_w, m.codes_w, m.kpad, m.rowsum_w, stream));
-    CU(launch_expand(x, rows_x, k, n_x, m.codes_x, m.kpad, m.rowsum_x, stream));
+    CU(launch_expand(w, rows_w, n_w, m.codes_w, m.rowsum_w, x, rows_x, n_x, m.codes_x,
+                     m.rowsum_x, k, m.kpad, ctx->num_sms, stream));
   }
-  ctx->launches += 2;
+  ctx->launches += 1;
   GemmArgs a{};
   a.codes_w = m.codes_w;
   a.codes_x = m.codes_x;
@@ -202,7 +204,13 @@ int run_matmul(apmm_ctx* ctx, const uint32_t* w, uint64_t rows_w, int n_w, const
   int launches = 0;
   {
     TimedLaunch t(ctx, 0, stream);
-    CU(launch_gemm_tc(a, stream, &launches));
+    // CTA-pair 256x256 tiles when they fill the machine, else 1-SM 128x256 tiles
+    const uint64_t pair_tiles = ((rows_w + 255) / 256) * ((rows_x + kPairN - 1) / kPairN);
+    if (pair_tiles >= static_cast<uint64_t>(ctx->num_sms / 2) && !ctx->force_single_sm) {
+      CU(launch_gemm_pair(a, stream, &launches));
+    } else {
+      CU(launch_gemm_tc(a, stream, &launches));
+    }
   }
   ctx->launches += static_cast<uint64_t>(launches);
   return APMM_OK;
@@ -276,6 +284,7 @@ int apmm_ctx_create(apmm_ctx** out, int device) {
   auto* ctx = new apmm_ctx();
   ctx->device = device;
   ctx->num_sms = prop.multiProcessorCount;
+  if (const char* f = std::getenv("APMM_FORCE_1SM")) ctx->force_single_sm = f[0] == '1';
   cudaError_t e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
   if (e != cudaSuccess) {
     delete ctx;

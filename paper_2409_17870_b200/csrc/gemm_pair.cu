@@ -1,0 +1,293 @@
+// gemm_pair.cu -- K3 (large tiles): the WnAm bipolar-INT GEMM on a CTA PAIR
+// (tcgen05 cta_group::2), 256 x 256 output tile per pair.
+//
+// Same arithmetic as gemm_tc.cu (one u8 x u8 kind::i8 MMA recovers every 2^(i+j)-weighted
+// plane pair; rank-1 correction in the epilogue), but each MMA spans both SMs of a TPC:
+// CTA r holds W rows [tm*256 + r*128, +128) (A) and X rows [tn*256 + r*128, +128) (B);
+// the leader's tcgen05.mma.cta_group::2 (M=256, N=256, K=32) reads A and B from both
+// CTAs' shared memory and writes a 128 x 256 s32 accumulator into each CTA's TMEM. Per
+// SM this halves the operand bytes per MAC relative to the 1-SM 128x256 tile (32 KB per
+// 128-K stage instead of 48 KB), which leaves room for 6 stages.
+//
+// Roles (both CTAs unless noted):
+//   warp 0     TMA producer: own halves of A and B; completion bytes land on the LEADER's
+//              full barrier (leader arms it with the pair's 64 KB)
+//   warp 1     (leader) MMA issuer; tcgen05.commit multicast frees smem slots in both CTAs
+//              and signals both CTAs' epilogues
+//   warp 2     TMEM allocator (cta_group::2, 512 columns = 2 accumulator buffers)
+//   warps 4-7  epilogue: tcgen05.ld -> rank-1 recovery (or fp64 dequant) -> 128B-swizzled
+//              smem staging -> TMA bulk tensor store; arrive on the leader's tmem_empty
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "internal.h"
+#include "ptx.cuh"
+
+namespace apmm_b200 {
+namespace {
+
+using namespace apmm_ptx;
+
+constexpr int kHalf = 128;                   // rows of A and of B held per CTA
+constexpr int kStages = 6;
+constexpr int kAS = kHalf * kBK;             // 16 KB
+constexpr int kStageBytes = 2 * kHalf * kBK; // A + B = 32 KB per CTA per stage
+constexpr int kThreads = 256;
+constexpr int kEpiBuf = 32 * 32 * 4;         // one 32x32 x 4B staging tile
+constexpr uint32_t kTmemCols = 512;
+constexpr int kSmemBytes = kStages * kStageBytes + 4 * 2 * kEpiBuf + 1024 + 256;
+constexpr uint32_t kIdesc = idesc_i8_u8u8(2 * kHalf, kPairN);
+
+struct Params {
+  const int32_t* rowsum_w;
+  const int32_t* rowsum_x;
+  int32_t* y;
+  float* yf;
+  const double* s_w;
+  const double* s_x;
+  int gran_w, gran_x;
+  uint32_t rows_w, rows_x;
+  uint32_t kblocks;
+  uint32_t tiles_m, tiles_n;
+  uint32_t coef_w, coef_x, c0;
+  uint32_t tma_store;  // 1: epilogue stores through tmap_y
+};
+
+__device__ __forceinline__ uint32_t dequant_bits(uint32_t v, double sw, double sx) {
+  return __float_as_uint(static_cast<float>(__dmul_rn(__dmul_rn(double(int(v)), sw), sx)));
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    gemm_u8_pair_kernel(const __grid_constant__ CUtensorMap tmap_w,
+                        const __grid_constant__ CUtensorMap tmap_x,
+                        const __grid_constant__ CUtensorMap tmap_y, const Params p) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t base_u32 = smem_u32(smem_raw);
+  uint8_t* smem = smem_raw + (((base_u32 + 1023u) & ~1023u) - base_u32);
+  uint8_t* stages = smem;
+  uint8_t* staging = smem + kStages * kStageBytes;
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(staging + 4 * 2 * kEpiBuf);
+  uint64_t* empty_bar = full_bar + kStages;
+  uint64_t* tmem_full = empty_bar + kStages;
+  uint64_t* tmem_empty = tmem_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
+
+  const uint32_t warp = warp_id();
+  const uint32_t lane = lane_id();
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const uint32_t cluster = blockIdx.x >> 1;
+  const uint32_t nclusters = gridDim.x >> 1;
+  const uint32_t num_tiles = p.tiles_m * p.tiles_n;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmap_w);
+    tma_prefetch_desc(&tmap_x);
+    if (p.tma_store) tma_prefetch_desc(&tmap_y);
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tmem_full[s], 1);
+      mbar_init(&tmem_empty[s], 8);  // 4 epilogue warps x 2 CTAs
+    }
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc_pair<kTmemCols>(tmem_slot);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ---------------- TMA producer (both CTAs) ----------------
+    if (elect_one()) {
+      const uint64_t hint = policy_evict_last();
+      uint32_t stage = 0, phase = 0;
+      for (uint32_t t = cluster; t < num_tiles; t += nclusters) {
+        const uint32_t tm = t % p.tiles_m, tn = t / p.tiles_m;
+        for (uint32_t kb = 0; kb < p.kblocks; ++kb) {
+          mbar_wait(&empty_bar[stage], phase ^ 1);
+          if (leader) mbar_arrive_expect_tx(&full_bar[stage], 2 * kStageBytes);
+          const uint32_t fb = mapa(smem_u32(&full_bar[stage]), 0);
+          uint8_t* st = stages + stage * kStageBytes;
+          tma_load_2d_pair(st, &tmap_w, fb, int32_t(kb * kBK), int32_t(tm * 2 * kHalf + rank * kHalf),
+                           hint);
+          tma_load_2d_pair(st + kAS, &tmap_x, fb, int32_t(kb * kBK),
+                           int32_t(tn * kPairN + rank * kHalf), hint);
+          if (++stage == kStages) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // ---------------- MMA issuer (leader only) ----------------
+    if (leader && elect_one()) {
+      uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0;
+      for (uint32_t t = cluster; t < num_tiles; t += nclusters) {
+        mbar_wait(&tmem_empty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * kPairN;
+        for (uint32_t kb = 0; kb < p.kblocks; ++kb) {
+          mbar_wait(&full_bar[stage], phase);
+          tc_fence_after();
+          const uint32_t st = smem_u32(stages + stage * kStageBytes);
+          const uint64_t adesc = umma_desc_sw128(st);
+          const uint64_t bdesc = umma_desc_sw128(st + kAS);
+#pragma unroll
+          for (uint32_t k = 0; k < kBK / 32; ++k) {
+            mma_i8_pair(d_tmem, adesc + 2 * k, bdesc + 2 * k, kIdesc, (kb | k) != 0);
+          }
+          mma_commit_pair_mc(&empty_bar[stage], 0x3);
+          if (++stage == kStages) { stage = 0; phase ^= 1; }
+        }
+        mma_commit_pair_mc(&tmem_full[acc], 0x3);
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      }
+    }
+    __syncwarp();
+  } else if (warp >= 4) {
+    // ---------------- epilogue (both CTAs) ----------------
+    const uint32_t q = warp & 3;
+    uint32_t acc = 0, acc_phase = 0, nbuf = 0;
+    for (uint32_t t = cluster; t < num_tiles; t += nclusters) {
+      const uint32_t tm = t % p.tiles_m, tn = t / p.tiles_m;
+      const uint32_t row0 = tm * 2 * kHalf + rank * kHalf + q * 32;
+      const uint32_t row = row0 + lane;
+      const bool row_ok = row < p.rows_w;
+      const uint32_t rsw = row_ok ? static_cast<uint32_t>(__ldg(p.rowsum_w + row)) : 0u;
+      const uint32_t row_term = p.c0 - p.coef_w * rsw;
+      double sw = 0.0;
+      if (p.yf) sw = p.gran_w ? (row_ok ? p.s_w[row] : 0.0) : p.s_w[0];
+
+      mbar_wait(&tmem_full[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t t_addr = tmem_base + ((q * 32u) << 16) + acc * kPairN;
+#pragma unroll 1
+      for (uint32_t c = 0; c < kPairN / 32; ++c) {
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(t_addr + c * 32, r);
+        tmem_ld_wait();
+        const uint32_t col0 = tn * kPairN + c * 32;
+        const int4* rsx4 = reinterpret_cast<const int4*>(p.rowsum_x + col0);
+#pragma unroll
+        for (int j4 = 0; j4 < 8; ++j4) {
+          const int4 rs = __ldg(rsx4 + j4);
+          r[4 * j4 + 0] = 4u * r[4 * j4 + 0] + row_term - p.coef_x * uint32_t(rs.x);
+          r[4 * j4 + 1] = 4u * r[4 * j4 + 1] + row_term - p.coef_x * uint32_t(rs.y);
+          r[4 * j4 + 2] = 4u * r[4 * j4 + 2] + row_term - p.coef_x * uint32_t(rs.z);
+          r[4 * j4 + 3] = 4u * r[4 * j4 + 3] + row_term - p.coef_x * uint32_t(rs.w);
+        }
+        if (p.yf) {
+          if (p.gran_x) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              const uint32_t cj = col0 + j < p.rows_x ? col0 + j : 0;
+              r[j] = dequant_bits(r[j], sw, __ldg(p.s_x + cj));
+            }
+          } else {
+            const double sx = p.s_x[0];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) r[j] = dequant_bits(r[j], sw, sx);
+          }
+        }
+        if (p.tma_store) {
+          uint8_t* buf = staging + (q * 2 + nbuf) * kEpiBuf;
+          nbuf ^= 1;
+          if (lane == 0) bulk_wait_read<1>();  // the store that last read `buf` is done
+          __syncwarp();
+          const uint32_t base = smem_u32(buf) + lane * 128u;
+#pragma unroll
+          for (uint32_t ch = 0; ch < 8; ++ch) {  // SWIZZLE_128B: 16B chunk ch -> ch ^ (row & 7)
+            st_shared_v4(base + ((ch ^ (lane & 7u)) << 4), r[4 * ch], r[4 * ch + 1],
+                         r[4 * ch + 2], r[4 * ch + 3]);
+          }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&tmap_y, buf, int32_t(col0), int32_t(row0));
+            bulk_commit();
+          }
+        } else if (row_ok && col0 < p.rows_x) {
+          uint32_t* dst = (p.y ? reinterpret_cast<uint32_t*>(p.y) : reinterpret_cast<uint32_t*>(p.yf)) +
+                          uint64_t(row) * p.rows_x + col0;
+#pragma unroll
+          for (uint32_t j = 0; j < 32; ++j) {
+            if (col0 + j < p.rows_x) dst[j] = r[j];
+          }
+        }
+        __syncwarp();
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(mapa(smem_u32(&tmem_empty[acc]), 0));
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    }
+    if (lane == 0) bulk_wait<0>();
+    __syncwarp();
+  }
+
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc_pair<kTmemCols>(tmem_base);
+}
+
+}  // namespace
+
+cudaError_t launch_gemm_pair(const GemmArgs& a, cudaStream_t s, int* launches) {
+  CUtensorMap tw, tx, ty;
+  if (encode_tmap_2d(&tw, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, a.codes_w, a.kpad, a.rows_w, a.kpad,
+                     kBK, kHalf) != CUDA_SUCCESS ||
+      encode_tmap_2d(&tx, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, a.codes_x, a.kpad, a.rows_x, a.kpad,
+                     kBK, kHalf) != CUDA_SUCCESS) {
+    return cudaErrorInvalidValue;
+  }
+  void* out = a.y ? static_cast<void*>(a.y) : static_cast<void*>(a.yf);
+  const bool tma_store = (a.rows_x % 4 == 0) && (reinterpret_cast<uintptr_t>(out) % 16 == 0);
+  if (tma_store) {
+    if (encode_tmap_2d(&ty, a.y ? CU_TENSOR_MAP_DATA_TYPE_INT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                       4, out, a.rows_x, a.rows_w, a.rows_x * 4, 32, 32) != CUDA_SUCCESS) {
+      return cudaErrorInvalidValue;
+    }
+  } else {
+    ty = tw;  // unused
+  }
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(gemm_u8_pair_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  Params p{};
+  p.rowsum_w = a.rowsum_w;
+  p.rowsum_x = a.rowsum_x;
+  p.y = a.y;
+  p.yf = a.yf;
+  p.s_w = a.s_w;
+  p.s_x = a.s_x;
+  p.gran_w = a.gran_w;
+  p.gran_x = a.gran_x;
+  p.rows_w = static_cast<uint32_t>(a.rows_w);
+  p.rows_x = static_cast<uint32_t>(a.rows_x);
+  p.kblocks = static_cast<uint32_t>(a.kpad / kBK);
+  p.tiles_m = static_cast<uint32_t>((a.rows_w + 2 * kHalf - 1) / (2 * kHalf));
+  p.tiles_n = static_cast<uint32_t>((a.rows_x + kPairN - 1) / kPairN);
+  const uint32_t A = (1u << a.n_w) - 1u, B = (1u << a.n_x) - 1u;
+  p.coef_w = 2u * B;
+  p.coef_x = 2u * A;
+  p.c0 = static_cast<uint32_t>(a.k_logical) * A * B;
+  p.tma_store = tma_store ? 1u : 0u;
+  const uint32_t tiles = p.tiles_m * p.tiles_n;
+  const uint32_t max_clusters = static_cast<uint32_t>(a.num_sms / 2);
+  const uint32_t clusters = tiles < max_clusters ? tiles : max_clusters;
+  gemm_u8_pair_kernel<<<2 * clusters, kThreads, kSmemBytes, s>>>(tw, tx, ty, p);
+  *launches += 1;
+  return cudaGetLastError();
+}
+
+}  // namespace apmm_b200

@@ -172,27 +172,32 @@ __global__ void __launch_bounds__(kThreads, 1)
           v[4 * j4 + 2] = 4u * r[4 * j4 + 2] + row_term - p.coef_x * uint32_t(rs.z);
           v[4 * j4 + 3] = 4u * r[4 * j4 + 3] + row_term - p.coef_x * uint32_t(rs.w);
         }
-        const uint64_t off = uint64_t(row) * p.rows_x + col0;
-        const bool full = col0 + 32 <= p.rows_x;
-        if (!row_ok || col0 >= p.rows_x) {
-          // nothing to store for this lane
-        } else if (p.y) {
-          int32_t* dst = p.y + off;
-          if (full && (p.rows_x % 4 == 0)) {
+        if (row_ok && col0 < p.rows_x) {
+          const uint64_t off = uint64_t(row) * p.rows_x + col0;
+          if (p.y) {
+            int32_t* dst = p.y + off;
+            if (col0 + 32 <= p.rows_x && (p.rows_x % 4 == 0)) {
 #pragma unroll
-            for (int j4 = 0; j4 < 8; ++j4) {
-              reinterpret_cast<int4*>(dst)[j4] =
-                  make_int4(int(v[4 * j4]), int(v[4 * j4 + 1]), int(v[4 * j4 + 2]),
-                            int(v[4 * j4 + 3]));
+              for (int j4 = 0; j4 < 8; ++j4) {
+                reinterpret_cast<int4*>(dst)[j4] =
+                    make_int4(int(v[4 * j4]), int(v[4 * j4 + 1]), int(v[4 * j4 + 2]),
+                              int(v[4 * j4 + 3]));
+              }
+            } else {
+#pragma unroll
+              for (uint32_t j = 0; j < 32; ++j) {
+                if (col0 + j < p.rows_x) dst[j] = int(v[j]);
+              }
             }
           } else {
-            for (uint32_t j = 0; j < 32 && col0 + j < p.rows_x; ++j) dst[j] = int(v[j]);
-          }
-        } else {
-          float* dst = p.yf + off;
-          for (uint32_t j = 0; j < 32 && col0 + j < p.rows_x; ++j) {
-            const double sx = p.gran_x ? p.s_x[col0 + j] : p.s_x[0];
-            dst[j] = static_cast<float>(static_cast<double>(int(v[j])) * sw * sx);
+            float* dst = p.yf + off;
+#pragma unroll
+            for (uint32_t j = 0; j < 32; ++j) {
+              if (col0 + j < p.rows_x) {
+                const double sx = p.gran_x ? p.s_x[col0 + j] : p.s_x[0];
+                dst[j] = static_cast<float>(__dmul_rn(__dmul_rn(double(int(v[j])), sw), sx));
+              }
+            }
           }
         }
         __syncwarp();  // reconverge before the next .sync.aligned tcgen05.ld
@@ -214,8 +219,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 cudaError_t launch_gemm_tc(const GemmArgs& a, cudaStream_t s, int* launches) {
   CUtensorMap tw, tx;
-  if (encode_tmap_u8_2d(&tw, a.codes_w, a.kpad, a.rows_w, kBK, kBM) != CUDA_SUCCESS ||
-      encode_tmap_u8_2d(&tx, a.codes_x, a.kpad, a.rows_x, kBK, kBN) != CUDA_SUCCESS) {
+  if (encode_tmap_2d(&tw, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, a.codes_w, a.kpad, a.rows_w, a.kpad,
+                     kBK, kBM) != CUDA_SUCCESS ||
+      encode_tmap_2d(&tx, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, a.codes_x, a.kpad, a.rows_x, a.kpad,
+                     kBK, kBN) != CUDA_SUCCESS) {
     return cudaErrorInvalidValue;
   }
   static bool attr_set = false;

@@ -12,14 +12,18 @@ constexpr int kBM = 128;        // weight rows per CTA tile (MMA M, TMEM lanes)
 constexpr int kBN = 256;        // feature rows per CTA tile (MMA N)
 constexpr int kBK = 128;        // K bytes per pipeline stage (one 128-B swizzle row)
 constexpr int kKAlign = kBK;    // device code rows are padded to a multiple of this
+constexpr int kPairN = 256;     // feature rows per CTA-pair tile (gemm_pair.cu, MMA N)
 constexpr int kRowsumPad = kBN; // rowsum_x is zero-padded to a multiple of this
 
 inline uint64_t round_up(uint64_t v, uint64_t m) { return (v + m - 1) / m * m; }
 
 // ---- prep.cu -------------------------------------------------------------------------
-// planes (reference layout) -> u8 codes [rows x kpad] (zero K padding) + rowsum[rows].
-cudaError_t launch_expand(const uint32_t* planes, uint64_t rows, uint64_t cols, int n,
-                          uint8_t* codes, uint64_t kpad, int32_t* rowsum, cudaStream_t s);
+// Both operands' planes (reference layout) -> u8 codes [rows x kpad] (zero K padding, K
+// permuted identically within each 32-column group) + rowsum[rows], one launch.
+cudaError_t launch_expand(const uint32_t* w_planes, uint64_t rows_w, int n_w,
+                          uint8_t* w_codes, int32_t* w_rowsum, const uint32_t* x_planes,
+                          uint64_t rows_x, int n_x, uint8_t* x_codes, int32_t* x_rowsum,
+                          uint64_t cols, uint64_t kpad, int num_sms, cudaStream_t s);
 cudaError_t launch_pack(const uint8_t* codes, uint64_t rows, uint64_t cols, int n,
                         uint32_t* planes, cudaStream_t s);
 cudaError_t launch_unpack(const uint32_t* planes, uint64_t rows, uint64_t cols, int n,
@@ -49,9 +53,13 @@ struct GemmArgs {
 };
 // Returns the number of kernel launches it enqueued via *launches.
 cudaError_t launch_gemm_tc(const GemmArgs& a, cudaStream_t s, int* launches);
+// ---- gemm_pair.cu (CTA-pair, 256x256 tiles) -------------------------------------------
+cudaError_t launch_gemm_pair(const GemmArgs& a, cudaStream_t s, int* launches);
 
 // Tensor-map encoder obtained from the driver through the runtime (no -lcuda).
-CUresult encode_tmap_u8_2d(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer,
-                           uint32_t box_inner, uint32_t box_outer);
+// 2-D row-major tensor [outer x inner] with `stride_bytes` between rows, 128B swizzle.
+CUresult encode_tmap_2d(CUtensorMap* map, CUtensorMapDataType dtype, uint32_t elem_bytes,
+                        const void* base, uint64_t inner, uint64_t outer, uint64_t stride_bytes,
+                        uint32_t box_inner, uint32_t box_outer);
 
 }  // namespace apmm_b200

@@ -21,47 +21,90 @@ namespace {
 
 constexpr int kThreads = 256;
 
-// Spread a 4-bit nibble x into bit 0 of four bytes: (x*0x00204081) places bit b at
-// 7b+b = 8b with no carries (partial products occupy disjoint bit ranges).
-__device__ __forceinline__ uint32_t spread4(uint32_t x) { return (x * 0x00204081u) & 0x01010101u; }
-
 // ---- K1: planes -> u8 codes ------------------------------------------------------------
-// One block per row. Thread handles 32-column words w; each word yields 32 code bytes.
-// rowsum(U) = sum_k u_k = sum_i 2^i popc(plane_i) -- computed from the planes directly.
-__global__ void __launch_bounds__(kThreads) expand_kernel(const uint32_t* __restrict__ planes,
-                                                           uint32_t rows, uint32_t wpr, int n,
-                                                           uint32_t tail_mask,
-                                                           uint8_t* __restrict__ codes,
-                                                           uint32_t kpad_words,
-                                                           int32_t* __restrict__ rowsum) {
-  const uint32_t r = blockIdx.x;
+// Both GEMM operands in ONE launch (rows [0, rows_w) are W, the rest X), one warp per row,
+// lanes striding over the 32-column words. A lane turns the n plane words of a 32-column
+// group into 32 code bytes with an 8x8 bit transpose done SIMD across the 4 byte lanes of
+// a 32-bit register (3 delta-swap stages, ~60 ALU ops for any n <= 8; rows i >= n are
+// compile-time zero and fold away). The transpose leaves code(k = 8b + c) in byte b of
+// output word c, i.e. the 32 codes of a group are stored in the K order
+// (c, b) -> 4c + b instead of 8b + c. Both operands use the same order, and
+// sum_k u_w(k) u_x(k) is invariant under a common permutation of k, so the GEMM result is
+// unchanged; the zero padding lanes stay zero.
+// rowsum(U) = sum_k u_k = sum_i 2^i popc(plane_i) comes straight from the planes.
+struct ExpandOperand {
+  const uint32_t* planes;
+  uint8_t* codes;
+  int32_t* rowsum;
+  uint32_t rows;
+  int n;
+};
+
+__device__ __forceinline__ void swap_bits(uint32_t& a, uint32_t& b, int s, uint32_t m) {
+  const uint32_t t = ((a >> s) ^ b) & m;
+  b ^= t;
+  a ^= t << s;
+}
+
+template <int N>
+__device__ __forceinline__ int32_t expand_row(const ExpandOperand& op, uint32_t r, uint32_t wpr,
+                                              uint32_t tail_mask, uint32_t kpad_words,
+                                              uint32_t lane) {
   int32_t sum = 0;
-  uint8_t* dst_row = codes + uint64_t(r) * kpad_words * 32u;
-  for (uint32_t w = threadIdx.x; w < kpad_words; w += blockDim.x) {
-    uint32_t out[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    if (w < wpr) {
-      for (int i = 0; i < n; ++i) {
-        uint32_t b = __ldg(planes + (uint64_t(i) * rows + r) * wpr + w);
-        if (w == wpr - 1) b &= tail_mask;  // padding lanes are zero by contract; enforce it
-        sum += __popc(b) << i;
+  uint8_t* dst_row = op.codes + uint64_t(r) * kpad_words * 32u;
+  for (uint32_t w = lane; w < kpad_words; w += 32) {
+    uint32_t x[8];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) out[j] |= spread4((b >> (4 * j)) & 0xFu) << i;
+    for (int i = 0; i < 8; ++i) x[i] = 0u;
+    if (w < wpr) {
+      const uint32_t mask = (w == wpr - 1) ? tail_mask : 0xffffffffu;
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        x[i] = __ldg(op.planes + (uint64_t(i) * op.rows + r) * wpr + w) & mask;
+        sum += __popc(x[i]) << i;
       }
     }
-    uint4* d = reinterpret_cast<uint4*>(dst_row + uint64_t(w) * 32u);
-    d[0] = make_uint4(out[0], out[1], out[2], out[3]);
-    d[1] = make_uint4(out[4], out[5], out[6], out[7]);
-  }
-  // block reduction of the row sum
-  __shared__ int32_t red[kThreads / 32];
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = sum;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int32_t s = 0;
-    for (int i = 0; i < int(blockDim.x / 32); ++i) s += red[i];
-    rowsum[r] = s;
+    for (int i = 0; i < 4; ++i) swap_bits(x[i], x[i + 4], 4, 0x0F0F0F0Fu);
+#pragma unroll
+    for (int i = 0; i < 8; i += 4) {
+      swap_bits(x[i], x[i + 2], 2, 0x33333333u);
+      swap_bits(x[i + 1], x[i + 3], 2, 0x33333333u);
+    }
+#pragma unroll
+    for (int i = 0; i < 8; i += 2) swap_bits(x[i], x[i + 1], 1, 0x55555555u);
+    uint4* d = reinterpret_cast<uint4*>(dst_row + uint64_t(w) * 32u);
+    d[0] = make_uint4(x[0], x[1], x[2], x[3]);
+    d[1] = make_uint4(x[4], x[5], x[6], x[7]);
+  }
+  return sum;
+}
+
+__global__ void __launch_bounds__(kThreads) expand_kernel(ExpandOperand a, ExpandOperand b,
+                                                           uint32_t wpr, uint32_t tail_mask,
+                                                           uint32_t kpad_words) {
+  const uint32_t warps = blockDim.x >> 5;
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t total = a.rows + b.rows;
+  for (uint32_t gr = blockIdx.x * warps + (threadIdx.x >> 5); gr < total;
+       gr += gridDim.x * warps) {
+    const bool is_a = gr < a.rows;
+    const ExpandOperand& op = is_a ? a : b;
+    const uint32_t r = is_a ? gr : gr - a.rows;
+    int32_t sum = 0;
+    switch (op.n) {
+      case 1: sum = expand_row<1>(op, r, wpr, tail_mask, kpad_words, lane); break;
+      case 2: sum = expand_row<2>(op, r, wpr, tail_mask, kpad_words, lane); break;
+      case 3: sum = expand_row<3>(op, r, wpr, tail_mask, kpad_words, lane); break;
+      case 4: sum = expand_row<4>(op, r, wpr, tail_mask, kpad_words, lane); break;
+      case 5: sum = expand_row<5>(op, r, wpr, tail_mask, kpad_words, lane); break;
+      case 6: sum = expand_row<6>(op, r, wpr, tail_mask, kpad_words, lane); break;
+      case 7: sum = expand_row<7>(op, r, wpr, tail_mask, kpad_words, lane); break;
+      default: sum = expand_row<8>(op, r, wpr, tail_mask, kpad_words, lane); break;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    if (lane == 0) op.rowsum[r] = sum;
   }
 }
 
@@ -221,15 +264,21 @@ unsigned blocks_for(uint64_t threads) {
 
 }  // namespace
 
-cudaError_t launch_expand(const uint32_t* planes, uint64_t rows, uint64_t cols, int n,
-                          uint8_t* codes, uint64_t kpad, int32_t* rowsum, cudaStream_t s) {
+cudaError_t launch_expand(const uint32_t* w_planes, uint64_t rows_w, int n_w,
+                          uint8_t* w_codes, int32_t* w_rowsum, const uint32_t* x_planes,
+                          uint64_t rows_x, int n_x, uint8_t* x_codes, int32_t* x_rowsum,
+                          uint64_t cols, uint64_t kpad, int num_sms, cudaStream_t s) {
   const uint32_t wpr = static_cast<uint32_t>((cols + 31) / 32);
   const uint32_t tail = static_cast<uint32_t>(cols & 31);
   const uint32_t tail_mask = tail ? ((1u << tail) - 1u) : 0xffffffffu;
-  const uint32_t kpad_words = static_cast<uint32_t>(kpad / 32);
-  const int threads = kpad_words >= 256 ? 256 : (kpad_words >= 128 ? 128 : 64);
-  expand_kernel<<<static_cast<unsigned>(rows), threads, 0, s>>>(
-      planes, static_cast<uint32_t>(rows), wpr, n, tail_mask, codes, kpad_words, rowsum);
+  const ExpandOperand a{w_planes, w_codes, w_rowsum, static_cast<uint32_t>(rows_w), n_w};
+  const ExpandOperand b{x_planes, x_codes, x_rowsum, static_cast<uint32_t>(rows_x), n_x};
+  const uint64_t warps_needed = rows_w + rows_x;
+  uint64_t blocks = (warps_needed + kThreads / 32 - 1) / (kThreads / 32);
+  const uint64_t cap = uint64_t(num_sms) * 8;  // 8 resident 256-thread blocks per SM
+  if (blocks > cap) blocks = cap;
+  expand_kernel<<<static_cast<unsigned>(blocks), kThreads, 0, s>>>(
+      a, b, wpr, tail_mask, static_cast<uint32_t>(kpad / 32));
   return cudaGetLastError();
 }
 
@@ -271,8 +320,9 @@ cudaError_t launch_quantize_pack(const double* x, uint64_t rows, uint64_t cols, 
 }
 
 // ---- tensor maps ------------------------------------------------------------------------------
-CUresult encode_tmap_u8_2d(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer,
-                           uint32_t box_inner, uint32_t box_outer) {
+CUresult encode_tmap_2d(CUtensorMap* map, CUtensorMapDataType dtype, uint32_t /*elem_bytes*/,
+                        const void* base, uint64_t inner, uint64_t outer, uint64_t stride_bytes,
+                        uint32_t box_inner, uint32_t box_outer) {
   static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
   if (!encode) {
     cudaDriverEntryPointQueryResult q;
@@ -285,11 +335,11 @@ CUresult encode_tmap_u8_2d(CUtensorMap* map, const void* base, uint64_t inner, u
     encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
   }
   const cuuint64_t dims[2] = {inner, outer};
-  const cuuint64_t strides[1] = {inner};  // bytes, for dim 1
+  const cuuint64_t strides[1] = {stride_bytes};
   const cuuint32_t box[2] = {box_inner, box_outer};
   const cuuint32_t elem_strides[2] = {1, 1};
-  return encode(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box,
-                elem_strides, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+  return encode(map, dtype, 2, const_cast<void*>(base), dims, strides, box, elem_strides,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
 }
 
