@@ -301,10 +301,9 @@ def run_ours(args, rank, world, local_rank):
         step()
         torch.cuda.synchronize()
 
-    # -- timed region: exactly K steps, barrier + synchronize on both sides
-    ctx.kernel_time(0)
-    ctx.kernel_time(1)
-    ctx.enable_timing(True)
+    # -- timed region: exactly K steps, barrier + synchronize on both sides. No per-kernel
+    #    events in here: an event record between two launches would break the programmatic
+    #    dependent launch that overlaps the next call's expand with this call's GEMM.
     launches0 = ctx.launch_count()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
@@ -315,10 +314,22 @@ def run_ours(args, rank, world, local_rank):
     ev1.record(stream)
     torch.cuda.synchronize()
     barrier()
-    ctx.enable_timing(False)
     launches = ctx.launch_count() - launches0
     clk = clocks.stop()
     ms = ev0.elapsed_time(ev1)
+    # -- kernel pass (roofline): the same K steps again with every GEMM / expand launch
+    #    bracketed by CUDA events on its launch stream (serialises expand and GEMM)
+    ctx.kernel_time(0)
+    ctx.kernel_time(1)
+    ctx.enable_timing(True)
+    ek0, ek1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ek0.record(stream)
+    for _ in range(args.steps):
+        step()
+    ek1.record(stream)
+    torch.cuda.synchronize()
+    ctx.enable_timing(False)
+    ms_serial = ek0.elapsed_time(ek1)
     gemm_ms, gemm_n = ctx.kernel_time(0)
     exp_ms, exp_n = ctx.kernel_time(1)
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
@@ -399,8 +410,11 @@ def run_ours(args, rank, world, local_rank):
                      "peak_source": ("2 x measured bf16 burst (MEASURED_PEAKS.json bf16_tflops); "
                                      "dense i8 = 2x dense bf16 on B200" if bf16 else
                                      "2 x fallback bf16 1590 (B200_PROFILING.md)"),
-                     "gemm_ms_avg": gemm_avg_ms, "gemm_share_of_step": gemm_ms / ms,
-                     "expand_share_of_step": exp_ms / ms},
+                     "gemm_us_avg": 1e3 * gemm_avg_ms,
+                     "expand_us_avg": 1e3 * exp_ms / max(exp_n, 1),
+                     "serialized_ms_per_step": ms_serial / args.steps,
+                     "gemm_share_of_serialized_step": gemm_ms / ms_serial,
+                     "expand_share_of_serialized_step": exp_ms / ms_serial},
     }
     if world == 1 and not args.no_cpu_baseline:
         try:

@@ -32,7 +32,8 @@ struct apmm_ctx {
   uint64_t launches = 0;
   // measurement: event pairs around launches of kernel class 0 (GEMM) / 1 (expand)
   bool timing = false;
-  bool force_single_sm = false;  // APMM_FORCE_1SM=1: always use the 1-SM kernel (testing)
+  bool force_single_sm = false;
+  int ws_half = 0;  // which half of the ping-pong workspace the next matmul uses  // APMM_FORCE_1SM=1: always use the 1-SM kernel (testing)
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pending[2];
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> spare;
 };
@@ -122,16 +123,22 @@ struct MatmulWs {
   uint64_t kpad;
 };
 
-size_t matmul_ws_bytes(uint64_t rows_w, uint64_t rows_x, uint64_t k) {
+// Two halves (ping-pong): consecutive calls alternate, so the next call's expand can run
+// while this call's GEMM still reads its half (PDL overlap, see prep.cu / gemm_pair.cu).
+size_t matmul_half_bytes(uint64_t rows_w, uint64_t rows_x, uint64_t k) {
   const uint64_t kpad = round_up(k, kKAlign);
   return align_up(rows_w * kpad) + align_up(rows_x * kpad) + align_up(rows_w * 4) +
          align_up(round_up(rows_x, kRowsumPad) * 4);
 }
 
-MatmulWs carve(void* ws, uint64_t rows_w, uint64_t rows_x, uint64_t k) {
+size_t matmul_ws_bytes(uint64_t rows_w, uint64_t rows_x, uint64_t k) {
+  return 2 * matmul_half_bytes(rows_w, rows_x, k);
+}
+
+MatmulWs carve(void* ws, uint64_t rows_w, uint64_t rows_x, uint64_t k, int half) {
   MatmulWs m;
   m.kpad = round_up(k, kKAlign);
-  uint8_t* p = static_cast<uint8_t*>(ws);
+  uint8_t* p = static_cast<uint8_t*>(ws) + (half ? matmul_half_bytes(rows_w, rows_x, k) : 0);
   m.codes_w = p;
   p += align_up(rows_w * m.kpad);
   m.codes_x = p;
@@ -172,14 +179,12 @@ int run_matmul(apmm_ctx* ctx, const uint32_t* w, uint64_t rows_w, int n_w, const
   int st = ensure(&ctx->ws, &ctx->ws_bytes, matmul_ws_bytes(rows_w, rows_x, k), ctx->device);
   if (st) return st;
   CU(cudaSetDevice(ctx->device));
-  const MatmulWs m = carve(ctx->ws, rows_w, rows_x, k);
+  const MatmulWs m = carve(ctx->ws, rows_w, rows_x, k, ctx->ws_half);
+  ctx->ws_half ^= 1;
   const uint64_t rsx_pad = round_up(rows_x, kRowsumPad);
-  if (rsx_pad > rows_x) {
-    CU(cudaMemsetAsync(m.rowsum_x + rows_x, 0, (rsx_pad - rows_x) * 4, stream));
-  }
   {
     TimedLaunch t(ctx, 1, stream);
-    CU(launch_expand(w, rows_w, n_w, m.codes_w, m.rowsum_w, x, rows_x, n_x, m.codes_x,
+    CU(launch_expand(w, rows_w, n_w, m.codes_w, m.rowsum_w, x, rows_x, rsx_pad, n_x, m.codes_x,
                      m.rowsum_x, k, m.kpad, ctx->num_sms, stream));
   }
   ctx->launches += 1;

@@ -101,6 +101,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // PDL: everything above overlapped the previous kernel; from here on we read the
+  // operand workspace and write Y, so wait for the expand kernel (which itself completes
+  // only after the previous GEMM). Then let the NEXT call's expand start on the spare
+  // issue slots / registers of this SM while our tensor cores run.
+  pdl_wait();
+  if (threadIdx.x == 0) pdl_trigger();
 
   if (warp == 0) {
     // ---------------- TMA producer (both CTAs) ----------------
@@ -153,6 +159,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     // ---------------- epilogue (both CTAs) ----------------
     const uint32_t q = warp & 3;
     uint32_t acc = 0, acc_phase = 0, nbuf = 0;
+    const uint64_t store_hint = policy_evict_first();  // Y streams out; keep operands in L2
     for (uint32_t t = cluster; t < num_tiles; t += nclusters) {
       const uint32_t tm = t % p.tiles_m, tn = t / p.tiles_m;
       const uint32_t row0 = tm * 2 * kHalf + rank * kHalf + q * 32;
@@ -208,7 +215,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {
-            tma_store_2d(&tmap_y, buf, int32_t(col0), int32_t(row0));
+            tma_store_2d(&tmap_y, buf, int32_t(col0), int32_t(row0), store_hint);
             bulk_commit();
           }
         } else if (row_ok && col0 < p.rows_x) {
@@ -285,9 +292,19 @@ cudaError_t launch_gemm_pair(const GemmArgs& a, cudaStream_t s, int* launches) {
   const uint32_t tiles = p.tiles_m * p.tiles_n;
   const uint32_t max_clusters = static_cast<uint32_t>(a.num_sms / 2);
   const uint32_t clusters = tiles < max_clusters ? tiles : max_clusters;
-  gemm_u8_pair_kernel<<<2 * clusters, kThreads, kSmemBytes, s>>>(tw, tx, ty, p);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(2 * clusters);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = kSmemBytes;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_u8_pair_kernel, tw, tx, ty, p);
   *launches += 1;
-  return cudaGetLastError();
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 }  // namespace apmm_b200

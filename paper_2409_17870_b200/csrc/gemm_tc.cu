@@ -94,6 +94,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_wait();  // see gemm_pair.cu: expand done (and, through it, the previous GEMM)
+  if (threadIdx.x == 0) pdl_trigger();
 
   if (warp == 0) {
     // ---------------- TMA producer ----------------
@@ -252,9 +254,19 @@ cudaError_t launch_gemm_tc(const GemmArgs& a, cudaStream_t s, int* launches) {
   p.c0 = static_cast<uint32_t>(a.k_logical) * A * B;  // wraps mod 2^32 by design
   const uint32_t tiles = p.tiles_m * p.tiles_n;
   const uint32_t grid = tiles < uint32_t(a.num_sms) ? tiles : uint32_t(a.num_sms);
-  gemm_u8_tc_kernel<<<grid, kThreads, kSmemBytes, s>>>(tw, tx, p);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = kSmemBytes;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_u8_tc_kernel, tw, tx, p);
   *launches += 1;
-  return cudaGetLastError();
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 }  // namespace apmm_b200

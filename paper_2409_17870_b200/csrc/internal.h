@@ -20,10 +20,12 @@ inline uint64_t round_up(uint64_t v, uint64_t m) { return (v + m - 1) / m * m; }
 // ---- prep.cu -------------------------------------------------------------------------
 // Both operands' planes (reference layout) -> u8 codes [rows x kpad] (zero K padding, K
 // permuted identically within each 32-column group) + rowsum[rows], one launch.
+// rowsum_x[rows_x, rows_x_pad) is zeroed. Launched with PDL (see prep.cu).
 cudaError_t launch_expand(const uint32_t* w_planes, uint64_t rows_w, int n_w,
                           uint8_t* w_codes, int32_t* w_rowsum, const uint32_t* x_planes,
-                          uint64_t rows_x, int n_x, uint8_t* x_codes, int32_t* x_rowsum,
-                          uint64_t cols, uint64_t kpad, int num_sms, cudaStream_t s);
+                          uint64_t rows_x, uint64_t rows_x_pad, int n_x, uint8_t* x_codes,
+                          int32_t* x_rowsum, uint64_t cols, uint64_t kpad, int num_sms,
+                          cudaStream_t s);
 cudaError_t launch_pack(const uint8_t* codes, uint64_t rows, uint64_t cols, int n,
                         uint32_t* planes, cudaStream_t s);
 cudaError_t launch_unpack(const uint32_t* planes, uint64_t rows, uint64_t cols, int n,

@@ -37,13 +37,32 @@ struct ExpandOperand {
   uint8_t* codes;
   int32_t* rowsum;
   uint32_t rows;
+  uint32_t rows_pad;  // rowsum[rows, rows_pad) is zeroed (GEMM epilogue reads whole tiles)
   int n;
 };
 
-__device__ __forceinline__ void swap_bits(uint32_t& a, uint32_t& b, int s, uint32_t m) {
-  const uint32_t t = ((a >> s) ^ b) & m;
-  b ^= t;
-  a ^= t << s;
+constexpr int kExpandThreads = 128;  // small blocks: fit beside a resident GEMM CTA
+constexpr int kExpandUnroll = 4;     // words per lane with loads in flight together
+
+// 8x8 bit transpose inside every byte lane of x[0..7] (row i = plane i). Each swap is the
+// select form  b' = (b & ~m) | ((a >> s) & m),  a' = (a & ~(m << s)) | ((b << s) & (m << s)):
+// 4 ops per pair (SHF + LOP3 each), 12 pairs.
+__device__ __forceinline__ void swap_sel(uint32_t& a, uint32_t& b, int s, uint32_t m) {
+  const uint32_t na = (a & ~(m << s)) | ((b << s) & (m << s));
+  b = (b & ~m) | ((a >> s) & m);
+  a = na;
+}
+
+__device__ __forceinline__ void transpose8(uint32_t (&x)[8]) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i) swap_sel(x[i], x[i + 4], 4, 0x0F0F0F0Fu);
+#pragma unroll
+  for (int i = 0; i < 8; i += 4) {
+    swap_sel(x[i], x[i + 2], 2, 0x33333333u);
+    swap_sel(x[i + 1], x[i + 3], 2, 0x33333333u);
+  }
+#pragma unroll
+  for (int i = 0; i < 8; i += 2) swap_sel(x[i], x[i + 1], 1, 0x55555555u);
 }
 
 template <int N>
@@ -52,37 +71,43 @@ __device__ __forceinline__ int32_t expand_row(const ExpandOperand& op, uint32_t 
                                               uint32_t lane) {
   int32_t sum = 0;
   uint8_t* dst_row = op.codes + uint64_t(r) * kpad_words * 32u;
-  for (uint32_t w = lane; w < kpad_words; w += 32) {
-    uint32_t x[8];
+  const uint32_t* src = op.planes + uint64_t(r) * wpr;
+  const uint64_t pstride = uint64_t(op.rows) * wpr;
+  for (uint32_t w0 = 0; w0 < kpad_words; w0 += 32 * kExpandUnroll) {
+    uint32_t x[kExpandUnroll][8];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) x[i] = 0u;
-    if (w < wpr) {
-      const uint32_t mask = (w == wpr - 1) ? tail_mask : 0xffffffffu;
+    for (int u = 0; u < kExpandUnroll; ++u) {  // all loads first (memory-level parallelism)
+      const uint32_t w = w0 + lane + 32 * u;
+      const uint32_t mask = w < wpr ? (w == wpr - 1 ? tail_mask : 0xffffffffu) : 0u;
+      const uint32_t wc = w < wpr ? w : 0;
 #pragma unroll
-      for (int i = 0; i < N; ++i) {
-        x[i] = __ldg(op.planes + (uint64_t(i) * op.rows + r) * wpr + w) & mask;
-        sum += __popc(x[i]) << i;
+      for (int i = 0; i < 8; ++i) x[u][i] = i < N ? (__ldg(src + i * pstride + wc) & mask) : 0u;
+    }
+#pragma unroll
+    for (int u = 0; u < kExpandUnroll; ++u) {
+      const uint32_t w = w0 + lane + 32 * u;
+#pragma unroll
+      for (int i = 0; i < N; ++i) sum += __popc(x[u][i]) << i;
+      transpose8(x[u]);
+      if (w < kpad_words) {
+        uint4* d = reinterpret_cast<uint4*>(dst_row + uint64_t(w) * 32u);
+        d[0] = make_uint4(x[u][0], x[u][1], x[u][2], x[u][3]);
+        d[1] = make_uint4(x[u][4], x[u][5], x[u][6], x[u][7]);
       }
     }
-#pragma unroll
-    for (int i = 0; i < 4; ++i) swap_bits(x[i], x[i + 4], 4, 0x0F0F0F0Fu);
-#pragma unroll
-    for (int i = 0; i < 8; i += 4) {
-      swap_bits(x[i], x[i + 2], 2, 0x33333333u);
-      swap_bits(x[i + 1], x[i + 3], 2, 0x33333333u);
-    }
-#pragma unroll
-    for (int i = 0; i < 8; i += 2) swap_bits(x[i], x[i + 1], 1, 0x55555555u);
-    uint4* d = reinterpret_cast<uint4*>(dst_row + uint64_t(w) * 32u);
-    d[0] = make_uint4(x[0], x[1], x[2], x[3]);
-    d[1] = make_uint4(x[4], x[5], x[6], x[7]);
   }
   return sum;
 }
 
-__global__ void __launch_bounds__(kThreads) expand_kernel(ExpandOperand a, ExpandOperand b,
-                                                           uint32_t wpr, uint32_t tail_mask,
-                                                           uint32_t kpad_words) {
+// PDL protocol (see gemm_pair.cu): this kernel may start while the previous call's GEMM
+// still runs -- it only reads the caller's planes and writes the workspace half that the
+// GEMM two calls ago used (complete by construction) -- and it completes only after that
+// previous GEMM (griddepcontrol.wait at the end), so the next GEMM's wait on us also
+// covers it.
+__global__ void __launch_bounds__(kExpandThreads) expand_kernel(ExpandOperand a, ExpandOperand b,
+                                                                 uint32_t wpr, uint32_t tail_mask,
+                                                                 uint32_t kpad_words) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const uint32_t warps = blockDim.x >> 5;
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t total = a.rows + b.rows;
@@ -106,6 +131,11 @@ __global__ void __launch_bounds__(kThreads) expand_kernel(ExpandOperand a, Expan
     for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
     if (lane == 0) op.rowsum[r] = sum;
   }
+  if (blockIdx.x == 0) {
+    for (uint32_t r = a.rows + threadIdx.x; r < a.rows_pad; r += blockDim.x) a.rowsum[r] = 0;
+    for (uint32_t r = b.rows + threadIdx.x; r < b.rows_pad; r += blockDim.x) b.rowsum[r] = 0;
+  }
+  asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
 // ---- K1': codes -> planes (decompose_and_pack) -------------------------------------------
@@ -266,20 +296,35 @@ unsigned blocks_for(uint64_t threads) {
 
 cudaError_t launch_expand(const uint32_t* w_planes, uint64_t rows_w, int n_w,
                           uint8_t* w_codes, int32_t* w_rowsum, const uint32_t* x_planes,
-                          uint64_t rows_x, int n_x, uint8_t* x_codes, int32_t* x_rowsum,
-                          uint64_t cols, uint64_t kpad, int num_sms, cudaStream_t s) {
+                          uint64_t rows_x, uint64_t rows_x_pad, int n_x, uint8_t* x_codes,
+                          int32_t* x_rowsum, uint64_t cols, uint64_t kpad, int num_sms,
+                          cudaStream_t s) {
   const uint32_t wpr = static_cast<uint32_t>((cols + 31) / 32);
   const uint32_t tail = static_cast<uint32_t>(cols & 31);
   const uint32_t tail_mask = tail ? ((1u << tail) - 1u) : 0xffffffffu;
-  const ExpandOperand a{w_planes, w_codes, w_rowsum, static_cast<uint32_t>(rows_w), n_w};
-  const ExpandOperand b{x_planes, x_codes, x_rowsum, static_cast<uint32_t>(rows_x), n_x};
+  const ExpandOperand a{w_planes, w_codes, w_rowsum, static_cast<uint32_t>(rows_w),
+                        static_cast<uint32_t>(rows_w), n_w};
+  const ExpandOperand b{x_planes, x_codes, x_rowsum, static_cast<uint32_t>(rows_x),
+                        static_cast<uint32_t>(rows_x_pad), n_x};
   const uint64_t warps_needed = rows_w + rows_x;
-  uint64_t blocks = (warps_needed + kThreads / 32 - 1) / (kThreads / 32);
-  const uint64_t cap = uint64_t(num_sms) * 8;  // 8 resident 256-thread blocks per SM
+  uint64_t blocks = (warps_needed + kExpandThreads / 32 - 1) / (kExpandThreads / 32);
+  // one block per SM: all blocks fit beside a resident GEMM CTA (regs: 8 x 200 x 32 +
+  // 4 x 80 x 32 <= 64K), so none is left waiting behind blocks parked in griddepcontrol.wait
+  const uint64_t cap = uint64_t(num_sms);
   if (blocks > cap) blocks = cap;
-  expand_kernel<<<static_cast<unsigned>(blocks), kThreads, 0, s>>>(
-      a, b, wpr, tail_mask, static_cast<uint32_t>(kpad / 32));
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(blocks));
+  cfg.blockDim = dim3(kExpandThreads);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, expand_kernel, a, b, wpr, tail_mask,
+                                     static_cast<uint32_t>(kpad / 32));
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 cudaError_t launch_pack(const uint8_t* codes, uint64_t rows, uint64_t cols, int n,

@@ -182,15 +182,23 @@ APMM_DEV void mma_commit_pair_mc(uint64_t* bar, uint16_t mask) {
       : "memory");
 }
 
+// ---- programmatic dependent launch (PDL) -----------------------------------------
+// wait: block until every prerequisite grid has completed and its memory is visible.
+APMM_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// launch_dependents: let the next kernel in the stream be scheduled (it still waits).
+APMM_DEV void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // ---- TMA store (epilogue) ----------------------------------------------------------
 APMM_DEV void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
-APMM_DEV void tma_store_2d(const void* tmap, const void* smem_src, int32_t c0, int32_t c1) {
-  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
-                   reinterpret_cast<uint64_t>(tmap)),
-               "r"(smem_u32(smem_src)), "r"(c0), "r"(c1)
-               : "memory");
+APMM_DEV void tma_store_2d(const void* tmap, const void* smem_src, int32_t c0, int32_t c1,
+                          uint64_t cache_hint) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%2, %3}], [%1], "
+      "%4;" ::"l"(reinterpret_cast<uint64_t>(tmap)),
+      "r"(smem_u32(smem_src)), "r"(c0), "r"(c1), "l"(cache_hint)
+      : "memory");
 }
 APMM_DEV void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 template <int N>
