@@ -33,7 +33,9 @@ struct apmm_ctx {
   // measurement: event pairs around launches of kernel class 0 (GEMM) / 1 (expand)
   bool timing = false;
   bool force_single_sm = false;
-  int ws_half = 0;  // which half of the ping-pong workspace the next matmul uses  // APMM_FORCE_1SM=1: always use the 1-SM kernel (testing)
+  int ws_half = 0;  // which half of the ping-pong workspace the next matmul uses
+  bool dbg_waits = false;  // APMM_DEBUG_WAITS=1: MMA-issuer wait-cycle counters (dev only)
+  void* dbg = nullptr;  // APMM_FORCE_1SM=1: always use the 1-SM kernel (testing)
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pending[2];
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> spare;
 };
@@ -206,6 +208,10 @@ int run_matmul(apmm_ctx* ctx, const uint32_t* w, uint64_t rows_w, int n_w, const
   a.s_x = s_x;
   a.gran_x = gran_x;
   a.num_sms = ctx->num_sms;
+  if (ctx->dbg_waits) {
+    if (!ctx->dbg) CU(cudaMalloc(&ctx->dbg, 64));
+    a.dbg = static_cast<unsigned long long*>(ctx->dbg);
+  }
   int launches = 0;
   {
     TimedLaunch t(ctx, 0, stream);
@@ -290,6 +296,7 @@ int apmm_ctx_create(apmm_ctx** out, int device) {
   ctx->device = device;
   ctx->num_sms = prop.multiProcessorCount;
   if (const char* f = std::getenv("APMM_FORCE_1SM")) ctx->force_single_sm = f[0] == '1';
+  if (const char* f = std::getenv("APMM_DEBUG_WAITS")) ctx->dbg_waits = f[0] == '1';
   cudaError_t e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
   if (e != cudaSuccess) {
     delete ctx;
@@ -304,6 +311,15 @@ int apmm_ctx_destroy(apmm_ctx* ctx) {
   if (!ctx) return APMM_OK;
   cudaSetDevice(ctx->device);
   cudaDeviceSynchronize();
+  if (ctx->dbg) {
+    unsigned long long h[4] = {0, 0, 0, 0};
+    cudaMemcpy(h, ctx->dbg, sizeof(h), cudaMemcpyDeviceToHost);
+    std::fprintf(stderr,
+                 "[apmm debug] MMA issuer: %.1f%% of cycles waiting on TMA (full), %.1f%% on "
+                 "epilogue (tmem_empty), over %llu issuer runs\n",
+                 h[2] ? 100.0 * h[0] / h[2] : 0.0, h[2] ? 100.0 * h[1] / h[2] : 0.0, h[3]);
+    cudaFree(ctx->dbg);
+  }
   if (ctx->ws) cudaFree(ctx->ws);
   if (ctx->io) cudaFree(ctx->io);
   if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);

@@ -53,6 +53,7 @@ struct Params {
   uint32_t tiles_m, tiles_n;
   uint32_t coef_w, coef_x, c0;
   uint32_t tma_store;  // 1: epilogue stores through tmap_y
+  unsigned long long* dbg;  // optional wait-cycle counters (APMM_DEBUG_WAITS), else null
 };
 
 __device__ __forceinline__ uint32_t dequant_bits(uint32_t v, double sw, double sx) {
@@ -133,12 +134,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     // ---------------- MMA issuer (leader only) ----------------
     if (leader && elect_one()) {
       uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0;
+      unsigned long long w_full = 0, w_tmem = 0, t_begin = clock64();
       for (uint32_t t = cluster; t < num_tiles; t += nclusters) {
+        unsigned long long c0 = p.dbg ? clock64() : 0;
         mbar_wait(&tmem_empty[acc], acc_phase ^ 1);
+        if (p.dbg) w_tmem += clock64() - c0;
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * kPairN;
         for (uint32_t kb = 0; kb < p.kblocks; ++kb) {
+          c0 = p.dbg ? clock64() : 0;
           mbar_wait(&full_bar[stage], phase);
+          if (p.dbg) w_full += clock64() - c0;
           tc_fence_after();
           const uint32_t st = smem_u32(stages + stage * kStageBytes);
           const uint64_t adesc = umma_desc_sw128(st);
@@ -152,6 +158,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
         mma_commit_pair_mc(&tmem_full[acc], 0x3);
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      }
+      if (p.dbg) {
+        atomicAdd(p.dbg + 0, w_full);
+        atomicAdd(p.dbg + 1, w_tmem);
+        atomicAdd(p.dbg + 2, clock64() - t_begin);
+        atomicAdd(p.dbg + 3, 1ull);
       }
     }
     __syncwarp();
@@ -289,6 +301,7 @@ cudaError_t launch_gemm_pair(const GemmArgs& a, cudaStream_t s, int* launches) {
   p.coef_x = 2u * A;
   p.c0 = static_cast<uint32_t>(a.k_logical) * A * B;
   p.tma_store = tma_store ? 1u : 0u;
+  p.dbg = a.dbg;
   const uint32_t tiles = p.tiles_m * p.tiles_n;
   const uint32_t max_clusters = static_cast<uint32_t>(a.num_sms / 2);
   const uint32_t clusters = tiles < max_clusters ? tiles : max_clusters;

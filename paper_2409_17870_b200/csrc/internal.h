@@ -52,6 +52,7 @@ struct GemmArgs {
   const double* s_x;
   int gran_x;
   int num_sms;
+  unsigned long long* dbg = nullptr;  // optional wait-cycle counters (dev instrumentation)
 };
 // Returns the number of kernel launches it enqueued via *launches.
 cudaError_t launch_gemm_tc(const GemmArgs& a, cudaStream_t s, int* launches);
