@@ -45,6 +45,9 @@ def workload_gemms(name: str):
     if name == "llama7b":
         return [(n, m, k, 2, 4) for (n, k) in ((4096, 4096), (11008, 4096), (4096, 11008))
                 for m in (2048,)]
+    if name == "llama7b_small":
+        return [(n, m, k, 2, 4) for (n, k) in ((4096, 4096), (11008, 4096), (4096, 11008))
+                for m in (1, 16)]
     if name == "decode":
         return [(8192, m, 8192, 3, 8) for m in (1, 8, 16)]
     if name == "ffn70b":
@@ -57,6 +60,7 @@ WORKLOAD_DESC = {
     "w2a4_4096": "W2A4 M=N=K=4096",
     "llama7b": "BASELINE configs[2]: Llama-2-7B linear shapes W2A4, M=2048 tokens",
     "decode": "BASELINE configs[3]: decode W3A8 K=N=8192, M in {1,8,16}",
+    "llama7b_small": "BASELINE configs[3]: Llama-2-7B linear shapes W2A4, M in {1,16} tokens",
     "ffn70b": "BASELINE configs[4]: Llama-2-70B FFN 28672x8192 W2A4, M=4096",
 }
 
@@ -384,9 +388,26 @@ def run_ours(args, rank, world, local_rank):
     traffic = load_traffic()
     bf16 = peaks.get("bf16_tflops")
     i8_peak = 2.0 * bf16 if bf16 else 2.0 * 1590.0
+    hbm_peak = peaks.get("hbm_gbs") or 7672.0
     gemm_avg_ms = gemm_ms / max(gemm_n, 1)
-    achieved = (args.steps * ops_step / max(gemm_n, 1)) / (gemm_avg_ms * 1e-3) / 1e12
-    tr = traffic.get("gemm_u8_tc_kernel", {}).get(args.workload)
+    bytes_step = sum(algorithmic_bytes(g) for g in gemms)
+    # which roofline bounds the dominant kernel: compare the two ideal times per step
+    hbm_bound = bytes_step / (hbm_peak * 1e9) > ops_step / (i8_peak * 1e12)
+    skinny = all(g[1] <= 64 for g in gemms)
+    kname = ("skinny_kernel (weight planes -> mma.sync u8 fragments)" if skinny else
+             "gemm_u8_pair_kernel / gemm_u8_tc_kernel (tcgen05.mma kind::i8)")
+    if hbm_bound:
+        achieved = (args.steps * bytes_step / max(gemm_n, 1)) / (gemm_avg_ms * 1e-3) / 1e9
+        peak, unit = hbm_peak, "GB/s"
+        peak_src = ("MEASURED_PEAKS.json hbm_gbs (copy bandwidth)" if peaks.get("hbm_gbs")
+                    else "B200_PROFILING.md fallback")
+    else:
+        achieved = (args.steps * ops_step / max(gemm_n, 1)) / (gemm_avg_ms * 1e-3) / 1e12
+        peak, unit = i8_peak, "TFLOP/s"
+        peak_src = ("2 x measured bf16 burst (MEASURED_PEAKS.json bf16_tflops); "
+                    "dense i8 = 2x dense bf16 on B200" if bf16 else
+                    "2 x fallback bf16 1590 (B200_PROFILING.md)")
+    tr = traffic.get(args.workload)
     line = {
         "metric": "effective TOPS (2MNK/s) of WnAm bipolar-INT GEMM",
         "value": value, "unit": "TOPS", "n_gpus": world, "steps": args.steps,
@@ -404,12 +425,11 @@ def run_ours(args, rank, world, local_rank):
         "gpu_launches": int(launches),
         "e2e": {"value": e2e_val, "unit": "TOPS", "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h), "api": "apmm_matmul_ap (host C ABI, pinned buffers)"},
-        "roofline": {"bound": "tensor", "achieved": achieved, "peak": i8_peak, "unit": "TFLOP/s",
-                     "frac": achieved / i8_peak, "traffic": tr,
-                     "kernel": "gemm_u8_tc_kernel (tcgen05.mma kind::i8)",
-                     "peak_source": ("2 x measured bf16 burst (MEASURED_PEAKS.json bf16_tflops); "
-                                     "dense i8 = 2x dense bf16 on B200" if bf16 else
-                                     "2 x fallback bf16 1590 (B200_PROFILING.md)"),
+        "roofline": {"bound": "hbm" if hbm_bound else "tensor", "achieved": achieved,
+                     "peak": peak, "unit": unit, "frac": achieved / peak, "traffic": tr,
+                     "kernel": kname, "peak_source": peak_src,
+                     "algorithmic_bytes_per_step": bytes_step,
+                     "algorithmic_ops_per_step": ops_step,
                      "gemm_us_avg": 1e3 * gemm_avg_ms,
                      "expand_us_avg": 1e3 * exp_ms / max(exp_n, 1),
                      "serialized_ms_per_step": ms_serial / args.steps,
@@ -434,7 +454,7 @@ def main():
     ap_.add_argument("--warmup", type=int, default=3)
     ap_.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap_.add_argument("--workload", default="sweep4096",
-                     choices=["sweep4096", "w2a4_4096", "llama7b", "decode", "ffn70b"])
+                     choices=list(WORKLOAD_DESC))
     ap_.add_argument("--no-cpu-baseline", action="store_true")
     ap_.add_argument("--profile", action="store_true",
                      help="for ncu: no heat phase, no e2e, no CPU baseline (numbers invalid)")

@@ -34,6 +34,9 @@ struct apmm_ctx {
   bool timing = false;
   bool force_single_sm = false;
   int ws_half = 0;  // which half of the ping-pong workspace the next matmul uses
+  void* sk_ws = nullptr;  // K5 split-K accumulators (zero between calls)
+  size_t sk_ws_bytes = 0;
+  bool force_tc = false;  // APMM_FORCE_TC=1: never use K5 (testing)
   bool dbg_waits = false;  // APMM_DEBUG_WAITS=1: MMA-issuer wait-cycle counters (dev only)
   void* dbg = nullptr;  // APMM_FORCE_1SM=1: always use the 1-SM kernel (testing)
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pending[2];
@@ -184,6 +187,52 @@ int run_matmul(apmm_ctx* ctx, const uint32_t* w, uint64_t rows_w, int n_w, const
   const MatmulWs m = carve(ctx->ws, rows_w, rows_x, k, ctx->ws_half);
   ctx->ws_half ^= 1;
   const uint64_t rsx_pad = round_up(rows_x, kRowsumPad);
+  if (rows_x <= kSkinnyMaxRowsX && !ctx->force_tc) {
+    // few feature rows: expand only X, stream the weight planes through K5
+    const size_t need = skinny_ws_bytes(rows_w, rows_x);
+    if (need > ctx->sk_ws_bytes) {
+      if (ctx->sk_ws) {
+        CU(cudaDeviceSynchronize());
+        CU(cudaFree(ctx->sk_ws));
+        ctx->sk_ws = nullptr;
+        ctx->sk_ws_bytes = 0;
+      }
+      const size_t sz = need + need / 4;
+      CU(cudaMalloc(&ctx->sk_ws, sz));
+      CU(cudaMemset(ctx->sk_ws, 0, sz));
+      ctx->sk_ws_bytes = sz;
+    }
+    {
+      TimedLaunch t(ctx, 1, stream);
+      CU(launch_expand(nullptr, 0, n_w, nullptr, nullptr, x, rows_x, rsx_pad, n_x, m.codes_x,
+                       m.rowsum_x, k, m.kpad, ctx->num_sms, stream));
+    }
+    ctx->launches += 1;
+    SkinnyArgs s{};
+    s.w_planes = w;
+    s.codes_x = m.codes_x;
+    s.rowsum_x = m.rowsum_x;
+    s.rows_w = rows_w;
+    s.rows_x = rows_x;
+    s.k = k;
+    s.kpad = m.kpad;
+    s.n_w = n_w;
+    s.n_x = n_x;
+    s.y = y;
+    s.yf = yf;
+    s.s_w = s_w;
+    s.gran_w = gran_w;
+    s.s_x = s_x;
+    s.gran_x = gran_x;
+    s.num_sms = ctx->num_sms;
+    s.ws = ctx->sk_ws;
+    {
+      TimedLaunch t(ctx, 0, stream);
+      CU(launch_skinny(s, stream));
+    }
+    ctx->launches += 1;
+    return APMM_OK;
+  }
   {
     TimedLaunch t(ctx, 1, stream);
     CU(launch_expand(w, rows_w, n_w, m.codes_w, m.rowsum_w, x, rows_x, rsx_pad, n_x, m.codes_x,
@@ -297,6 +346,7 @@ int apmm_ctx_create(apmm_ctx** out, int device) {
   ctx->num_sms = prop.multiProcessorCount;
   if (const char* f = std::getenv("APMM_FORCE_1SM")) ctx->force_single_sm = f[0] == '1';
   if (const char* f = std::getenv("APMM_DEBUG_WAITS")) ctx->dbg_waits = f[0] == '1';
+  if (const char* f = std::getenv("APMM_FORCE_TC")) ctx->force_tc = f[0] == '1';
   cudaError_t e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
   if (e != cudaSuccess) {
     delete ctx;
@@ -321,6 +371,7 @@ int apmm_ctx_destroy(apmm_ctx* ctx) {
     cudaFree(ctx->dbg);
   }
   if (ctx->ws) cudaFree(ctx->ws);
+  if (ctx->sk_ws) cudaFree(ctx->sk_ws);
   if (ctx->io) cudaFree(ctx->io);
   if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
   for (auto* v : {&ctx->pending[0], &ctx->pending[1], &ctx->spare}) {

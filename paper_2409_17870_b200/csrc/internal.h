@@ -59,6 +59,26 @@ cudaError_t launch_gemm_tc(const GemmArgs& a, cudaStream_t s, int* launches);
 // ---- gemm_pair.cu (CTA-pair, 256x256 tiles) -------------------------------------------
 cudaError_t launch_gemm_pair(const GemmArgs& a, cudaStream_t s, int* launches);
 
+// ---- skinny.cu (few feature rows: weight planes streamed from HBM into mma.sync) -----
+constexpr uint64_t kSkinnyMaxRowsX = 64;  // feature rows handled by K5
+struct SkinnyArgs {
+  const uint32_t* w_planes;  // reference layout [n_w][rows_w][ceil(k/32)]
+  const uint8_t* codes_x;    // [rows_x x kpad] (expand order)
+  const int32_t* rowsum_x;   // [rows_x]
+  uint64_t rows_w, rows_x, k, kpad;
+  int n_w, n_x;
+  int32_t* y;
+  float* yf;
+  const double* s_w;
+  int gran_w;
+  const double* s_x;
+  int gran_x;
+  int num_sms;
+  void* ws;  // skinny_ws_bytes(rows_w, rows_x), all zero on entry; left zero on exit
+};
+size_t skinny_ws_bytes(uint64_t rows_w, uint64_t rows_x);
+cudaError_t launch_skinny(const SkinnyArgs& a, cudaStream_t s);
+
 // Tensor-map encoder obtained from the driver through the runtime (no -lcuda).
 // 2-D row-major tensor [outer x inner] with `stride_bytes` between rows, 128B swizzle.
 CUresult encode_tmap_2d(CUtensorMap* map, CUtensorMapDataType dtype, uint32_t elem_bytes,

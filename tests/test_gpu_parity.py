@@ -101,6 +101,50 @@ def test_tile_shapes_and_edges(gpu, oracle):
         assert np.array_equal(gpu_matmul(ap, ctx, oracle, wc, nw, xc, nx), want), (m, n, k)
 
 
+@pytest.fixture(scope="module")
+def gpu_tc(gpu):
+    """A second context pinned to the tensor-core (expand + tcgen05) path for every shape,
+    so small shapes also exercise it (APMM_FORCE_TC is read at context creation)."""
+    ap, _ = gpu
+    os.environ["APMM_FORCE_TC"] = "1"
+    try:
+        ctx = ap.Context(0)
+    finally:
+        del os.environ["APMM_FORCE_TC"]
+    return ap, ctx
+
+
+def test_randomized_corpus_tensor_core_path(gpu_tc, oracle):
+    ap, ctx = gpu_tc
+    rng = oracle.rng(31)
+    for _ in range(200):
+        m, n, k = rng.range(1, 40), rng.range(1, 80), rng.range(1, 300)
+        nw, nx = rng.range(1, 8), rng.range(1, 8)
+        wc, xc = rng.random_codes(m, k, nw), rng.random_codes(n, k, nx)
+        assert np.array_equal(gpu_matmul(ap, ctx, oracle, wc, nw, xc, nx),
+                              oracle.decoded_matmul(wc, nw, xc, nx)), (m, n, k, nw, nx)
+
+
+@pytest.mark.parametrize("m_tok", [1, 2, 7, 8, 9, 16, 17, 31, 33, 64])
+def test_skinny_path_shapes(gpu, gpu_tc, oracle, m_tok):
+    """Few feature rows (K5: weight planes streamed into mma.sync): ragged rows, ragged K,
+    the unaligned (scalar-load) path, every weight width, and the single-accumulator variant
+    (K*(2^n_w-1)*(2^n_x-1) >= 2^28). Checked against the oracle and the tensor-core path."""
+    ap, ctx = gpu
+    _, ctx_tc = gpu_tc
+    rng = oracle.rng(500 + m_tok)
+    for (n_out, k, nw, nx) in [(300, 1000, 3, 8), (129, 4096, 2, 4), (1000, 777, 8, 8),
+                               (257, 8232, 4, 8), (40, 70200, 4, 8), (33, 40, 1, 1),
+                               (130, 100, 5, 3), (128, 2048, 1, 2), (17, 33025, 8, 8)]:
+        wc, xc = rng.random_codes(n_out, k, nw), rng.random_codes(m_tok, k, nx)
+        wp, xp = oracle.pack(wc, nw), oracle.pack(xc, nx)
+        want = oracle.matmul_ap_mt(wp, n_out, nw, xp, m_tok, nx, k, os.cpu_count() or 4)
+        w = ap.PackedBitPlanes(n_out, k, ap.BitWidth(nw), wp)
+        x = ap.PackedBitPlanes(m_tok, k, ap.BitWidth(nx), xp)
+        assert np.array_equal(ap.matmul_ap(w, x, ctx=ctx), want), (n_out, m_tok, k, nw, nx)
+        assert np.array_equal(ap.matmul_ap(w, x, ctx=ctx_tc), want), (n_out, m_tok, k, nw, nx)
+
+
 def test_schedule_independence(gpu, oracle):
     ap, ctx = gpu
     rng = oracle.rng(707)  # acceptance.cpp:268-294: 100x100x300 W3A4, 9 configs
