@@ -36,6 +36,8 @@ struct apmm_ctx {
   int ws_half = 0;  // which half of the ping-pong workspace the next matmul uses
   void* sk_ws = nullptr;  // K5 split-K accumulators (zero between calls)
   size_t sk_ws_bytes = 0;
+  void* sk_scratch = nullptr;  // K5 feature fragments (ping-pong halves) + weight repack
+  size_t sk_scratch_bytes = 0;
   bool force_tc = false;  // APMM_FORCE_TC=1: never use K5 (testing)
   bool dbg_waits = false;  // APMM_DEBUG_WAITS=1: MMA-issuer wait-cycle counters (dev only)
   void* dbg = nullptr;  // APMM_FORCE_1SM=1: always use the 1-SM kernel (testing)
@@ -181,16 +183,11 @@ struct TimedLaunch {
 int run_matmul(apmm_ctx* ctx, const uint32_t* w, uint64_t rows_w, int n_w, const double* s_w,
                int gran_w, const uint32_t* x, uint64_t rows_x, int n_x, const double* s_x,
                int gran_x, uint64_t k, int32_t* y, float* yf, cudaStream_t stream) {
-  int st = ensure(&ctx->ws, &ctx->ws_bytes, matmul_ws_bytes(rows_w, rows_x, k), ctx->device);
-  if (st) return st;
   CU(cudaSetDevice(ctx->device));
-  const MatmulWs m = carve(ctx->ws, rows_w, rows_x, k, ctx->ws_half);
-  ctx->ws_half ^= 1;
-  const uint64_t rsx_pad = round_up(rows_x, kRowsumPad);
   if (rows_x <= kSkinnyMaxRowsX && !ctx->force_tc) {
-    // few feature rows: expand only X, stream the weight planes through K5
-    const size_t need = skinny_ws_bytes(rows_w, rows_x);
-    if (need > ctx->sk_ws_bytes) {
+    // few feature rows: feature prep + K5, the weight planes streamed once from HBM
+    const size_t need = skinny_acc_bytes(rows_w, rows_x);
+    if (need > ctx->sk_ws_bytes) {  // split-K accumulators; zero at rest
       if (ctx->sk_ws) {
         CU(cudaDeviceSynchronize());
         CU(cudaFree(ctx->sk_ws));
@@ -202,20 +199,15 @@ int run_matmul(apmm_ctx* ctx, const uint32_t* w, uint64_t rows_w, int n_w, const
       CU(cudaMemset(ctx->sk_ws, 0, sz));
       ctx->sk_ws_bytes = sz;
     }
-    {
-      TimedLaunch t(ctx, 1, stream);
-      CU(launch_expand(nullptr, 0, n_w, nullptr, nullptr, x, rows_x, rsx_pad, n_x, m.codes_x,
-                       m.rowsum_x, k, m.kpad, ctx->num_sms, stream));
-    }
-    ctx->launches += 1;
+    int st = ensure(&ctx->sk_scratch, &ctx->sk_scratch_bytes,
+                    skinny_scratch_bytes(rows_w, rows_x, k, n_w, w), ctx->device);
+    if (st) return st;
     SkinnyArgs s{};
     s.w_planes = w;
-    s.codes_x = m.codes_x;
-    s.rowsum_x = m.rowsum_x;
+    s.x_planes = x;
     s.rows_w = rows_w;
     s.rows_x = rows_x;
     s.k = k;
-    s.kpad = m.kpad;
     s.n_w = n_w;
     s.n_x = n_x;
     s.y = y;
@@ -225,14 +217,22 @@ int run_matmul(apmm_ctx* ctx, const uint32_t* w, uint64_t rows_w, int n_w, const
     s.s_x = s_x;
     s.gran_x = gran_x;
     s.num_sms = ctx->num_sms;
-    s.ws = ctx->sk_ws;
+    s.acc_ws = ctx->sk_ws;
+    s.scratch_ws = ctx->sk_scratch;
+    s.ws_half = ctx->ws_half;
+    ctx->ws_half ^= 1;
     {
       TimedLaunch t(ctx, 0, stream);
       CU(launch_skinny(s, stream));
     }
-    ctx->launches += 1;
+    ctx->launches += 2;  // feature prep + streaming kernel
     return APMM_OK;
   }
+  int st = ensure(&ctx->ws, &ctx->ws_bytes, matmul_ws_bytes(rows_w, rows_x, k), ctx->device);
+  if (st) return st;
+  const MatmulWs m = carve(ctx->ws, rows_w, rows_x, k, ctx->ws_half);
+  ctx->ws_half ^= 1;
+  const uint64_t rsx_pad = round_up(rows_x, kRowsumPad);
   {
     TimedLaunch t(ctx, 1, stream);
     CU(launch_expand(w, rows_w, n_w, m.codes_w, m.rowsum_w, x, rows_x, rsx_pad, n_x, m.codes_x,
@@ -372,6 +372,7 @@ int apmm_ctx_destroy(apmm_ctx* ctx) {
   }
   if (ctx->ws) cudaFree(ctx->ws);
   if (ctx->sk_ws) cudaFree(ctx->sk_ws);
+  if (ctx->sk_scratch) cudaFree(ctx->sk_scratch);
   if (ctx->io) cudaFree(ctx->io);
   if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
   for (auto* v : {&ctx->pending[0], &ctx->pending[1], &ctx->spare}) {

@@ -60,12 +60,11 @@ cudaError_t launch_gemm_tc(const GemmArgs& a, cudaStream_t s, int* launches);
 cudaError_t launch_gemm_pair(const GemmArgs& a, cudaStream_t s, int* launches);
 
 // ---- skinny.cu (few feature rows: weight planes streamed from HBM into mma.sync) -----
-constexpr uint64_t kSkinnyMaxRowsX = 64;  // feature rows handled by K5
+constexpr uint64_t kSkinnyMaxRowsX = 63;  // feature rows handled by K5 (+1 ones column <= 64)
 struct SkinnyArgs {
   const uint32_t* w_planes;  // reference layout [n_w][rows_w][ceil(k/32)]
-  const uint8_t* codes_x;    // [rows_x x kpad] (expand order)
-  const int32_t* rowsum_x;   // [rows_x]
-  uint64_t rows_w, rows_x, k, kpad;
+  const uint32_t* x_planes;  // reference layout [n_x][rows_x][ceil(k/32)]
+  uint64_t rows_w, rows_x, k;
   int n_w, n_x;
   int32_t* y;
   float* yf;
@@ -74,9 +73,13 @@ struct SkinnyArgs {
   const double* s_x;
   int gran_x;
   int num_sms;
-  void* ws;  // skinny_ws_bytes(rows_w, rows_x), all zero on entry; left zero on exit
+  void* acc_ws;      // skinny_acc_bytes(): split-K accumulators, zero on entry, left zero
+  void* scratch_ws;  // skinny_scratch_bytes(): feature fragments (2 halves) + weight repack
+  int ws_half;       // ping-pong half for the feature fragments (PDL overlap of calls)
 };
-size_t skinny_ws_bytes(uint64_t rows_w, uint64_t rows_x);
+size_t skinny_acc_bytes(uint64_t rows_w, uint64_t rows_x);
+size_t skinny_scratch_bytes(uint64_t rows_w, uint64_t rows_x, uint64_t k, int n_w,
+                            const void* w_planes);
 cudaError_t launch_skinny(const SkinnyArgs& a, cudaStream_t s);
 
 // Tensor-map encoder obtained from the driver through the runtime (no -lcuda).
@@ -84,5 +87,9 @@ cudaError_t launch_skinny(const SkinnyArgs& a, cudaStream_t s);
 CUresult encode_tmap_2d(CUtensorMap* map, CUtensorMapDataType dtype, uint32_t elem_bytes,
                         const void* base, uint64_t inner, uint64_t outer, uint64_t stride_bytes,
                         uint32_t box_inner, uint32_t box_outer);
+// 3-D u32 tensor, no swizzle, zero OOB fill: dims {inner, mid, outer}, byte strides of the
+// mid and outer dimensions (multiples of 16).
+CUresult encode_tmap_3d_u32(CUtensorMap* map, const void* base, const uint64_t (&dims)[3],
+                            const uint64_t (&stride_bytes)[2], const uint32_t (&box)[3]);
 
 }  // namespace apmm_b200

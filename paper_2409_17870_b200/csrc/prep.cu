@@ -365,9 +365,8 @@ cudaError_t launch_quantize_pack(const double* x, uint64_t rows, uint64_t cols, 
 }
 
 // ---- tensor maps ------------------------------------------------------------------------------
-CUresult encode_tmap_2d(CUtensorMap* map, CUtensorMapDataType dtype, uint32_t /*elem_bytes*/,
-                        const void* base, uint64_t inner, uint64_t outer, uint64_t stride_bytes,
-                        uint32_t box_inner, uint32_t box_outer) {
+namespace {
+PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
   static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
   if (!encode) {
     cudaDriverEntryPointQueryResult q;
@@ -375,16 +374,38 @@ CUresult encode_tmap_2d(CUtensorMap* map, CUtensorMapDataType dtype, uint32_t /*
     if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &fn, 12000, cudaEnableDefault,
                                          &q) != cudaSuccess ||
         q != cudaDriverEntryPointSuccess || fn == nullptr) {
-      return CUDA_ERROR_NOT_FOUND;
+      return nullptr;
     }
     encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
   }
+  return encode;
+}
+}  // namespace
+
+CUresult encode_tmap_2d(CUtensorMap* map, CUtensorMapDataType dtype, uint32_t /*elem_bytes*/,
+                        const void* base, uint64_t inner, uint64_t outer, uint64_t stride_bytes,
+                        uint32_t box_inner, uint32_t box_outer) {
+  auto encode = tmap_encoder();
+  if (!encode) return CUDA_ERROR_NOT_FOUND;
   const cuuint64_t dims[2] = {inner, outer};
   const cuuint64_t strides[1] = {stride_bytes};
   const cuuint32_t box[2] = {box_inner, box_outer};
   const cuuint32_t elem_strides[2] = {1, 1};
   return encode(map, dtype, 2, const_cast<void*>(base), dims, strides, box, elem_strides,
                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+}
+
+CUresult encode_tmap_3d_u32(CUtensorMap* map, const void* base, const uint64_t (&dims)[3],
+                            const uint64_t (&stride_bytes)[2], const uint32_t (&box)[3]) {
+  auto encode = tmap_encoder();
+  if (!encode) return CUDA_ERROR_NOT_FOUND;
+  const cuuint64_t d[3] = {dims[0], dims[1], dims[2]};
+  const cuuint64_t st[2] = {stride_bytes[0], stride_bytes[1]};
+  const cuuint32_t b[3] = {box[0], box[1], box[2]};
+  const cuuint32_t es[3] = {1, 1, 1};
+  return encode(map, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, const_cast<void*>(base), d, st, b, es,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
 }
 

@@ -1,43 +1,54 @@
 // skinny.cu -- K5: the WnAm bipolar-INT GEMM for few feature rows (decode / small-M LLM
-// shapes), HBM-bound on the packed weight planes.
+// shapes), HBM-bound on the packed weight planes. Two launches per matmul_ap call: a tiny
+// feature-prep kernel (X planes -> MMA fragment order, once) and the streaming kernel.
 //
-// Why a separate kernel. With M_tok <= 64 the GEMM does ~2*M ops per weight code, so the
+// Why a separate path. With M_tok < 64 the GEMM does ~2*M ops per weight code, so the
 // roofline is the HBM read of the packed weight planes (n_w bits per weight). The large-M
 // path (expand -> u8 codes in HBM -> tcgen05 GEMM) would write and re-read 8/n_w times
-// those bytes. Here the weight planes go from HBM straight into registers (128-bit
-// non-allocating loads), are turned into u8 code fragments in registers by a partial 8x8
-// bit transpose, and feed legacy-pipe mma.sync m16n8k32 u8 x u8 -> s32 MMAs. Tensor-core
-// throughput is irrelevant at this M; what matters is the ALU cost per weight code, which
-// the transpose keeps at ~0.7 ops/code for n_w <= 4 (see below).
+// those bytes. Here every warp streams its weight tiles (16 rows x 512 columns x n_w
+// planes) from HBM with its own TMA ring in shared memory, turns them into u8 code
+// fragments in registers by a partial 8x8 bit transpose, and feeds legacy-pipe mma.sync
+// m16n8k32 u8 x u8 -> s32 MMAs (measured ~1.1 POPS on this part, scripts/imma_probe.cu:
+// far above what M < 64 needs). What bounds it besides HBM is the instruction count per
+// weight code: the transpose costs ~0.7 ops/code for n_w <= 4 and is split evenly over the
+// ALU and FMA pipes (shifts as IMAD / IMAD.HI), rowsum(U_w) comes out of the MMA through
+// an all-ones feature column (no POPC), and the loop has no divisions.
 //
 // The algebra is the same as the large-M path: one u8 x u8 MMA
 // of the unsigned codes performs the whole 2^(i+j)-weighted plane-pair recovery of the
-// reference's matmul_ap (kernel.cpp:187-254); the rank-1 term is applied in the epilogue.
+// reference's matmul_ap (kernel.cpp:187-254); the rank-1 term is applied in the epilogue:
+//   Y = 4 * sum_k u_w u_x - 2B * rowsum(U_w) - 2A * rowsum(U_x) + K*A*B   (mod 2^32).
+// The first two terms are linear in K, so each K slice contributes 4*S_s - 2B*rsw_s; the
+// slice-0 CTAs add the X term and the constant once.
 //
 // Fragment mapping (PTX m16n8k32 .u8): thread (g = lane/4, t = lane%4) supplies A rows g
 // and g+8 and B column g at K slots {4t+b, 16+4t+b}. The K order inside the MMA is free as
 // long as A and B agree, and the slot -> column map below depends only on (t, slot), never
 // on g:
-//   thread t loads plane words [16c + 4t, +4) (128 columns) of its two weight rows;
+//   thread t takes plane words [16c + 4t, +4) (128 columns) of its two weight rows;
 //   a 32-column word is bit-transposed so that register r, byte B holds column 8B + r;
-//   X codes come from the expand kernel in exactly that order (byte 4r+B of a 32-byte
-//   group = column 8B + r), so the B fragment of the MMA that uses A registers (r, r+1)
-//   is X's group registers (r, r+1).
-// For n_w <= 4 only two of the three delta-swap stages run: register r (r < 4) then holds
-// column 8B+r in its low nibble and column 8B+4+r in its high nibble. `x & 0x0F0F0F0F`
-// gives the first, `x & 0xF0F0F0F0` gives 16x the second; the latter goes into a separate
-// accumulator that is divided by 16 at the end (exact: the host admits this variant only
-// when K*(2^n_w-1)*(2^n_x-1) < 2^28, so 16x the partial sum fits in 32 bits).
+//   the prep kernel transposes X the same way, so the B fragment of the MMA that uses A
+//   registers (r, r+1) is X's registers (r, r+1) of the same word.
+// For n_w <= 4 only two of the three delta-swap stages run on W: register r (r < 4) then
+// holds column 8B+r in its low nibble and column 8B+4+r in its high nibble.
+// `x & 0x0F0F0F0F` gives the first, `x - lo` gives 16x the second; the latter goes into a
+// separate accumulator that is divided by 16 at the end (exact: the host admits this
+// variant only when K*(2^n_w-1)*(2^n_x-1) < 2^28, so 16x any partial sum fits in 32 bits).
 //
-// Work split: CTA = 8 warps x 16 weight rows = 128 rows; grid.y splits K into slices of
-// whole 512-column chunks. Each CTA stages its X slice in shared memory in per-lane
-// fragment order (conflict-free 128-bit reads), accumulates its partial products in
-// registers, and adds them into an int32 workspace with wrapping atomics (exact mod 2^32,
-// order-independent). The last CTA of a row block (counter) applies the rank-1 recovery
-// / dequant epilogue, writes Y, and re-zeroes the workspace for the next call.
+// Work split (host planner, plan_for): K is cut into S slices of whole 512-column chunks;
+// a persistent CTA owns one slice for its lifetime (one bulk copy stages its X slice in
+// shared memory) and walks a strided list of row tiles of 16*R weight rows. Its warps are
+// R row groups x (warps/R) K groups; the K groups' partial sums meet in shared memory
+// (red.shared.add). With S == 1 the CTA applies the recovery / dequant epilogue and
+// writes Y directly. With S > 1 partial sums go to an int32 workspace with wrapping
+// atomics (exact mod 2^32, order-independent); the last CTA of a tile (counter)
+// finalises it and re-zeroes the workspace for the next call.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 
 #include "internal.h"
 #include "ptx.cuh"
@@ -45,35 +56,50 @@
 namespace apmm_b200 {
 namespace {
 
-constexpr int kSkThreads = 256;
-constexpr int kSkWarps = kSkThreads / 32;
-constexpr int kChunkWords = 16;  // 512 columns per warp iteration
-constexpr uint32_t kSkSmemMax = 96u * 1024u;  // X slice budget per CTA
+constexpr int kChunkWords = 16;  // 512 columns per warp step
+constexpr uint32_t kSkSmem = 224u * 1024u;  // dynamic budget (227 KB opt-in max minus static)
+constexpr int kPrepThreads = 256;
+
+// 16 warps where the register budget allows, else 8.
+__host__ __device__ constexpr int sk_threads(int n, int nt) { return (n <= 3 && nt <= 4) ? 512 : 256; }
+// Per-warp TMA ring: a slot holds one work item, n planes x 16 rows x 64 B = n KB. Depth
+// chosen for ~130 KB of weight planes in flight per SM.
+__host__ __device__ constexpr int sk_stages(int n, int nt) {
+  return sk_threads(n, nt) == 512 ? (n == 1 ? 8 : n == 2 ? 4 : 3)
+                                  : (n == 1 ? 16 : n == 2 ? 8 : n == 3 ? 6 : n == 4 ? 4 : 2);
+}
+__host__ __device__ constexpr uint32_t slot_bytes(int n) { return static_cast<uint32_t>(n) * 1024u; }
+__host__ __device__ constexpr uint32_t ring_bytes(int n, int nt) {
+  return static_cast<uint32_t>(sk_threads(n, nt) / 32 * sk_stages(n, nt)) * slot_bytes(n);
+}
+// Shared-memory X layout per 512-column chunk: [w 0..3][nt][half 0..1][lane 0..31] x 16 B.
+// Lane (g, t) of n-tile nt, word w, half h holds code registers [4h, 4h+4) of feature row
+// nt*8+g, word 16*chunk + 4t + w (register r, byte B = code of column 8B + r).
+__host__ __device__ constexpr uint32_t chunk_bytes(int nt) { return 4u * nt * 2u * 32u * 16u; }
+// cross-warp reduction buffer: [16 R][m_pad] u32, R <= 8
+__host__ __device__ constexpr uint32_t red_bytes(int nt, uint32_t r) { return 16u * r * nt * 8u * 4u; }
 
 struct SkinnyParams {
-  const uint32_t* w;         // weight planes, reference layout [n_w][rows_w][wpr]
-  const uint8_t* xc;         // feature codes [rows_x][kpad], expand order
-  const int32_t* rowsum_x;   // [rows_x]
-  uint32_t rows_w, rows_x, wpr, kpad_words;
-  uint32_t chunks_total, chunks_per_slice;
-  uint32_t* acc;             // [row_blocks * 128][m_pad], zero on entry and on exit
-  uint32_t* acc_rs;          // [row_blocks * 128] partial rowsum(U_w)
-  uint32_t* counters;        // [row_blocks]
+  const uint8_t* xfrag;      // prep output: [chunks_total][chunk_bytes(NT)]
+  const int32_t* rsx;        // prep output: rowsum(U_x) parts [rows_x][rsx_parts]
+  uint32_t rsx_parts;
+  uint32_t rows_w, rows_x, wpr, n_planes;
+  uint32_t chunks_total;     // ceil(wpr / 16)
+  uint32_t slices, slice_chunks;
+  uint32_t rgroups;          // R: 16-row groups per tile (warps_k = warps / R)
+  uint32_t n_tiles;          // ceil(rows_w / (16 R))
+  uint32_t ring_off, red_off;  // shared-memory carve-up (bytes)
+  uint32_t* acc;             // S > 1: [n_tiles * 16R][m_pad], zero on entry and exit
+  uint32_t* counters;        // S > 1: [n_tiles]
   int32_t* y;
   float* yf;
   const double* s_w;
   const double* s_x;
   int gran_w, gran_x;
   uint32_t coef_w, coef_x, c0;
+  // multipliers kept in the parameter bank so ptxas emits IMAD (FMA pipe), not SHF/IADD
+  uint32_t m2, m4, m16, neg1;
 };
-
-APMM_DEV uint4 ld_stream_v4(const uint32_t* p) {
-  uint4 r;
-  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
-               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-               : "l"(p));
-  return r;
-}
 
 APMM_DEV void mma_u8(uint32_t (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
                      uint32_t b0, uint32_t b1) {
@@ -84,214 +110,308 @@ APMM_DEV void mma_u8(uint32_t (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, ui
       : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
 
-APMM_DEV void swap_sel(uint32_t& a, uint32_t& b, int s, uint32_t m) {
-  const uint32_t na = (a & ~(m << s)) | ((b << s) & (m << s));
-  b = (b & ~m) | ((a >> s) & m);
+APMM_DEV void tma_load_3d(uint32_t dst, const void* tmap, uint32_t bar, int32_t c0, int32_t c1,
+                          int32_t c2, uint64_t hint) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "l"(hint)
+      : "memory");
+}
+// One bulk (non-tensor) TMA copy global -> this CTA's shared memory, completing on `bar`.
+APMM_DEV void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+      "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
+}
+APMM_DEV uint32_t mulhi(uint32_t a, uint32_t b) { return __umulhi(a, b); }
+
+// Delta swap in select form with both shifts on the FMA pipe (IMAD / IMAD.HI) and the two
+// selects as LOP3 on the ALU pipe.
+template <int S>
+APMM_DEV void swap_sel(uint32_t& a, uint32_t& b, uint32_t m, uint32_t mul_s) {
+  const uint32_t bs = b * mul_s;                      // b << S
+  const uint32_t as = mulhi(a, 1u << (32 - S));       // a >> S
+  const uint32_t na = (a & ~(m << S)) | (bs & (m << S));
+  b = (b & ~m) | (as & m);
   a = na;
 }
 
-// Four plane words of one weight row (row = plane index in x[]), for 4 consecutive words.
-template <int N>
-struct RowWords {
-  uint4 p[N];
-};
-
-template <int N, bool VEC>
-APMM_DEV void load_row(RowWords<N>& r, const uint32_t* base, uint64_t pstride, uint32_t w0,
-                       uint32_t wpr, bool row_ok) {
-#pragma unroll
-  for (int i = 0; i < N; ++i) {
-    const uint32_t* p = base + i * pstride;
-    if (VEC && row_ok && w0 + 3 < wpr) {
-      r.p[i] = ld_stream_v4(p + w0);
-    } else {
-      r.p[i].x = row_ok && w0 + 0 < wpr ? __ldg(p + w0 + 0) : 0u;
-      r.p[i].y = row_ok && w0 + 1 < wpr ? __ldg(p + w0 + 1) : 0u;
-      r.p[i].z = row_ok && w0 + 2 < wpr ? __ldg(p + w0 + 2) : 0u;
-      r.p[i].w = row_ok && w0 + 3 < wpr ? __ldg(p + w0 + 3) : 0u;
-    }
-  }
-}
-
-template <int N>
-APMM_DEV uint32_t word_of(const RowWords<N>& r, int i, int w) {
-  return w == 0 ? r.p[i].x : w == 1 ? r.p[i].y : w == 2 ? r.p[i].z : r.p[i].w;
-}
-
-// Codes of one 32-column word. SPLIT (N <= 4): lo[r] = codes of columns 8B+r, hi[r] = 16x
-// codes of columns 8B+4+r (r < 4). Otherwise full[r] = codes of columns 8B+r (r < 8).
+// Codes of one 32-column word (x[i] = plane i word, zero for i >= N). SPLIT (N <= 4):
+// o[r] = codes of columns 8B+r, o[4+r] = 16x codes of columns 8B+4+r (r < 4). Otherwise
+// o[r] = codes of columns 8B+r (r < 8).
 template <int N, bool SPLIT>
-APMM_DEV void codes_of_word(const RowWords<N>& rw, int w, uint32_t (&o)[8], int32_t& rowsum) {
-  uint32_t x[8];
-#pragma unroll
-  for (int i = 0; i < 8; ++i) x[i] = i < N ? word_of(rw, i, w) : 0u;
-#pragma unroll
-  for (int i = 0; i < N; ++i) rowsum += __popc(x[i]) << i;
+APMM_DEV void codes_of_word(uint32_t (&x)[8], uint32_t (&o)[8], const SkinnyParams& p) {
   if (SPLIT) {
-    swap_sel(x[0], x[2], 2, 0x33333333u);
-    swap_sel(x[1], x[3], 2, 0x33333333u);
-    swap_sel(x[0], x[1], 1, 0x55555555u);
-    swap_sel(x[2], x[3], 1, 0x55555555u);
+    swap_sel<2>(x[0], x[2], 0x33333333u, p.m4);
+    swap_sel<2>(x[1], x[3], 0x33333333u, p.m4);
+    swap_sel<1>(x[0], x[1], 0x55555555u, p.m2);
+    swap_sel<1>(x[2], x[3], 0x55555555u, p.m2);
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
       o[r] = x[r] & 0x0F0F0F0Fu;
-      o[4 + r] = x[r] & 0xF0F0F0F0u;
+      o[4 + r] = o[r] * p.neg1 + x[r];  // x - lo = the high nibbles, 16x
     }
   } else {
 #pragma unroll
-    for (int i = 0; i < 4; ++i) swap_sel(x[i], x[i + 4], 4, 0x0F0F0F0Fu);
+    for (int i = 0; i < 4; ++i) swap_sel<4>(x[i], x[i + 4], 0x0F0F0F0Fu, p.m16);
 #pragma unroll
     for (int i = 0; i < 8; i += 4) {
-      swap_sel(x[i], x[i + 2], 2, 0x33333333u);
-      swap_sel(x[i + 1], x[i + 3], 2, 0x33333333u);
+      swap_sel<2>(x[i], x[i + 2], 0x33333333u, p.m4);
+      swap_sel<2>(x[i + 1], x[i + 3], 0x33333333u, p.m4);
     }
 #pragma unroll
-    for (int i = 0; i < 8; i += 2) swap_sel(x[i], x[i + 1], 1, 0x55555555u);
+    for (int i = 0; i < 8; i += 2) swap_sel<1>(x[i], x[i + 1], 0x55555555u, p.m2);
 #pragma unroll
     for (int r = 0; r < 8; ++r) o[r] = x[r];
   }
 }
 
-// Shared-memory X layout per 512-column chunk: [w 0..3][nt][half 0..1][lane 0..31] x 16 B.
-// Lane (g, t) of n-tile nt, word w, half h holds bytes [16h, 16h+16) of the 32-byte code
-// group of feature row nt*8+g, word 16*chunk + 4t + w.
-template <int NT>
-__host__ __device__ constexpr uint32_t chunk_smem_bytes() {
-  return 4u * NT * 2u * 32u * 16u;
+// Plain 8x8 transpose for the prep kernel (register r, byte B <- column 8B + r).
+APMM_DEV void transpose8(uint32_t (&x)[8]) {
+  auto sw = [](uint32_t& a, uint32_t& b, int s, uint32_t m) {
+    const uint32_t na = (a & ~(m << s)) | ((b << s) & (m << s));
+    b = (b & ~m) | ((a >> s) & m);
+    a = na;
+  };
+#pragma unroll
+  for (int i = 0; i < 4; ++i) sw(x[i], x[i + 4], 4, 0x0F0F0F0Fu);
+#pragma unroll
+  for (int i = 0; i < 8; i += 4) {
+    sw(x[i], x[i + 2], 2, 0x33333333u);
+    sw(x[i + 1], x[i + 3], 2, 0x33333333u);
+  }
+#pragma unroll
+  for (int i = 0; i < 8; i += 2) sw(x[i], x[i + 1], 1, 0x55555555u);
 }
 
-// Two CTAs per SM where the register budget (128) allows it without spilling.
-template <int N, int NT>
-constexpr int sk_min_blocks() {
-  return (N <= 4 && NT <= 4) ? 2 : 1;
+// ---- feature prep: X planes -> fragment-order codes, ones column, rowsum(U_x) ----------
+// grid (ceil(chunks_total*16 / 256), m_pad); thread = (feature slot, 32-column word).
+// Slot m_pad-1 (always >= rows_x) is the all-ones column whose MMA output is rowsum(U_w).
+// PDL: reads only the caller's X planes before griddepcontrol.wait; writes its workspace
+// half (last read by the call before the previous one, complete by construction) and
+// completes only after the previous kernel in the stream, like the expand kernel.
+__global__ void __launch_bounds__(kPrepThreads) prep_x_kernel(const uint32_t* __restrict__ x,
+                                                              uint32_t rows_x, uint32_t wpr,
+                                                              int n_x, uint32_t words_pad,
+                                                              uint32_t nt_count,
+                                                              uint8_t* __restrict__ xfrag,
+                                                              int32_t* __restrict__ rsx_part) {
+  apmm_ptx::pdl_trigger();
+  const uint32_t tok = blockIdx.y, W = blockIdx.x * kPrepThreads + threadIdx.x;
+  const uint32_t m_pad = nt_count * 8u;
+  uint32_t v[8];
+  int32_t rs = 0;
+  if (tok < rows_x) {
+    const uint64_t pstride = uint64_t(rows_x) * wpr;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      v[i] = (i < n_x && W < wpr) ? __ldg(x + i * pstride + uint64_t(tok) * wpr + W) : 0u;
+      if (i < n_x) rs += __popc(v[i]) << i;
+    }
+    transpose8(v);
+  } else {
+    const uint32_t fill = (tok == m_pad - 1) ? 0x01010101u : 0u;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = fill;
+  }
+  apmm_ptx::pdl_wait();  // the workspace half may be written only now
+  if (W < words_pad) {
+    const uint32_t cl = W / kChunkWords, t = (W % kChunkWords) >> 2, w = W & 3u;
+    const uint32_t nt = tok >> 3, g = tok & 7u;
+    uint4* dst = reinterpret_cast<uint4*>(xfrag + uint64_t(cl) * chunk_bytes(nt_count)) +
+                 ((w * nt_count + nt) * 2u) * 32u + g * 4u + t;
+    dst[0] = make_uint4(v[0], v[1], v[2], v[3]);
+    dst[32] = make_uint4(v[4], v[5], v[6], v[7]);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) rs += __shfl_xor_sync(0xffffffffu, rs, o);
+  __shared__ int32_t part[kPrepThreads / 32];
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = rs;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int32_t s = 0;
+    for (int i = 0; i < kPrepThreads / 32; ++i) s += part[i];
+    rsx_part[uint64_t(tok) * gridDim.x + blockIdx.x] = s;
+  }
 }
 
-template <int N, int NT, bool SPLIT, bool VEC>
-__global__ void __launch_bounds__(kSkThreads, sk_min_blocks<N, NT>()) skinny_kernel(const SkinnyParams p) {
-  extern __shared__ __align__(16) uint8_t xs[];
-  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+template <int N, int NT, bool SPLIT>
+__global__ void __launch_bounds__(sk_threads(N, NT), 1)
+    skinny_kernel(const __grid_constant__ CUtensorMap tmap_w, const SkinnyParams p) {
+  constexpr int THREADS = sk_threads(N, NT);
+  constexpr int WARPS = THREADS / 32;
+  constexpr int STAGES = sk_stages(N, NT);
+  constexpr uint32_t SLOT = slot_bytes(N);
+  constexpr uint32_t M_PAD = NT * 8u;
+  constexpr uint32_t ONES = M_PAD - 1u;  // the all-ones feature column -> rowsum(U_w)
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ __align__(8) uint64_t full_bar[WARPS * STAGES];
+  __shared__ __align__(8) uint64_t xbar;
+  __shared__ uint32_t rsx_s[M_PAD];
+  __shared__ uint32_t s_last;
+
+  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t g = lane >> 2, t = lane & 3;
-  const uint32_t row_blk = blockIdx.x;
-  const uint32_t row_a = row_blk * 128u + warp * 16u + g, row_b = row_a + 8u;
-  const bool ok_a = row_a < p.rows_w, ok_b = row_b < p.rows_w;
-  const uint32_t c_begin = blockIdx.y * p.chunks_per_slice;
-  const uint32_t c_end = min(c_begin + p.chunks_per_slice, p.chunks_total);
-  const uint64_t pstride = uint64_t(p.rows_w) * p.wpr;
-  const uint32_t* wa = p.w + uint64_t(ok_a ? row_a : 0) * p.wpr;
-  const uint32_t* wb = p.w + uint64_t(ok_b ? row_b : 0) * p.wpr;
+  const uint32_t warps_k = WARPS / p.rgroups;
+  const uint32_t wr = warp / warps_k, wk = warp % warps_k;
+  const uint32_t tile_rows = 16u * p.rgroups;
 
-  // The weight planes are inputs of this call: their first loads may overlap the feature
-  // expand kernel still running ahead of us (PDL); the X codes may not.
-  RowWords<N> cur_a, cur_b, nxt_a, nxt_b;
-  load_row<N, VEC>(cur_a, wa, pstride, c_begin * kChunkWords + 4 * t, p.wpr, ok_a);
-  load_row<N, VEC>(cur_b, wb, pstride, c_begin * kChunkWords + 4 * t, p.wpr, ok_b);
-  apmm_ptx::pdl_wait();
+  // persistent CTA: slice = blockIdx.x % S, tiles j0, j0 + gs, ... (gs CTAs per slice)
+  const uint32_t slice = blockIdx.x % p.slices;
+  const uint32_t j0 = blockIdx.x / p.slices, gs = gridDim.x / p.slices;
+  const uint32_t s_begin = slice * p.slice_chunks;
+  const uint32_t s_end = min(s_begin + p.slice_chunks, p.chunks_total);
+  const uint32_t cpw = (p.slice_chunks + warps_k - 1) / warps_k;  // chunks per warp per tile
+  const uint32_t my_tiles = j0 < p.n_tiles ? (p.n_tiles - j0 + gs - 1) / gs : 0u;
 
-  // ---- stage the X slice (fragment order) ----
-  {
-    const uint32_t nchunks = c_end - c_begin;
-    const uint32_t pieces = nchunks * (chunk_smem_bytes<NT>() / 16u);
-    for (uint32_t q = threadIdx.x; q < pieces; q += kSkThreads) {
-      const uint32_t ln = q & 31u, h = (q >> 5) & 1u;
-      const uint32_t rest = q >> 6;  // (chunk_local * 4 + w) * NT + nt
-      const uint32_t nt = rest % NT, cw = rest / NT;
-      const uint32_t w = cw & 3u, cl = cw >> 2;
-      const uint32_t tok = nt * 8u + (ln >> 2);
-      const uint32_t word = (c_begin + cl) * kChunkWords + 4u * (ln & 3u) + w;
-      uint4 v = make_uint4(0u, 0u, 0u, 0u);
-      if (tok < p.rows_x && word < p.kpad_words) {
-        v = __ldg(reinterpret_cast<const uint4*>(p.xc + uint64_t(tok) * p.kpad_words * 32u +
-                                                 uint64_t(word) * 32u + h * 16u));
+  uint8_t* xs = smem;
+  const uint32_t ring = apmm_ptx::smem_u32(smem + p.ring_off) + warp * (STAGES * SLOT);
+  uint32_t* red = reinterpret_cast<uint32_t*>(smem + p.red_off);  // [tile_rows][M_PAD]
+  uint64_t* bars = full_bar + warp * STAGES;
+
+  if (lane == 0) {
+    for (int s = 0; s < STAGES; ++s) apmm_ptx::mbar_init(&bars[s], 1);
+    if (warp == 0) apmm_ptx::mbar_init(&xbar, 1);
+    apmm_ptx::fence_mbar_init();
+    apmm_ptx::tma_prefetch_desc(&tmap_w);
+  }
+  __syncwarp();
+  const uint64_t hint = apmm_ptx::policy_evict_first();  // weights are read exactly once
+
+  // ---- per-warp TMA ring: item cursor (tile index, chunk step) ----
+  uint32_t is_tile = 0, is_c = 0, is_slot = 0;
+  auto issue = [&]() {
+    if (is_tile < my_tiles) {
+      const uint32_t chunk = s_begin + is_c * warps_k + wk;
+      if (chunk < s_end && lane == 0) {
+        const uint32_t row0 = (j0 + is_tile * gs) * tile_rows + wr * 16u;
+        apmm_ptx::mbar_arrive_expect_tx(&bars[is_slot], p.n_planes * 1024u);
+        tma_load_3d(ring + is_slot * SLOT, &tmap_w, apmm_ptx::smem_u32(&bars[is_slot]),
+                    int32_t(chunk * kChunkWords), int32_t(row0), 0, hint);
       }
-      reinterpret_cast<uint4*>(xs)[q] = v;
+      if (++is_c == cpw) { is_c = 0; ++is_tile; }
+    }
+    if (++is_slot == STAGES) is_slot = 0;
+  };
+
+  // The weight planes are inputs of this call, so their loads may overlap the prep kernel
+  // still running ahead of us (PDL); X, the workspace and Y only after pdl_wait.
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) issue();
+  apmm_ptx::pdl_wait();
+  __syncthreads();  // xbar initialised
+  const uint32_t xbytes = (s_end > s_begin ? s_end - s_begin : 0u) * chunk_bytes(NT);
+  if (tid == 0) {
+    apmm_ptx::mbar_arrive_expect_tx(&xbar, xbytes);
+    const uint8_t* src = p.xfrag + uint64_t(s_begin) * chunk_bytes(NT);
+    for (uint32_t off = 0; off < xbytes; off += 32768u) {
+      bulk_g2s(apmm_ptx::smem_u32(xs + off), src + off, min(32768u, xbytes - off),
+               apmm_ptx::smem_u32(&xbar));
     }
   }
+  // slice 0 adds the X term and the constant once; rsx_s is zero elsewhere
+  for (uint32_t q = tid; q < M_PAD; q += THREADS) {
+    int32_t s = 0;
+    if (slice == 0 && q < p.rows_x) {
+      for (uint32_t k = 0; k < p.rsx_parts; ++k) s += __ldg(p.rsx + uint64_t(q) * p.rsx_parts + k);
+    }
+    rsx_s[q] = static_cast<uint32_t>(s);
+  }
+  for (uint32_t q = tid; q < tile_rows * M_PAD; q += THREADS) red[q] = 0u;
+  apmm_ptx::mbar_wait(&xbar, 0);
   __syncthreads();
+  const uint32_t cterm = slice == 0 ? p.c0 : 0u;
 
   uint32_t lo[NT][4], hi[NT][4];
 #pragma unroll
   for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
     for (int e = 0; e < 4; ++e) lo[nt][e] = hi[nt][e] = 0u;
-  int32_t rs_a = 0, rs_b = 0;
 
-  const uint4* xs4 = reinterpret_cast<const uint4*>(xs);
-  for (uint32_t c = c_begin; c < c_end; ++c) {
-    if (c + 1 < c_end) {
-      load_row<N, VEC>(nxt_a, wa, pstride, (c + 1) * kChunkWords + 4 * t, p.wpr, ok_a);
-      load_row<N, VEC>(nxt_b, wb, pstride, (c + 1) * kChunkWords + 4 * t, p.wpr, ok_b);
-    }
-    const uint4* xchunk = xs4 + (c - c_begin) * (chunk_smem_bytes<NT>() / 16u);
+  uint32_t cs_slot = 0, phase_bits = 0;
+  for (uint32_t ti = 0; ti < my_tiles; ++ti) {
+    const uint32_t tile = j0 + ti * gs;
+    for (uint32_t c = 0; c < cpw; ++c) {
+      __syncwarp();  // every lane is done with the slot the next issue overwrites
+      issue();
+      const uint32_t chunk = s_begin + c * warps_k + wk;
+      if (chunk < s_end) {
+        apmm_ptx::mbar_wait(&bars[cs_slot], (phase_bits >> cs_slot) & 1u);
+        phase_bits ^= 1u << cs_slot;
+        // slot layout (TMA box {16 words, 16 rows, planes}): [plane][row][16 words]
+        const uint8_t* slot = smem + p.ring_off + (warp * STAGES + cs_slot) * SLOT + g * 64u + t * 16u;
+        uint4 wa[N], wb[N];
 #pragma unroll
-    for (int w = 0; w < 4; ++w) {
-      uint32_t ca[8], cb[8];
-      codes_of_word<N, SPLIT>(cur_a, w, ca, rs_a);
-      codes_of_word<N, SPLIT>(cur_b, w, cb, rs_b);
+        for (int pl = 0; pl < N; ++pl) {
+          const bool live = SPLIT || uint32_t(pl) < p.n_planes;
+          wa[pl] = live ? *reinterpret_cast<const uint4*>(slot + pl * 1024) : make_uint4(0, 0, 0, 0);
+          wb[pl] = live ? *reinterpret_cast<const uint4*>(slot + pl * 1024 + 512) : make_uint4(0, 0, 0, 0);
+        }
+        const uint4* xchunk = reinterpret_cast<const uint4*>(xs + (chunk - s_begin) * chunk_bytes(NT));
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+          uint32_t xa[8], xb[8], ca[8], cb[8];
+#pragma unroll
+          for (int pl = 0; pl < 8; ++pl) {
+            if (pl < N) {
+              const uint4& A = wa[pl < N ? pl : 0];
+              const uint4& B = wb[pl < N ? pl : 0];
+              xa[pl] = w == 0 ? A.x : w == 1 ? A.y : w == 2 ? A.z : A.w;
+              xb[pl] = w == 0 ? B.x : w == 1 ? B.y : w == 2 ? B.z : B.w;
+            } else {
+              xa[pl] = xb[pl] = 0u;
+            }
+          }
+          codes_of_word<N, SPLIT>(xa, ca, p);
+          codes_of_word<N, SPLIT>(xb, cb, p);
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) {
+            const uint4 x0 = xchunk[((w * NT + nt) * 2 + 0) * 32 + lane];
+            const uint4 x1 = xchunk[((w * NT + nt) * 2 + 1) * 32 + lane];
+            mma_u8(lo[nt], ca[0], cb[0], ca[1], cb[1], x0.x, x0.y);
+            mma_u8(lo[nt], ca[2], cb[2], ca[3], cb[3], x0.z, x0.w);
+            if (SPLIT) {
+              mma_u8(hi[nt], ca[4], cb[4], ca[5], cb[5], x1.x, x1.y);
+              mma_u8(hi[nt], ca[6], cb[6], ca[7], cb[7], x1.z, x1.w);
+            } else {
+              mma_u8(lo[nt], ca[4], cb[4], ca[5], cb[5], x1.x, x1.y);
+              mma_u8(lo[nt], ca[6], cb[6], ca[7], cb[7], x1.z, x1.w);
+            }
+          }
+        }
+      }
+      if (++cs_slot == STAGES) cs_slot = 0;
+    }
+
+    // ---------------- end of tile: combine the K groups, epilogue ----------------
+    if (ti + 1 == my_tiles) apmm_ptx::pdl_trigger();  // last tile: the next call may start
+    {
+      uint32_t* mine = red + (wr * 16u) * M_PAD;
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) {
-        const uint4 x0 = xchunk[((w * NT + nt) * 2 + 0) * 32 + lane];
-        const uint4 x1 = xchunk[((w * NT + nt) * 2 + 1) * 32 + lane];
-        if (SPLIT) {
-          mma_u8(lo[nt], ca[0], cb[0], ca[1], cb[1], x0.x, x0.y);
-          mma_u8(lo[nt], ca[2], cb[2], ca[3], cb[3], x0.z, x0.w);
-          mma_u8(hi[nt], ca[4], cb[4], ca[5], cb[5], x1.x, x1.y);
-          mma_u8(hi[nt], ca[6], cb[6], ca[7], cb[7], x1.z, x1.w);
-        } else {
-          mma_u8(lo[nt], ca[0], cb[0], ca[1], cb[1], x0.x, x0.y);
-          mma_u8(lo[nt], ca[2], cb[2], ca[3], cb[3], x0.z, x0.w);
-          mma_u8(lo[nt], ca[4], cb[4], ca[5], cb[5], x1.x, x1.y);
-          mma_u8(lo[nt], ca[6], cb[6], ca[7], cb[7], x1.z, x1.w);
+        const uint32_t c = nt * 8u + 2u * t;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const uint32_t v = lo[nt][e] + (SPLIT ? (hi[nt][e] >> 4) : 0u);
+          atomicAdd(mine + (g + (e >= 2 ? 8u : 0u)) * M_PAD + c + (e & 1), v);
+          lo[nt][e] = hi[nt][e] = 0u;
         }
       }
     }
-    cur_a = nxt_a;
-    cur_b = nxt_b;
-  }
-
-  // ---- partial sums -> workspace (wrapping adds: exact and order-independent) ----
-  const uint32_t m_pad = NT * 8u;
-#pragma unroll
-  for (int nt = 0; nt < NT; ++nt) {
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const uint32_t row = (e < 2) ? row_a : row_b;
-      const uint32_t tok = nt * 8u + 2u * t + (e & 1u);
-      const uint32_t s = lo[nt][e] + (SPLIT ? (hi[nt][e] >> 4) : 0u);
-      atomicAdd(p.acc + uint64_t(row) * m_pad + tok, s);
-    }
-  }
-  rs_a += __shfl_xor_sync(0xffffffffu, rs_a, 1);
-  rs_a += __shfl_xor_sync(0xffffffffu, rs_a, 2);
-  rs_b += __shfl_xor_sync(0xffffffffu, rs_b, 1);
-  rs_b += __shfl_xor_sync(0xffffffffu, rs_b, 2);
-  if (t == 0) {
-    atomicAdd(p.acc_rs + row_a, static_cast<uint32_t>(rs_a));
-    atomicAdd(p.acc_rs + row_b, static_cast<uint32_t>(rs_b));
-  }
-
-  // ---- last CTA of this row block: rank-1 recovery / dequant epilogue ----
-  __shared__ uint32_t last;
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    const uint32_t prev = atomicAdd(p.counters + row_blk, 1u);
-    last = (prev == gridDim.y - 1) ? 1u : 0u;
-  }
-  __syncthreads();
-  if (!last) return;
-  __threadfence();
-  // allow the next call's expand to start (it writes the other workspace half and waits
-  // for us before it completes)
-  apmm_ptx::pdl_trigger();
-  const uint32_t total = 128u * m_pad;
-  for (uint32_t i = threadIdx.x; i < total; i += kSkThreads) {
-    const uint32_t row = row_blk * 128u + i / m_pad, tok = i % m_pad;
-    uint32_t* ap = p.acc + uint64_t(row) * m_pad + tok;
-    if (row < p.rows_w && tok < p.rows_x) {
-      const uint32_t s = __ldcg(ap);
-      const uint32_t rsw = __ldcg(p.acc_rs + row);
-      const uint32_t rsx = static_cast<uint32_t>(__ldg(p.rowsum_x + tok));
-      const uint32_t v = 4u * s + p.c0 - p.coef_w * rsw - p.coef_x * rsx;
+    __syncthreads();
+    const uint32_t elems = tile_rows * M_PAD;
+    for (uint32_t e = tid; e < elems; e += THREADS) {
+      const uint32_t rl = e / M_PAD, tok = e % M_PAD;
+      const uint32_t row = tile * tile_rows + rl;
+      if (row >= p.rows_w || tok >= p.rows_x) continue;
+      const uint32_t v = 4u * red[e] - p.coef_w * red[rl * M_PAD + ONES] -
+                         p.coef_x * rsx_s[tok] + cterm;
+      if (p.slices > 1) {
+        atomicAdd(p.acc + (uint64_t(tile) * tile_rows + rl) * M_PAD + tok, v);
+        continue;
+      }
       const uint64_t o = uint64_t(row) * p.rows_x + tok;
       if (p.yf) {
         const double sw = p.gran_w ? p.s_w[row] : p.s_w[0];
@@ -301,27 +421,54 @@ __global__ void __launch_bounds__(kSkThreads, sk_min_blocks<N, NT>()) skinny_ker
         p.y[o] = static_cast<int32_t>(v);
       }
     }
-    __stcg(ap, 0u);
+    __syncthreads();  // every reader of red is done
+    for (uint32_t e = tid; e < elems; e += THREADS) red[e] = 0u;
+    if (p.slices > 1 && tid == 0) {
+      __threadfence();
+      const uint32_t prev = atomicAdd(p.counters + tile, 1u);
+      s_last = (prev == p.slices - 1) ? 1u : 0u;
+    }
+    __syncthreads();  // red zeroed before the next tile's adds; s_last visible
+    if (p.slices > 1 && s_last) {  // the last slice of this tile: finalise, re-zero
+      __threadfence();
+      for (uint32_t e = tid; e < elems; e += THREADS) {
+        const uint32_t rl = e / M_PAD, tok = e % M_PAD;
+        const uint32_t row = tile * tile_rows + rl;
+        if (row >= p.rows_w || tok >= p.rows_x) continue;
+        uint32_t* ap = p.acc + (uint64_t(tile) * tile_rows + rl) * M_PAD + tok;
+        const uint32_t yv = __ldcg(ap);
+        const uint64_t o = uint64_t(row) * p.rows_x + tok;
+        if (p.yf) {
+          const double sw = p.gran_w ? p.s_w[row] : p.s_w[0];
+          const double sx = p.gran_x ? p.s_x[tok] : p.s_x[0];
+          p.yf[o] = static_cast<float>(__dmul_rn(__dmul_rn(double(int32_t(yv)), sw), sx));
+        } else {
+          p.y[o] = static_cast<int32_t>(yv);
+        }
+        __stcg(ap, 0u);
+      }
+      if (tid == 0) p.counters[tile] = 0u;
+    }
+    // s_last is next written after the next tile's first barrier
   }
-  __syncthreads();
-  for (uint32_t i = threadIdx.x; i < 128u; i += kSkThreads) __stcg(p.acc_rs + row_blk * 128u + i, 0u);
-  if (threadIdx.x == 0) p.counters[row_blk] = 0u;
+  if (my_tiles == 0) apmm_ptx::pdl_trigger();
 }
 
-template <int N, int NT, bool SPLIT, bool VEC>
-cudaError_t launch_t(const SkinnyParams& p, dim3 grid, uint32_t smem, cudaStream_t s) {
-  auto kern = skinny_kernel<N, NT, SPLIT, VEC>;
+template <int N, int NT, bool SPLIT>
+cudaError_t launch_t(const CUtensorMap& tm, const SkinnyParams& p, unsigned grid, uint32_t smem,
+                     cudaStream_t s) {
+  auto kern = skinny_kernel<N, NT, SPLIT>;
   static bool attr_set = false;  // one per instantiation
   cudaError_t e;
   if (!attr_set) {
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(kSkSmemMax));
+                             static_cast<int>(kSkSmem));
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = grid;
-  cfg.blockDim = dim3(kSkThreads);
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(sk_threads(N, NT));
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
@@ -329,102 +476,207 @@ cudaError_t launch_t(const SkinnyParams& p, dim3 grid, uint32_t smem, cudaStream
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  e = cudaLaunchKernelEx(&cfg, kern, p);
+  e = cudaLaunchKernelEx(&cfg, kern, tm, p);
   return e != cudaSuccess ? e : cudaGetLastError();
 }
 
-template <int NT, bool SPLIT, bool VEC>
-cudaError_t dispatch_n(int n, const SkinnyParams& p, dim3 grid, uint32_t smem, cudaStream_t s) {
-  if constexpr (SPLIT) {
-    switch (n) {
-      case 1: return launch_t<1, NT, SPLIT, VEC>(p, grid, smem, s);
-      case 2: return launch_t<2, NT, SPLIT, VEC>(p, grid, smem, s);
-      case 3: return launch_t<3, NT, SPLIT, VEC>(p, grid, smem, s);
-      default: return launch_t<4, NT, SPLIT, VEC>(p, grid, smem, s);
-    }
-  } else {
-  switch (n) {
-    case 1: case 2: case 3: case 4: return launch_t<4, NT, false, VEC>(p, grid, smem, s);
-    case 5: return launch_t<5, NT, false, VEC>(p, grid, smem, s);
-    case 6: return launch_t<6, NT, false, VEC>(p, grid, smem, s);
-    case 7: return launch_t<7, NT, false, VEC>(p, grid, smem, s);
-    default: return launch_t<8, NT, false, VEC>(p, grid, smem, s);
-  }
-  }
-}
+// Kernel variants: SPLIT for n_w <= 4 (N = n_w exactly); otherwise the full transpose with
+// N = 4 (n_w <= 4) or N = 8 (n_w 5..8), unused planes masked at run time.
+int kernel_n(int n_w, bool split) { return split ? n_w : (n_w <= 4 ? 4 : 8); }
 
 template <int NT>
-cudaError_t dispatch_nt(int n, bool split, bool vec, const SkinnyParams& p, dim3 grid,
-                        uint32_t smem, cudaStream_t s) {
+cudaError_t dispatch_n(int n_w, bool split, const CUtensorMap& tm, const SkinnyParams& p,
+                       unsigned grid, uint32_t smem, cudaStream_t s) {
   if (split) {
-    return vec ? dispatch_n<NT, true, true>(n, p, grid, smem, s)
-               : dispatch_n<NT, true, false>(n, p, grid, smem, s);
+    switch (n_w) {
+      case 1: return launch_t<1, NT, true>(tm, p, grid, smem, s);
+      case 2: return launch_t<2, NT, true>(tm, p, grid, smem, s);
+      case 3: return launch_t<3, NT, true>(tm, p, grid, smem, s);
+      default: return launch_t<4, NT, true>(tm, p, grid, smem, s);
+    }
   }
-  return vec ? dispatch_n<NT, false, true>(n, p, grid, smem, s)
-             : dispatch_n<NT, false, false>(n, p, grid, smem, s);
+  return n_w <= 4 ? launch_t<4, NT, false>(tm, p, grid, smem, s)
+                  : launch_t<8, NT, false>(tm, p, grid, smem, s);
+}
+
+// Work plan: R (16-row groups per tile), S (K slices), grid. Minimises the per-warp
+// critical path in 512-column chunk steps, ceil(tiles / CTAs per slice) *
+// (ceil(slice_chunks / warps_k) + per-tile epilogue cost), plus a charge for the split-K
+// atomics, subject to the X slice fitting shared memory.
+struct Plan {
+  uint32_t r, s, slice_chunks, n_tiles, grid, smem, ring_off, red_off;
+};
+
+Plan plan_for(uint64_t rows_w, uint32_t chunks, int n, int nt, int num_sms) {
+  const uint32_t warps = static_cast<uint32_t>(sk_threads(n, nt) / 32);
+  Plan best{};
+  double best_cost = 1e30;
+  for (uint32_t r = 1; r <= 8 && r <= warps; r <<= 1) {
+    const uint32_t fixed = ring_bytes(n, nt) + red_bytes(nt, r);
+    const uint32_t max_slice = fixed < kSkSmem ? (kSkSmem - fixed) / chunk_bytes(nt) : 0u;
+    const uint32_t warps_k = warps / r;
+    const uint64_t n_tiles = (rows_w + 16 * r - 1) / (16 * r);
+    for (uint32_t s = 1; s <= chunks; ++s) {
+      const uint32_t sc = (chunks + s - 1) / s;
+      if (sc > max_slice) continue;
+      if ((chunks + sc - 1) / sc != s) continue;  // same plan as a smaller s
+      const uint32_t per_slice = static_cast<uint32_t>(num_sms) / s;
+      if (per_slice == 0) break;
+      const uint64_t gs = n_tiles < per_slice ? n_tiles : per_slice;
+      const double rounds = static_cast<double>((n_tiles + gs - 1) / gs);
+      const double steps = rounds * ((sc + warps_k - 1) / warps_k + 0.6);
+      // split K: partial-sum atomics + the finalising pass
+      const double cost = steps + (s > 1 ? 0.25 * rounds + 1.0 : 0.0);
+      if (cost < best_cost - 1e-9) {
+        best_cost = cost;
+        best.r = r;
+        best.s = s;
+        best.slice_chunks = sc;
+        best.n_tiles = static_cast<uint32_t>(n_tiles);
+        best.grid = static_cast<uint32_t>(gs * s);
+      }
+    }
+  }
+  best.ring_off = best.slice_chunks * chunk_bytes(nt);
+  best.red_off = best.ring_off + ring_bytes(n, nt);
+  best.smem = best.red_off + red_bytes(nt, best.r);
+  return best;
+}
+
+uint32_t nt_of(uint64_t rows_x) { return static_cast<uint32_t>(rows_x / 8 + 1); }  // + ones column
+bool needs_repack(uint64_t k, const void* w) {
+  return ((k + 31) / 32) % 4 != 0 || reinterpret_cast<uintptr_t>(w) % 16 != 0;
+}
+uint64_t frag_half_bytes(uint64_t rows_x, uint64_t k) {
+  const uint64_t wpr = (k + 31) / 32;
+  const uint64_t chunks = (wpr + kChunkWords - 1) / kChunkWords;
+  const uint64_t prep_blocks = (chunks * kChunkWords + kPrepThreads - 1) / kPrepThreads;
+  return round_up(chunks * chunk_bytes(static_cast<int>(nt_of(rows_x))) +
+                  nt_of(rows_x) * 8 * prep_blocks * 4, 256);
 }
 
 }  // namespace
 
-uint32_t skinny_m_pad(uint64_t rows_x) {
-  const uint32_t nt = rows_x <= 8 ? 1u : rows_x <= 16 ? 2u : rows_x <= 32 ? 4u : 8u;
-  return nt * 8u;
+size_t skinny_acc_bytes(uint64_t rows_w, uint64_t rows_x) {
+  // tiles of 16R rows, R <= 8: rows padded to 128 cover every plan; + tile counters
+  const uint64_t rows = (rows_w + 127) / 128 * 128;
+  return rows * nt_of(rows_x) * 8 * 4 + (rows / 16 + 1) * 4;
 }
 
-size_t skinny_ws_bytes(uint64_t rows_w, uint64_t rows_x) {
-  const uint64_t blocks = (rows_w + 127) / 128;
-  return blocks * 128 * skinny_m_pad(rows_x) * 4 + blocks * 128 * 4 + blocks * 4;
+size_t skinny_scratch_bytes(uint64_t rows_w, uint64_t rows_x, uint64_t k, int n_w,
+                            const void* w_planes) {
+  size_t b = 2 * frag_half_bytes(rows_x, k);
+  if (needs_repack(k, w_planes)) b += uint64_t(n_w) * rows_w * round_up((k + 31) / 32, 4) * 4;
+  return b;
 }
 
 cudaError_t launch_skinny(const SkinnyArgs& a, cudaStream_t s) {
   SkinnyParams p{};
-  const uint32_t m_pad = skinny_m_pad(a.rows_x);
-  const int nt = static_cast<int>(m_pad / 8);
-  const uint64_t blocks = (a.rows_w + 127) / 128;
-  p.w = a.w_planes;
-  p.xc = a.codes_x;
-  p.rowsum_x = a.rowsum_x;
+  const uint32_t nt = nt_of(a.rows_x);
+  const uint32_t m_pad = nt * 8u;
   p.rows_w = static_cast<uint32_t>(a.rows_w);
   p.rows_x = static_cast<uint32_t>(a.rows_x);
   p.wpr = static_cast<uint32_t>((a.k + 31) / 32);
-  p.kpad_words = static_cast<uint32_t>(a.kpad / 32);
+  p.n_planes = static_cast<uint32_t>(a.n_w);
   p.chunks_total = (p.wpr + kChunkWords - 1) / kChunkWords;
-  // K slices: enough CTAs for ~2 per SM, but no more X restaging than needed, and the X
-  // slice must fit the shared-memory budget.
-  const uint32_t per_chunk = 4u * nt * 2u * 32u * 16u;
-  const uint32_t max_chunks_smem = kSkSmemMax / per_chunk;
-  const uint64_t want_ctas = 2ull * static_cast<uint64_t>(a.num_sms);
-  uint64_t slices = (want_ctas + blocks - 1) / blocks;
-  if (slices < 1) slices = 1;
-  if (slices > p.chunks_total) slices = p.chunks_total;
-  uint32_t cps = static_cast<uint32_t>((p.chunks_total + slices - 1) / slices);
-  if (cps > max_chunks_smem) cps = max_chunks_smem;
-  if (cps < 1) cps = 1;
-  p.chunks_per_slice = cps;
-  const uint32_t nslices = (p.chunks_total + cps - 1) / cps;
-  uint8_t* ws = static_cast<uint8_t*>(a.ws);
-  p.acc = reinterpret_cast<uint32_t*>(ws);
-  p.acc_rs = reinterpret_cast<uint32_t*>(ws + blocks * 128 * m_pad * 4);
-  p.counters = reinterpret_cast<uint32_t*>(ws + blocks * 128 * m_pad * 4 + blocks * 128 * 4);
+  const uint32_t A = (1u << a.n_w) - 1u, B = (1u << a.n_x) - 1u;
+  const bool split = a.n_w <= 4 && static_cast<double>(a.k) * A * B < 268435456.0;
+  const int kn = kernel_n(a.n_w, split);
+  const Plan pl = plan_for(a.rows_w, p.chunks_total, kn, static_cast<int>(nt), a.num_sms);
+  if (pl.grid == 0) return cudaErrorInvalidConfiguration;
+  static const bool show = std::getenv("APMM_DEBUG_PLAN") != nullptr;
+
+  // scratch: [half 0 | half 1] feature fragments + rowsum(U_x) parts, then the repack
+  uint8_t* scratch = static_cast<uint8_t*>(a.scratch_ws);
+  const uint64_t half_bytes = frag_half_bytes(a.rows_x, a.k);
+  uint8_t* xfrag = scratch + (a.ws_half ? half_bytes : 0);
+  const uint64_t frag_bytes = uint64_t(p.chunks_total) * chunk_bytes(static_cast<int>(nt));
+  int32_t* rsx = reinterpret_cast<int32_t*>(xfrag + frag_bytes);
+  const uint32_t prep_blocks = (p.chunks_total * kChunkWords + kPrepThreads - 1) / kPrepThreads;
+
+  // weights: TMA needs 16-byte row pitch and base; otherwise repack (stream-ordered copy)
+  const uint32_t* w = a.w_planes;
+  uint64_t pitch_words = p.wpr;
+  if (needs_repack(a.k, a.w_planes)) {
+    pitch_words = round_up(p.wpr, 4);
+    uint32_t* rw = reinterpret_cast<uint32_t*>(scratch + 2 * half_bytes);
+    const size_t rows = size_t(a.n_w) * a.rows_w;
+    cudaError_t e = cudaMemsetAsync(rw, 0, rows * pitch_words * 4, s);
+    if (e == cudaSuccess) {
+      e = cudaMemcpy2DAsync(rw, pitch_words * 4, a.w_planes, size_t(p.wpr) * 4, size_t(p.wpr) * 4,
+                            rows, cudaMemcpyDeviceToDevice, s);
+    }
+    if (e != cudaSuccess) return e;
+    w = rw;
+  }
+  CUtensorMap tm;
+  {
+    const uint64_t dims[3] = {p.wpr, a.rows_w, static_cast<uint64_t>(a.n_w)};
+    const uint64_t strides[2] = {pitch_words * 4, pitch_words * 4 * a.rows_w};
+    const uint32_t box[3] = {static_cast<uint32_t>(kChunkWords), 16u, static_cast<uint32_t>(a.n_w)};
+    if (encode_tmap_3d_u32(&tm, w, dims, strides, box) != CUDA_SUCCESS) return cudaErrorInvalidValue;
+  }
+  if (show) {
+    std::fprintf(stderr, "[apmm skinny] %llux%llux%llu W%dA%d: R=%u S=%u slice_chunks=%u tiles=%u "
+                 "grid=%u smem=%u split=%d repack=%d\n", (unsigned long long)a.rows_w,
+                 (unsigned long long)a.rows_x, (unsigned long long)a.k, a.n_w, a.n_x, pl.r, pl.s,
+                 pl.slice_chunks, pl.n_tiles, pl.grid, pl.smem, int(split),
+                 int(needs_repack(a.k, a.w_planes)));
+  }
+  const uint64_t rows_pad = uint64_t(pl.n_tiles) * 16u * pl.r;
+  p.acc = static_cast<uint32_t*>(a.acc_ws);
+  p.counters = p.acc + rows_pad * m_pad;
+  p.xfrag = xfrag;
+  p.rsx = rsx;
+  p.rsx_parts = prep_blocks;
+  p.rgroups = pl.r;
+  p.slices = pl.s;
+  p.slice_chunks = pl.slice_chunks;
+  p.n_tiles = pl.n_tiles;
+  p.ring_off = pl.ring_off;
+  p.red_off = pl.red_off;
   p.y = a.y;
   p.yf = a.yf;
   p.s_w = a.s_w;
   p.s_x = a.s_x;
   p.gran_w = a.gran_w;
   p.gran_x = a.gran_x;
-  const uint32_t A = (1u << a.n_w) - 1u, B = (1u << a.n_x) - 1u;
   p.coef_w = 2u * B;
   p.coef_x = 2u * A;
   p.c0 = static_cast<uint32_t>(a.k) * A * B;
-  const bool split = a.n_w <= 4 && static_cast<double>(a.k) * A * B < 268435456.0;
-  const bool vec = (p.wpr % 4u) == 0u && (reinterpret_cast<uintptr_t>(a.w_planes) % 16u) == 0u;
-  const dim3 grid(static_cast<unsigned>(blocks), nslices);
-  const uint32_t smem = cps * per_chunk;
+  p.m2 = 2u;
+  p.m4 = 4u;
+  p.m16 = 16u;
+  p.neg1 = 0xFFFFFFFFu;
+
+  {  // feature prep (same shared-memory carveout as the streaming kernel: no reconfig)
+    static bool carve_set = false;
+    if (!carve_set) {
+      cudaFuncSetAttribute(prep_x_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+      carve_set = true;
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(prep_blocks, m_pad);
+    cfg.blockDim = dim3(kPrepThreads);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, prep_x_kernel, a.x_planes, p.rows_x, p.wpr, a.n_x,
+                                       p.chunks_total * kChunkWords, nt, xfrag, rsx);
+    if (e != cudaSuccess) return e;
+  }
   switch (nt) {
-    case 1: return dispatch_nt<1>(a.n_w, split, vec, p, grid, smem, s);
-    case 2: return dispatch_nt<2>(a.n_w, split, vec, p, grid, smem, s);
-    case 4: return dispatch_nt<4>(a.n_w, split, vec, p, grid, smem, s);
-    default: return dispatch_nt<8>(a.n_w, split, vec, p, grid, smem, s);
+    case 1: return dispatch_n<1>(a.n_w, split, tm, p, pl.grid, pl.smem, s);
+    case 2: return dispatch_n<2>(a.n_w, split, tm, p, pl.grid, pl.smem, s);
+    case 3: return dispatch_n<3>(a.n_w, split, tm, p, pl.grid, pl.smem, s);
+    case 4: return dispatch_n<4>(a.n_w, split, tm, p, pl.grid, pl.smem, s);
+    case 5: return dispatch_n<5>(a.n_w, split, tm, p, pl.grid, pl.smem, s);
+    case 6: return dispatch_n<6>(a.n_w, split, tm, p, pl.grid, pl.smem, s);
+    case 7: return dispatch_n<7>(a.n_w, split, tm, p, pl.grid, pl.smem, s);
+    default: return dispatch_n<8>(a.n_w, split, tm, p, pl.grid, pl.smem, s);
   }
 }
 
