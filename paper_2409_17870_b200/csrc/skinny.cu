@@ -57,33 +57,36 @@ namespace apmm_b200 {
 namespace {
 
 constexpr int kChunkWords = 16;  // 512 columns per warp step
-constexpr uint32_t kSkSmem = 224u * 1024u;  // dynamic budget (227 KB opt-in max minus static)
+constexpr uint32_t kSkSmemSM = 224u * 1024u;  // dynamic budget per SM (227 KB max minus static)
 constexpr int kPrepThreads = 256;
 
-// 16 warps where the register budget allows, else 8.
+// One persistent CTA per SM: 16 warps where registers allow, else 8. (Two smaller CTAs per
+// SM were measured slower: the halved shared memory forces more K slices, and the split-K
+// finalisation tail costs more than the earlier start of the next call gains.)
 __host__ __device__ constexpr int sk_threads(int n, int nt) { return (n <= 3 && nt <= 4) ? 512 : 256; }
-// Per-warp TMA ring: a slot holds one work item, n planes x 16 rows x 64 B = n KB. Depth
-// chosen for ~130 KB of weight planes in flight per SM.
-__host__ __device__ constexpr int sk_stages(int n, int nt) {
-  return sk_threads(n, nt) == 512 ? (n == 1 ? 8 : n == 2 ? 4 : 3)
-                                  : (n == 1 ? 16 : n == 2 ? 8 : n == 3 ? 6 : n == 4 ? 4 : 2);
+__host__ __device__ constexpr int sk_ctas_per_sm(int, int) { return 1; }
+__host__ __device__ constexpr uint32_t sk_smem_budget(int n, int nt) {
+  return kSkSmemSM / sk_ctas_per_sm(n, nt);
 }
+// Per-warp TMA ring: a slot holds one work item, n planes x 16 rows x 64 B = n KB. The
+// depth (2..kMaxStages) is chosen at launch from the shared memory the X slice leaves.
+constexpr int kMaxStages = 16;
 __host__ __device__ constexpr uint32_t slot_bytes(int n) { return static_cast<uint32_t>(n) * 1024u; }
-__host__ __device__ constexpr uint32_t ring_bytes(int n, int nt) {
-  return static_cast<uint32_t>(sk_threads(n, nt) / 32 * sk_stages(n, nt)) * slot_bytes(n);
-}
-// Shared-memory X layout per 512-column chunk: [w 0..3][nt][half 0..1][lane 0..31] x 16 B.
-// Lane (g, t) of n-tile nt, word w, half h holds code registers [4h, 4h+4) of feature row
-// nt*8+g, word 16*chunk + 4t + w (register r, byte B = code of column 8B + r).
-__host__ __device__ constexpr uint32_t chunk_bytes(int nt) { return 4u * nt * 2u * 32u * 16u; }
+// Shared-memory X layout per 512-column chunk, real feature rows only (M = rows_x):
+// [w 0..3][half 0..1][feature row 0..M-1][t 0..3] x 16 B. Thread (g, t) of n-tile nt
+// takes feature row nt*8+g, word 16*chunk + 4t + w, code registers [4h, 4h+4) (register
+// r, byte B = code of column 8B + r). A warp's 128-bit reads are 512 contiguous bytes.
+// Rows >= M are zero codes and the all-ones column (slot 8*NT-1) is a register constant.
+__host__ __device__ constexpr uint32_t chunk_bytes_m(uint32_t m) { return 512u * m; }
 // cross-warp reduction buffer: [16 R][m_pad] u32, R <= 8
 __host__ __device__ constexpr uint32_t red_bytes(int nt, uint32_t r) { return 16u * r * nt * 8u * 4u; }
 
 struct SkinnyParams {
-  const uint8_t* xfrag;      // prep output: [chunks_total][chunk_bytes(NT)]
+  const uint8_t* xfrag;      // prep output: [chunks_total][chunk_bytes_m(rows_x)]
   const int32_t* rsx;        // prep output: rowsum(U_x) parts [rows_x][rsx_parts]
   uint32_t rsx_parts;
   uint32_t rows_w, rows_x, wpr, n_planes;
+  uint32_t stages;           // per-warp ring depth (2..kMaxStages)
   uint32_t chunks_total;     // ceil(wpr / 16)
   uint32_t slices, slice_chunks;
   uint32_t rgroups;          // R: 16-row groups per tile (warps_k = warps / R)
@@ -99,7 +102,14 @@ struct SkinnyParams {
   uint32_t coef_w, coef_x, c0;
   // multipliers kept in the parameter bank so ptxas emits IMAD (FMA pipe), not SHF/IADD
   uint32_t m2, m4, m16, neg1;
+  unsigned long long* ts;    // APMM_SKINNY_TS=1 (dev only): per-CTA phase timestamps, else null
 };
+
+APMM_DEV unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 APMM_DEV void mma_u8(uint32_t (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
                      uint32_t b0, uint32_t b1) {
@@ -186,44 +196,34 @@ APMM_DEV void transpose8(uint32_t (&x)[8]) {
   for (int i = 0; i < 8; i += 2) sw(x[i], x[i + 1], 1, 0x55555555u);
 }
 
-// ---- feature prep: X planes -> fragment-order codes, ones column, rowsum(U_x) ----------
-// grid (ceil(chunks_total*16 / 256), m_pad); thread = (feature slot, 32-column word).
-// Slot m_pad-1 (always >= rows_x) is the all-ones column whose MMA output is rowsum(U_w).
+// ---- feature prep: X planes -> fragment-order codes + rowsum(U_x) -----------------------
+// grid (ceil(chunks_total*16 / 256), rows_x); thread = (feature row, 32-column word).
 // PDL: reads only the caller's X planes before griddepcontrol.wait; writes its workspace
 // half (last read by the call before the previous one, complete by construction) and
 // completes only after the previous kernel in the stream, like the expand kernel.
 __global__ void __launch_bounds__(kPrepThreads) prep_x_kernel(const uint32_t* __restrict__ x,
                                                               uint32_t rows_x, uint32_t wpr,
                                                               int n_x, uint32_t words_pad,
-                                                              uint32_t nt_count,
                                                               uint8_t* __restrict__ xfrag,
                                                               int32_t* __restrict__ rsx_part) {
   apmm_ptx::pdl_trigger();
   const uint32_t tok = blockIdx.y, W = blockIdx.x * kPrepThreads + threadIdx.x;
-  const uint32_t m_pad = nt_count * 8u;
   uint32_t v[8];
   int32_t rs = 0;
-  if (tok < rows_x) {
-    const uint64_t pstride = uint64_t(rows_x) * wpr;
+  const uint64_t pstride = uint64_t(rows_x) * wpr;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      v[i] = (i < n_x && W < wpr) ? __ldg(x + i * pstride + uint64_t(tok) * wpr + W) : 0u;
-      if (i < n_x) rs += __popc(v[i]) << i;
-    }
-    transpose8(v);
-  } else {
-    const uint32_t fill = (tok == m_pad - 1) ? 0x01010101u : 0u;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) v[i] = fill;
+  for (int i = 0; i < 8; ++i) {
+    v[i] = (i < n_x && W < wpr) ? __ldg(x + i * pstride + uint64_t(tok) * wpr + W) : 0u;
+    if (i < n_x) rs += __popc(v[i]) << i;
   }
+  transpose8(v);
   apmm_ptx::pdl_wait();  // the workspace half may be written only now
   if (W < words_pad) {
     const uint32_t cl = W / kChunkWords, t = (W % kChunkWords) >> 2, w = W & 3u;
-    const uint32_t nt = tok >> 3, g = tok & 7u;
-    uint4* dst = reinterpret_cast<uint4*>(xfrag + uint64_t(cl) * chunk_bytes(nt_count)) +
-                 ((w * nt_count + nt) * 2u) * 32u + g * 4u + t;
+    uint4* dst = reinterpret_cast<uint4*>(xfrag + uint64_t(cl) * chunk_bytes_m(rows_x)) +
+                 ((w * 2u) * rows_x + tok) * 4u + t;
     dst[0] = make_uint4(v[0], v[1], v[2], v[3]);
-    dst[32] = make_uint4(v[4], v[5], v[6], v[7]);
+    dst[rows_x * 4u] = make_uint4(v[4], v[5], v[6], v[7]);
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) rs += __shfl_xor_sync(0xffffffffu, rs, o);
@@ -238,22 +238,22 @@ __global__ void __launch_bounds__(kPrepThreads) prep_x_kernel(const uint32_t* __
 }
 
 template <int N, int NT, bool SPLIT>
-__global__ void __launch_bounds__(sk_threads(N, NT), 1)
+__global__ void __launch_bounds__(sk_threads(N, NT), sk_ctas_per_sm(N, NT))
     skinny_kernel(const __grid_constant__ CUtensorMap tmap_w, const SkinnyParams p) {
   constexpr int THREADS = sk_threads(N, NT);
   constexpr int WARPS = THREADS / 32;
-  constexpr int STAGES = sk_stages(N, NT);
   constexpr uint32_t SLOT = slot_bytes(N);
   constexpr uint32_t M_PAD = NT * 8u;
   constexpr uint32_t ONES = M_PAD - 1u;  // the all-ones feature column -> rowsum(U_w)
   extern __shared__ __align__(128) uint8_t smem[];
-  __shared__ __align__(8) uint64_t full_bar[WARPS * STAGES];
+  __shared__ __align__(8) uint64_t full_bar[WARPS * kMaxStages];
   __shared__ __align__(8) uint64_t xbar;
   __shared__ uint32_t rsx_s[M_PAD];
   __shared__ uint32_t s_last;
 
   const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t g = lane >> 2, t = lane & 3;
+  if (p.ts && tid == 0) p.ts[blockIdx.x * 8 + 0] = gtime();
   const uint32_t warps_k = WARPS / p.rgroups;
   const uint32_t wr = warp / warps_k, wk = warp % warps_k;
   const uint32_t tile_rows = 16u * p.rgroups;
@@ -267,12 +267,14 @@ __global__ void __launch_bounds__(sk_threads(N, NT), 1)
   const uint32_t my_tiles = j0 < p.n_tiles ? (p.n_tiles - j0 + gs - 1) / gs : 0u;
 
   uint8_t* xs = smem;
-  const uint32_t ring = apmm_ptx::smem_u32(smem + p.ring_off) + warp * (STAGES * SLOT);
+  const uint32_t stages = p.stages;
+  const uint32_t ring = apmm_ptx::smem_u32(smem + p.ring_off) + warp * (stages * SLOT);
   uint32_t* red = reinterpret_cast<uint32_t*>(smem + p.red_off);  // [tile_rows][M_PAD]
-  uint64_t* bars = full_bar + warp * STAGES;
+  uint64_t* bars = full_bar + warp * kMaxStages;
+  const uint32_t xchunk_bytes = chunk_bytes_m(p.rows_x);
 
   if (lane == 0) {
-    for (int s = 0; s < STAGES; ++s) apmm_ptx::mbar_init(&bars[s], 1);
+    for (uint32_t s = 0; s < stages; ++s) apmm_ptx::mbar_init(&bars[s], 1);
     if (warp == 0) apmm_ptx::mbar_init(&xbar, 1);
     apmm_ptx::fence_mbar_init();
     apmm_ptx::tma_prefetch_desc(&tmap_w);
@@ -293,19 +295,19 @@ __global__ void __launch_bounds__(sk_threads(N, NT), 1)
       }
       if (++is_c == cpw) { is_c = 0; ++is_tile; }
     }
-    if (++is_slot == STAGES) is_slot = 0;
+    if (++is_slot == stages) is_slot = 0;
   };
 
   // The weight planes are inputs of this call, so their loads may overlap the prep kernel
   // still running ahead of us (PDL); X, the workspace and Y only after pdl_wait.
-#pragma unroll
-  for (int s = 0; s < STAGES - 1; ++s) issue();
+  for (uint32_t s = 0; s + 1 < stages; ++s) issue();
   apmm_ptx::pdl_wait();
+  if (p.ts && tid == 0) p.ts[blockIdx.x * 8 + 1] = gtime();
   __syncthreads();  // xbar initialised
-  const uint32_t xbytes = (s_end > s_begin ? s_end - s_begin : 0u) * chunk_bytes(NT);
+  const uint32_t xbytes = (s_end > s_begin ? s_end - s_begin : 0u) * xchunk_bytes;
   if (tid == 0) {
     apmm_ptx::mbar_arrive_expect_tx(&xbar, xbytes);
-    const uint8_t* src = p.xfrag + uint64_t(s_begin) * chunk_bytes(NT);
+    const uint8_t* src = p.xfrag + uint64_t(s_begin) * xchunk_bytes;
     for (uint32_t off = 0; off < xbytes; off += 32768u) {
       bulk_g2s(apmm_ptx::smem_u32(xs + off), src + off, min(32768u, xbytes - off),
                apmm_ptx::smem_u32(&xbar));
@@ -322,6 +324,7 @@ __global__ void __launch_bounds__(sk_threads(N, NT), 1)
   for (uint32_t q = tid; q < tile_rows * M_PAD; q += THREADS) red[q] = 0u;
   apmm_ptx::mbar_wait(&xbar, 0);
   __syncthreads();
+  if (p.ts && tid == 0) p.ts[blockIdx.x * 8 + 2] = gtime();
   const uint32_t cterm = slice == 0 ? p.c0 : 0u;
 
   uint32_t lo[NT][4], hi[NT][4];
@@ -341,7 +344,7 @@ __global__ void __launch_bounds__(sk_threads(N, NT), 1)
         apmm_ptx::mbar_wait(&bars[cs_slot], (phase_bits >> cs_slot) & 1u);
         phase_bits ^= 1u << cs_slot;
         // slot layout (TMA box {16 words, 16 rows, planes}): [plane][row][16 words]
-        const uint8_t* slot = smem + p.ring_off + (warp * STAGES + cs_slot) * SLOT + g * 64u + t * 16u;
+        const uint8_t* slot = smem + p.ring_off + (warp * stages + cs_slot) * SLOT + g * 64u + t * 16u;
         uint4 wa[N], wb[N];
 #pragma unroll
         for (int pl = 0; pl < N; ++pl) {
@@ -349,7 +352,8 @@ __global__ void __launch_bounds__(sk_threads(N, NT), 1)
           wa[pl] = live ? *reinterpret_cast<const uint4*>(slot + pl * 1024) : make_uint4(0, 0, 0, 0);
           wb[pl] = live ? *reinterpret_cast<const uint4*>(slot + pl * 1024 + 512) : make_uint4(0, 0, 0, 0);
         }
-        const uint4* xchunk = reinterpret_cast<const uint4*>(xs + (chunk - s_begin) * chunk_bytes(NT));
+        const uint4* xchunk = reinterpret_cast<const uint4*>(xs + (chunk - s_begin) * xchunk_bytes);
+        const uint32_t m4 = p.rows_x * 4u;
 #pragma unroll
         for (int w = 0; w < 4; ++w) {
           uint32_t xa[8], xb[8], ca[8], cb[8];
@@ -368,8 +372,15 @@ __global__ void __launch_bounds__(sk_threads(N, NT), 1)
           codes_of_word<N, SPLIT>(xb, cb, p);
 #pragma unroll
           for (int nt = 0; nt < NT; ++nt) {
-            const uint4 x0 = xchunk[((w * NT + nt) * 2 + 0) * 32 + lane];
-            const uint4 x1 = xchunk[((w * NT + nt) * 2 + 1) * 32 + lane];
+            const uint32_t tok = nt * 8u + g;
+            uint4 x0, x1;
+            if (tok < p.rows_x) {
+              x0 = xchunk[(w * 2u + 0u) * m4 + tok * 4u + t];
+              x1 = xchunk[(w * 2u + 1u) * m4 + tok * 4u + t];
+            } else {  // zero codes, or the all-ones column (slot ONES) -> rowsum(U_w)
+              const uint32_t f = tok == ONES ? 0x01010101u : 0u;
+              x0 = x1 = make_uint4(f, f, f, f);
+            }
             mma_u8(lo[nt], ca[0], cb[0], ca[1], cb[1], x0.x, x0.y);
             mma_u8(lo[nt], ca[2], cb[2], ca[3], cb[3], x0.z, x0.w);
             if (SPLIT) {
@@ -382,8 +393,10 @@ __global__ void __launch_bounds__(sk_threads(N, NT), 1)
           }
         }
       }
-      if (++cs_slot == STAGES) cs_slot = 0;
+      if (++cs_slot == stages) cs_slot = 0;
+      if (p.ts && tid == 0 && ti == 0 && c == 0) p.ts[blockIdx.x * 8 + 3] = gtime();
     }
+    if (p.ts && tid == 0 && ti == 0) p.ts[blockIdx.x * 8 + 4] = gtime();
 
     // ---------------- end of tile: combine the K groups, epilogue ----------------
     if (ti + 1 == my_tiles) apmm_ptx::pdl_trigger();  // last tile: the next call may start
@@ -452,6 +465,7 @@ __global__ void __launch_bounds__(sk_threads(N, NT), 1)
     // s_last is next written after the next tile's first barrier
   }
   if (my_tiles == 0) apmm_ptx::pdl_trigger();
+  if (p.ts && tid == 0) p.ts[blockIdx.x * 8 + 5] = gtime();
 }
 
 template <int N, int NT, bool SPLIT>
@@ -462,7 +476,7 @@ cudaError_t launch_t(const CUtensorMap& tm, const SkinnyParams& p, unsigned grid
   cudaError_t e;
   if (!attr_set) {
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(kSkSmem));
+                             static_cast<int>(sk_smem_budget(N, NT)));
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
@@ -504,29 +518,40 @@ cudaError_t dispatch_n(int n_w, bool split, const CUtensorMap& tm, const SkinnyP
 // (ceil(slice_chunks / warps_k) + per-tile epilogue cost), plus a charge for the split-K
 // atomics, subject to the X slice fitting shared memory.
 struct Plan {
-  uint32_t r, s, slice_chunks, n_tiles, grid, smem, ring_off, red_off;
+  uint32_t r, s, slice_chunks, n_tiles, grid, smem, ring_off, red_off, stages;
 };
 
-Plan plan_for(uint64_t rows_w, uint32_t chunks, int n, int nt, int num_sms) {
+// Work plan: R (16-row groups per tile), S (K slices), ring depth, grid. The cost counts a
+// warp's critical path in item steps (one item = 16 rows x 512 columns): the compute,
+// ceil(tiles / CTAs per slice) * (ceil(slice_chunks / warps_k) + epilogue), plus memory
+// round trips, ceil(items / items in flight) * ~3 steps, plus the split-K atomics. The X
+// slice, the ring and the reduction buffer share the CTA's shared memory.
+Plan plan_for(uint64_t rows_w, uint64_t rows_x, uint32_t chunks, int n, int nt, int num_sms) {
   const uint32_t warps = static_cast<uint32_t>(sk_threads(n, nt) / 32);
+  const uint32_t stage_all = warps * slot_bytes(n);  // one ring stage of every warp
+  const uint32_t budget = sk_smem_budget(n, nt);
+  const uint32_t ctas = static_cast<uint32_t>(num_sms * sk_ctas_per_sm(n, nt));
   Plan best{};
   double best_cost = 1e30;
   for (uint32_t r = 1; r <= 8 && r <= warps; r <<= 1) {
-    const uint32_t fixed = ring_bytes(n, nt) + red_bytes(nt, r);
-    const uint32_t max_slice = fixed < kSkSmem ? (kSkSmem - fixed) / chunk_bytes(nt) : 0u;
     const uint32_t warps_k = warps / r;
     const uint64_t n_tiles = (rows_w + 16 * r - 1) / (16 * r);
     for (uint32_t s = 1; s <= chunks; ++s) {
       const uint32_t sc = (chunks + s - 1) / s;
-      if (sc > max_slice) continue;
       if ((chunks + sc - 1) / sc != s) continue;  // same plan as a smaller s
-      const uint32_t per_slice = static_cast<uint32_t>(num_sms) / s;
+      const uint32_t used = sc * chunk_bytes_m(static_cast<uint32_t>(rows_x)) + red_bytes(nt, r);
+      if (used + 2 * stage_all + 1024u > budget) continue;  // 1 KB: ring alignment
+      uint32_t stages = (budget - used - 1024u) / stage_all;
+      if (stages > kMaxStages) stages = kMaxStages;
+      const uint32_t per_slice = ctas / s;
       if (per_slice == 0) break;
       const uint64_t gs = n_tiles < per_slice ? n_tiles : per_slice;
-      const double rounds = static_cast<double>((n_tiles + gs - 1) / gs);
-      const double steps = rounds * ((sc + warps_k - 1) / warps_k + 0.6);
-      // split K: partial-sum atomics + the finalising pass
-      const double cost = steps + (s > 1 ? 0.25 * rounds + 1.0 : 0.0);
+      const uint64_t rounds = (n_tiles + gs - 1) / gs;
+      const uint32_t cpw = (sc + warps_k - 1) / warps_k;
+      const double items = static_cast<double>(rounds * cpw);
+      const double trips = static_cast<double>((rounds * cpw + stages - 2) / (stages - 1));
+      const double cost = static_cast<double>(rounds) * (cpw + 0.6) + 3.0 * trips +
+                          (s > 1 ? 0.25 * rounds + 1.0 : 0.0) + 0.0 * items;
       if (cost < best_cost - 1e-9) {
         best_cost = cost;
         best.r = r;
@@ -534,11 +559,13 @@ Plan plan_for(uint64_t rows_w, uint32_t chunks, int n, int nt, int num_sms) {
         best.slice_chunks = sc;
         best.n_tiles = static_cast<uint32_t>(n_tiles);
         best.grid = static_cast<uint32_t>(gs * s);
+        best.stages = stages;
       }
     }
   }
-  best.ring_off = best.slice_chunks * chunk_bytes(nt);
-  best.red_off = best.ring_off + ring_bytes(n, nt);
+  best.ring_off = best.slice_chunks * chunk_bytes_m(static_cast<uint32_t>(rows_x));
+  best.ring_off = (best.ring_off + 1023u) & ~1023u;
+  best.red_off = best.ring_off + best.stages * stage_all;
   best.smem = best.red_off + red_bytes(nt, best.r);
   return best;
 }
@@ -551,8 +578,8 @@ uint64_t frag_half_bytes(uint64_t rows_x, uint64_t k) {
   const uint64_t wpr = (k + 31) / 32;
   const uint64_t chunks = (wpr + kChunkWords - 1) / kChunkWords;
   const uint64_t prep_blocks = (chunks * kChunkWords + kPrepThreads - 1) / kPrepThreads;
-  return round_up(chunks * chunk_bytes(static_cast<int>(nt_of(rows_x))) +
-                  nt_of(rows_x) * 8 * prep_blocks * 4, 256);
+  return round_up(chunks * chunk_bytes_m(static_cast<uint32_t>(rows_x)) +
+                  rows_x * prep_blocks * 4, 256);
 }
 
 }  // namespace
@@ -582,7 +609,7 @@ cudaError_t launch_skinny(const SkinnyArgs& a, cudaStream_t s) {
   const uint32_t A = (1u << a.n_w) - 1u, B = (1u << a.n_x) - 1u;
   const bool split = a.n_w <= 4 && static_cast<double>(a.k) * A * B < 268435456.0;
   const int kn = kernel_n(a.n_w, split);
-  const Plan pl = plan_for(a.rows_w, p.chunks_total, kn, static_cast<int>(nt), a.num_sms);
+  const Plan pl = plan_for(a.rows_w, a.rows_x, p.chunks_total, kn, static_cast<int>(nt), a.num_sms);
   if (pl.grid == 0) return cudaErrorInvalidConfiguration;
   static const bool show = std::getenv("APMM_DEBUG_PLAN") != nullptr;
 
@@ -590,7 +617,7 @@ cudaError_t launch_skinny(const SkinnyArgs& a, cudaStream_t s) {
   uint8_t* scratch = static_cast<uint8_t*>(a.scratch_ws);
   const uint64_t half_bytes = frag_half_bytes(a.rows_x, a.k);
   uint8_t* xfrag = scratch + (a.ws_half ? half_bytes : 0);
-  const uint64_t frag_bytes = uint64_t(p.chunks_total) * chunk_bytes(static_cast<int>(nt));
+  const uint64_t frag_bytes = uint64_t(p.chunks_total) * chunk_bytes_m(p.rows_x);
   int32_t* rsx = reinterpret_cast<int32_t*>(xfrag + frag_bytes);
   const uint32_t prep_blocks = (p.chunks_total * kChunkWords + kPrepThreads - 1) / kPrepThreads;
 
@@ -618,9 +645,9 @@ cudaError_t launch_skinny(const SkinnyArgs& a, cudaStream_t s) {
   }
   if (show) {
     std::fprintf(stderr, "[apmm skinny] %llux%llux%llu W%dA%d: R=%u S=%u slice_chunks=%u tiles=%u "
-                 "grid=%u smem=%u split=%d repack=%d\n", (unsigned long long)a.rows_w,
+                 "grid=%u smem=%u stages=%u split=%d repack=%d\n", (unsigned long long)a.rows_w,
                  (unsigned long long)a.rows_x, (unsigned long long)a.k, a.n_w, a.n_x, pl.r, pl.s,
-                 pl.slice_chunks, pl.n_tiles, pl.grid, pl.smem, int(split),
+                 pl.slice_chunks, pl.n_tiles, pl.grid, pl.smem, pl.stages, int(split),
                  int(needs_repack(a.k, a.w_planes)));
   }
   const uint64_t rows_pad = uint64_t(pl.n_tiles) * 16u * pl.r;
@@ -630,6 +657,7 @@ cudaError_t launch_skinny(const SkinnyArgs& a, cudaStream_t s) {
   p.rsx = rsx;
   p.rsx_parts = prep_blocks;
   p.rgroups = pl.r;
+  p.stages = pl.stages;
   p.slices = pl.s;
   p.slice_chunks = pl.slice_chunks;
   p.n_tiles = pl.n_tiles;
@@ -648,6 +676,13 @@ cudaError_t launch_skinny(const SkinnyArgs& a, cudaStream_t s) {
   p.m4 = 4u;
   p.m16 = 16u;
   p.neg1 = 0xFFFFFFFFu;
+  static const bool want_ts = std::getenv("APMM_SKINNY_TS") != nullptr;
+  static unsigned long long* ts_buf = nullptr;
+  if (want_ts) {
+    if (!ts_buf) cudaMalloc(&ts_buf, 1024 * 8 * sizeof(unsigned long long));
+    cudaMemsetAsync(ts_buf, 0, 1024 * 8 * sizeof(unsigned long long), s);
+    p.ts = ts_buf;
+  }
 
   {  // feature prep (same shared-memory carveout as the streaming kernel: no reconfig)
     static bool carve_set = false;
@@ -656,7 +691,7 @@ cudaError_t launch_skinny(const SkinnyArgs& a, cudaStream_t s) {
       carve_set = true;
     }
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(prep_blocks, m_pad);
+    cfg.gridDim = dim3(prep_blocks, p.rows_x);
     cfg.blockDim = dim3(kPrepThreads);
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
@@ -665,9 +700,43 @@ cudaError_t launch_skinny(const SkinnyArgs& a, cudaStream_t s) {
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     cudaError_t e = cudaLaunchKernelEx(&cfg, prep_x_kernel, a.x_planes, p.rows_x, p.wpr, a.n_x,
-                                       p.chunks_total * kChunkWords, nt, xfrag, rsx);
+                                       p.chunks_total * kChunkWords, xfrag, rsx);
     if (e != cudaSuccess) return e;
   }
+  cudaError_t res;
+  switch (nt) {
+    case 1: res = dispatch_n<1>(a.n_w, split, tm, p, pl.grid, pl.smem, s); break;
+    case 2: res = dispatch_n<2>(a.n_w, split, tm, p, pl.grid, pl.smem, s); break;
+    case 3: res = dispatch_n<3>(a.n_w, split, tm, p, pl.grid, pl.smem, s); break;
+    case 4: res = dispatch_n<4>(a.n_w, split, tm, p, pl.grid, pl.smem, s); break;
+    case 5: res = dispatch_n<5>(a.n_w, split, tm, p, pl.grid, pl.smem, s); break;
+    case 6: res = dispatch_n<6>(a.n_w, split, tm, p, pl.grid, pl.smem, s); break;
+    case 7: res = dispatch_n<7>(a.n_w, split, tm, p, pl.grid, pl.smem, s); break;
+    default: res = dispatch_n<8>(a.n_w, split, tm, p, pl.grid, pl.smem, s); break;
+  }
+  if (want_ts && res == cudaSuccess) {  // dev only: per-phase CTA timeline (us from first start)
+    unsigned long long h[1024 * 8];
+    cudaStreamSynchronize(s);
+    cudaMemcpy(h, ts_buf, pl.grid * 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+    unsigned long long t0 = ~0ull;
+    for (uint32_t b = 0; b < pl.grid; ++b) t0 = h[b * 8] && h[b * 8] < t0 ? h[b * 8] : t0;
+    const char* names[6] = {"start", "pdl_wait", "x_ready", "item0", "tile0", "end"};
+    for (int k = 0; k < 6; ++k) {
+      double mn = 1e30, mx = 0, sum = 0;
+      uint32_t cnt = 0;
+      for (uint32_t b = 0; b < pl.grid; ++b) {
+        if (!h[b * 8 + k]) continue;
+        const double v = (h[b * 8 + k] - t0) * 1e-3;
+        mn = v < mn ? v : mn;
+        mx = v > mx ? v : mx;
+        sum += v;
+        ++cnt;
+      }
+      std::fprintf(stderr, "[apmm skinny ts] %-8s min %7.2f avg %7.2f max %7.2f us (%u CTAs)\n",
+                   names[k], cnt ? mn : 0.0, cnt ? sum / cnt : 0.0, mx, cnt);
+    }
+  }
+  return res;
   switch (nt) {
     case 1: return dispatch_n<1>(a.n_w, split, tm, p, pl.grid, pl.smem, s);
     case 2: return dispatch_n<2>(a.n_w, split, tm, p, pl.grid, pl.smem, s);
