@@ -21,6 +21,8 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 
 #include "internal.h"
 #include "ptx.cuh"
@@ -39,6 +41,7 @@ constexpr int kEpiBuf = 32 * 32 * 4;         // one 32x32 x 4B staging tile
 constexpr uint32_t kTmemCols = 512;
 constexpr int kSmemBytes = kStages * kStageBytes + 4 * 2 * kEpiBuf + 1024 + 256;
 constexpr uint32_t kIdesc = idesc_i8_u8u8(2 * kHalf, kPairN);
+constexpr uint32_t kIdescHalf = idesc_i8_u8u8(2 * kHalf, kPairN / 2);
 
 struct Params {
   const int32_t* rowsum_w;
@@ -53,6 +56,8 @@ struct Params {
   uint32_t tiles_m, tiles_n;
   uint32_t coef_w, coef_x, c0;
   uint32_t tma_store;  // 1: epilogue stores through tmap_y
+  uint32_t n_full;     // tiles [0, n_full) are 256 x 256; the remaining full tiles of the
+                       // last partial wave run as two 256 x 128 halves each (CL == 2 only)
   unsigned long long* dbg;  // optional wait-cycle counters (APMM_DEBUG_WAITS), else null
 };
 
@@ -60,9 +65,27 @@ __device__ __forceinline__ uint32_t dequant_bits(uint32_t v, double sw, double s
   return __float_as_uint(static_cast<float>(__dmul_rn(__dmul_rn(double(int(v)), sw), sx)));
 }
 
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+// CL = 2: one CTA pair per cluster. CL = 4: two pairs per cluster computing vertically
+// adjacent tiles (W rows tm and tm+1, same X rows): each X half is loaded once per cluster
+// and multicast into both pairs (CTA q and q+2), cutting the L2 -> SMEM bytes per MAC by
+// a quarter; a stage is released only when both pairs' MMAs have consumed it.
+// Tile t of the persistent schedule: W row tile (256 rows), first X row, and X row count.
+// Wave-quantization fix: with T full tiles on P pairs, the r = T mod P tiles of the last
+// partial wave (r <= P/2) are split into 2r half-width tiles, so that wave costs half.
+struct TileInfo {
+  uint32_t tm, col0, ncols;
+};
+__device__ __forceinline__ TileInfo tile_info(uint32_t t, uint32_t tiles_m, uint32_t n_full) {
+  if (t < n_full) return {t % tiles_m, (t / tiles_m) * kPairN, kPairN};
+  const uint32_t h = t - n_full, f = n_full + (h >> 1);
+  return {f % tiles_m, (f / tiles_m) * kPairN + (h & 1u) * (kPairN / 2), kPairN / 2};
+}
+
+template <int CL>
+__global__ void __launch_bounds__(kThreads, 1)
     gemm_u8_pair_kernel(const __grid_constant__ CUtensorMap tmap_w,
                         const __grid_constant__ CUtensorMap tmap_x,
+                        const __grid_constant__ CUtensorMap tmap_x64,
                         const __grid_constant__ CUtensorMap tmap_y, const Params p) {
   extern __shared__ uint8_t smem_raw[];
   const uint32_t base_u32 = smem_u32(smem_raw);
@@ -78,18 +101,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
   const uint32_t rank = cluster_ctarank();
-  const bool leader = rank == 0;
-  const uint32_t cluster = blockIdx.x >> 1;
-  const uint32_t nclusters = gridDim.x >> 1;
-  const uint32_t num_tiles = p.tiles_m * p.tiles_n;
+  const uint32_t q = rank & 1u;              // role within the pair (0 = MMA leader)
+  const uint32_t pr = rank >> 1;             // pair index within the cluster
+  const uint32_t lead_rank = rank & ~1u;     // my pair's leader
+  const bool leader = q == 0;
+  const uint32_t cluster = blockIdx.x / CL;
+  const uint32_t nclusters = gridDim.x / CL;
+  constexpr uint32_t kPairs = CL / 2;
+  const uint32_t tiles_mc = (p.tiles_m + kPairs - 1) / kPairs;  // cluster tiles along W rows
+  const uint32_t num_tiles =
+      CL == 2 ? p.n_full + 2 * (p.tiles_m * p.tiles_n - p.n_full) : tiles_mc * p.tiles_n;
+  constexpr uint16_t kAllMask = static_cast<uint16_t>((1u << CL) - 1u);
+  const uint16_t pair_mask = static_cast<uint16_t>(0x3u << (2u * pr));
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmap_w);
     tma_prefetch_desc(&tmap_x);
+    if (CL == 2) tma_prefetch_desc(&tmap_x64);
     if (p.tma_store) tma_prefetch_desc(&tmap_y);
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full_bar[s], 1);
-      mbar_init(&empty_bar[s], 1);
+      mbar_init(&empty_bar[s], kPairs);  // one MMA commit per pair
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tmem_full[s], 1);
@@ -115,16 +147,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const uint64_t hint = policy_evict_last();
       uint32_t stage = 0, phase = 0;
       for (uint32_t t = cluster; t < num_tiles; t += nclusters) {
-        const uint32_t tm = t % p.tiles_m, tn = t / p.tiles_m;
+        const TileInfo ti = CL == 2 ? tile_info(t, p.tiles_m, p.n_full)
+                                    : TileInfo{(t % tiles_mc) * kPairs + pr, (t / tiles_mc) * kPairN, kPairN};
+        const uint32_t tm = ti.tm;
+        const bool half = ti.ncols != kPairN;
         for (uint32_t kb = 0; kb < p.kblocks; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
-          if (leader) mbar_arrive_expect_tx(&full_bar[stage], 2 * kStageBytes);
-          const uint32_t fb = mapa(smem_u32(&full_bar[stage]), 0);
+          if (leader) mbar_arrive_expect_tx(&full_bar[stage], half ? 3 * kAS : 2 * kStageBytes);
+          const uint32_t fb = mapa(smem_u32(&full_bar[stage]), lead_rank);
           uint8_t* st = stages + stage * kStageBytes;
-          tma_load_2d_pair(st, &tmap_w, fb, int32_t(kb * kBK), int32_t(tm * 2 * kHalf + rank * kHalf),
+          tma_load_2d_pair(st, &tmap_w, fb, int32_t(kb * kBK), int32_t(tm * 2 * kHalf + q * kHalf),
                            hint);
-          tma_load_2d_pair(st + kAS, &tmap_x, fb, int32_t(kb * kBK),
-                           int32_t(tn * kPairN + rank * kHalf), hint);
+          if (CL == 2) {
+            if (half) {
+              tma_load_2d_pair(st + kAS, &tmap_x64, fb, int32_t(kb * kBK),
+                               int32_t(ti.col0 + q * (kHalf / 2)), hint);
+            } else {
+              tma_load_2d_pair(st + kAS, &tmap_x, fb, int32_t(kb * kBK),
+                               int32_t(ti.col0 + q * kHalf), hint);
+            }
+          } else if ((kb & 1u) == pr) {  // the pairs take turns loading the shared X half
+            tma_load_2d_pair_mc(st + kAS, &tmap_x, fb, int32_t(kb * kBK),
+                                int32_t(ti.col0 + q * kHalf),
+                                static_cast<uint16_t>((1u << q) | (1u << (q + 2))), hint);
+          }
           if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
       }
@@ -137,10 +183,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       unsigned long long w_full = 0, w_tmem = 0, t_begin = clock64();
       for (uint32_t t = cluster; t < num_tiles; t += nclusters) {
         unsigned long long c0 = p.dbg ? clock64() : 0;
+        (void)c0;
         mbar_wait(&tmem_empty[acc], acc_phase ^ 1);
         if (p.dbg) w_tmem += clock64() - c0;
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * kPairN;
+        const uint32_t idesc =
+            (CL == 2 && tile_info(t, p.tiles_m, p.n_full).ncols != kPairN) ? kIdescHalf : kIdesc;
         for (uint32_t kb = 0; kb < p.kblocks; ++kb) {
           c0 = p.dbg ? clock64() : 0;
           mbar_wait(&full_bar[stage], phase);
@@ -151,12 +200,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           const uint64_t bdesc = umma_desc_sw128(st + kAS);
 #pragma unroll
           for (uint32_t k = 0; k < kBK / 32; ++k) {
-            mma_i8_pair(d_tmem, adesc + 2 * k, bdesc + 2 * k, kIdesc, (kb | k) != 0);
+            mma_i8_pair(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) != 0);
           }
-          mma_commit_pair_mc(&empty_bar[stage], 0x3);
+          mma_commit_pair_mc(&empty_bar[stage], kAllMask);  // frees the slot in every CTA
           if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
-        mma_commit_pair_mc(&tmem_full[acc], 0x3);
+        mma_commit_pair_mc(&tmem_full[acc], pair_mask);
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
       if (p.dbg) {
@@ -169,12 +218,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     __syncwarp();
   } else if (warp >= 4) {
     // ---------------- epilogue (both CTAs) ----------------
-    const uint32_t q = warp & 3;
+    const uint32_t wq = warp & 3;
     uint32_t acc = 0, acc_phase = 0, nbuf = 0;
     const uint64_t store_hint = policy_evict_first();  // Y streams out; keep operands in L2
     for (uint32_t t = cluster; t < num_tiles; t += nclusters) {
-      const uint32_t tm = t % p.tiles_m, tn = t / p.tiles_m;
-      const uint32_t row0 = tm * 2 * kHalf + rank * kHalf + q * 32;
+      const TileInfo ti = CL == 2 ? tile_info(t, p.tiles_m, p.n_full)
+                                  : TileInfo{(t % tiles_mc) * kPairs + pr, (t / tiles_mc) * kPairN, kPairN};
+      const uint32_t tm = ti.tm;
+      const uint32_t row0 = tm * 2 * kHalf + q * kHalf + wq * 32;
       const uint32_t row = row0 + lane;
       const bool row_ok = row < p.rows_w;
       const uint32_t rsw = row_ok ? static_cast<uint32_t>(__ldg(p.rowsum_w + row)) : 0u;
@@ -184,13 +235,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 
       mbar_wait(&tmem_full[acc], acc_phase);
       tc_fence_after();
-      const uint32_t t_addr = tmem_base + ((q * 32u) << 16) + acc * kPairN;
+      const uint32_t t_addr = tmem_base + ((wq * 32u) << 16) + acc * kPairN;
 #pragma unroll 1
-      for (uint32_t c = 0; c < kPairN / 32; ++c) {
+      for (uint32_t c = 0; c < ti.ncols / 32; ++c) {
         uint32_t r[32];
         tmem_ld_32x32b_x32(t_addr + c * 32, r);
         tmem_ld_wait();
-        const uint32_t col0 = tn * kPairN + c * 32;
+        const uint32_t col0 = ti.col0 + c * 32;
         const int4* rsx4 = reinterpret_cast<const int4*>(p.rowsum_x + col0);
 #pragma unroll
         for (int j4 = 0; j4 < 8; ++j4) {
@@ -214,7 +265,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           }
         }
         if (p.tma_store) {
-          uint8_t* buf = staging + (q * 2 + nbuf) * kEpiBuf;
+          uint8_t* buf = staging + (wq * 2 + nbuf) * kEpiBuf;
           nbuf ^= 1;
           if (lane == 0) bulk_wait_read<1>();  // the store that last read `buf` is done
           __syncwarp();
@@ -242,7 +293,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(mapa(smem_u32(&tmem_empty[acc]), 0));
+      if (lane == 0) mbar_arrive_cluster(mapa(smem_u32(&tmem_empty[acc]), lead_rank));
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
     if (lane == 0) bulk_wait<0>();
@@ -258,11 +309,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 }  // namespace
 
 cudaError_t launch_gemm_pair(const GemmArgs& a, cudaStream_t s, int* launches) {
-  CUtensorMap tw, tx, ty;
+  CUtensorMap tw, tx, tx64, ty;
   if (encode_tmap_2d(&tw, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, a.codes_w, a.kpad, a.rows_w, a.kpad,
                      kBK, kHalf) != CUDA_SUCCESS ||
       encode_tmap_2d(&tx, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, a.codes_x, a.kpad, a.rows_x, a.kpad,
-                     kBK, kHalf) != CUDA_SUCCESS) {
+                     kBK, kHalf) != CUDA_SUCCESS ||
+      encode_tmap_2d(&tx64, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, a.codes_x, a.kpad, a.rows_x, a.kpad,
+                     kBK, kHalf / 2) != CUDA_SUCCESS) {
     return cudaErrorInvalidValue;
   }
   void* out = a.y ? static_cast<void*>(a.y) : static_cast<void*>(a.yf);
@@ -277,8 +330,12 @@ cudaError_t launch_gemm_pair(const GemmArgs& a, cudaStream_t s, int* launches) {
   }
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_u8_pair_kernel,
+    cudaError_t e = cudaFuncSetAttribute(gemm_u8_pair_kernel<2>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+    if (e == cudaSuccess) {
+      e = cudaFuncSetAttribute(gemm_u8_pair_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               kSmemBytes);
+    }
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
@@ -302,20 +359,57 @@ cudaError_t launch_gemm_pair(const GemmArgs& a, cudaStream_t s, int* launches) {
   p.c0 = static_cast<uint32_t>(a.k_logical) * A * B;
   p.tma_store = tma_store ? 1u : 0u;
   p.dbg = a.dbg;
-  const uint32_t tiles = p.tiles_m * p.tiles_n;
-  const uint32_t max_clusters = static_cast<uint32_t>(a.num_sms / 2);
-  const uint32_t clusters = tiles < max_clusters ? tiles : max_clusters;
+  // clusters of 4 (X multicast across two pairs) when there are enough cluster tiles to
+  // fill the machine, else plain pairs. APMM_PAIR_CLUSTER=2|4 forces one (testing).
+  static const int forced = [] {
+    const char* f = std::getenv("APMM_PAIR_CLUSTER");
+    return f ? std::atoi(f) : 0;
+  }();
+  const uint32_t quad_tiles = ((p.tiles_m + 1) / 2) * p.tiles_n;
+  const uint32_t max_quads = static_cast<uint32_t>(a.num_sms / 4);
+  // Default: pairs. Clusters of 4 cut L2 bytes by a quarter but only 33 fit (GPC
+  // boundaries -> 132 SMs) and measured no faster (profiles/r01_notes.md).
+  const int cl = forced == 2 || forced == 4 ? forced : 2;
+  (void)max_quads;
+  const uint32_t full_tiles = p.tiles_m * p.tiles_n;
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(2 * clusters);
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = kSmemBytes;
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
+  attr[1].id = cudaLaunchAttributeClusterDimension;
+  attr[1].val.clusterDim.x = static_cast<unsigned>(cl);
+  attr[1].val.clusterDim.y = 1;
+  attr[1].val.clusterDim.z = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_u8_pair_kernel, tw, tx, ty, p);
+  cfg.numAttrs = 2;
+  // persistent grid = the clusters that can be co-resident (clusters cannot straddle GPCs,
+  // so for 4-CTA clusters this can be fewer than num_sms / 4)
+  static int max_active[5] = {0, 0, 0, 0, 0};
+  if (!max_active[cl]) {
+    cfg.gridDim = dim3(static_cast<unsigned>(a.num_sms / cl * cl));
+    int n = 0;
+    cudaError_t oe = cl == 4 ? cudaOccupancyMaxActiveClusters(&n, gemm_u8_pair_kernel<4>, &cfg)
+                             : cudaOccupancyMaxActiveClusters(&n, gemm_u8_pair_kernel<2>, &cfg);
+    max_active[cl] = (oe == cudaSuccess && n > 0) ? n : a.num_sms / cl;
+    if (std::getenv("APMM_DEBUG_PLAN")) {
+      std::fprintf(stderr, "[apmm pair] cluster %d: %d co-resident clusters\n", cl, max_active[cl]);
+    }
+  }
+  const uint32_t max_clusters = static_cast<uint32_t>(max_active[cl]);
+  // last-wave split (pairs only): r = T mod P tiles become 2r half-width tiles if r <= P/2
+  p.n_full = full_tiles;
+  if (cl == 2 && std::getenv("APMM_NO_TAIL_SPLIT") == nullptr) {
+    const uint32_t r = full_tiles % max_clusters;
+    if (r != 0 && 2 * r <= max_clusters) p.n_full = full_tiles - r;
+  }
+  const uint32_t tiles = cl == 4 ? quad_tiles : p.n_full + 2 * (full_tiles - p.n_full);
+  const uint32_t clusters = tiles < max_clusters ? tiles : max_clusters;
+  cfg.gridDim = dim3(cl * clusters);
+  cudaError_t e = cl == 4 ? cudaLaunchKernelEx(&cfg, gemm_u8_pair_kernel<4>, tw, tx, tx64, ty, p)
+                          : cudaLaunchKernelEx(&cfg, gemm_u8_pair_kernel<2>, tw, tx, tx64, ty, p);
   *launches += 1;
   return e != cudaSuccess ? e : cudaGetLastError();
 }

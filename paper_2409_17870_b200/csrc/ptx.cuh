@@ -153,6 +153,17 @@ APMM_DEV void tma_load_2d_pair(void* smem_dst, const void* tmap, uint32_t bar_cl
       "l"(cache_hint)
       : "memory");
 }
+// Pair load multicast to every CTA in `mask` (same smem offset); each destination pair's
+// leader barrier (at `bar_cluster_addr`'s offset) receives its bytes.
+APMM_DEV void tma_load_2d_pair_mc(void* smem_dst, const void* tmap, uint32_t bar_cluster_addr,
+                                  int32_t c0, int32_t c1, uint16_t mask, uint64_t cache_hint) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes."
+      "multicast::cluster.L2::cache_hint [%0], [%1, {%4, %5}], [%2], %3, %6;" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(bar_cluster_addr), "h"(mask), "r"(c0), "r"(c1),
+      "l"(cache_hint)
+      : "memory");
+}
 template <uint32_t kCols>
 APMM_DEV void tmem_alloc_pair(uint32_t* smem_result) {
   asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
