@@ -426,7 +426,8 @@ def run_ours(args, rank, world, local_rank):
         peak_src = ("2 x measured bf16 burst (MEASURED_PEAKS.json bf16_tflops); "
                     "dense i8 = 2x dense bf16 on B200" if bf16 else
                     "2 x fallback bf16 1590 (B200_PROFILING.md)")
-    tr = traffic.get(args.workload)
+    tr_ent = traffic.get(args.workload) or {}
+    tr = tr_ent.get("bytes")  # dram read+write bytes per launch (ncu --set full), or None
     line = {
         "metric": "effective TOPS (2MNK/s) of WnAm bipolar-INT GEMM",
         "value": value, "unit": "TOPS", "n_gpus": world, "steps": args.steps,
@@ -447,6 +448,7 @@ def run_ours(args, rank, world, local_rank):
                 "d2h_bytes_per_step": int(d2h), "api": "apmm_matmul_ap (host C ABI, pinned buffers)"},
         "roofline": {"bound": "hbm" if hbm_bound else "tensor", "achieved": achieved,
                      "peak": peak, "unit": unit, "frac": achieved / peak, "traffic": tr,
+                     "traffic_source": tr_ent.get("kernel"),
                      "kernel": kname, "peak_source": peak_src,
                      "algorithmic_bytes_per_step": bytes_step,
                      "algorithmic_ops_per_step": ops_step,

@@ -233,9 +233,15 @@ int run_matmul(apmm_ctx* ctx, const uint32_t* w, uint64_t rows_w, int n_w, const
   const MatmulWs m = carve(ctx->ws, rows_w, rows_x, k, ctx->ws_half);
   ctx->ws_half ^= 1;
   const uint64_t rsx_pad = round_up(rows_x, kRowsumPad);
+  // CTA-pair 256x256 tiles when they fill the machine, else 1-SM 128x256 tiles. The pair
+  // kernel expands the weight planes on chip when TMA can address them (K3f), so K1 then
+  // only expands X and produces rowsum(U_w).
+  const uint64_t pair_tiles = ((rows_w + 255) / 256) * ((rows_x + kPairN - 1) / kPairN);
+  const bool pair = pair_tiles >= static_cast<uint64_t>(ctx->num_sms / 2) && !ctx->force_single_sm;
+  const bool fused = pair && gemm_fused_supported(w, k);
   {
     TimedLaunch t(ctx, 1, stream);
-    CU(launch_expand(w, rows_w, n_w, m.codes_w, m.rowsum_w, x, rows_x, rsx_pad, n_x, m.codes_x,
+    CU(launch_expand(w, rows_w, n_w, fused ? nullptr : m.codes_w, m.rowsum_w, x, rows_x, rsx_pad, n_x, m.codes_x,
                      m.rowsum_x, k, m.kpad, ctx->num_sms, stream));
   }
   ctx->launches += 1;
@@ -258,15 +264,18 @@ int run_matmul(apmm_ctx* ctx, const uint32_t* w, uint64_t rows_w, int n_w, const
   a.gran_x = gran_x;
   a.num_sms = ctx->num_sms;
   if (ctx->dbg_waits) {
-    if (!ctx->dbg) CU(cudaMalloc(&ctx->dbg, 64));
+    if (!ctx->dbg) {
+      CU(cudaMalloc(&ctx->dbg, 128));
+      CU(cudaMemset(ctx->dbg, 0, 128));
+    }
     a.dbg = static_cast<unsigned long long*>(ctx->dbg);
   }
   int launches = 0;
   {
     TimedLaunch t(ctx, 0, stream);
-    // CTA-pair 256x256 tiles when they fill the machine, else 1-SM 128x256 tiles
-    const uint64_t pair_tiles = ((rows_w + 255) / 256) * ((rows_x + kPairN - 1) / kPairN);
-    if (pair_tiles >= static_cast<uint64_t>(ctx->num_sms / 2) && !ctx->force_single_sm) {
+    if (fused) {
+      CU(launch_gemm_pair_wplanes(a, w, stream, &launches));
+    } else if (pair) {
       CU(launch_gemm_pair(a, stream, &launches));
     } else {
       CU(launch_gemm_tc(a, stream, &launches));
@@ -362,12 +371,21 @@ int apmm_ctx_destroy(apmm_ctx* ctx) {
   cudaSetDevice(ctx->device);
   cudaDeviceSynchronize();
   if (ctx->dbg) {
-    unsigned long long h[4] = {0, 0, 0, 0};
+    unsigned long long h[16] = {};
     cudaMemcpy(h, ctx->dbg, sizeof(h), cudaMemcpyDeviceToHost);
     std::fprintf(stderr,
-                 "[apmm debug] MMA issuer: %.1f%% of cycles waiting on TMA (full), %.1f%% on "
+                 "[apmm debug] MMA issuer: %.1f%% of cycles waiting on operands (full), %.1f%% on "
                  "epilogue (tmem_empty), over %llu issuer runs\n",
                  h[2] ? 100.0 * h[0] / h[2] : 0.0, h[2] ? 100.0 * h[1] / h[2] : 0.0, h[3]);
+    if (h[8]) {
+      std::fprintf(stderr,
+                   "[apmm debug] fused transform warps: %.1f%% waiting for free operand slots, "
+                   "%.1f%% storing + next block's planes -> codes (of which %.1f%% waiting for "
+                   "raw planes), %.1f%% fence + arrive; "
+                   "%.0f cycles per warp run over %llu runs\n",
+                   h[7] ? 100.0 * h[4] / h[7] : 0.0, h[7] ? 100.0 * h[5] / h[7] : 0.0,
+                   h[7] ? 100.0 * h[9] / h[7] : 0.0, h[7] ? 100.0 * h[6] / h[7] : 0.0, double(h[7]) / h[8], h[8]);
+    }
     cudaFree(ctx->dbg);
   }
   if (ctx->ws) cudaFree(ctx->ws);

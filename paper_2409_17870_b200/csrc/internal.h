@@ -20,7 +20,8 @@ inline uint64_t round_up(uint64_t v, uint64_t m) { return (v + m - 1) / m * m; }
 // ---- prep.cu -------------------------------------------------------------------------
 // Both operands' planes (reference layout) -> u8 codes [rows x kpad] (zero K padding, K
 // permuted identically within each 32-column group) + rowsum[rows], one launch.
-// rowsum_x[rows_x, rows_x_pad) is zeroed. Launched with PDL (see prep.cu).
+// rowsum_x[rows_x, rows_x_pad) is zeroed. Launched with PDL (see prep.cu). w_codes may be
+// null: then only rowsum_w is produced for W (the fused GEMM expands W on chip).
 cudaError_t launch_expand(const uint32_t* w_planes, uint64_t rows_w, int n_w,
                           uint8_t* w_codes, int32_t* w_rowsum, const uint32_t* x_planes,
                           uint64_t rows_x, uint64_t rows_x_pad, int n_x, uint8_t* x_codes,
@@ -58,6 +59,14 @@ struct GemmArgs {
 cudaError_t launch_gemm_tc(const GemmArgs& a, cudaStream_t s, int* launches);
 // ---- gemm_pair.cu (CTA-pair, 256x256 tiles) -------------------------------------------
 cudaError_t launch_gemm_pair(const GemmArgs& a, cudaStream_t s, int* launches);
+
+// ---- gemm_fused.cu (CTA pair, weight planes expanded on chip by transform warps) -------
+// Needs the planes' row pitch (ceil(k/32) words) to be a multiple of 16 bytes and a 16-byte
+// aligned base (TMA); a.codes_w is unused (K1 then runs with w_codes == nullptr and only
+// produces rowsum_w).
+bool gemm_fused_supported(const uint32_t* w_planes, uint64_t k);
+cudaError_t launch_gemm_pair_wplanes(const GemmArgs& a, const uint32_t* w_planes,
+                                     cudaStream_t s, int* launches);
 
 // ---- skinny.cu (few feature rows: weight planes streamed from HBM into mma.sync) -----
 constexpr uint64_t kSkinnyMaxRowsX = 63;  // feature rows handled by K5 (+1 ones column <= 64)

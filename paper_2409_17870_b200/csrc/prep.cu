@@ -65,6 +65,23 @@ __device__ __forceinline__ void transpose8(uint32_t (&x)[8]) {
   for (int i = 0; i < 8; i += 2) swap_sel(x[i], x[i + 1], 1, 0x55555555u);
 }
 
+// rowsum only (operand expanded elsewhere): sum_i 2^i popc(plane_i), lanes over words.
+template <int N>
+__device__ __forceinline__ int32_t rowsum_row(const ExpandOperand& op, uint32_t r, uint32_t wpr,
+                                              uint32_t tail_mask, uint32_t lane) {
+  int32_t sum = 0;
+  const uint32_t* src = op.planes + uint64_t(r) * wpr;
+  const uint64_t pstride = uint64_t(op.rows) * wpr;
+  for (uint32_t w = lane; w < wpr; w += 32) {
+    const uint32_t mask = w == wpr - 1 ? tail_mask : 0xffffffffu;
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      if (i < op.n) sum += __popc(__ldg(src + i * pstride + w) & mask) << i;
+    }
+  }
+  return sum;
+}
+
 template <int N>
 __device__ __forceinline__ int32_t expand_row(const ExpandOperand& op, uint32_t r, uint32_t wpr,
                                               uint32_t tail_mask, uint32_t kpad_words,
@@ -117,7 +134,15 @@ __global__ void __launch_bounds__(kExpandThreads) expand_kernel(ExpandOperand a,
     const ExpandOperand& op = is_a ? a : b;
     const uint32_t r = is_a ? gr : gr - a.rows;
     int32_t sum = 0;
-    switch (op.n) {
+    if (op.codes == nullptr) {
+      switch (op.n) {
+        case 1: sum = rowsum_row<1>(op, r, wpr, tail_mask, lane); break;
+        case 2: sum = rowsum_row<2>(op, r, wpr, tail_mask, lane); break;
+        case 3: sum = rowsum_row<3>(op, r, wpr, tail_mask, lane); break;
+        case 4: sum = rowsum_row<4>(op, r, wpr, tail_mask, lane); break;
+        default: sum = rowsum_row<8>(op, r, wpr, tail_mask, lane); break;
+      }
+    } else switch (op.n) {
       case 1: sum = expand_row<1>(op, r, wpr, tail_mask, kpad_words, lane); break;
       case 2: sum = expand_row<2>(op, r, wpr, tail_mask, kpad_words, lane); break;
       case 3: sum = expand_row<3>(op, r, wpr, tail_mask, kpad_words, lane); break;

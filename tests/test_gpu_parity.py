@@ -224,6 +224,56 @@ def _row_sample_check(ap, ctx, oracle, n_out, m_tok, k, nw, nx, seed, sample=48)
     return y
 
 
+@pytest.mark.parametrize("nw,nx,n_out,m_tok,k", [
+    (1, 2, 2304, 2560, 4096), (2, 4, 2305, 2561, 4200), (3, 8, 2304, 2560, 4224),
+    (4, 4, 2560, 2304, 4096), (5, 3, 2304, 2560, 4096), (6, 2, 2304, 2304, 2048),
+    (7, 7, 2304, 2560, 4096), (8, 8, 2305, 2500, 4100), (8, 8, 2304, 2560, 4096)])
+def test_fused_weight_plane_gemm(gpu, oracle, nw, nx, n_out, m_tok, k):
+    """K3f (weight planes expanded on chip by transform warps; opt-in APMM_FUSED=1) against
+    the oracle on sampled rows and, on the full output, against the default two-kernel path
+    (K1 expands both operands, APMM_NO_FUSED=1). Shapes fill >= 74 CTA pairs, so the pair path runs; they cover every
+    weight width, ragged rows, the half-width last-wave tiles, a tail word (K % 32 != 0
+    with ceil(K/32) % 4 == 0) and K whose word count is not a multiple of 4 (not fused)."""
+    import torch
+    ap, ctx = gpu
+    os.environ["APMM_FUSED"] = "1"
+    try:
+        y = _row_sample_check(ap, ctx, oracle, n_out, m_tok, k, nw, nx, seed=nw * 100 + nx,
+                              sample=24)
+    finally:
+        del os.environ["APMM_FUSED"]
+    dev = torch.device("cuda", 0)
+    g = torch.Generator(device=dev)
+    g.manual_seed(nw * 100 + nx)
+    wc = torch.randint(0, 1 << nw, (n_out, k), generator=g, device=dev, dtype=torch.uint8)
+    xc = torch.randint(0, 1 << nx, (m_tok, k), generator=g, device=dev, dtype=torch.uint8)
+    wpr = (k + 31) // 32
+    wp = torch.empty(nw * n_out * wpr, dtype=torch.int32, device=dev)
+    xp = torch.empty(nx * m_tok * wpr, dtype=torch.int32, device=dev)
+    ap.cu_pack(wc, n_out, k, nw, wp, ctx)
+    ap.cu_pack(xc, m_tok, k, nx, xp, ctx)
+    y2 = torch.empty((n_out, m_tok), dtype=torch.int32, device=dev)
+    os.environ["APMM_NO_FUSED"] = "1"
+    try:
+        ap.cu_matmul_ap(wp, n_out, nw, xp, m_tok, nx, k, y2, ctx)
+        torch.cuda.synchronize()
+    finally:
+        del os.environ["APMM_NO_FUSED"]
+    assert torch.equal(y, y2), (n_out, m_tok, k, nw, nx)
+    # dequant through the fused kernel: same fp64 epilogue as the two-kernel path
+    sw = torch.rand(n_out, dtype=torch.float64, device=dev)
+    sx = torch.rand(m_tok, dtype=torch.float64, device=dev)
+    f1 = torch.empty((n_out, m_tok), dtype=torch.float32, device=dev)
+    os.environ["APMM_FUSED"] = "1"
+    try:
+        ap.cu_matmul_ap_dequant(wp, n_out, nw, sw, 1, xp, m_tok, nx, sx, 1, k, f1, ctx)
+    finally:
+        del os.environ["APMM_FUSED"]
+    want = ((y2.double() * sw[:, None]) * sx[None, :]).float()
+    torch.cuda.synchronize()
+    assert torch.equal(f1, want)
+
+
 @pytest.mark.parametrize("nw,nx", [(1, 2), (2, 4), (3, 8), (4, 8)])
 def test_config2_4096_cubed_row_sampled(gpu, oracle, nw, nx):
     ap, ctx = gpu
