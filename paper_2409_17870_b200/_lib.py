@@ -9,7 +9,8 @@ import ctypes as C
 import os
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libapmm_b200.so")
+# APMM_LIB (dev only) points the loader at another build of the same ABI, e.g. to A/B a change
+LIB_PATH = os.environ.get("APMM_LIB") or os.path.join(PKG, "libapmm_b200.so")
 
 u64, i32, i64, vp = C.c_uint64, C.c_int, C.c_int64, C.c_void_p
 

@@ -225,7 +225,7 @@ int run_matmul(apmm_ctx* ctx, const uint32_t* w, uint64_t rows_w, int n_w, const
       TimedLaunch t(ctx, 0, stream);
       CU(launch_skinny(s, stream));
     }
-    ctx->launches += 2;  // feature prep + streaming kernel
+    ctx->launches += rows_x <= 1 ? 1 : 2;  // (feature prep +) streaming kernel
     return APMM_OK;
   }
   int st = ensure(&ctx->ws, &ctx->ws_bytes, matmul_ws_bytes(rows_w, rows_x, k), ctx->device);

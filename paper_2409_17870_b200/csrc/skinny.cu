@@ -71,6 +71,7 @@ __host__ __device__ constexpr uint32_t sk_smem_budget(int n, int nt) {
 // Per-warp TMA ring: a slot holds one work item, n planes x 16 rows x 64 B = n KB. The
 // depth (2..kMaxStages) is chosen at launch from the shared memory the X slice leaves.
 constexpr int kMaxStages = 16;
+constexpr int kXPieces = 16;  // X slice copy pieces (barriers)
 __host__ __device__ constexpr uint32_t slot_bytes(int n) { return static_cast<uint32_t>(n) * 1024u; }
 // Shared-memory X layout per 512-column chunk, real feature rows only (M = rows_x):
 // [w 0..3][half 0..1][feature row 0..M-1][t 0..3] x 16 B. Thread (g, t) of n-tile nt
@@ -78,11 +79,18 @@ __host__ __device__ constexpr uint32_t slot_bytes(int n) { return static_cast<ui
 // r, byte B = code of column 8B + r). A warp's 128-bit reads are 512 contiguous bytes.
 // Rows >= M are zero codes and the all-ones column (slot 8*NT-1) is a register constant.
 __host__ __device__ constexpr uint32_t chunk_bytes_m(uint32_t m) { return 512u * m; }
+// Fragment rows per chunk: the real feature rows, then a zero row and an all-ones row, so
+// that every lane's B fragment is a plain shared load (lanes of padded MMA columns point at
+// the zero row, the rowsum column at the ones row; no per-MMA register moves).
+__host__ __device__ constexpr uint32_t frag_rows(uint32_t rows_x) { return rows_x + 2u; }
 // cross-warp reduction buffer: [16 R][m_pad] u32, R <= 8
 __host__ __device__ constexpr uint32_t red_bytes(int nt, uint32_t r) { return 16u * r * nt * 8u * 4u; }
 
 struct SkinnyParams {
-  const uint8_t* xfrag;      // prep output: [chunks_total][chunk_bytes_m(rows_x)]
+  const uint8_t* xfrag;      // prep output: [chunks_total][chunk_bytes_m(frag_rows(rows_x))]
+  const uint32_t* x_planes;  // inprep: reference layout [n_x][rows_x][wpr]
+  uint32_t inprep;           // 1: this kernel builds its X slice itself (no prep kernel)
+  uint32_t n_x, k_logical;
   const int32_t* rsx;        // prep output: rowsum(U_x) parts [rows_x][rsx_parts]
   uint32_t rsx_parts;
   uint32_t rows_w, rows_x, wpr, n_planes;
@@ -139,13 +147,23 @@ APMM_DEV uint32_t mulhi(uint32_t a, uint32_t b) { return __umulhi(a, b); }
 
 // Delta swap in select form with both shifts on the FMA pipe (IMAD / IMAD.HI) and the two
 // selects as LOP3 on the ALU pipe.
+// sel(a, b, m) = (a & ~m) | (b & m) as one LOP3 (written in PTX so the compiler keeps the
+// select form instead of re-associating it into AND/OR chains around the multiplies).
+template <uint32_t M>
+APMM_DEV uint32_t sel(uint32_t a, uint32_t b) {
+  uint32_t r;
+  asm("lop3.b32 %0, %1, %2, %3, 0xD8;" : "=r"(r) : "r"(a), "r"(b), "n"(M));
+  return r;
+}
 template <int S>
 APMM_DEV void swap_sel(uint32_t& a, uint32_t& b, uint32_t m, uint32_t mul_s) {
   const uint32_t bs = b * mul_s;                      // b << S
   const uint32_t as = mulhi(a, 1u << (32 - S));       // a >> S
-  const uint32_t na = (a & ~(m << S)) | (bs & (m << S));
-  b = (b & ~m) | (as & m);
+  const uint32_t na = S == 1 ? sel<0xAAAAAAAAu>(a, bs) : S == 2 ? sel<0xCCCCCCCCu>(a, bs)
+                                                                : sel<0xF0F0F0F0u>(a, bs);
+  b = S == 1 ? sel<0x55555555u>(b, as) : S == 2 ? sel<0x33333333u>(b, as) : sel<0x0F0F0F0Fu>(b, as);
   a = na;
+  (void)m;
 }
 
 // Codes of one 32-column word (x[i] = plane i word, zero for i >= N). SPLIT (N <= 4):
@@ -208,29 +226,32 @@ __global__ void __launch_bounds__(kPrepThreads) prep_x_kernel(const uint32_t* __
                                                               int32_t* __restrict__ rsx_part) {
   apmm_ptx::pdl_trigger();
   const uint32_t tok = blockIdx.y, W = blockIdx.x * kPrepThreads + threadIdx.x;
+  const uint32_t xr = frag_rows(rows_x);
   uint32_t v[8];
   int32_t rs = 0;
   const uint64_t pstride = uint64_t(rows_x) * wpr;
+  const bool real = tok < rows_x;
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
-    v[i] = (i < n_x && W < wpr) ? __ldg(x + i * pstride + uint64_t(tok) * wpr + W) : 0u;
-    if (i < n_x) rs += __popc(v[i]) << i;
+    v[i] = (real && i < n_x && W < wpr) ? __ldg(x + i * pstride + uint64_t(tok) * wpr + W)
+                                        : (tok == rows_x + 1u ? 0x01010101u : 0u);
+    if (real && i < n_x) rs += __popc(v[i]) << i;
   }
-  transpose8(v);
+  if (real) transpose8(v);
   apmm_ptx::pdl_wait();  // the workspace half may be written only now
   if (W < words_pad) {
     const uint32_t cl = W / kChunkWords, t = (W % kChunkWords) >> 2, w = W & 3u;
-    uint4* dst = reinterpret_cast<uint4*>(xfrag + uint64_t(cl) * chunk_bytes_m(rows_x)) +
-                 ((w * 2u) * rows_x + tok) * 4u + t;
+    uint4* dst = reinterpret_cast<uint4*>(xfrag + uint64_t(cl) * chunk_bytes_m(xr)) +
+                 ((w * 2u) * xr + tok) * 4u + t;
     dst[0] = make_uint4(v[0], v[1], v[2], v[3]);
-    dst[rows_x * 4u] = make_uint4(v[4], v[5], v[6], v[7]);
+    dst[xr * 4u] = make_uint4(v[4], v[5], v[6], v[7]);
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) rs += __shfl_xor_sync(0xffffffffu, rs, o);
   __shared__ int32_t part[kPrepThreads / 32];
   if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = rs;
   __syncthreads();
-  if (threadIdx.x == 0) {
+  if (threadIdx.x == 0 && real) {
     int32_t s = 0;
     for (int i = 0; i < kPrepThreads / 32; ++i) s += part[i];
     rsx_part[uint64_t(tok) * gridDim.x + blockIdx.x] = s;
@@ -247,7 +268,7 @@ __global__ void __launch_bounds__(sk_threads(N, NT), sk_ctas_per_sm(N, NT))
   constexpr uint32_t ONES = M_PAD - 1u;  // the all-ones feature column -> rowsum(U_w)
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ __align__(8) uint64_t full_bar[WARPS * kMaxStages];
-  __shared__ __align__(8) uint64_t xbar;
+  __shared__ __align__(8) uint64_t xbars[kXPieces];  // X slice arrival, per piece of chunks
   __shared__ uint32_t rsx_s[M_PAD];
   __shared__ uint32_t s_last;
 
@@ -271,11 +292,13 @@ __global__ void __launch_bounds__(sk_threads(N, NT), sk_ctas_per_sm(N, NT))
   const uint32_t ring = apmm_ptx::smem_u32(smem + p.ring_off) + warp * (stages * SLOT);
   uint32_t* red = reinterpret_cast<uint32_t*>(smem + p.red_off);  // [tile_rows][M_PAD]
   uint64_t* bars = full_bar + warp * kMaxStages;
-  const uint32_t xchunk_bytes = chunk_bytes_m(p.rows_x);
+  const uint32_t xchunk_bytes = chunk_bytes_m(frag_rows(p.rows_x));
 
   if (lane == 0) {
     for (uint32_t s = 0; s < stages; ++s) apmm_ptx::mbar_init(&bars[s], 1);
-    if (warp == 0) apmm_ptx::mbar_init(&xbar, 1);
+    if (warp == 0) {
+      for (int i = 0; i < kXPieces; ++i) apmm_ptx::mbar_init(&xbars[i], 1);
+    }
     apmm_ptx::fence_mbar_init();
     apmm_ptx::tma_prefetch_desc(&tmap_w);
   }
@@ -303,29 +326,76 @@ __global__ void __launch_bounds__(sk_threads(N, NT), sk_ctas_per_sm(N, NT))
   for (uint32_t s = 0; s + 1 < stages; ++s) issue();
   apmm_ptx::pdl_wait();
   if (p.ts && tid == 0) p.ts[blockIdx.x * 8 + 1] = gtime();
-  __syncthreads();  // xbar initialised
-  const uint32_t xbytes = (s_end > s_begin ? s_end - s_begin : 0u) * xchunk_bytes;
-  if (tid == 0) {
-    apmm_ptx::mbar_arrive_expect_tx(&xbar, xbytes);
-    const uint8_t* src = p.xfrag + uint64_t(s_begin) * xchunk_bytes;
-    for (uint32_t off = 0; off < xbytes; off += 32768u) {
-      bulk_g2s(apmm_ptx::smem_u32(xs + off), src + off, min(32768u, xbytes - off),
-               apmm_ptx::smem_u32(&xbar));
+  __syncthreads();  // xbars initialised
+  const uint32_t xpc = (p.slice_chunks + kXPieces - 1) / kXPieces;  // chunks per X piece
+  if (p.inprep) {
+    // Feature prep in the prologue (few feature rows): this CTA's K slice of X planes ->
+    // fragment-order codes in shared memory, its rowsum(U_x) share, and the zero / ones
+    // rows. One thread per (fragment row, 32-column word): n_x words -> 8x8 transpose.
+    for (uint32_t q = tid; q < M_PAD; q += THREADS) rsx_s[q] = 0u;
+    for (uint32_t q = tid; q < tile_rows * M_PAD; q += THREADS) red[q] = 0u;
+    __syncthreads();
+    const uint32_t slice_words = (s_end > s_begin ? s_end - s_begin : 0u) * kChunkWords;
+    const uint32_t xr = frag_rows(p.rows_x);
+    const uint64_t pstride = uint64_t(p.rows_x) * p.wpr;
+    for (uint32_t idx = tid; idx < xr * slice_words; idx += THREADS) {
+      const uint32_t tok = idx / slice_words, wl = idx - tok * slice_words;
+      const uint32_t W = s_begin * kChunkWords + wl;
+      const bool real = tok < p.rows_x;
+      uint32_t v[8];
+      uint32_t rs = 0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        v[i] = (real && uint32_t(i) < p.n_x && W < p.wpr)
+                   ? __ldg(p.x_planes + i * pstride + uint64_t(tok) * p.wpr + W)
+                   : (tok == p.rows_x + 1u ? 0x01010101u : 0u);
+        if (real) rs += uint32_t(__popc(v[i])) << i;
+      }
+      if (real) transpose8(v);
+      const uint32_t cl = wl / kChunkWords, t4 = (wl % kChunkWords) >> 2, w = wl & 3u;
+      uint4* dst = reinterpret_cast<uint4*>(xs + cl * xchunk_bytes) + ((w * 2u) * xr + tok) * 4u + t4;
+      dst[0] = make_uint4(v[0], v[1], v[2], v[3]);
+      dst[xr * 4u] = make_uint4(v[4], v[5], v[6], v[7]);
+      if (rs) atomicAdd(&rsx_s[tok], rs);
     }
-  }
-  // slice 0 adds the X term and the constant once; rsx_s is zero elsewhere
-  for (uint32_t q = tid; q < M_PAD; q += THREADS) {
-    int32_t s = 0;
-    if (slice == 0 && q < p.rows_x) {
-      for (uint32_t k = 0; k < p.rsx_parts; ++k) s += __ldg(p.rsx + uint64_t(q) * p.rsx_parts + k);
+    __syncthreads();
+  } else {
+    const uint32_t xbytes = (s_end > s_begin ? s_end - s_begin : 0u) * xchunk_bytes;
+    if (tid == 0) {
+      // one bulk copy (and barrier) per piece of `xpc` chunks, so warps start on their
+      // first chunk while the rest of the slice is still arriving
+      const uint8_t* src = p.xfrag + uint64_t(s_begin) * xchunk_bytes;
+      const uint32_t piece = xpc * xchunk_bytes;
+      for (uint32_t off = 0, i = 0; off < xbytes; off += piece, ++i) {
+        const uint32_t b = min(piece, xbytes - off);
+        apmm_ptx::mbar_arrive_expect_tx(&xbars[i], b);
+        for (uint32_t o2 = 0; o2 < b; o2 += 32768u) {
+          bulk_g2s(apmm_ptx::smem_u32(xs + off + o2), src + off + o2, min(32768u, b - o2),
+                   apmm_ptx::smem_u32(&xbars[i]));
+        }
+      }
     }
-    rsx_s[q] = static_cast<uint32_t>(s);
+    // slice 0 adds the X term of the whole K (prep kernel's rowsum parts)
+    for (uint32_t q = tid; q < M_PAD; q += THREADS) {
+      int32_t s = 0;
+      if (slice == 0 && q < p.rows_x) {
+        for (uint32_t k = 0; k < p.rsx_parts; ++k) s += __ldg(p.rsx + uint64_t(q) * p.rsx_parts + k);
+      }
+      rsx_s[q] = static_cast<uint32_t>(s);
+    }
+    for (uint32_t q = tid; q < tile_rows * M_PAD; q += THREADS) red[q] = 0u;
+    __syncthreads();
   }
-  for (uint32_t q = tid; q < tile_rows * M_PAD; q += THREADS) red[q] = 0u;
-  apmm_ptx::mbar_wait(&xbar, 0);
-  __syncthreads();
   if (p.ts && tid == 0) p.ts[blockIdx.x * 8 + 2] = gtime();
-  const uint32_t cterm = slice == 0 ? p.c0 : 0u;
+  // The terms are linear in K: with the prep kernel, slice 0 adds the X term and the whole
+  // constant; with in-kernel prep every slice adds its own X term and K_slice * A * B.
+  uint32_t cterm = slice == 0 ? p.c0 : 0u;
+  if (p.inprep) {
+    const uint32_t k_lo = s_begin * kChunkWords * 32u;
+    const uint32_t k_hi = min(s_end * kChunkWords * 32u, p.k_logical);
+    cterm = (k_hi > k_lo ? k_hi - k_lo : 0u) * (p.coef_w / 2u) * (p.coef_x / 2u);
+  }
+
 
   uint32_t lo[NT][4], hi[NT][4];
 #pragma unroll
@@ -333,6 +403,14 @@ __global__ void __launch_bounds__(sk_threads(N, NT), sk_ctas_per_sm(N, NT))
 #pragma unroll
     for (int e = 0; e < 4; ++e) lo[nt][e] = hi[nt][e] = 0u;
 
+  // B-fragment row of each n-tile for this lane: the feature row, else the zero row, or the
+  // all-ones row for the rowsum(U_w) column
+  uint32_t xrow[NT];
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) {
+    const uint32_t tok = nt * 8u + g;
+    xrow[nt] = tok < p.rows_x ? tok : (tok == ONES ? p.rows_x + 1u : p.rows_x);
+  }
   uint32_t cs_slot = 0, phase_bits = 0;
   for (uint32_t ti = 0; ti < my_tiles; ++ti) {
     const uint32_t tile = j0 + ti * gs;
@@ -341,6 +419,7 @@ __global__ void __launch_bounds__(sk_threads(N, NT), sk_ctas_per_sm(N, NT))
       issue();
       const uint32_t chunk = s_begin + c * warps_k + wk;
       if (chunk < s_end) {
+        if (!p.inprep) apmm_ptx::mbar_wait(&xbars[(chunk - s_begin) / xpc], 0);
         apmm_ptx::mbar_wait(&bars[cs_slot], (phase_bits >> cs_slot) & 1u);
         phase_bits ^= 1u << cs_slot;
         // slot layout (TMA box {16 words, 16 rows, planes}): [plane][row][16 words]
@@ -353,7 +432,7 @@ __global__ void __launch_bounds__(sk_threads(N, NT), sk_ctas_per_sm(N, NT))
           wb[pl] = live ? *reinterpret_cast<const uint4*>(slot + pl * 1024 + 512) : make_uint4(0, 0, 0, 0);
         }
         const uint4* xchunk = reinterpret_cast<const uint4*>(xs + (chunk - s_begin) * xchunk_bytes);
-        const uint32_t m4 = p.rows_x * 4u;
+        const uint32_t m4 = frag_rows(p.rows_x) * 4u;
 #pragma unroll
         for (int w = 0; w < 4; ++w) {
           uint32_t xa[8], xb[8], ca[8], cb[8];
@@ -372,15 +451,8 @@ __global__ void __launch_bounds__(sk_threads(N, NT), sk_ctas_per_sm(N, NT))
           codes_of_word<N, SPLIT>(xb, cb, p);
 #pragma unroll
           for (int nt = 0; nt < NT; ++nt) {
-            const uint32_t tok = nt * 8u + g;
-            uint4 x0, x1;
-            if (tok < p.rows_x) {
-              x0 = xchunk[(w * 2u + 0u) * m4 + tok * 4u + t];
-              x1 = xchunk[(w * 2u + 1u) * m4 + tok * 4u + t];
-            } else {  // zero codes, or the all-ones column (slot ONES) -> rowsum(U_w)
-              const uint32_t f = tok == ONES ? 0x01010101u : 0u;
-              x0 = x1 = make_uint4(f, f, f, f);
-            }
+            const uint4 x0 = xchunk[(w * 2u + 0u) * m4 + xrow[nt] * 4u + t];
+            const uint4 x1 = xchunk[(w * 2u + 1u) * m4 + xrow[nt] * 4u + t];
             mma_u8(lo[nt], ca[0], cb[0], ca[1], cb[1], x0.x, x0.y);
             mma_u8(lo[nt], ca[2], cb[2], ca[3], cb[3], x0.z, x0.w);
             if (SPLIT) {
@@ -526,7 +598,8 @@ struct Plan {
 // ceil(tiles / CTAs per slice) * (ceil(slice_chunks / warps_k) + epilogue), plus memory
 // round trips, ceil(items / items in flight) * ~3 steps, plus the split-K atomics. The X
 // slice, the ring and the reduction buffer share the CTA's shared memory.
-Plan plan_for(uint64_t rows_w, uint64_t rows_x, uint32_t chunks, int n, int nt, int num_sms) {
+Plan plan_for(uint64_t rows_w, uint64_t rows_x, uint32_t chunks, int n, int nt, int num_sms,
+              int stage_cap = 0) {
   const uint32_t warps = static_cast<uint32_t>(sk_threads(n, nt) / 32);
   const uint32_t stage_all = warps * slot_bytes(n);  // one ring stage of every warp
   const uint32_t budget = sk_smem_budget(n, nt);
@@ -539,10 +612,11 @@ Plan plan_for(uint64_t rows_w, uint64_t rows_x, uint32_t chunks, int n, int nt, 
     for (uint32_t s = 1; s <= chunks; ++s) {
       const uint32_t sc = (chunks + s - 1) / s;
       if ((chunks + sc - 1) / sc != s) continue;  // same plan as a smaller s
-      const uint32_t used = sc * chunk_bytes_m(static_cast<uint32_t>(rows_x)) + red_bytes(nt, r);
+      const uint32_t used = sc * chunk_bytes_m(frag_rows(static_cast<uint32_t>(rows_x))) + red_bytes(nt, r);
       if (used + 2 * stage_all + 1024u > budget) continue;  // 1 KB: ring alignment
       uint32_t stages = (budget - used - 1024u) / stage_all;
       if (stages > kMaxStages) stages = kMaxStages;
+      if (stage_cap >= 2 && stages > static_cast<uint32_t>(stage_cap)) stages = stage_cap;
       const uint32_t per_slice = ctas / s;
       if (per_slice == 0) break;
       const uint64_t gs = n_tiles < per_slice ? n_tiles : per_slice;
@@ -563,7 +637,7 @@ Plan plan_for(uint64_t rows_w, uint64_t rows_x, uint32_t chunks, int n, int nt, 
       }
     }
   }
-  best.ring_off = best.slice_chunks * chunk_bytes_m(static_cast<uint32_t>(rows_x));
+  best.ring_off = best.slice_chunks * chunk_bytes_m(frag_rows(static_cast<uint32_t>(rows_x)));
   best.ring_off = (best.ring_off + 1023u) & ~1023u;
   best.red_off = best.ring_off + best.stages * stage_all;
   best.smem = best.red_off + red_bytes(nt, best.r);
@@ -578,7 +652,7 @@ uint64_t frag_half_bytes(uint64_t rows_x, uint64_t k) {
   const uint64_t wpr = (k + 31) / 32;
   const uint64_t chunks = (wpr + kChunkWords - 1) / kChunkWords;
   const uint64_t prep_blocks = (chunks * kChunkWords + kPrepThreads - 1) / kPrepThreads;
-  return round_up(chunks * chunk_bytes_m(static_cast<uint32_t>(rows_x)) +
+  return round_up(chunks * chunk_bytes_m(frag_rows(static_cast<uint32_t>(rows_x))) +
                   rows_x * prep_blocks * 4, 256);
 }
 
@@ -609,7 +683,24 @@ cudaError_t launch_skinny(const SkinnyArgs& a, cudaStream_t s) {
   const uint32_t A = (1u << a.n_w) - 1u, B = (1u << a.n_x) - 1u;
   const bool split = a.n_w <= 4 && static_cast<double>(a.k) * A * B < 268435456.0;
   const int kn = kernel_n(a.n_w, split);
-  const Plan pl = plan_for(a.rows_w, a.rows_x, p.chunks_total, kn, static_cast<int>(nt), a.num_sms);
+  // Ring depth 2 per warp: with deeper rings every warp requests its whole share at once,
+  // HBM serves the requests in arbitrary order and warps wait for their first item while
+  // later items arrive (8192^2 W3A8 M=1: 9.7 us at depth 4, 8.4 us at depth 2,
+  // profiles/r01b_skinny_stage_sweep.txt). 16 warps x 2 slots still keep ~100 KB per SM in
+  // flight, above what HBM latency x bandwidth needs. APMM_SK_STAGES overrides (dev).
+  static const int stage_cap = [] {
+    const char* e = std::getenv("APMM_SK_STAGES");
+    return e ? std::atoi(e) : 2;
+  }();
+  static const int inprep_env = [] {
+    const char* e = std::getenv("APMM_SK_INPREP");
+    return e ? std::atoi(e) : -1;
+  }();
+  const Plan pl = plan_for(a.rows_w, a.rows_x, p.chunks_total, kn, static_cast<int>(nt), a.num_sms,
+                           stage_cap);
+  // In-kernel feature prep pays only for a single feature row (saves the prep launch and its
+  // PDL round trip; for more rows the redundant per-CTA transposes cost more).
+  const bool inprep = inprep_env >= 0 ? inprep_env != 0 : a.rows_x <= 1;
   if (pl.grid == 0) return cudaErrorInvalidConfiguration;
   static const bool show = std::getenv("APMM_DEBUG_PLAN") != nullptr;
 
@@ -617,7 +708,7 @@ cudaError_t launch_skinny(const SkinnyArgs& a, cudaStream_t s) {
   uint8_t* scratch = static_cast<uint8_t*>(a.scratch_ws);
   const uint64_t half_bytes = frag_half_bytes(a.rows_x, a.k);
   uint8_t* xfrag = scratch + (a.ws_half ? half_bytes : 0);
-  const uint64_t frag_bytes = uint64_t(p.chunks_total) * chunk_bytes_m(p.rows_x);
+  const uint64_t frag_bytes = uint64_t(p.chunks_total) * chunk_bytes_m(frag_rows(p.rows_x));
   int32_t* rsx = reinterpret_cast<int32_t*>(xfrag + frag_bytes);
   const uint32_t prep_blocks = (p.chunks_total * kChunkWords + kPrepThreads - 1) / kPrepThreads;
 
@@ -654,6 +745,10 @@ cudaError_t launch_skinny(const SkinnyArgs& a, cudaStream_t s) {
   p.acc = static_cast<uint32_t*>(a.acc_ws);
   p.counters = p.acc + rows_pad * m_pad;
   p.xfrag = xfrag;
+  p.x_planes = a.x_planes;
+  p.inprep = inprep ? 1u : 0u;
+  p.n_x = static_cast<uint32_t>(a.n_x);
+  p.k_logical = static_cast<uint32_t>(a.k);
   p.rsx = rsx;
   p.rsx_parts = prep_blocks;
   p.rgroups = pl.r;
@@ -684,14 +779,14 @@ cudaError_t launch_skinny(const SkinnyArgs& a, cudaStream_t s) {
     p.ts = ts_buf;
   }
 
-  {  // feature prep (same shared-memory carveout as the streaming kernel: no reconfig)
+  if (!inprep) {  // feature prep (same shared-memory carveout as the streaming kernel: no reconfig)
     static bool carve_set = false;
     if (!carve_set) {
       cudaFuncSetAttribute(prep_x_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
       carve_set = true;
     }
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(prep_blocks, p.rows_x);
+    cfg.gridDim = dim3(prep_blocks, frag_rows(p.rows_x));
     cfg.blockDim = dim3(kPrepThreads);
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
