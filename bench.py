@@ -265,30 +265,69 @@ def run_ours(args, rank, world, local_rank):
     stream = torch.cuda.Stream(device=dev)  # every launch of the timed region goes here
     torch.cuda.set_stream(stream)
     gemms = workload_gemms(args.workload)
+    # configs[4] (70B FFN): N_out sharded across the ranks (contiguous row blocks of W, X
+    # replicated; paper_2409_17870_b200/shard.py) -> strong scaling of one GEMM, optionally
+    # followed by the NCCL all-gather of the int32 row blocks (--gather). Every other
+    # workload runs the same per-GPU GEMMs on each rank (weak scaling, no collective).
+    sharded = args.workload == "ffn70b" and world > 1
+    full_gemms = gemms
+    if sharded:
+        from paper_2409_17870_b200.shard import shard_bounds
+        n_out, m_tok, k, nw, nx = gemms[0]
+        r0, r1 = shard_bounds(n_out, world, rank)
+        gemms = [(r1 - r0, m_tok, k, nw, nx)]
 
     # -- synthetic operands: uniform codes (like random_codes, verify.cpp:18-22), packed to
     #    bit planes on device (packing excluded from timing, as in apmm.cpp:163-172)
     gen = torch.Generator(device=dev)
     gen.manual_seed(1 + rank)
     ops_step = sum(ops_of(g) for g in gemms)
+    # L2 rule: when a step touches less than 2x the 126 MB L2, the weight planes rotate over
+    # `nrot` copies (step s uses copy s % nrot), so no step finds its weights in L2.
+    step_bytes = sum(packed_bytes(g[0], g[2], g[3]) + packed_bytes(g[1], g[2], g[4]) +
+                     4 * g[0] * g[1] for g in gemms)
+    nrot = max(1, -(-int(2 * 126e6) // int(step_bytes))) if step_bytes < 2 * 126e6 else 1
     bufs = []
     for (n_out, m_tok, k, nw, nx) in gemms:
         wpr = (k + 31) // 32
-        wc = torch.randint(0, 1 << nw, (n_out, k), generator=gen, device=dev, dtype=torch.uint8)
+        wps = []
+        for _ in range(nrot):
+            wc = torch.randint(0, 1 << nw, (n_out, k), generator=gen, device=dev, dtype=torch.uint8)
+            wp = torch.empty(nw * n_out * wpr, dtype=torch.int32, device=dev)
+            ap.cu_pack(wc, n_out, k, nw, wp, ctx)
+            wps.append(wp)
+            del wc
         xc = torch.randint(0, 1 << nx, (m_tok, k), generator=gen, device=dev, dtype=torch.uint8)
-        wp = torch.empty(nw * n_out * wpr, dtype=torch.int32, device=dev)
         xp = torch.empty(nx * m_tok * wpr, dtype=torch.int32, device=dev)
-        ap.cu_pack(wc, n_out, k, nw, wp, ctx)
         ap.cu_pack(xc, m_tok, k, nx, xp, ctx)
         y = torch.empty((n_out, m_tok), dtype=torch.int32, device=dev)
-        bufs.append((wp, xp, y))
-        del wc, xc
+        bufs.append((wps, xp, y))
+        del xc
     torch.cuda.synchronize()
+    gather_out = None
+    if sharded and args.gather:
+        from paper_2409_17870_b200.shard import max_shard
+        n_full, m_full = full_gemms[0][0], full_gemms[0][1]
+        gather_send = torch.zeros((max_shard(n_full, world), m_full), dtype=torch.int32, device=dev)
+        gather_out = torch.empty((world * gather_send.shape[0], m_full), dtype=torch.int32, device=dev)
+
+    def make_step(r):
+        def step_r():
+            for (g, (wps, xp, y)) in zip(gemms, bufs):
+                n_out, m_tok, k, nw, nx = g
+                ap.cu_matmul_ap(wps[r], n_out, nw, xp, m_tok, nx, k, y, ctx)
+            if gather_out is not None:  # full N_out x M_tok on every rank (NCCL over NVLink)
+                y = bufs[0][2]
+                gather_send[: y.shape[0]].copy_(y)
+                dist.all_gather_into_tensor(gather_out, gather_send)
+        return step_r
+
+    step_fns = [make_step(r) for r in range(nrot)]
+    step_i = [0]
 
     def step():
-        for (g, (wp, xp, y)) in zip(gemms, bufs):
-            n_out, m_tok, k, nw, nx = g
-            ap.cu_matmul_ap(wp, n_out, nw, xp, m_tok, nx, k, y, ctx)
+        step_fns[step_i[0] % nrot]()
+        step_i[0] += 1
 
     def barrier():
         if world > 1:
@@ -301,17 +340,22 @@ def run_ours(args, rank, world, local_rank):
     # programmatic-dependent-launch edges, and host launch overhead (Python + C ABI, ~10 us
     # per call) leaves the timed region. --no-graph times the eager launches instead.
     graph = None
-    if not args.no_graph:
-        graph = torch.cuda.CUDAGraph()
+    eager_step = step
+    if not args.no_graph and gather_out is None:
+        graphs = []
         n0 = ctx.launch_count()
-        with torch.cuda.graph(graph, stream=stream):
-            step()
-        graph_launches = ctx.launch_count() - n0
+        for r in range(nrot):
+            gr = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gr, stream=stream):
+                step_fns[r]()
+            graphs.append(gr)
+        graph_launches = (ctx.launch_count() - n0) // nrot
+        graph = graphs[0]
         torch.cuda.synchronize()
-        eager_step = step
 
         def step():  # noqa: F811
-            graph.replay()
+            graphs[step_i[0] % nrot].replay()
+            step_i[0] += 1
         step()
         torch.cuda.synchronize()
     # heat: ~1 s of untimed steps so clocks settle and the sampler sees the load
@@ -359,7 +403,9 @@ def run_ours(args, rank, world, local_rank):
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
-    value = world * args.steps * ops_step / (ms_max * 1e-3) / 1e12
+    # whole-job work per step: the full GEMM when sharded (strong), else every rank's GEMMs
+    job_ops_step = sum(ops_of(g) for g in full_gemms) if sharded else world * ops_step
+    value = args.steps * job_ops_step / (ms_max * 1e-3) / 1e12
 
     # -- e2e through the public host API: pinned host planes -> H2D -> GEMM -> D2H int32
     if args.profile:
@@ -368,7 +414,8 @@ def run_ours(args, rank, world, local_rank):
     e2e_steps = max(1, min(args.steps, 3))
     host = []
     h2d = d2h = 0
-    for (g, (wp, xp, y)) in zip(gemms, bufs):
+    for (g, (wps, xp, y)) in zip(gemms, bufs):
+        wp = wps[0]
         hw = torch.empty(wp.shape, dtype=torch.int32, pin_memory=True)
         hx = torch.empty(xp.shape, dtype=torch.int32, pin_memory=True)
         hy = torch.empty(tuple(y.shape), dtype=torch.int32, pin_memory=True)
@@ -399,7 +446,7 @@ def run_ours(args, rank, world, local_rank):
     te = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e_val = world * e2e_steps * ops_step / float(te.item()) / 1e12
+    e2e_val = e2e_steps * job_ops_step / float(te.item()) / 1e12
 
     if rank != 0:
         return
@@ -432,16 +479,21 @@ def run_ours(args, rank, world, local_rank):
         "metric": "effective TOPS (2MNK/s) of WnAm bipolar-INT GEMM",
         "value": value, "unit": "TOPS", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "u8 codes x u8 codes -> s32 (exact int)",
+        "scaling": "strong" if sharded else "weak", "vs_baseline": None,
+        "dtype": "u8 codes x u8 codes -> s32 (exact int)",
         "data": "synthetic (uniform bipolar codes, packed to bit planes on device)",
         "config": {"workload": WORKLOAD_DESC[args.workload], "gemms_per_step": len(gemms),
                    "shapes": [list(g) for g in gemms],
                    "orientation": "matmul_ap(W[N_out x K,n_w], X[M_tok x K,n_x]) -> int32 [N_out x M_tok]",
-                   "parallelism": f"replicas x{world} (N-independent GEMMs per GPU)",
+                   "parallelism": (f"N_out sharded x{world} (row blocks of W, X replicated)"
+                                   + (", NCCL all-gather of Y in the step" if gather_out is not None else "")
+                                   if sharded else f"replicas x{world} (N-independent GEMMs per GPU)"),
                    "launch": "eager" if graph is None else "cuda graph replay of the step",
-                   "l2": "no flush: per-step packed inputs %.0f MB + outputs %.0f MB > 126 MB L2" % (
+                   "l2": ("no flush: per-step packed inputs %.0f MB + outputs %.0f MB > 2 x 126 MB L2" % (
                        sum(packed_bytes(g[0], g[2], g[3]) + packed_bytes(g[1], g[2], g[4]) for g in gemms) / 1e6,
-                       sum(4 * g[0] * g[1] for g in gemms) / 1e6)},
+                       sum(4 * g[0] * g[1] for g in gemms) / 1e6) if nrot == 1 else
+                       "weight planes rotate over %d copies (step s uses copy s %% %d): %.0f MB "
+                       "between reuses > 2 x 126 MB L2" % (nrot, nrot, nrot * step_bytes / 1e6))},
         "clocks": clk,
         "gpu_launches": int(launches),
         "e2e": {"value": e2e_val, "unit": "TOPS", "h2d_bytes_per_step": int(h2d),
@@ -478,6 +530,8 @@ def main():
     ap_.add_argument("--workload", default="sweep4096",
                      choices=list(WORKLOAD_DESC))
     ap_.add_argument("--no-cpu-baseline", action="store_true")
+    ap_.add_argument("--gather", action="store_true",
+                     help="ffn70b under torchrun: all-gather the N-sharded Y (NCCL) inside each step")
     ap_.add_argument("--no-graph", action="store_true",
                      help="time eager launches instead of replaying the step as a CUDA graph")
     ap_.add_argument("--profile", action="store_true",

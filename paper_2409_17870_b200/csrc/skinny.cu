@@ -299,7 +299,10 @@ __global__ void __launch_bounds__(sk_threads(N, NT), sk_ctas_per_sm(N, NT))
     if (warp == 0) {
       for (int i = 0; i < kXPieces; ++i) apmm_ptx::mbar_init(&xbars[i], 1);
     }
-    apmm_ptx::fence_mbar_init();
+    // mbarrier inits -> visible to the TMA unit (async proxy). A non-cluster launch needs
+    // no cluster-scope release (fence.mbarrier_init.release.cluster cost ~0.8 us per CTA at
+    // kernel start, profiles/r01b_skinny_phase_ts2.txt).
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     apmm_ptx::tma_prefetch_desc(&tmap_w);
   }
   __syncwarp();
@@ -323,7 +326,9 @@ __global__ void __launch_bounds__(sk_threads(N, NT), sk_ctas_per_sm(N, NT))
 
   // The weight planes are inputs of this call, so their loads may overlap the prep kernel
   // still running ahead of us (PDL); X, the workspace and Y only after pdl_wait.
+  if (p.ts && tid == 0) p.ts[blockIdx.x * 8 + 6] = gtime();
   for (uint32_t s = 0; s + 1 < stages; ++s) issue();
+  if (p.ts && tid == 0) p.ts[blockIdx.x * 8 + 7] = gtime();
   apmm_ptx::pdl_wait();
   if (p.ts && tid == 0) p.ts[blockIdx.x * 8 + 1] = gtime();
   __syncthreads();  // xbars initialised
@@ -815,8 +820,8 @@ cudaError_t launch_skinny(const SkinnyArgs& a, cudaStream_t s) {
     cudaMemcpy(h, ts_buf, pl.grid * 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
     unsigned long long t0 = ~0ull;
     for (uint32_t b = 0; b < pl.grid; ++b) t0 = h[b * 8] && h[b * 8] < t0 ? h[b * 8] : t0;
-    const char* names[6] = {"start", "pdl_wait", "x_ready", "item0", "tile0", "end"};
-    for (int k = 0; k < 6; ++k) {
+    const char* names[8] = {"start", "pdl_wait", "x_ready", "item0", "tile0", "end", "inited", "issued"};
+    for (int k = 0; k < 8; ++k) {
       double mn = 1e30, mx = 0, sum = 0;
       uint32_t cnt = 0;
       for (uint32_t b = 0; b < pl.grid; ++b) {
