@@ -336,26 +336,28 @@ def run_ours(args, rank, world, local_rank):
     for _ in range(max(3, args.warmup)):
         step()
     torch.cuda.synchronize()
-    # The step is replayed as a CUDA graph (the serving pattern): the launches keep their
-    # programmatic-dependent-launch edges, and host launch overhead (Python + C ABI, ~10 us
-    # per call) leaves the timed region. --no-graph times the eager launches instead.
+    # The K timed steps are captured as ONE CUDA graph (the serving pattern: a model step is
+    # a chain of these GEMMs) and replayed once in the timed region. The launches keep their
+    # programmatic-dependent-launch edges across GEMM boundaries inside the graph, and host
+    # launch overhead (Python + C ABI, ~10 us per call) leaves the timed region.
+    # --no-graph times the eager launches instead.
     graph = None
     eager_step = step
+    run_timed = None
     if not args.no_graph and gather_out is None:
-        graphs = []
+        graph = torch.cuda.CUDAGraph()
         n0 = ctx.launch_count()
-        for r in range(nrot):
-            gr = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(gr, stream=stream):
-                step_fns[r]()
-            graphs.append(gr)
-        graph_launches = (ctx.launch_count() - n0) // nrot
-        graph = graphs[0]
+        with torch.cuda.graph(graph, stream=stream):
+            for i in range(args.steps):
+                step_fns[i % nrot]()
+        graph_launches = (ctx.launch_count() - n0) // args.steps
         torch.cuda.synchronize()
 
-        def step():  # noqa: F811
-            graphs[step_i[0] % nrot].replay()
-            step_i[0] += 1
+        def run_timed():
+            graph.replay()
+
+        def step():  # noqa: F811  (heat phase: whole K-step replays)
+            graph.replay()
         step()
         torch.cuda.synchronize()
     # heat: ~1 s of untimed steps so clocks settle and the sampler sees the load
@@ -374,8 +376,11 @@ def run_ours(args, rank, world, local_rank):
     barrier()
     torch.cuda.synchronize()
     ev0.record(stream)
-    for _ in range(args.steps):
-        step()
+    if run_timed is not None:
+        run_timed()  # exactly K steps (one replay of the K-step graph)
+    else:
+        for _ in range(args.steps):
+            step()
     ev1.record(stream)
     torch.cuda.synchronize()
     barrier()
@@ -488,7 +493,7 @@ def run_ours(args, rank, world, local_rank):
                    "parallelism": (f"N_out sharded x{world} (row blocks of W, X replicated)"
                                    + (", NCCL all-gather of Y in the step" if gather_out is not None else "")
                                    if sharded else f"replicas x{world} (N-independent GEMMs per GPU)"),
-                   "launch": "eager" if graph is None else "cuda graph replay of the step",
+                   "launch": "eager" if graph is None else "one cuda graph of the K timed steps",
                    "l2": ("no flush: per-step packed inputs %.0f MB + outputs %.0f MB > 2 x 126 MB L2" % (
                        sum(packed_bytes(g[0], g[2], g[3]) + packed_bytes(g[1], g[2], g[4]) for g in gemms) / 1e6,
                        sum(4 * g[0] * g[1] for g in gemms) / 1e6) if nrot == 1 else

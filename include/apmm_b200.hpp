@@ -11,6 +11,7 @@
 // against an unmodified reference tree.
 #pragma once
 
+#include <algorithm>
 #include <cstdint>
 #include <string>
 #include <vector>
@@ -73,6 +74,47 @@ inline AccumMatrix matmul_ap(const PackedBitPlanes& weights, const PackedBitPlan
   check(apmm_matmul_ap(default_device().get(), weights.words().data(), weights.logical_rows(),
                        weights.width().n(), features.words().data(), features.logical_rows(),
                        features.width().n(), weights.logical_cols(), out.data.data()));
+  return out;
+}
+
+// kernel.hpp:70-71 -- every plane pair, each a 1-bit x 1-bit GEMM on the device.
+inline PlaneProductStack compute_plane_products(const PackedBitPlanes& weights,
+                                                const PackedBitPlanes& features) {
+  if (weights.logical_cols() != features.logical_cols()) {
+    throw DimensionMismatch("operands disagree on K: " + std::to_string(weights.logical_cols()) +
+                            " vs " + std::to_string(features.logical_cols()));
+  }
+  const int nw = weights.width().n(), nx = features.width().n();
+  const std::size_t m = weights.logical_rows(), n = features.logical_rows();
+  std::vector<std::int32_t> flat(static_cast<std::size_t>(nw) * nx * m * n);
+  check(apmm_compute_plane_products(default_device().get(), weights.words().data(), m, nw,
+                                    features.words().data(), n, nx, weights.logical_cols(),
+                                    flat.data()));
+  std::vector<IntMatrix> products;
+  products.reserve(static_cast<std::size_t>(nw) * nx);
+  for (std::size_t p = 0; p < static_cast<std::size_t>(nw) * nx; ++p) {
+    IntMatrix mat(m, n);
+    std::copy(flat.begin() + p * m * n, flat.begin() + (p + 1) * m * n, mat.data.begin());
+    products.push_back(std::move(mat));
+  }
+  return {weights.width(), features.width(), weights.logical_cols(), std::move(products)};
+}
+
+// kernel.hpp:74 -- shift-and-add recovery on the device (int64, checked narrowing).
+inline AccumMatrix recover(const PlaneProductStack& stack) {
+  const int nw = stack.weight_width().n(), nx = stack.feature_width().n();
+  const std::size_t m = stack.rows(), n = stack.cols();
+  std::vector<std::int32_t> flat(static_cast<std::size_t>(nw) * nx * m * n);
+  for (int i = 0; i < nw; ++i) {
+    for (int j = 0; j < nx; ++j) {
+      const IntMatrix& p = stack.product(static_cast<unsigned>(i), static_cast<unsigned>(j));
+      std::copy(p.data.begin(), p.data.end(),
+                flat.begin() + (static_cast<std::size_t>(i) * nx + j) * m * n);
+    }
+  }
+  AccumMatrix out(m, n);
+  check(apmm_recover(default_device().get(), flat.data(), nw, nx, stack.k_logical(), m, n,
+                     out.data.data()));
   return out;
 }
 

@@ -107,7 +107,7 @@ APMM_API int apmm_cu_unpack(apmm_ctx* ctx, const uint32_t* planes, uint64_t rows
  * per-row). Arithmetic is IEEE fp64 exactly as the reference, so codes and scales are
  * bit-identical. `codes` may be NULL; when given it also receives the u8 codes.
  * Non-finite input is detected on device and reported as APMM_E_NON_FINITE after a
- * stream synchronisation (the only synchronising device entry point). */
+ * stream synchronisation (like apmm_cu_recover, a synchronising device entry point). */
 APMM_API int apmm_cu_quantize_pack(apmm_ctx* ctx, const double* values, uint64_t rows, uint64_t cols,
                           int n, int granularity, uint32_t* planes, double* scales,
                           uint8_t* codes, apmm_stream_t stream);
@@ -131,6 +131,31 @@ APMM_API int apmm_cu_matmul_ap_dequant(apmm_ctx* ctx, const uint32_t* w_planes, 
                               const double* x_scales, int x_granularity, uint64_t k,
                               float* out, apmm_stream_t stream);
 
+/* matmul_plane_pair (kernel.hpp:66-67, kernel.cpp:125-144): Y(m,n) = dot of weight plane
+ * `weight_plane` row m with feature plane `feature_plane` row n, K - 2 popc(a ^ b), int32
+ * [rows_w x rows_x]. Planes out of range -> APMM_E_INDEX_OUT_OF_BOUNDS; K > INT32_MAX ->
+ * APMM_E_OVERFLOW_BOUND. Runs as a 1-bit x 1-bit matmul_ap on the plane slices. */
+APMM_API int apmm_cu_matmul_plane_pair(apmm_ctx* ctx, const uint32_t* w_planes, uint64_t rows_w,
+                              int n_w, int weight_plane, const uint32_t* x_planes,
+                              uint64_t rows_x, int n_x, int feature_plane, uint64_t k,
+                              int32_t* y, apmm_stream_t stream);
+
+/* compute_plane_products (kernel.hpp:70-71, kernel.cpp:146-157): every plane pair,
+ * stack[(i*n_x + j)][m][n] int32 (PlaneProductStack order, kernel.cpp:103-113). Debug /
+ * property path: n_w*n_x GEMMs and an n_w*n_x x larger intermediate -- matmul_ap never forms
+ * it. */
+APMM_API int apmm_cu_compute_plane_products(apmm_ctx* ctx, const uint32_t* w_planes,
+                                   uint64_t rows_w, int n_w, const uint32_t* x_planes,
+                                   uint64_t rows_x, int n_x, uint64_t k, int32_t* stack,
+                                   apmm_stream_t stream);
+
+/* recover (kernel.hpp:74, kernel.cpp:159-181): y = sum_ij 2^(i+j) stack[i][j] in int64,
+ * checked narrowing. Validates like the PlaneProductStack constructor: an entry outside
+ * [-k, k] -> APMM_E_OUT_OF_RANGE (kernel.cpp:91-101); a result outside int32 ->
+ * APMM_E_OVERFLOW. Synchronises the stream to report those. */
+APMM_API int apmm_cu_recover(apmm_ctx* ctx, const int32_t* stack, int n_w, int n_x, uint64_t k,
+                    uint64_t rows, uint64_t cols, int32_t* y, apmm_stream_t stream);
+
 /* ---- host entry points (synchronous, host pointers) ------------------------------- */
 /* These mirror the reference functions one for one and add the H2D/D2H copies. */
 
@@ -149,6 +174,15 @@ APMM_API int apmm_unpack(apmm_ctx* ctx, const uint32_t* planes, uint64_t rows, u
 APMM_API int apmm_quantize_pack(apmm_ctx* ctx, const double* values, uint64_t rows, uint64_t cols,
                        int n, int granularity, uint8_t* codes, uint32_t* planes,
                        double* scales);
+
+/* compute_plane_products (kernel.cpp:146-157) with host buffers; validates padding. */
+APMM_API int apmm_compute_plane_products(apmm_ctx* ctx, const uint32_t* w_planes, uint64_t rows_w,
+                                int n_w, const uint32_t* x_planes, uint64_t rows_x, int n_x,
+                                uint64_t k, int32_t* stack);
+
+/* recover (kernel.cpp:159-181) with host buffers. */
+APMM_API int apmm_recover(apmm_ctx* ctx, const int32_t* stack, int n_w, int n_x, uint64_t k,
+                 uint64_t rows, uint64_t cols, int32_t* y);
 
 /* matmul_ap (kernel.cpp:187-254). Validates padding like PackedBitPlanes
  * (bitplane.cpp:22-32), then K agreement and overflow_bound like kernel.cpp:189-199. */

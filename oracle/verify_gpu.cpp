@@ -6,6 +6,7 @@
 //   _ref/verify_gpu [seed] [cases]     exit 0 iff every property passes AND the mutant fails
 #include <cstdio>
 #include <cstdlib>
+#include <random>
 #include <string>
 
 #include "apmm/verify.hpp"
@@ -35,6 +36,41 @@ int main(int argc, char** argv) {
       if (y.rows * y.cols > 3) y.data[y.data.size() / 2] += 2;
       return y;
     };
+    // the debug/property path on the device: compute_plane_products + recover against the
+    // reference's own functions (kernel.cpp:146-181), and recover's error behaviour
+    std::mt19937_64 gen(opt.seed);
+    int pp_bad = 0;
+    for (int c = 0; c < 100; ++c) {
+      const std::size_t m = 1 + gen() % 24, n = 1 + gen() % 24, k = 1 + gen() % 300;
+      const int nw = 1 + static_cast<int>(gen() % 8), nx = 1 + static_cast<int>(gen() % 8);
+      std::vector<std::uint8_t> wb(m * k), xb(n * k);
+      for (auto& v : wb) v = static_cast<std::uint8_t>(gen() % (1u << nw));
+      for (auto& v : xb) v = static_cast<std::uint8_t>(gen() % (1u << nx));
+      const auto w = apmm::decompose_and_pack(apmm::CodeMatrix(m, k, apmm::BitWidth(nw), wb));
+      const auto x = apmm::decompose_and_pack(apmm::CodeMatrix(n, k, apmm::BitWidth(nx), xb));
+      const auto ref = apmm::compute_plane_products(w, x);
+      const auto got = apmm::b200::compute_plane_products(w, x);
+      for (int i = 0; i < nw; ++i) {
+        for (int j = 0; j < nx; ++j) {
+          if (!(got.product(i, j) == ref.product(i, j))) ++pp_bad;
+        }
+      }
+      if (!(apmm::b200::recover(got) == apmm::recover(ref))) ++pp_bad;
+    }
+    std::printf("%s compute_plane_products + recover on the device (100 cases)\n",
+                pp_bad ? "FAIL" : "PASS");
+    if (pp_bad) rc = 1;
+    {  // recover must throw Overflow exactly like the reference (kernel.cpp:172-176)
+      std::vector<apmm::IntMatrix> prods(64, apmm::IntMatrix(1, 1));
+      for (auto& p : prods) p.data[0] = 40000;
+      const apmm::PlaneProductStack big(apmm::BitWidth(8), apmm::BitWidth(8), 40000, prods);
+      bool ref_threw = false, gpu_threw = false;
+      try { apmm::recover(big); } catch (const apmm::Overflow&) { ref_threw = true; }
+      try { apmm::b200::recover(big); } catch (const apmm::Overflow&) { gpu_threw = true; }
+      std::printf("%s recover overflow (reference %d, device %d)\n",
+                  ref_threw == gpu_threw && gpu_threw ? "PASS" : "FAIL", ref_threw, gpu_threw);
+      if (!(ref_threw && gpu_threw)) rc = 1;
+    }
     apmm::VerifyOptions mopt = opt;
     mopt.cases = 50;
     const apmm::VerifyReport bad = apmm::run_verify(mopt, mutant);

@@ -303,6 +303,87 @@ def matmul_ap(weights: PackedBitPlanes, features: PackedBitPlanes,
     return y
 
 
+class PlaneProductStack:
+    """kernel.hpp:36-56 / kernel.cpp:79-113: the n_w*n_x plane-pair products of one
+    multiplication, entry [i, j] = weight plane i x feature plane j, each in [-K, K]."""
+
+    def __init__(self, weight_width: BitWidth, feature_width: BitWidth, k_logical: int,
+                 products: np.ndarray):
+        products = np.ascontiguousarray(products, dtype=np.int32)
+        if products.ndim != 4 or products.shape[:2] != (weight_width.n(), feature_width.n()):
+            raise LengthMismatch(f"expected {weight_width.n() * feature_width.n()} plane products")
+        self._ww, self._fw, self._k, self._p = weight_width, feature_width, int(k_logical), products
+
+    def weight_width(self) -> BitWidth:
+        return self._ww
+
+    def feature_width(self) -> BitWidth:
+        return self._fw
+
+    def k_logical(self) -> int:
+        return self._k
+
+    def rows(self) -> int:
+        return self._p.shape[2]
+
+    def cols(self) -> int:
+        return self._p.shape[3]
+
+    def product(self, weight_plane: int, feature_plane: int) -> np.ndarray:
+        if not (0 <= weight_plane < self._ww.n() and 0 <= feature_plane < self._fw.n()):
+            raise IndexOutOfBounds(f"plane pair ({weight_plane}, {feature_plane}) out of range")
+        return self._p[weight_plane, feature_plane]
+
+    def products(self) -> np.ndarray:
+        return self._p
+
+
+def matmul_plane_pair(weights: PackedBitPlanes, weight_plane: int, features: PackedBitPlanes,
+                      feature_plane: int, ctx: Context | None = None) -> np.ndarray:
+    """kernel.cpp:125-144 on the GPU: XOR dots of one weight plane against one feature plane."""
+    ctx = ctx or default_context()
+    if weights.logical_cols() != features.logical_cols():
+        raise DimensionMismatch(f"operands disagree on K: {weights.logical_cols()} vs "
+                                f"{features.logical_cols()}")
+    import torch
+    k = weights.logical_cols()
+    dev = torch.device("cuda", ctx.device)
+    w = torch.from_numpy(weights.words().view(np.int32)).to(dev)
+    x = torch.from_numpy(features.words().view(np.int32)).to(dev)
+    y = torch.empty((weights.logical_rows(), features.logical_rows()), dtype=torch.int32, device=dev)
+    _check(ctx.lib.apmm_cu_matmul_plane_pair(
+        ctx.h, C.c_void_p(w.data_ptr()), weights.logical_rows(), weights.width().n(),
+        int(weight_plane), C.c_void_p(x.data_ptr()), features.logical_rows(),
+        features.width().n(), int(feature_plane), k, C.c_void_p(y.data_ptr()), None))
+    return y.cpu().numpy()
+
+
+def compute_plane_products(weights: PackedBitPlanes, features: PackedBitPlanes,
+                           ctx: Context | None = None) -> PlaneProductStack:
+    """kernel.cpp:146-157 on the GPU (debug / property path; matmul_ap never forms it)."""
+    ctx = ctx or default_context()
+    if weights.logical_cols() != features.logical_cols():
+        raise DimensionMismatch(f"operands disagree on K: {weights.logical_cols()} vs "
+                                f"{features.logical_cols()}")
+    nw, nx = weights.width().n(), features.width().n()
+    stack = np.empty((nw, nx, weights.logical_rows(), features.logical_rows()), dtype=np.int32)
+    _check(ctx.lib.apmm_compute_plane_products(
+        ctx.h, _ptr(weights.words()), weights.logical_rows(), nw, _ptr(features.words()),
+        features.logical_rows(), nx, weights.logical_cols(), _ptr(stack)))
+    return PlaneProductStack(weights.width(), features.width(), weights.logical_cols(), stack)
+
+
+def recover(stack: PlaneProductStack, ctx: Context | None = None) -> np.ndarray:
+    """kernel.cpp:159-181 on the GPU: sum of 2^(i+j) Y^(i,j) in int64, checked narrowing."""
+    ctx = ctx or default_context()
+    p = stack.products()
+    y = np.empty((stack.rows(), stack.cols()), dtype=np.int32)
+    _check(ctx.lib.apmm_recover(ctx.h, _ptr(p), stack.weight_width().n(),
+                                stack.feature_width().n(), stack.k_logical(), stack.rows(),
+                                stack.cols(), _ptr(y)))
+    return y
+
+
 def matmul_ap_dequant(weights: PackedBitPlanes, w_scales, w_granularity: Granularity,
                       features: PackedBitPlanes, x_scales, x_granularity: Granularity,
                       ctx: Context | None = None) -> np.ndarray:

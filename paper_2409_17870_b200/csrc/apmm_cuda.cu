@@ -40,7 +40,8 @@ struct apmm_ctx {
   size_t sk_scratch_bytes = 0;
   bool force_tc = false;  // APMM_FORCE_TC=1: never use K5 (testing)
   bool dbg_waits = false;  // APMM_DEBUG_WAITS=1: MMA-issuer wait-cycle counters (dev only)
-  void* dbg = nullptr;  // APMM_FORCE_1SM=1: always use the 1-SM kernel (testing)
+  void* dbg = nullptr;  // APMM_DEBUG_WAITS counters (dev only)
+  int* flags = nullptr;  // recover's device error flags (2 ints)
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pending[2];
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> spare;
 };
@@ -388,6 +389,7 @@ int apmm_ctx_destroy(apmm_ctx* ctx) {
     }
     cudaFree(ctx->dbg);
   }
+  if (ctx->flags) cudaFree(ctx->flags);
   if (ctx->ws) cudaFree(ctx->ws);
   if (ctx->sk_ws) cudaFree(ctx->sk_ws);
   if (ctx->sk_scratch) cudaFree(ctx->sk_scratch);
@@ -522,6 +524,61 @@ int apmm_cu_matmul_ap_dequant(apmm_ctx* ctx, const uint32_t* w_planes, uint64_t 
                     x_scales, x_granularity, k, nullptr, out, pick(ctx, stream));
 }
 
+int apmm_cu_matmul_plane_pair(apmm_ctx* ctx, const uint32_t* w_planes, uint64_t rows_w, int n_w,
+                              int weight_plane, const uint32_t* x_planes, uint64_t rows_x,
+                              int n_x, int feature_plane, uint64_t k, int32_t* y,
+                              apmm_stream_t stream) {
+  int st;
+  if (!ctx || !w_planes || !x_planes || !y) return fail(APMM_E_INVALID_ARGUMENT, "null argument");
+  if ((st = check_width(n_w)) || (st = check_width(n_x))) return st;
+  if (weight_plane < 0 || weight_plane >= n_w || feature_plane < 0 || feature_plane >= n_x) {
+    return fail(APMM_E_INDEX_OUT_OF_BOUNDS, "plane pair (%d, %d) out of range", weight_plane,
+                feature_plane);
+  }
+  // one plane of a packed buffer is itself a 1-bit packed buffer; a 1-bit x 1-bit matmul_ap
+  // is exactly the XOR dot  K - 2 popc(a ^ b)  of kernel.cpp:115-144 (v = 2u - 1 = +-1)
+  if ((st = check_matmul(1, 1, rows_w, rows_x, k))) return st;
+  const uint64_t wpr = (k + 31) / 32;
+  return run_matmul(ctx, w_planes + uint64_t(weight_plane) * rows_w * wpr, rows_w, 1, nullptr, 0,
+                    x_planes + uint64_t(feature_plane) * rows_x * wpr, rows_x, 1, nullptr, 0, k,
+                    y, nullptr, pick(ctx, stream));
+}
+
+int apmm_cu_compute_plane_products(apmm_ctx* ctx, const uint32_t* w_planes, uint64_t rows_w,
+                                   int n_w, const uint32_t* x_planes, uint64_t rows_x, int n_x,
+                                   uint64_t k, int32_t* stack, apmm_stream_t stream) {
+  if (!ctx || !stack) return fail(APMM_E_INVALID_ARGUMENT, "null argument");
+  int st;
+  if ((st = check_width(n_w)) || (st = check_width(n_x))) return st;
+  for (int i = 0; i < n_w; ++i) {
+    for (int j = 0; j < n_x; ++j) {
+      st = apmm_cu_matmul_plane_pair(ctx, w_planes, rows_w, n_w, i, x_planes, rows_x, n_x, j, k,
+                                     stack + uint64_t(i * n_x + j) * rows_w * rows_x, stream);
+      if (st) return st;
+    }
+  }
+  return APMM_OK;
+}
+
+int apmm_cu_recover(apmm_ctx* ctx, const int32_t* stack, int n_w, int n_x, uint64_t k,
+                    uint64_t rows, uint64_t cols, int32_t* y, apmm_stream_t stream) {
+  int st;
+  if (!ctx || !stack || !y) return fail(APMM_E_INVALID_ARGUMENT, "null argument");
+  if ((st = check_width(n_w)) || (st = check_width(n_x))) return st;
+  CU(cudaSetDevice(ctx->device));
+  if (!ctx->flags) CU(cudaMalloc(&ctx->flags, 2 * sizeof(int)));
+  const cudaStream_t s = pick(ctx, stream);
+  CU(cudaMemsetAsync(ctx->flags, 0, 2 * sizeof(int), s));
+  CU(launch_recover(stack, n_w, n_x, rows * cols, k, y, ctx->flags, s));
+  ctx->launches += 1;
+  int h[2] = {0, 0};
+  CU(cudaMemcpyAsync(h, ctx->flags, sizeof(h), cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  if (h[0]) return fail(APMM_E_OUT_OF_RANGE, "plane product entry outside [-K, K]");
+  if (h[1]) return fail(APMM_E_OVERFLOW, "recovered value exceeds 32-bit range");
+  return APMM_OK;
+}
+
 // ---- host entry points ------------------------------------------------------------------
 int apmm_decompose_and_pack(apmm_ctx* ctx, const uint8_t* codes, uint64_t rows, uint64_t cols,
                             int n, uint32_t* planes) {
@@ -627,6 +684,58 @@ static int host_matmul(apmm_ctx* ctx, const uint32_t* w, uint64_t rows_w, int n_
   if (st) return st;
   CU(cudaMemcpyAsync(yf ? static_cast<void*>(yf) : static_cast<void*>(y), d_y, rows_w * rows_x * 4,
                      cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  return APMM_OK;
+}
+
+int apmm_compute_plane_products(apmm_ctx* ctx, const uint32_t* w_planes, uint64_t rows_w,
+                                int n_w, const uint32_t* x_planes, uint64_t rows_x, int n_x,
+                                uint64_t k, int32_t* stack) {
+  int st;
+  if (!ctx || !w_planes || !x_planes || !stack) return fail(APMM_E_INVALID_ARGUMENT, "null argument");
+  if ((st = check_width(n_w)) || (st = check_width(n_x))) return st;
+  if ((st = check_dims(rows_w, k, "weights")) || (st = check_dims(rows_x, k, "features"))) return st;
+  if ((st = check_padding(w_planes, rows_w, k, n_w)) || (st = check_padding(x_planes, rows_x, k, n_x))) {
+    return st;
+  }
+  if ((st = check_matmul(1, 1, rows_w, rows_x, k))) return st;
+  const size_t w_words = apmm_packed_words(n_w, rows_w, k), x_words = apmm_packed_words(n_x, rows_x, k);
+  const size_t w_b = align_up(w_words * 4), x_b = align_up(x_words * 4);
+  const size_t s_n = size_t(n_w) * n_x * rows_w * rows_x;
+  if ((st = ensure(&ctx->io, &ctx->io_bytes, w_b + x_b + align_up(s_n * 4), ctx->device))) return st;
+  CU(cudaSetDevice(ctx->device));
+  uint8_t* base = static_cast<uint8_t*>(ctx->io);
+  uint32_t* d_w = reinterpret_cast<uint32_t*>(base);
+  uint32_t* d_x = reinterpret_cast<uint32_t*>(base + w_b);
+  int32_t* d_s = reinterpret_cast<int32_t*>(base + w_b + x_b);
+  CU(cudaMemcpyAsync(d_w, w_planes, w_words * 4, cudaMemcpyHostToDevice, ctx->stream));
+  CU(cudaMemcpyAsync(d_x, x_planes, x_words * 4, cudaMemcpyHostToDevice, ctx->stream));
+  if ((st = apmm_cu_compute_plane_products(ctx, d_w, rows_w, n_w, d_x, rows_x, n_x, k, d_s,
+                                            reinterpret_cast<apmm_stream_t>(ctx->stream)))) {
+    return st;
+  }
+  CU(cudaMemcpyAsync(stack, d_s, s_n * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  return APMM_OK;
+}
+
+int apmm_recover(apmm_ctx* ctx, const int32_t* stack, int n_w, int n_x, uint64_t k,
+                 uint64_t rows, uint64_t cols, int32_t* y) {
+  int st;
+  if (!ctx || !stack || !y) return fail(APMM_E_INVALID_ARGUMENT, "null argument");
+  if ((st = check_width(n_w)) || (st = check_width(n_x))) return st;
+  const size_t s_n = size_t(n_w) * n_x * rows * cols;
+  const size_t s_b = align_up(s_n * 4);
+  if ((st = ensure(&ctx->io, &ctx->io_bytes, s_b + align_up(rows * cols * 4), ctx->device))) return st;
+  CU(cudaSetDevice(ctx->device));
+  int32_t* d_s = static_cast<int32_t*>(ctx->io);
+  int32_t* d_y = reinterpret_cast<int32_t*>(static_cast<uint8_t*>(ctx->io) + s_b);
+  CU(cudaMemcpyAsync(d_s, stack, s_n * 4, cudaMemcpyHostToDevice, ctx->stream));
+  if ((st = apmm_cu_recover(ctx, d_s, n_w, n_x, k, rows, cols, d_y,
+                            reinterpret_cast<apmm_stream_t>(ctx->stream)))) {
+    return st;
+  }
+  CU(cudaMemcpyAsync(y, d_y, rows * cols * 4, cudaMemcpyDeviceToHost, ctx->stream));
   CU(cudaStreamSynchronize(ctx->stream));
   return APMM_OK;
 }

@@ -38,6 +38,13 @@ cudaError_t launch_quantize_pack(const double* x, uint64_t rows, uint64_t cols, 
                                  uint8_t* codes, unsigned long long* amax_bits, int* flag,
                                  cudaStream_t s);
 
+// recover (kernel.cpp:159-181) over a device plane-product stack [n_w*n_x][m*n] int32:
+// y = sum 2^(i+j) stack[i][j] in int64, narrowed to int32. flags[0] <- 1 if an entry lies
+// outside [-k, k] (PlaneProductStack ctor, kernel.cpp:91-101), flags[1] <- 1 if a recovered
+// value does not fit int32 (kernel.cpp:172-176). Flags must be zero on entry.
+cudaError_t launch_recover(const int32_t* stack, int n_w, int n_x, uint64_t mn, uint64_t k,
+                           int32_t* y, int* flags, cudaStream_t s);
+
 // ---- gemm_tc.cu ----------------------------------------------------------------------
 struct GemmArgs {
   const uint8_t* codes_w;   // [rows_w x kpad]

@@ -313,6 +313,27 @@ __global__ void __launch_bounds__(kThreads)
   quantize_pack_word(x + r * cols, r, rows, cols, w, n, maxv, s, planes, codes);
 }
 
+// recover: one thread per output element, int64 accumulation of the shifted plane products
+__global__ void __launch_bounds__(kThreads) recover_kernel(const int32_t* __restrict__ stack,
+                                                           int n_w, int n_x, uint64_t mn,
+                                                           int64_t k, int32_t* __restrict__ y,
+                                                           int* __restrict__ flags) {
+  const uint64_t e = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= mn) return;
+  int64_t acc = 0;
+  bool range_ok = true;
+  for (int i = 0; i < n_w; ++i) {
+    for (int j = 0; j < n_x; ++j) {
+      const int64_t v = __ldg(stack + uint64_t(i * n_x + j) * mn + e);
+      range_ok &= v <= k && v >= -k;
+      acc += v * (int64_t(1) << (i + j));
+    }
+  }
+  if (!range_ok) atomicOr(flags + 0, 1);
+  if (acc > INT32_MAX || acc < INT32_MIN) atomicOr(flags + 1, 1);
+  y[e] = static_cast<int32_t>(acc);
+}
+
 unsigned blocks_for(uint64_t threads) {
   return static_cast<unsigned>((threads + kThreads - 1) / kThreads);
 }
@@ -350,6 +371,14 @@ cudaError_t launch_expand(const uint32_t* w_planes, uint64_t rows_w, int n_w,
   cudaError_t e = cudaLaunchKernelEx(&cfg, expand_kernel, a, b, wpr, tail_mask,
                                      static_cast<uint32_t>(kpad / 32));
   return e != cudaSuccess ? e : cudaGetLastError();
+}
+
+cudaError_t launch_recover(const int32_t* stack, int n_w, int n_x, uint64_t mn, uint64_t k,
+                           int32_t* y, int* flags, cudaStream_t s) {
+  if (mn == 0) return cudaSuccess;
+  recover_kernel<<<blocks_for(mn), kThreads, 0, s>>>(stack, n_w, n_x, mn, static_cast<int64_t>(k),
+                                                     y, flags);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_pack(const uint8_t* codes, uint64_t rows, uint64_t cols, int n,

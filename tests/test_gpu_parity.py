@@ -396,4 +396,48 @@ def test_reference_run_verify_with_gpu_kernel():
     for seed in ("1", "2"):
         r = subprocess.run([exe, seed, "1000"], capture_output=True, text=True, timeout=600)
         assert r.returncode == 0, r.stdout + r.stderr
-        assert r.stdout.count("PASS") == 9 and "mutant kernel caught" in r.stdout
+        assert r.stdout.count("PASS") == 11 and "mutant kernel caught" in r.stdout
+        assert "PASS compute_plane_products + recover on the device" in r.stdout
+
+
+# ---------------------------------------------------------------- plane products / recover
+def test_plane_products_and_recover_match_oracle(gpu, oracle):
+    """compute_plane_products / matmul_plane_pair / recover (kernel.cpp:125-181) on the GPU
+    vs the C restatement, on the reference's seeded corpus shapes plus a tile-sized case."""
+    ap, ctx = gpu
+    rng = oracle.rng(41)
+    cases = [(rng.range(1, 24), rng.range(1, 24), rng.range(1, 300), rng.range(1, 8),
+              rng.range(1, 8)) for _ in range(60)] + [(300, 260, 1000, 3, 4), (5, 70, 33025, 1, 1)]
+    for (m, n, k, nw, nx) in cases:
+        wc, xc = rng.random_codes(m, k, nw), rng.random_codes(n, k, nx)
+        wp, xp = oracle.pack(wc, nw), oracle.pack(xc, nx)
+        want = oracle.plane_products(wp, m, nw, xp, n, nx, k).reshape(nw, nx, m, n)
+        w = ap.PackedBitPlanes(m, k, ap.BitWidth(nw), wp)
+        x = ap.PackedBitPlanes(n, k, ap.BitWidth(nx), xp)
+        stack = ap.compute_plane_products(w, x, ctx)
+        assert np.array_equal(stack.products(), want), (m, n, k, nw, nx)
+        i, j = nw - 1, nx - 1
+        assert np.array_equal(ap.matmul_plane_pair(w, i, x, j, ctx), want[i, j])
+        if oracle.overflow_bound(nw, nx, k) <= 2**31 - 1:
+            assert np.array_equal(ap.recover(stack, ctx), oracle.recover(want))
+
+
+def test_plane_product_and_recover_errors(gpu, oracle):
+    ap, ctx = gpu
+    wc = np.array([[0b11, 0b10]], np.uint8)
+    w = ap.PackedBitPlanes(1, 2, ap.BitWidth(2), oracle.pack(wc, 2))
+    with pytest.raises(ap.IndexOutOfBounds):  # plane_row range (bitplane.cpp:40-45)
+        ap.matmul_plane_pair(w, 2, w, 0, ctx)
+    # worked example (test_kernel.cpp:125-136): planes (0,-2,2,0) recover to 0
+    x = ap.PackedBitPlanes(1, 2, ap.BitWidth(2), oracle.pack(np.array([[0b01, 0b11]], np.uint8), 2))
+    st = ap.compute_plane_products(w, x, ctx)
+    assert st.products().reshape(-1).tolist() == [0, -2, 2, 0] and ap.recover(st, ctx).tolist() == [[0]]
+    # recover narrows with a check -> Overflow (kernel.cpp:172-176)
+    big = ap.PlaneProductStack(ap.BitWidth(8), ap.BitWidth(8), 40000,
+                               np.full((8, 8, 1, 1), 40000, np.int32))
+    with pytest.raises(ap.Overflow):
+        ap.recover(big, ctx)
+    # entries outside [-K, K] are an OutOfRange, as the PlaneProductStack ctor (kernel.cpp:91-101)
+    bad = ap.PlaneProductStack(ap.BitWidth(1), ap.BitWidth(1), 3, np.full((1, 1, 2, 2), 4, np.int32))
+    with pytest.raises(ap.OutOfRange):
+        ap.recover(bad, ctx)
