@@ -390,17 +390,33 @@ def run_ours(args, rank, world, local_rank):
     clk = clocks.stop()
     ms = ev0.elapsed_time(ev1)
     # -- kernel pass (roofline): the same K steps again with every GEMM / expand launch
-    #    bracketed by CUDA events on its launch stream (serialises expand and GEMM)
+    #    bracketed by CUDA events on its launch stream (serialises expand and GEMM). In
+    #    graph mode the bracketed steps are captured as a graph too, so the event pairs
+    #    time the kernels, not the host's launch gaps (decode kernels are shorter than the
+    #    ~10 us Python + C ABI call).
     ctx.kernel_time(0)
     ctx.kernel_time(1)
-    ctx.enable_timing(True)
     ek0, ek1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    ek0.record(stream)
-    for _ in range(args.steps):
-        (eager_step if graph is not None else step)()
-    ek1.record(stream)
-    torch.cuda.synchronize()
-    ctx.enable_timing(False)
+    if graph is not None:
+        ctx.enable_timing(True)
+        kgraph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(kgraph, stream=stream):
+            for i in range(args.steps):
+                step_fns[i % nrot]()
+        ctx.enable_timing(False)
+        torch.cuda.synchronize()
+        ek0.record(stream)
+        kgraph.replay()
+        ek1.record(stream)
+        torch.cuda.synchronize()
+    else:
+        ctx.enable_timing(True)
+        ek0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ek1.record(stream)
+        torch.cuda.synchronize()
+        ctx.enable_timing(False)
     ms_serial = ek0.elapsed_time(ek1)
     gemm_ms, gemm_n = ctx.kernel_time(0)
     exp_ms, exp_n = ctx.kernel_time(1)

@@ -92,6 +92,10 @@ struct SkinnyArgs {
   void* acc_ws;      // skinny_acc_bytes(): split-K accumulators, zero on entry, left zero
   void* scratch_ws;  // skinny_scratch_bytes(): feature fragments (2 halves) + weight repack
   int ws_half;       // ping-pong half for the feature fragments (PDL overlap of calls)
+  // measurement (bench kernel pass): when non-null, recorded right before / after the
+  // streaming kernel's launch (after the feature-prep kernel), with `ev_flags`
+  cudaEvent_t ev_start = nullptr, ev_stop = nullptr;
+  unsigned ev_flags = 0;
 };
 size_t skinny_acc_bytes(uint64_t rows_w, uint64_t rows_x);
 size_t skinny_scratch_bytes(uint64_t rows_w, uint64_t rows_x, uint64_t k, int n_w,

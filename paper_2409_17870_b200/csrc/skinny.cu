@@ -90,6 +90,7 @@ struct SkinnyParams {
   const uint8_t* xfrag;      // prep output: [chunks_total][chunk_bytes_m(frag_rows(rows_x))]
   const uint32_t* x_planes;  // inprep: reference layout [n_x][rows_x][wpr]
   uint32_t inprep;           // 1: this kernel builds its X slice itself (no prep kernel)
+  uint32_t prefetch;         // L2 prefetch distance in ring items (0: off)
   uint32_t n_x, k_logical;
   const int32_t* rsx;        // prep output: rowsum(U_x) parts [rows_x][rsx_parts]
   uint32_t rsx_parts;
@@ -135,6 +136,13 @@ APMM_DEV void tma_load_3d(uint32_t dst, const void* tmap, uint32_t bar, int32_t 
       " [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(dst),
       "l"(reinterpret_cast<uint64_t>(tmap)), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "l"(hint)
       : "memory");
+}
+// Prefetch one weight tile into L2 (no shared memory, no completion).
+APMM_DEV void tma_prefetch_l2_3d(const void* tmap, int32_t c0, int32_t c1, int32_t c2) {
+  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global [%0, {%1, %2, %3}];" ::"l"(
+                   reinterpret_cast<uint64_t>(tmap)),
+               "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
 }
 // One bulk (non-tensor) TMA copy global -> this CTA's shared memory, completing on `bar`.
 APMM_DEV void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
@@ -309,8 +317,23 @@ __global__ void __launch_bounds__(sk_threads(N, NT), sk_ctas_per_sm(N, NT))
   const uint64_t hint = apmm_ptx::policy_evict_first();  // weights are read exactly once
 
   // ---- per-warp TMA ring: item cursor (tile index, chunk step) ----
+  // L2 prefetch cursor, kPrefetch items ahead of the ring: the weight stream runs at HBM
+  // rate from the kernel's first microsecond (through the start-up and in whatever order
+  // HBM serves it) while the shallow shared-memory ring refills from L2.
+  uint32_t pf_tile = 0, pf_c = 0;
+  auto prefetch_next = [&]() {
+    if (pf_tile < my_tiles) {
+      const uint32_t chunk = s_begin + pf_c * warps_k + wk;
+      if (chunk < s_end && lane == 0) {
+        const uint32_t row0 = (j0 + pf_tile * gs) * tile_rows + wr * 16u;
+        tma_prefetch_l2_3d(&tmap_w, int32_t(chunk * kChunkWords), int32_t(row0), 0);
+      }
+      if (++pf_c == cpw) { pf_c = 0; ++pf_tile; }
+    }
+  };
   uint32_t is_tile = 0, is_c = 0, is_slot = 0;
   auto issue = [&]() {
+    prefetch_next();
     if (is_tile < my_tiles) {
       const uint32_t chunk = s_begin + is_c * warps_k + wk;
       if (chunk < s_end && lane == 0) {
@@ -327,6 +350,7 @@ __global__ void __launch_bounds__(sk_threads(N, NT), sk_ctas_per_sm(N, NT))
   // The weight planes are inputs of this call, so their loads may overlap the prep kernel
   // still running ahead of us (PDL); X, the workspace and Y only after pdl_wait.
   if (p.ts && tid == 0) p.ts[blockIdx.x * 8 + 6] = gtime();
+  for (uint32_t i = 0; i < stages - 1 + p.prefetch; ++i) prefetch_next();
   for (uint32_t s = 0; s + 1 < stages; ++s) issue();
   if (p.ts && tid == 0) p.ts[blockIdx.x * 8 + 7] = gtime();
   apmm_ptx::pdl_wait();
@@ -752,6 +776,11 @@ cudaError_t launch_skinny(const SkinnyArgs& a, cudaStream_t s) {
   p.xfrag = xfrag;
   p.x_planes = a.x_planes;
   p.inprep = inprep ? 1u : 0u;
+  static const uint32_t prefetch = [] {
+    const char* e = std::getenv("APMM_SK_PREFETCH");
+    return e ? static_cast<uint32_t>(std::atoi(e)) : 0u;  // measured no gain (r01b_skinny_prefetch_sweep.txt)
+  }();
+  p.prefetch = prefetch;
   p.n_x = static_cast<uint32_t>(a.n_x);
   p.k_logical = static_cast<uint32_t>(a.k);
   p.rsx = rsx;
@@ -803,6 +832,7 @@ cudaError_t launch_skinny(const SkinnyArgs& a, cudaStream_t s) {
                                        p.chunks_total * kChunkWords, xfrag, rsx);
     if (e != cudaSuccess) return e;
   }
+  if (a.ev_start) cudaEventRecordWithFlags(a.ev_start, s, a.ev_flags);
   cudaError_t res;
   switch (nt) {
     case 1: res = dispatch_n<1>(a.n_w, split, tm, p, pl.grid, pl.smem, s); break;
@@ -814,6 +844,7 @@ cudaError_t launch_skinny(const SkinnyArgs& a, cudaStream_t s) {
     case 7: res = dispatch_n<7>(a.n_w, split, tm, p, pl.grid, pl.smem, s); break;
     default: res = dispatch_n<8>(a.n_w, split, tm, p, pl.grid, pl.smem, s); break;
   }
+  if (a.ev_stop) cudaEventRecordWithFlags(a.ev_stop, s, a.ev_flags);
   if (want_ts && res == cudaSuccess) {  // dev only: per-phase CTA timeline (us from first start)
     unsigned long long h[1024 * 8];
     cudaStreamSynchronize(s);
