@@ -42,11 +42,16 @@ struct apmm_ctx {
   bool dbg_waits = false;  // APMM_DEBUG_WAITS=1: MMA-issuer wait-cycle counters (dev only)
   void* dbg = nullptr;  // APMM_DEBUG_WAITS counters (dev only)
   int* flags = nullptr;  // recover's device error flags (2 ints)
+  // host entry points' transfer pipeline: H2D / D2H copy streams and their events
+  cudaStream_t s_in = nullptr, s_out = nullptr;
+  cudaEvent_t pipe_ev[16] = {};
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pending[2];
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> spare;
 };
 
 namespace {
+
+constexpr uint64_t kPipeBlocks = 8;  // host_matmul row blocks in flight (events: 2 per block)
 
 thread_local std::string g_last_error;
 
@@ -407,6 +412,11 @@ int apmm_ctx_destroy(apmm_ctx* ctx) {
   if (ctx->sk_scratch) cudaFree(ctx->sk_scratch);
   if (ctx->io) cudaFree(ctx->io);
   if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+  if (ctx->s_in) cudaStreamDestroy(ctx->s_in);
+  if (ctx->s_out) cudaStreamDestroy(ctx->s_out);
+  for (auto& e : ctx->pipe_ev) {
+    if (e) cudaEventDestroy(e);
+  }
   for (auto* v : {&ctx->pending[0], &ctx->pending[1], &ctx->spare}) {
     for (auto& ev : *v) {
       cudaEventDestroy(ev.first);
@@ -658,6 +668,11 @@ int apmm_quantize_pack(apmm_ctx* ctx, const double* values, uint64_t rows, uint6
   return APMM_OK;
 }
 
+// Synchronous host entry point. Large calls are pipelined over row blocks of W (= row
+// blocks of Y): block b's weight planes go up on a copy stream while block b-1 computes on
+// the context stream and block b-2's results come down on a second copy stream, so the
+// PCIe transfers in both directions overlap each other and the GEMMs. Small calls run as
+// one block.
 static int host_matmul(apmm_ctx* ctx, const uint32_t* w, uint64_t rows_w, int n_w,
                        const double* s_w, int gran_w, const uint32_t* x, uint64_t rows_x,
                        int n_x, const double* s_x, int gran_x, uint64_t k, int32_t* y,
@@ -671,6 +686,7 @@ static int host_matmul(apmm_ctx* ctx, const uint32_t* w, uint64_t rows_w, int n_
     return st;
   }
   if ((st = check_matmul(n_w, n_x, rows_w, rows_x, k))) return st;
+  const uint64_t wpr = (k + 31) / 32;
   const size_t w_words = apmm_packed_words(n_w, rows_w, k), x_words = apmm_packed_words(n_x, rows_x, k);
   const size_t w_b = align_up(w_words * 4), x_b = align_up(x_words * 4);
   const size_t y_b = align_up(rows_w * rows_x * 4);
@@ -678,25 +694,57 @@ static int host_matmul(apmm_ctx* ctx, const uint32_t* w, uint64_t rows_w, int n_
   const size_t sw_b = yf ? align_up(sw_n * 8) : 0, sx_b = yf ? align_up(sx_n * 8) : 0;
   if ((st = ensure(&ctx->io, &ctx->io_bytes, w_b + x_b + y_b + sw_b + sx_b, ctx->device))) return st;
   CU(cudaSetDevice(ctx->device));
+  if (!ctx->s_in) {
+    CU(cudaStreamCreateWithFlags(&ctx->s_in, cudaStreamNonBlocking));
+    CU(cudaStreamCreateWithFlags(&ctx->s_out, cudaStreamNonBlocking));
+    for (auto& e : ctx->pipe_ev) CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
   uint8_t* base = static_cast<uint8_t*>(ctx->io);
   uint32_t* d_w = reinterpret_cast<uint32_t*>(base);
   uint32_t* d_x = reinterpret_cast<uint32_t*>(base + w_b);
-  void* d_y = base + w_b + x_b;
+  uint8_t* d_y = base + w_b + x_b;
   double* d_sw = reinterpret_cast<double*>(base + w_b + x_b + y_b);
   double* d_sx = reinterpret_cast<double*>(base + w_b + x_b + y_b + sw_b);
-  CU(cudaMemcpyAsync(d_w, w, w_words * 4, cudaMemcpyHostToDevice, ctx->stream));
-  CU(cudaMemcpyAsync(d_x, x, x_words * 4, cudaMemcpyHostToDevice, ctx->stream));
-  if (yf) {
-    CU(cudaMemcpyAsync(d_sw, s_w, sw_n * 8, cudaMemcpyHostToDevice, ctx->stream));
-    CU(cudaMemcpyAsync(d_sx, s_x, sx_n * 8, cudaMemcpyHostToDevice, ctx->stream));
+  // row blocks: multiples of 256 rows, ~8 MB of output each, at most kPipeBlocks
+  const uint64_t out_row_bytes = rows_x * 4;
+  uint64_t blk = rows_w;
+  if (rows_w * out_row_bytes > (16ull << 20) && rows_w >= 512) {
+    blk = round_up(std::max<uint64_t>((8ull << 20) / out_row_bytes, 256), 256);
+    blk = std::max<uint64_t>(blk, round_up((rows_w + kPipeBlocks - 1) / kPipeBlocks, 256));
+    if (blk > rows_w) blk = rows_w;
   }
-  st = run_matmul(ctx, d_w, rows_w, n_w, d_sw, gran_w, d_x, rows_x, n_x, d_sx, gran_x, k,
-                  yf ? nullptr : static_cast<int32_t*>(d_y), yf ? static_cast<float*>(d_y) : nullptr,
-                  ctx->stream);
-  if (st) return st;
-  CU(cudaMemcpyAsync(yf ? static_cast<void*>(yf) : static_cast<void*>(y), d_y, rows_w * rows_x * 4,
-                     cudaMemcpyDeviceToHost, ctx->stream));
-  CU(cudaStreamSynchronize(ctx->stream));
+  const uint64_t nblk = (rows_w + blk - 1) / blk;
+  const cudaStream_t sc = ctx->stream;
+  // features (and scales) first, on the input copy stream
+  CU(cudaMemcpyAsync(d_x, x, x_words * 4, cudaMemcpyHostToDevice, ctx->s_in));
+  if (yf) {
+    CU(cudaMemcpyAsync(d_sw, s_w, sw_n * 8, cudaMemcpyHostToDevice, ctx->s_in));
+    CU(cudaMemcpyAsync(d_sx, s_x, sx_n * 8, cudaMemcpyHostToDevice, ctx->s_in));
+  }
+  for (uint64_t bi = 0; bi < nblk; ++bi) {
+    const uint64_t r0 = bi * blk, rb = std::min(blk, rows_w - r0);
+    // block bi's planes -> a packed buffer of rb rows ([plane][rb][wpr]) at d_w + n_w*r0*wpr
+    uint32_t* d_wb = d_w + uint64_t(n_w) * r0 * wpr;
+    CU(cudaMemcpy2DAsync(d_wb, rb * wpr * 4, w + r0 * wpr, rows_w * wpr * 4, rb * wpr * 4, n_w,
+                         cudaMemcpyHostToDevice, ctx->s_in));
+    cudaEvent_t ev_in = ctx->pipe_ev[(2 * bi) % (2 * kPipeBlocks)];
+    cudaEvent_t ev_done = ctx->pipe_ev[(2 * bi + 1) % (2 * kPipeBlocks)];
+    CU(cudaEventRecord(ev_in, ctx->s_in));
+    CU(cudaStreamWaitEvent(sc, ev_in, 0));
+    void* d_yb = d_y + r0 * out_row_bytes;
+    st = run_matmul(ctx, d_wb, rb, n_w, yf ? d_sw + (gran_w == APMM_PER_ROW ? r0 : 0) : nullptr,
+                    gran_w, d_x, rows_x, n_x, d_sx, gran_x, k,
+                    yf ? nullptr : static_cast<int32_t*>(d_yb), yf ? static_cast<float*>(d_yb) : nullptr,
+                    sc);
+    if (st) return st;
+    CU(cudaEventRecord(ev_done, sc));
+    CU(cudaStreamWaitEvent(ctx->s_out, ev_done, 0));
+    uint8_t* h_y = yf ? reinterpret_cast<uint8_t*>(yf) : reinterpret_cast<uint8_t*>(y);
+    CU(cudaMemcpyAsync(h_y + r0 * out_row_bytes, d_yb, rb * out_row_bytes, cudaMemcpyDeviceToHost,
+                       ctx->s_out));
+  }
+  CU(cudaStreamSynchronize(ctx->s_out));
+  CU(cudaStreamSynchronize(sc));
   return APMM_OK;
 }
 

@@ -400,6 +400,34 @@ def test_reference_run_verify_with_gpu_kernel():
         assert "PASS compute_plane_products + recover on the device" in r.stdout
 
 
+def test_host_api_row_block_pipeline(gpu, oracle):
+    """The synchronous host entry points pipeline large calls over row blocks of W / Y
+    (H2D, GEMM and D2H on three streams): outputs > 16 MB, ragged last block, int32 and
+    dequant, against the oracle on sampled rows and the device entry point on all rows."""
+    import torch
+    ap, ctx = gpu
+    rng = np.random.default_rng(5)
+    for (m, n, k, nw, nx) in [(4173, 1100, 256, 3, 4), (2300, 2049, 96, 2, 2), (700, 40, 4000, 4, 8)]:
+        wc = rng.integers(0, 1 << nw, size=(m, k), dtype=np.uint8)
+        xc = rng.integers(0, 1 << nx, size=(n, k), dtype=np.uint8)
+        wp, xp = oracle.pack(wc, nw), oracle.pack(xc, nx)
+        w = ap.PackedBitPlanes(m, k, ap.BitWidth(nw), wp)
+        x = ap.PackedBitPlanes(n, k, ap.BitWidth(nx), xp)
+        got = ap.matmul_ap(w, x, ctx=ctx)
+        rows = np.unique(np.concatenate([[0, m - 1], rng.integers(0, m, 24)]))
+        want = oracle.matmul_ap_mt(oracle.pack(wc[rows], nw), len(rows), nw, xp, n, nx, k, 8)
+        assert np.array_equal(got[rows], want), (m, n, k)
+        dev = torch.device("cuda", 0)
+        yd = torch.empty((m, n), dtype=torch.int32, device=dev)
+        ap.cu_matmul_ap(torch.from_numpy(wp.view(np.int32)).to(dev), m, nw,
+                        torch.from_numpy(xp.view(np.int32)).to(dev), n, nx, k, yd, ctx)
+        torch.cuda.synchronize()
+        assert np.array_equal(got, yd.cpu().numpy()), (m, n, k)
+        sw, sx = rng.random(m), rng.random(n)
+        deq = ap.matmul_ap_dequant(w, sw, ap.Granularity.PerRow, x, sx, ap.Granularity.PerRow, ctx)
+        assert np.array_equal(deq, oracle.dequant_epilogue(got, sw, 1, sx, 1))
+
+
 # ---------------------------------------------------------------- plane products / recover
 def test_plane_products_and_recover_match_oracle(gpu, oracle):
     """compute_plane_products / matmul_plane_pair / recover (kernel.cpp:125-181) on the GPU
