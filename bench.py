@@ -88,6 +88,17 @@ def load_peaks():
         return {}
 
 
+def load_i8_ceiling():
+    """The pair GEMM's own tcgen05 kind::i8 ceiling (scripts/i8_mma_peak.py: the real kernel
+    with operand reloads switched off), reported beside the contract's peak."""
+    p = os.path.join(ROOT, "profiles", "i8_mma_peak.json")
+    try:
+        with open(p) as f:
+            return json.load(f).get("i8_tops")
+    except Exception:
+        return None
+
+
 def load_traffic():
     p = os.path.join(ROOT, "profiles", "traffic.json")
     try:
@@ -494,6 +505,7 @@ def run_ours(args, rank, world, local_rank):
         peak_src = ("2 x measured bf16 burst (MEASURED_PEAKS.json bf16_tflops); "
                     "dense i8 = 2x dense bf16 on B200" if bf16 else
                     "2 x fallback bf16 1590 (B200_PROFILING.md)")
+    i8_ceiling = load_i8_ceiling()
     tr_ent = traffic.get(args.workload) or {}
     tr = tr_ent.get("bytes")  # dram read+write bytes per launch (ncu --set full), or None
     line = {
@@ -522,6 +534,11 @@ def run_ours(args, rank, world, local_rank):
         "roofline": {"bound": "hbm" if hbm_bound else "tensor", "achieved": achieved,
                      "peak": peak, "unit": unit, "frac": achieved / peak, "traffic": tr,
                      "traffic_source": tr_ent.get("kernel"),
+                     "i8_mma_ceiling_tops": None if hbm_bound else i8_ceiling,
+                     "frac_of_i8_mma_ceiling": (achieved / i8_ceiling
+                                                if (i8_ceiling and not hbm_bound) else None),
+                     "i8_mma_ceiling_source": None if hbm_bound else
+                         "profiles/i8_mma_peak.json: this pair kernel with operand reloads off, 8192^3",
                      "kernel": kname, "peak_source": peak_src,
                      "algorithmic_bytes_per_step": bytes_step,
                      "algorithmic_ops_per_step": ops_step,

@@ -191,10 +191,16 @@ __device__ __forceinline__ uint32_t dequant_bits(uint32_t v, double sw, double s
 struct TileInfo {
   uint32_t tm, col0, ncols;
 };
-__device__ __forceinline__ TileInfo tile_info(uint32_t t, uint32_t tiles_m, uint32_t n_full) {
-  if (t < n_full) return {t % tiles_m, (t / tiles_m) * kPairN, kPairN};
+__device__ __forceinline__ TileInfo tile_info(uint32_t t, uint32_t tiles_m, uint32_t tiles_n,
+                                             uint32_t n_full) {
+  uint32_t tm, tn;
+  if (t < n_full) {
+    raster_tile(t, tiles_m, tiles_n, tm, tn);
+    return {tm, tn * kPairN, kPairN};
+  }
   const uint32_t h = t - n_full, f = n_full + (h >> 1);
-  return {f % tiles_m, (f / tiles_m) * kPairN + (h & 1u) * (kPairN / 2), kPairN / 2};
+  raster_tile(f, tiles_m, tiles_n, tm, tn);
+  return {tm, tn * kPairN + (h & 1u) * (kPairN / 2), kPairN / 2};
 }
 
 // NW: planes handled at compile time (1..4 exact; 8 covers 5..8 with runtime masking).
@@ -268,7 +274,7 @@ __global__ void __maxnreg__(kXformWarpsCfg == 4 ? 136 : 104)
       const uint64_t hint = policy_evict_last();
       uint32_t stage = 0, phase = 0;
       for (uint32_t t = cluster; t < num_tiles; t += nclusters) {
-        const TileInfo ti = tile_info(t, p.tiles_m, p.n_full);
+        const TileInfo ti = tile_info(t, p.tiles_m, p.tiles_n, p.n_full);
         const bool half = ti.ncols != kPairN;
         for (uint32_t kb = 0; kb < p.kblocks; ++kb) {
           mbar_wait_b(&empty_bar[stage], phase ^ 1, 1);
@@ -302,7 +308,7 @@ __global__ void __maxnreg__(kXformWarpsCfg == 4 ? 136 : 104)
         mbar_wait_b(&tmem_empty[acc], acc_phase ^ 1, 2, at);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * kPairN;
-        const uint32_t idesc = tile_info(t, p.tiles_m, p.n_full).ncols != kPairN ? kIdescHalf : kIdesc;
+        const uint32_t idesc = tile_info(t, p.tiles_m, p.tiles_n, p.n_full).ncols != kPairN ? kIdescHalf : kIdesc;
         for (uint32_t kb = 0; kb < p.kblocks; ++kb) {
           mbar_wait_b<true>(&full_bar[stage], phase, 3, af);
           tc_fence_after();
@@ -333,7 +339,7 @@ __global__ void __maxnreg__(kXformWarpsCfg == 4 ? 136 : 104)
       const uint64_t hint = policy_evict_last();
       uint32_t rs = 0, rphase = 0;
       for (uint32_t t = cluster; t < num_tiles; t += nclusters) {
-        const int32_t wrow = int32_t(tile_info(t, p.tiles_m, p.n_full).tm * 2 * kHalf + q * kHalf);
+        const int32_t wrow = int32_t(tile_info(t, p.tiles_m, p.tiles_n, p.n_full).tm * 2 * kHalf + q * kHalf);
         for (uint32_t kb = 0; kb < p.kblocks; kb += kRB) {
           mbar_wait_b(&raw_empty[rs], rphase ^ 1, 6);
           mbar_arrive_expect_tx(&raw_full[rs], p.n_w * kRawPlane);
@@ -449,7 +455,7 @@ __global__ void __maxnreg__(kXformWarpsCfg == 4 ? 136 : 104)
     uint32_t acc = 0, acc_phase = 0, nbuf = 0;
     const uint64_t store_hint = policy_evict_first();
     for (uint32_t t = cluster; t < num_tiles; t += nclusters) {
-      const TileInfo ti = tile_info(t, p.tiles_m, p.n_full);
+      const TileInfo ti = tile_info(t, p.tiles_m, p.tiles_n, p.n_full);
       const uint32_t row0 = ti.tm * 2 * kHalf + q * kHalf + wq * 32;
       const uint32_t row = row0 + lane;
       const bool row_ok = row < p.rows_w;

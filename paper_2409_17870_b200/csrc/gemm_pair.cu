@@ -59,6 +59,7 @@ struct Params {
   uint32_t n_full;     // tiles [0, n_full) are 256 x 256; the remaining full tiles of the
                        // last partial wave run as two 256 x 128 halves each (CL == 2 only)
   unsigned long long* dbg;  // optional wait-cycle counters (APMM_DEBUG_WAITS), else null
+  uint32_t peak_probe;      // APMM_PEAK_PROBE=1 (measurement only): no operand reloads
 };
 
 __device__ __forceinline__ uint32_t dequant_bits(uint32_t v, double sw, double sx) {
@@ -75,10 +76,16 @@ __device__ __forceinline__ uint32_t dequant_bits(uint32_t v, double sw, double s
 struct TileInfo {
   uint32_t tm, col0, ncols;
 };
-__device__ __forceinline__ TileInfo tile_info(uint32_t t, uint32_t tiles_m, uint32_t n_full) {
-  if (t < n_full) return {t % tiles_m, (t / tiles_m) * kPairN, kPairN};
+__device__ __forceinline__ TileInfo tile_info(uint32_t t, uint32_t tiles_m, uint32_t tiles_n,
+                                             uint32_t n_full) {
+  uint32_t tm, tn;
+  if (t < n_full) {
+    raster_tile(t, tiles_m, tiles_n, tm, tn);
+    return {tm, tn * kPairN, kPairN};
+  }
   const uint32_t h = t - n_full, f = n_full + (h >> 1);
-  return {f % tiles_m, (f / tiles_m) * kPairN + (h & 1u) * (kPairN / 2), kPairN / 2};
+  raster_tile(f, tiles_m, tiles_n, tm, tn);
+  return {tm, tn * kPairN + (h & 1u) * (kPairN / 2), kPairN / 2};
 }
 
 template <int CL>
@@ -145,14 +152,23 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ---------------- TMA producer (both CTAs) ----------------
     if (elect_one()) {
       const uint64_t hint = policy_evict_last();
-      uint32_t stage = 0, phase = 0;
+      uint32_t stage = 0, phase = 0, loaded = 0;
       for (uint32_t t = cluster; t < num_tiles; t += nclusters) {
-        const TileInfo ti = CL == 2 ? tile_info(t, p.tiles_m, p.n_full)
+        const TileInfo ti = CL == 2 ? tile_info(t, p.tiles_m, p.tiles_n, p.n_full)
                                     : TileInfo{(t % tiles_mc) * kPairs + pr, (t / tiles_mc) * kPairN, kPairN};
         const uint32_t tm = ti.tm;
         const bool half = ti.ncols != kPairN;
         for (uint32_t kb = 0; kb < p.kblocks; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
+          if (p.peak_probe && loaded >= kStages) {
+            // measurement mode (APMM_PEAK_PROBE=1, results wrong): after one ring fill the
+            // stages are re-used without loads -> the tcgen05 kind::i8 pipe's own ceiling
+            // with this kernel's schedule, MMA issue and epilogue
+            if (leader) mbar_arrive_expect_tx(&full_bar[stage], 0);
+            if (++stage == kStages) { stage = 0; phase ^= 1; }
+            continue;
+          }
+          ++loaded;
           if (leader) mbar_arrive_expect_tx(&full_bar[stage], half ? 3 * kAS : 2 * kStageBytes);
           const uint32_t fb = mapa(smem_u32(&full_bar[stage]), lead_rank);
           uint8_t* st = stages + stage * kStageBytes;
@@ -189,7 +205,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * kPairN;
         const uint32_t idesc =
-            (CL == 2 && tile_info(t, p.tiles_m, p.n_full).ncols != kPairN) ? kIdescHalf : kIdesc;
+            (CL == 2 && tile_info(t, p.tiles_m, p.tiles_n, p.n_full).ncols != kPairN) ? kIdescHalf : kIdesc;
         for (uint32_t kb = 0; kb < p.kblocks; ++kb) {
           c0 = p.dbg ? clock64() : 0;
           mbar_wait(&full_bar[stage], phase);
@@ -222,7 +238,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t acc = 0, acc_phase = 0, nbuf = 0;
     const uint64_t store_hint = policy_evict_first();  // Y streams out; keep operands in L2
     for (uint32_t t = cluster; t < num_tiles; t += nclusters) {
-      const TileInfo ti = CL == 2 ? tile_info(t, p.tiles_m, p.n_full)
+      const TileInfo ti = CL == 2 ? tile_info(t, p.tiles_m, p.tiles_n, p.n_full)
                                   : TileInfo{(t % tiles_mc) * kPairs + pr, (t / tiles_mc) * kPairN, kPairN};
       const uint32_t tm = ti.tm;
       const uint32_t row0 = tm * 2 * kHalf + q * kHalf + wq * 32;
@@ -359,6 +375,8 @@ cudaError_t launch_gemm_pair(const GemmArgs& a, cudaStream_t s, int* launches) {
   p.c0 = static_cast<uint32_t>(a.k_logical) * A * B;
   p.tma_store = tma_store ? 1u : 0u;
   p.dbg = a.dbg;
+  static const uint32_t peak_probe = std::getenv("APMM_PEAK_PROBE") ? 1u : 0u;
+  p.peak_probe = peak_probe;
   // clusters of 4 (X multicast across two pairs) when there are enough cluster tiles to
   // fill the machine, else plain pairs. APMM_PAIR_CLUSTER=2|4 forces one (testing).
   static const int forced = [] {

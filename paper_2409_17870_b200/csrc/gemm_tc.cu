@@ -103,7 +103,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t hint = policy_evict_last();  // operands are re-read by many tiles
       uint32_t stage = 0, phase = 0;
       for (uint32_t t = blockIdx.x; t < num_tiles; t += gridDim.x) {
-        const uint32_t tm = t % p.tiles_m, tn = t / p.tiles_m;
+        uint32_t tm, tn;
+        raster_tile(t, p.tiles_m, p.tiles_n, tm, tn);
         for (uint32_t kb = 0; kb < p.kblocks; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
           mbar_arrive_expect_tx(&full_bar[stage], kAStage + kBStage);
@@ -147,7 +148,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t q = warp & 3;  // TMEM lane quadrant this warp may access
     uint32_t acc = 0, acc_phase = 0;
     for (uint32_t t = blockIdx.x; t < num_tiles; t += gridDim.x) {
-      const uint32_t tm = t % p.tiles_m, tn = t / p.tiles_m;
+      uint32_t tm, tn;
+        raster_tile(t, p.tiles_m, p.tiles_n, tm, tn);
       const uint32_t row = tm * kBM + q * 32 + lane;
       const bool row_ok = row < p.rows_w;
       const uint32_t rsw = row_ok ? static_cast<uint32_t>(__ldg(p.rowsum_w + row)) : 0u;

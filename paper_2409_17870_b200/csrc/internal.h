@@ -17,6 +17,22 @@ constexpr int kRowsumPad = kBN; // rowsum_x is zero-padded to a multiple of this
 
 inline uint64_t round_up(uint64_t v, uint64_t m) { return (v + m - 1) / m * m; }
 
+// Grouped tile raster for the persistent GEMMs: linear tile t -> (tm, tn) walking groups of
+// kRasterGroup W row tiles across every X column tile. A wave of 74 pair tiles then covers
+// ~8 W tiles x ~9 X tiles, so both operands' codes are reused from L2; with the plain
+// "tm fastest" order a tall W (70B FFN: 112 row tiles, 235 MB of codes) was re-streamed
+// from HBM once per X column tile.
+constexpr uint32_t kRasterGroup = 8;
+__host__ __device__ inline void raster_tile(uint32_t t, uint32_t tiles_m, uint32_t tiles_n,
+                                            uint32_t& tm, uint32_t& tn) {
+  const uint32_t per_group = kRasterGroup * tiles_n;
+  const uint32_t g = t / per_group, first = g * kRasterGroup;
+  const uint32_t gsize = tiles_m - first < kRasterGroup ? tiles_m - first : kRasterGroup;
+  const uint32_t r = t - g * per_group;
+  tm = first + r % gsize;
+  tn = r / gsize;
+}
+
 // ---- prep.cu -------------------------------------------------------------------------
 // Both operands' planes (reference layout) -> u8 codes [rows x kpad] (zero K padding, K
 // permuted identically within each 32-column group) + rowsum[rows], one launch.
