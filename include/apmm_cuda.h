@@ -156,6 +156,20 @@ APMM_API int apmm_cu_compute_plane_products(apmm_ctx* ctx, const uint32_t* w_pla
 APMM_API int apmm_cu_recover(apmm_ctx* ctx, const int32_t* stack, int n_w, int n_x, uint64_t k,
                     uint64_t rows, uint64_t cols, int32_t* y, apmm_stream_t stream);
 
+/* The reference flow quantize(X) -> decompose_and_pack -> matmul_ap -> dequant
+ * (tools/apmm.cpp:275-340, bipolar.cpp:72-100) with the feature quantizer writing the GEMM's
+ * u8 operand directly (no feature planes, no feature expansion):
+ * fp64 X [rows_x x k] -> x_scales (device, 1 or rows_x doubles) and
+ * out = (float)((double)Y * s_w * s_x) [rows_w x rows_x]. Bit-identical to
+ * apmm_cu_quantize_pack followed by apmm_cu_matmul_ap_dequant. Synchronises the stream
+ * once (after the quantizer) to report APMM_E_NON_FINITE before the overflow_bound check
+ * and the GEMM, in the reference's order. */
+APMM_API int apmm_cu_quantize_matmul_ap_dequant(apmm_ctx* ctx, const uint32_t* w_planes,
+                                       uint64_t rows_w, int n_w, const double* w_scales,
+                                       int w_granularity, const double* x_values,
+                                       uint64_t rows_x, uint64_t k, int n_x, int x_granularity,
+                                       double* x_scales, float* out, apmm_stream_t stream);
+
 /* ---- host entry points (synchronous, host pointers) ------------------------------- */
 /* These mirror the reference functions one for one and add the H2D/D2H copies. */
 

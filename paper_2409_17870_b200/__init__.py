@@ -11,5 +11,6 @@ from .apmm import (  # noqa: F401
     decompose_and_pack, unpack, quantize, matmul_ap, matmul_ap_dequant, overflow_bound,
     kernel_fn, cu_matmul_ap, cu_matmul_ap_dequant, cu_pack, cu_unpack, cu_quantize_pack,
     PlaneProductStack, matmul_plane_pair, compute_plane_products, recover,
+    cu_quantize_matmul_ap_dequant,
     version,
 )

@@ -32,6 +32,8 @@ _SIGNATURES = {
     "apmm_cu_matmul_ap": (i32, [vp, vp, u64, i32, vp, u64, i32, u64, vp, vp]),
     "apmm_cu_matmul_ap_dequant": (i32, [vp, vp, u64, i32, vp, i32, vp, u64, i32, vp, i32, u64,
                                         vp, vp]),
+    "apmm_cu_quantize_matmul_ap_dequant": (i32, [vp, vp, u64, i32, vp, i32, vp, u64, u64, i32, i32,
+                                                 vp, vp, vp]),
     "apmm_cu_matmul_plane_pair": (i32, [vp, vp, u64, i32, i32, vp, u64, i32, i32, u64, vp, vp]),
     "apmm_cu_compute_plane_products": (i32, [vp, vp, u64, i32, vp, u64, i32, u64, vp, vp]),
     "apmm_cu_recover": (i32, [vp, vp, i32, i32, u64, u64, u64, vp, vp]),

@@ -441,6 +441,18 @@ def cu_matmul_ap_dequant(w_planes, rows_w, n_w, w_scales, w_gran, x_planes, rows
         _stream_ptr(stream)))
 
 
+def cu_quantize_matmul_ap_dequant(w_planes, rows_w, n_w, w_scales, w_gran, x_values, rows_x, k,
+                                  n_x, x_gran, x_scales, out, ctx: Context | None = None,
+                                  stream=None) -> None:
+    """quantize(X) -> matmul_ap -> dequant in one call (apmm.cpp:275-340), the quantizer
+    writing the GEMM operand directly; x_scales receives X's scales (torch CUDA tensors)."""
+    ctx = ctx or default_context(w_planes.device.index or 0)
+    _check(ctx.lib.apmm_cu_quantize_matmul_ap_dequant(
+        ctx.h, C.c_void_p(w_planes.data_ptr()), rows_w, n_w, C.c_void_p(w_scales.data_ptr()),
+        int(w_gran), C.c_void_p(x_values.data_ptr()), rows_x, k, n_x, int(x_gran),
+        C.c_void_p(x_scales.data_ptr()), C.c_void_p(out.data_ptr()), _stream_ptr(stream)))
+
+
 def cu_pack(codes, rows, cols, n, planes, ctx: Context | None = None, stream=None) -> None:
     ctx = ctx or default_context(codes.device.index or 0)
     _check(ctx.lib.apmm_cu_pack(ctx.h, C.c_void_p(codes.data_ptr()), rows, cols, n,

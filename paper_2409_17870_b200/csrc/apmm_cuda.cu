@@ -42,6 +42,8 @@ struct apmm_ctx {
   bool dbg_waits = false;  // APMM_DEBUG_WAITS=1: MMA-issuer wait-cycle counters (dev only)
   void* dbg = nullptr;  // APMM_DEBUG_WAITS counters (dev only)
   int* flags = nullptr;  // recover's device error flags (2 ints)
+  void* qx = nullptr;  // fused quantize: feature planes (skinny) / absmax + flag scratch
+  size_t qx_bytes = 0;
   // host entry points' transfer pipeline: H2D / D2H copy streams and their events
   cudaStream_t s_in = nullptr, s_out = nullptr;
   cudaEvent_t pipe_ev[16] = {};
@@ -194,11 +196,14 @@ struct TimedLaunch {
   }
 };
 
+// x_ready: the feature operand is already in this call's workspace half as u8 codes +
+// rowsum (written by the fused quantize, K2 -> K3); then K1 expands W only and x is unused.
 int run_matmul(apmm_ctx* ctx, const uint32_t* w, uint64_t rows_w, int n_w, const double* s_w,
                int gran_w, const uint32_t* x, uint64_t rows_x, int n_x, const double* s_x,
-               int gran_x, uint64_t k, int32_t* y, float* yf, cudaStream_t stream) {
+               int gran_x, uint64_t k, int32_t* y, float* yf, cudaStream_t stream,
+               bool x_ready = false) {
   CU(cudaSetDevice(ctx->device));
-  if (rows_x <= kSkinnyMaxRowsX && !ctx->force_tc) {
+  if (rows_x <= kSkinnyMaxRowsX && !ctx->force_tc && !x_ready) {
     // few feature rows: feature prep + K5, the weight planes streamed once from HBM
     const size_t need = skinny_acc_bytes(rows_w, rows_x);
     if (need > ctx->sk_ws_bytes) {  // split-K accumulators; zero at rest
@@ -259,8 +264,9 @@ int run_matmul(apmm_ctx* ctx, const uint32_t* w, uint64_t rows_w, int n_w, const
   const bool fused = pair && gemm_fused_supported(w, k);
   {
     TimedLaunch t(ctx, 1, stream);
-    CU(launch_expand(w, rows_w, n_w, fused ? nullptr : m.codes_w, m.rowsum_w, x, rows_x, rsx_pad, n_x, m.codes_x,
-                     m.rowsum_x, k, m.kpad, ctx->num_sms, stream));
+    CU(launch_expand(w, rows_w, n_w, fused ? nullptr : m.codes_w, m.rowsum_w, x_ready ? nullptr : x,
+                     x_ready ? 0 : rows_x, x_ready ? 0 : rsx_pad, n_x, m.codes_x, m.rowsum_x, k,
+                     m.kpad, ctx->num_sms, stream));
   }
   ctx->launches += 1;
   GemmArgs a{};
@@ -407,6 +413,7 @@ int apmm_ctx_destroy(apmm_ctx* ctx) {
     cudaFree(ctx->dbg);
   }
   if (ctx->flags) cudaFree(ctx->flags);
+  if (ctx->qx) cudaFree(ctx->qx);
   if (ctx->ws) cudaFree(ctx->ws);
   if (ctx->sk_ws) cudaFree(ctx->sk_ws);
   if (ctx->sk_scratch) cudaFree(ctx->sk_scratch);
@@ -599,6 +606,55 @@ int apmm_cu_recover(apmm_ctx* ctx, const int32_t* stack, int n_w, int n_x, uint6
   if (h[0]) return fail(APMM_E_OUT_OF_RANGE, "plane product entry outside [-K, K]");
   if (h[1]) return fail(APMM_E_OVERFLOW, "recovered value exceeds 32-bit range");
   return APMM_OK;
+}
+
+int apmm_cu_quantize_matmul_ap_dequant(apmm_ctx* ctx, const uint32_t* w_planes, uint64_t rows_w,
+                                       int n_w, const double* w_scales, int w_granularity,
+                                       const double* x_values, uint64_t rows_x, uint64_t k,
+                                       int n_x, int x_granularity, double* x_scales, float* out,
+                                       apmm_stream_t stream) {
+  int st;
+  if (!ctx || !w_planes || !w_scales || !x_values || !x_scales || !out) {
+    return fail(APMM_E_INVALID_ARGUMENT, "null argument");
+  }
+  if (!valid_gran(w_granularity) || !valid_gran(x_granularity)) {
+    return fail(APMM_E_INVALID_ARGUMENT, "bad granularity");
+  }
+  if ((st = check_width(n_w)) || (st = check_width(n_x))) return st;
+  if ((st = check_dims(rows_x, k, "RealMatrix")) || (st = check_dims(rows_w, k, "weights"))) return st;
+  CU(cudaSetDevice(ctx->device));
+  const cudaStream_t s = pick(ctx, stream);
+  if (rows_x <= kSkinnyMaxRowsX && !ctx->force_tc) {
+    // few feature rows: the skinny kernel consumes planes -> quantize_pack into a scratch
+    // plane buffer, then the ordinary device matmul (both stream-ordered)
+    const size_t words = apmm_packed_words(n_x, rows_x, k);
+    if ((st = ensure(&ctx->qx, &ctx->qx_bytes, words * 4 + 64, ctx->device))) return st;
+    uint32_t* xp = static_cast<uint32_t*>(ctx->qx);
+    if ((st = apmm_cu_quantize_pack(ctx, x_values, rows_x, k, n_x, x_granularity, xp, x_scales,
+                                    nullptr, stream))) {
+      return st;
+    }
+    if ((st = check_matmul(n_w, n_x, rows_w, rows_x, k))) return st;
+    return run_matmul(ctx, w_planes, rows_w, n_w, w_scales, w_granularity, xp, rows_x, n_x,
+                      x_scales, x_granularity, k, nullptr, out, s);
+  }
+  // K2 -> K3: quantize straight into this call's workspace half (u8 codes in K1's layout +
+  // rowsum(U_x)); K1 then expands W only. The feature planes never exist.
+  if ((st = ensure(&ctx->ws, &ctx->ws_bytes, matmul_ws_bytes(rows_w, rows_x, k), ctx->device))) return st;
+  if ((st = ensure(&ctx->qx, &ctx->qx_bytes, 64, ctx->device))) return st;
+  const MatmulWs m = carve(ctx->ws, rows_w, rows_x, k, ctx->ws_half);
+  auto* amax = static_cast<unsigned long long*>(ctx->qx);
+  int* flag = reinterpret_cast<int*>(static_cast<uint8_t*>(ctx->qx) + 16);
+  CU(launch_quantize_pack(x_values, rows_x, k, n_x, x_granularity, nullptr, x_scales, nullptr,
+                          amax, flag, s, m.codes_x, m.rowsum_x, m.kpad, round_up(rows_x, kRowsumPad)));
+  ctx->launches += x_granularity == APMM_PER_ROW ? 1 : 2;
+  int h_flag = 0;  // quantize errors come first, as in the reference flow (apmm.cpp:275-327)
+  CU(cudaMemcpyAsync(&h_flag, flag, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  if (h_flag) return fail(APMM_E_NON_FINITE, "input contains NaN or infinity");
+  if ((st = check_matmul(n_w, n_x, rows_w, rows_x, k))) return st;
+  return run_matmul(ctx, w_planes, rows_w, n_w, w_scales, w_granularity, nullptr, rows_x, n_x,
+                    x_scales, x_granularity, k, nullptr, out, s, /*x_ready=*/true);
 }
 
 // ---- host entry points ------------------------------------------------------------------

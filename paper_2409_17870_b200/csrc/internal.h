@@ -49,10 +49,15 @@ cudaError_t launch_unpack(const uint32_t* planes, uint64_t rows, uint64_t cols, 
                           uint8_t* codes, cudaStream_t s);
 // fp64 quantize + pack. flag[0] receives 1 if any input is non-finite. `amax_bits` is a
 // scratch u64 (per-tensor absmax as ordered bits).
+// With gemm_codes != null it also (or, with planes == null, only) writes the GEMM operand
+// directly: u8 codes [rows][kpad] in K1's layout + rowsum[rows_pad] (zero padded) -- K2
+// feeding K3 without the bit planes and the X expansion.
 cudaError_t launch_quantize_pack(const double* x, uint64_t rows, uint64_t cols, int n,
                                  int granularity, uint32_t* planes, double* scales,
                                  uint8_t* codes, unsigned long long* amax_bits, int* flag,
-                                 cudaStream_t s);
+                                 cudaStream_t s, uint8_t* gemm_codes = nullptr,
+                                 int32_t* gemm_rowsum = nullptr, uint64_t kpad = 0,
+                                 uint64_t rowsum_pad = 0);
 
 // recover (kernel.cpp:159-181) over a device plane-product stack [n_w*n_x][m*n] int32:
 // y = sum 2^(i+j) stack[i][j] in int64, narrowed to int32. flags[0] <- 1 if an entry lies

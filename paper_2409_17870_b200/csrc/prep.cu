@@ -211,11 +211,21 @@ __device__ __forceinline__ uint32_t quantize_code(double x, double s, int maxv) 
   return static_cast<uint32_t>((qi + maxv) / 2);
 }
 
-__device__ __forceinline__ void quantize_pack_word(const double* __restrict__ xrow,
-                                                   uint64_t r, uint64_t rows, uint64_t cols,
-                                                   uint64_t w, int n, int maxv, double s,
-                                                   uint32_t* __restrict__ planes,
-                                                   uint8_t* __restrict__ codes) {
+// Optional GEMM-operand output (K2 feeding K3 without planes): `codes` = u8 codes
+// [rows][kpad] in K1's permuted order (column 8b + c of each 32-column group at byte 4c + b).
+struct GemmCodesOut {
+  uint8_t* codes;   // null: no GEMM-layout output
+  int32_t* rowsum;  // [rows_pad], zeroed by the launcher
+  uint64_t kpad;
+};
+
+// Returns the lane's code (0 past the row end) so callers can form rowsum(U).
+__device__ __forceinline__ uint32_t quantize_pack_word(const double* __restrict__ xrow,
+                                                       uint64_t r, uint64_t rows, uint64_t cols,
+                                                       uint64_t w, int n, int maxv, double s,
+                                                       uint32_t* __restrict__ planes,
+                                                       uint8_t* __restrict__ codes,
+                                                       const GemmCodesOut& g) {
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t wpr = (cols + 31) / 32;
   const uint64_t col = w * 32 + lane;
@@ -224,19 +234,32 @@ __device__ __forceinline__ void quantize_pack_word(const double* __restrict__ xr
     c = quantize_code(xrow[col], s, maxv);
     if (codes) codes[r * cols + col] = static_cast<uint8_t>(c);
   }
-  uint32_t mine = 0;
-  for (int i = 0; i < n; ++i) {
-    const uint32_t word = __ballot_sync(0xffffffffu, (c >> i) & 1u);
-    if (int(lane) == i) mine = word;
+  if (g.codes) {
+    g.codes[r * g.kpad + w * 32 + (lane & 7u) * 4 + (lane >> 3)] = static_cast<uint8_t>(c);
   }
-  if (int(lane) < n) planes[(uint64_t(lane) * rows + r) * wpr + w] = mine;
+  if (planes) {
+    uint32_t mine = 0;
+    for (int i = 0; i < n; ++i) {
+      const uint32_t word = __ballot_sync(0xffffffffu, (c >> i) & 1u);
+      if (int(lane) == i) mine = word;
+    }
+    if (int(lane) < n) planes[(uint64_t(lane) * rows + r) * wpr + w] = mine;
+  }
+  return c;
+}
+
+// zero K padding of the GEMM-layout codes: bytes [32 * wpr, kpad) of row r, one warp
+__device__ __forceinline__ void zero_code_tail(const GemmCodesOut& g, uint64_t r, uint64_t cols) {
+  const uint32_t lane = threadIdx.x & 31;
+  for (uint64_t b = ((cols + 31) / 32) * 32 + lane; b < g.kpad; b += 32) g.codes[r * g.kpad + b] = 0;
 }
 
 // Per-row granularity: one block per row (absmax reduce, then quantize+pack its words).
 __global__ void __launch_bounds__(kThreads)
     quantize_rows_kernel(const double* __restrict__ x, uint64_t rows, uint64_t cols, int n,
                          uint32_t* __restrict__ planes, double* __restrict__ scales,
-                         uint8_t* __restrict__ codes, int* __restrict__ flag) {
+                         uint8_t* __restrict__ codes, int* __restrict__ flag,
+                         GemmCodesOut g) {
   const uint64_t r = blockIdx.x;
   const double* xrow = x + r * cols;
   const int maxv = (1 << n) - 1;
@@ -265,8 +288,23 @@ __global__ void __launch_bounds__(kThreads)
   const double s = m == 0.0 ? 1.0 : __ddiv_rn(m, double(maxv));  // bipolar.cpp:91
   if (threadIdx.x == 0) scales[r] = s;
   const uint64_t wpr = (cols + 31) / 32;
+  int32_t rsum = 0;
   for (uint64_t w = threadIdx.x >> 5; w < wpr; w += blockDim.x / 32) {
-    quantize_pack_word(xrow, r, rows, cols, w, n, maxv, s, planes, codes);
+    rsum += static_cast<int32_t>(quantize_pack_word(xrow, r, rows, cols, w, n, maxv, s, planes,
+                                                    codes, g));
+  }
+  if (g.codes) {
+    if (threadIdx.x < 32) zero_code_tail(g, r, cols);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) rsum += __shfl_xor_sync(0xffffffffu, rsum, o);
+    __shared__ int32_t rred[kThreads / 32];
+    if ((threadIdx.x & 31) == 0) rred[threadIdx.x >> 5] = rsum;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int32_t t = 0;
+      for (int i = 0; i < int(blockDim.x / 32); ++i) t += rred[i];
+      g.rowsum[r] = t;
+    }
   }
 }
 
@@ -300,7 +338,7 @@ __global__ void __launch_bounds__(kThreads)
     quantize_tensor_kernel(const double* __restrict__ x, uint64_t rows, uint64_t cols, int n,
                            const unsigned long long* amax_bits, uint32_t* __restrict__ planes,
                            double* __restrict__ scales, uint8_t* __restrict__ codes,
-                           const int* flag) {
+                           const int* flag, GemmCodesOut g) {
   if (*flag) return;
   const int maxv = (1 << n) - 1;
   const double m = __longlong_as_double(static_cast<long long>(*amax_bits));
@@ -310,7 +348,14 @@ __global__ void __launch_bounds__(kThreads)
   const uint64_t gw = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   if (gw >= rows * wpr) return;
   const uint64_t r = gw / wpr, w = gw % wpr;
-  quantize_pack_word(x + r * cols, r, rows, cols, w, n, maxv, s, planes, codes);
+  int32_t c = static_cast<int32_t>(
+      quantize_pack_word(x + r * cols, r, rows, cols, w, n, maxv, s, planes, codes, g));
+  if (g.codes) {  // one atomic per (row, word) into the zeroed rowsum
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(g.rowsum + r, c);
+    if (w == wpr - 1) zero_code_tail(g, r, cols);
+  }
 }
 
 // recover: one thread per output element, int64 accumulation of the shifted plane products
@@ -397,13 +442,19 @@ cudaError_t launch_unpack(const uint32_t* planes, uint64_t rows, uint64_t cols, 
 cudaError_t launch_quantize_pack(const double* x, uint64_t rows, uint64_t cols, int n,
                                  int granularity, uint32_t* planes, double* scales,
                                  uint8_t* codes, unsigned long long* amax_bits, int* flag,
-                                 cudaStream_t s) {
+                                 cudaStream_t s, uint8_t* gemm_codes, int32_t* gemm_rowsum,
+                                 uint64_t kpad, uint64_t rowsum_pad) {
   cudaError_t e = cudaMemsetAsync(flag, 0, sizeof(int), s);
   if (e != cudaSuccess) return e;
+  const GemmCodesOut g{gemm_codes, gemm_rowsum, kpad};
+  if (gemm_codes) {  // rowsum: zero the padding (and, per tensor, the atomics' targets)
+    e = cudaMemsetAsync(gemm_rowsum, 0, rowsum_pad * sizeof(int32_t), s);
+    if (e != cudaSuccess) return e;
+  }
   if (granularity == 1) {
     quantize_rows_kernel<<<static_cast<unsigned>(rows), kThreads, 0, s>>>(x, rows, cols, n,
                                                                           planes, scales, codes,
-                                                                          flag);
+                                                                          flag, g);
     return cudaGetLastError();
   }
   e = cudaMemsetAsync(amax_bits, 0, sizeof(unsigned long long), s);
@@ -414,7 +465,7 @@ cudaError_t launch_quantize_pack(const double* x, uint64_t rows, uint64_t cols, 
   absmax_kernel<<<grid, kThreads, 0, s>>>(x, count, amax_bits, flag);
   const uint64_t warps = rows * ((cols + 31) / 32);
   quantize_tensor_kernel<<<blocks_for(warps * 32), kThreads, 0, s>>>(x, rows, cols, n, amax_bits,
-                                                                     planes, scales, codes, flag);
+                                                                     planes, scales, codes, flag, g);
   return cudaGetLastError();
 }
 

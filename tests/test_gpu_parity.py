@@ -428,6 +428,60 @@ def test_host_api_row_block_pipeline(gpu, oracle):
         assert np.array_equal(deq, oracle.dequant_epilogue(got, sw, 1, sx, 1))
 
 
+@pytest.mark.parametrize("rows_w,rows_x,k,nw,nx,gx", [
+    (300, 260, 1000, 3, 4, 1), (2305, 2561, 4200, 2, 4, 0), (513, 700, 33, 4, 8, 1),
+    (4096, 2048, 4096, 2, 4, 1), (300, 16, 1000, 3, 8, 0), (129, 1, 4096, 2, 4, 1)])
+def test_fused_quantize_matmul_dequant(gpu, oracle, rows_w, rows_x, k, nw, nx, gx):
+    """K2 -> K3 (quantizer writes the GEMM operand) == quantize_pack +
+    matmul_ap_dequant, bit for bit, including X's scales; skinny shapes go through planes."""
+    import torch
+    ap, ctx = gpu
+    dev = torch.device("cuda", 0)
+    g = torch.Generator(device=dev)
+    g.manual_seed(rows_w + rows_x + k)
+    wc = torch.randint(0, 1 << nw, (rows_w, k), generator=g, device=dev, dtype=torch.uint8)
+    wpr = (k + 31) // 32
+    wp = torch.empty(nw * rows_w * wpr, dtype=torch.int32, device=dev)
+    ap.cu_pack(wc, rows_w, k, nw, wp, ctx)
+    sw = torch.rand(rows_w, dtype=torch.float64, device=dev, generator=g)
+    xv = (torch.rand((rows_x, k), dtype=torch.float64, device=dev, generator=g) - 0.5) * 200
+    xv[xv.abs() < 10] = 0.0  # zeros, as the acceptance test's inputs (acceptance.cpp:247)
+    n_sx = rows_x if gx else 1
+    sx1 = torch.empty(n_sx, dtype=torch.float64, device=dev)
+    out1 = torch.empty((rows_w, rows_x), dtype=torch.float32, device=dev)
+    ap.cu_quantize_matmul_ap_dequant(wp, rows_w, nw, sw, 1, xv, rows_x, k, nx, gx, sx1, out1, ctx)
+    xp = torch.empty(nx * rows_x * wpr, dtype=torch.int32, device=dev)
+    sx2 = torch.empty(n_sx, dtype=torch.float64, device=dev)
+    ap.cu_quantize_pack(xv, rows_x, k, nx, gx, xp, sx2, ctx=ctx)
+    out2 = torch.empty((rows_w, rows_x), dtype=torch.float32, device=dev)
+    ap.cu_matmul_ap_dequant(wp, rows_w, nw, sw, 1, xp, rows_x, nx, sx2, gx, k, out2, ctx)
+    torch.cuda.synchronize()
+    assert torch.equal(sx1, sx2)
+    assert torch.equal(out1, out2), (out1 - out2).abs().max().item()
+    # and against the C restatement on a few rows: quantize, pack, matmul, dequant epilogue
+    codes, scales = oracle.quantize(xv.cpu().numpy(), nx, gx)
+    assert np.array_equal(scales, sx1.cpu().numpy())
+    rows = np.unique(np.array([0, rows_w - 1, rows_w // 2]))
+    wc_h = wc.cpu().numpy()[rows]
+    y = oracle.matmul_ap(oracle.pack(wc_h, nw), len(rows), nw, oracle.pack(codes, nx), rows_x, nx, k)
+    want = oracle.dequant_epilogue(y, sw.cpu().numpy()[rows], 1, scales, gx)
+    assert np.array_equal(out1.cpu().numpy()[rows], want)
+
+
+def test_fused_quantize_matmul_nonfinite(gpu):
+    import torch
+    ap, ctx = gpu
+    dev = torch.device("cuda", 0)
+    wp = torch.zeros(2 * 300 * 8, dtype=torch.int32, device=dev)
+    sw = torch.ones(300, dtype=torch.float64, device=dev)
+    xv = torch.zeros((100, 256), dtype=torch.float64, device=dev)
+    xv[3, 7] = float("nan")
+    with pytest.raises(ap.NonFinite):
+        ap.cu_quantize_matmul_ap_dequant(wp, 300, 2, sw, 1, xv, 100, 256, 4, 1,
+                                         torch.empty(100, dtype=torch.float64, device=dev),
+                                         torch.empty((300, 100), dtype=torch.float32, device=dev), ctx)
+
+
 # ---------------------------------------------------------------- plane products / recover
 def test_plane_products_and_recover_match_oracle(gpu, oracle):
     """compute_plane_products / matmul_plane_pair / recover (kernel.cpp:125-181) on the GPU
