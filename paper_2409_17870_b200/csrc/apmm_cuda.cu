@@ -262,9 +262,21 @@ int run_matmul(apmm_ctx* ctx, const uint32_t* w, uint64_t rows_w, int n_w, const
   const uint64_t pair_tiles = ((rows_w + 255) / 256) * ((rows_x + kPairN - 1) / kPairN);
   const bool pair = pair_tiles >= static_cast<uint64_t>(ctx->num_sms / 2) && !ctx->force_single_sm;
   const bool fused = pair && gemm_fused_supported(w, k);
+  // Mid-size calls (too few 256x256 tiles to fill the machine, e.g. M_tok = 64..1024), opt-in
+  // (APMM_MID=1): the weight planes are expanded on chip (each W row once per few N tiles)
+  // and K is split across CTA pairs, partials reduce-added into a zeroed Y. Bit-exact
+  // (tests) but measured slower than K1 + the 1-SM GEMM (4096x128x4096: 21.1 vs 18.3 us;
+  // profiles/r01b_mid_size.txt): the memset + K1 (W rowsum, latency-bound) + kernel start
+  // dominate at these sizes.
+  const char* mid_env = std::getenv("APMM_MID");
+  const bool mid_on = mid_env != nullptr && mid_env[0] == '1';
+  const bool mid = mid_on && !pair && !ctx->force_single_sm && !yf && rows_x > kSkinnyMaxRowsX &&
+                   rows_x % 4 == 0 && reinterpret_cast<uintptr_t>(y) % 16 == 0 &&
+                   gemm_wplanes_addressable(w, k) && std::getenv("APMM_NO_MID") == nullptr;
+  if (mid) CU(cudaMemsetAsync(y, 0, rows_w * rows_x * sizeof(int32_t), stream));
   {
     TimedLaunch t(ctx, 1, stream);
-    CU(launch_expand(w, rows_w, n_w, fused ? nullptr : m.codes_w, m.rowsum_w, x_ready ? nullptr : x,
+    CU(launch_expand(w, rows_w, n_w, (fused || mid) ? nullptr : m.codes_w, m.rowsum_w, x_ready ? nullptr : x,
                      x_ready ? 0 : rows_x, x_ready ? 0 : rsx_pad, n_x, m.codes_x, m.rowsum_x, k,
                      m.kpad, ctx->num_sms, stream));
   }
@@ -297,8 +309,8 @@ int run_matmul(apmm_ctx* ctx, const uint32_t* w, uint64_t rows_w, int n_w, const
   int launches = 0;
   {
     TimedLaunch t(ctx, 0, stream);
-    if (fused) {
-      CU(launch_gemm_pair_wplanes(a, w, stream, &launches));
+    if (fused || mid) {
+      CU(launch_gemm_pair_wplanes(a, w, stream, &launches, /*split_k=*/mid));
     } else if (pair) {
       CU(launch_gemm_pair(a, stream, &launches));
     } else {

@@ -90,6 +90,11 @@ struct Params {
   uint32_t n_w;        // runtime plane count (<= NW)
   uint32_t last_word;  // index of the last plane word of a row (wpr - 1)
   uint32_t tail_mask;  // valid bits of that word (reference padding is zero; masked anyway)
+  // split-K mode (mid-size calls that cannot fill the machine with tiles): work unit u =
+  // (tile u / split, K blocks [ks*kb_per, +kb_per) with ks = u % split); tiles are `ncols`
+  // wide; partial sums are TMA reduce-added into a pre-zeroed Y, the rank-1 term by ks == 0.
+  uint32_t split;   // 0: off (plain tiles, store epilogue)
+  uint32_t kb_per, ncols, tiles_n_split;
   uint32_t ablate;  // dev only (APMM_FUSED_ABLATE, results wrong): 1 skip A stores, 2 skip B loads
   unsigned long long* dbg;  // APMM_DEBUG_WAITS=1: wait-cycle counters per role, else null
 };
@@ -203,6 +208,30 @@ __device__ __forceinline__ TileInfo tile_info(uint32_t t, uint32_t tiles_m, uint
   return {tm, tn * kPairN + (h & 1u) * (kPairN / 2), kPairN / 2};
 }
 
+struct Unit {
+  TileInfo ti;
+  uint32_t kb0, kb1;
+  bool first;  // adds the rank-1 recovery term (the K range starting at 0)
+};
+__device__ __forceinline__ Unit unit_info(uint32_t u, const Params& p) {
+  if (!p.split) return {tile_info(u, p.tiles_m, p.tiles_n, p.n_full), 0u, p.kblocks, true};
+  const uint32_t t = u / p.split, ks = u - t * p.split;
+  uint32_t tm, tn;
+  raster_tile(t, p.tiles_m, p.tiles_n_split, tm, tn);
+  const uint32_t kb0 = ks * p.kb_per;
+  const uint32_t kb1 = kb0 + p.kb_per < p.kblocks ? kb0 + p.kb_per : p.kblocks;
+  return {{tm, tn * p.ncols, p.ncols}, kb0, kb1, ks == 0};
+}
+
+// TMA reduce-add of a staged 32x32 int32 tile into Y (split-K partial sums; exact mod 2^32)
+APMM_DEV void tma_reduce_add_2d(const void* tmap, const void* smem_src, int32_t c0, int32_t c1) {
+  asm volatile(
+      "cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+          reinterpret_cast<uint64_t>(tmap)),
+      "r"(smem_u32(smem_src)), "r"(c0), "r"(c1)
+      : "memory");
+}
+
 // NW: planes handled at compile time (1..4 exact; 8 covers 5..8 with runtime masking).
 template <int NW>
 // Register cap: 384 x 136 leaves room for one K1 block (128 x 80) beside the resident CTA,
@@ -239,7 +268,8 @@ __global__ void __maxnreg__(kXformWarpsCfg == 4 ? 136 : 104)
   const bool leader = q == 0;
   const uint32_t cluster = blockIdx.x / 2;
   const uint32_t nclusters = gridDim.x / 2;
-  const uint32_t num_tiles = p.n_full + 2 * (p.tiles_m * p.tiles_n - p.n_full);
+  const uint32_t num_tiles = p.split ? p.tiles_m * p.tiles_n_split * p.split
+                                    : p.n_full + 2 * (p.tiles_m * p.tiles_n - p.n_full);
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmap_wp);
@@ -274,9 +304,10 @@ __global__ void __maxnreg__(kXformWarpsCfg == 4 ? 136 : 104)
       const uint64_t hint = policy_evict_last();
       uint32_t stage = 0, phase = 0;
       for (uint32_t t = cluster; t < num_tiles; t += nclusters) {
-        const TileInfo ti = tile_info(t, p.tiles_m, p.tiles_n, p.n_full);
+        const Unit un = unit_info(t, p);
+        const TileInfo ti = un.ti;
         const bool half = ti.ncols != kPairN;
-        for (uint32_t kb = 0; kb < p.kblocks; ++kb) {
+        for (uint32_t kb = un.kb0; kb < un.kb1; ++kb) {
           mbar_wait_b(&empty_bar[stage], phase ^ 1, 1);
           uint8_t* st = stages + stage * kStageBytes;
           if (leader) mbar_arrive_expect_tx(&full_bar[stage], (p.ablate & 2) ? 0 : half ? kAS : 2 * kAS);
@@ -308,8 +339,9 @@ __global__ void __maxnreg__(kXformWarpsCfg == 4 ? 136 : 104)
         mbar_wait_b(&tmem_empty[acc], acc_phase ^ 1, 2, at);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * kPairN;
-        const uint32_t idesc = tile_info(t, p.tiles_m, p.tiles_n, p.n_full).ncols != kPairN ? kIdescHalf : kIdesc;
-        for (uint32_t kb = 0; kb < p.kblocks; ++kb) {
+        const Unit un = unit_info(t, p);
+        const uint32_t idesc = un.ti.ncols != kPairN ? kIdescHalf : kIdesc;
+        for (uint32_t kb = un.kb0; kb < un.kb1; ++kb) {
           mbar_wait_b<true>(&full_bar[stage], phase, 3, af);
           tc_fence_after();
           const uint32_t st = smem_u32(stages + stage * kStageBytes);
@@ -317,7 +349,7 @@ __global__ void __maxnreg__(kXformWarpsCfg == 4 ? 136 : 104)
           const uint64_t bdesc = umma_desc_sw128(st + kAS);
 #pragma unroll
           for (uint32_t k = 0; k < kBK / 32; ++k) {
-            mma_i8_pair(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) != 0);
+            mma_i8_pair(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb != un.kb0) || k != 0);
           }
           mma_commit_pair_mc(&empty_bar[stage], 0x3);
           if (++stage == kStages) { stage = 0; phase ^= 1; }
@@ -339,8 +371,9 @@ __global__ void __maxnreg__(kXformWarpsCfg == 4 ? 136 : 104)
       const uint64_t hint = policy_evict_last();
       uint32_t rs = 0, rphase = 0;
       for (uint32_t t = cluster; t < num_tiles; t += nclusters) {
-        const int32_t wrow = int32_t(tile_info(t, p.tiles_m, p.tiles_n, p.n_full).tm * 2 * kHalf + q * kHalf);
-        for (uint32_t kb = 0; kb < p.kblocks; kb += kRB) {
+        const Unit un = unit_info(t, p);
+        const int32_t wrow = int32_t(un.ti.tm * 2 * kHalf + q * kHalf);
+        for (uint32_t kb = un.kb0; kb < un.kb1; kb += kRB) {
           mbar_wait_b(&raw_empty[rs], rphase ^ 1, 6);
           mbar_arrive_expect_tx(&raw_full[rs], p.n_w * kRawPlane);
           tma_load_3d_local(smem_u32(raw_ring + rs * kRawBytes), &tmap_wp, smem_u32(&raw_full[rs]),
@@ -364,10 +397,26 @@ __global__ void __maxnreg__(kXformWarpsCfg == 4 ? 136 : 104)
     uint32_t stage = 0, phase = 0, rs = 0, rphase = 0;
     uint32_t x[kWPT][8];
     unsigned long long c_raw = 0;
-    const uint32_t total = ((num_tiles > cluster) ? (num_tiles - cluster + nclusters - 1) / nclusters : 0u) *
-                           p.kblocks;
+    // the flat sequence of (unit, K block) this CTA's MMA consumes: cursor (fu, fkb) = the
+    // block the next fetch() reads, within unit range [fkb0, fkb1)
+    uint32_t fu = cluster, fkb0 = 0, fkb1 = 0, fkb = 0;
+    auto cursor_load = [&]() {
+      if (fu < num_tiles) {
+        const Unit un = unit_info(fu, p);
+        fkb0 = un.kb0;
+        fkb1 = un.kb1;
+        fkb = fkb0;
+      }
+    };
+    cursor_load();
+    auto cursor_next = [&]() {
+      if (++fkb == fkb1) {
+        fu += nclusters;
+        cursor_load();
+      }
+    };
     auto fetch = [&](uint32_t kb) {  // raw planes of K block kb -> codes in x
-      const uint32_t j = kb % kRB;  // K block within the raw stage
+      const uint32_t j = (kb - fkb0) % kRB;  // K block within the raw stage (stages start at kb0)
       if (j == 0) {
         const unsigned long long r0 = p.dbg ? clock64() : 0;
         mbar_wait_b(&raw_full[rs], rphase, 4);
@@ -404,17 +453,17 @@ __global__ void __maxnreg__(kXformWarpsCfg == 4 ? 136 : 104)
       }
 #pragma unroll
       for (int u = 0; u < kWPT; ++u) transpose8(x[u]);
-      if (j == kRB - 1 || kb + 1 == p.kblocks) {
+      if (j == kRB - 1 || kb + 1 == fkb1) {
         __syncwarp();  // every lane's plane words are consumed: the slot may be refilled
         if (lane == 0) mbar_arrive(&raw_empty[rs]);
         if (++rs == kRawStages) { rs = 0; rphase ^= 1; }
       }
     };
-    uint32_t kb = 0;
     unsigned long long c_empty = 0, c_fetch = 0, c_pub = 0;
     const unsigned long long t_loop = clock64();
-    if (total) fetch(0);
-    for (uint32_t it = 0; it < total; ++it) {
+    bool have = fu < num_tiles;
+    if (have) fetch(fkb);
+    while (have) {
       const unsigned long long t0 = p.dbg ? clock64() : 0;
       mbar_wait_b(&empty_bar[stage], phase ^ 1, 7);  // the MMA is done with this A slot
       const unsigned long long t1 = p.dbg ? clock64() : 0;
@@ -427,8 +476,9 @@ __global__ void __maxnreg__(kXformWarpsCfg == 4 ? 136 : 104)
         st_shared_v4(arow + (((c + 1u) ^ sw) << 4), x[u][4], x[u][5], x[u][6], x[u][7]);
       }
       // next block's codes while the stores drain; then publish this stage
-      if (++kb == p.kblocks) kb = 0;
-      if (it + 1 < total) fetch(kb);
+      cursor_next();
+      have = fu < num_tiles;
+      if (have) fetch(fkb);
       const unsigned long long t2 = p.dbg ? clock64() : 0;
       if (!(p.ablate & 4)) fence_proxy_async_smem();  // generic stores -> async proxy (MMA)
       __syncwarp();
@@ -455,12 +505,15 @@ __global__ void __maxnreg__(kXformWarpsCfg == 4 ? 136 : 104)
     uint32_t acc = 0, acc_phase = 0, nbuf = 0;
     const uint64_t store_hint = policy_evict_first();
     for (uint32_t t = cluster; t < num_tiles; t += nclusters) {
-      const TileInfo ti = tile_info(t, p.tiles_m, p.tiles_n, p.n_full);
+      const Unit un = unit_info(t, p);
+      const TileInfo ti = un.ti;
       const uint32_t row0 = ti.tm * 2 * kHalf + q * kHalf + wq * 32;
       const uint32_t row = row0 + lane;
       const bool row_ok = row < p.rows_w;
       const uint32_t rsw = row_ok ? static_cast<uint32_t>(__ldg(p.rowsum_w + row)) : 0u;
-      const uint32_t row_term = p.c0 - p.coef_w * rsw;
+      // split-K: only the unit holding K block 0 adds the rank-1 recovery term
+      const uint32_t row_term = un.first ? p.c0 - p.coef_w * rsw : 0u;
+      const uint32_t coef_x = un.first ? p.coef_x : 0u;
       double swv = 0.0;
       if (p.yf) swv = p.gran_w ? (row_ok ? p.s_w[row] : 0.0) : p.s_w[0];
 
@@ -477,10 +530,10 @@ __global__ void __maxnreg__(kXformWarpsCfg == 4 ? 136 : 104)
 #pragma unroll
         for (int j4 = 0; j4 < 8; ++j4) {
           const int4 rs = __ldg(rsx4 + j4);
-          r[4 * j4 + 0] = 4u * r[4 * j4 + 0] + row_term - p.coef_x * uint32_t(rs.x);
-          r[4 * j4 + 1] = 4u * r[4 * j4 + 1] + row_term - p.coef_x * uint32_t(rs.y);
-          r[4 * j4 + 2] = 4u * r[4 * j4 + 2] + row_term - p.coef_x * uint32_t(rs.z);
-          r[4 * j4 + 3] = 4u * r[4 * j4 + 3] + row_term - p.coef_x * uint32_t(rs.w);
+          r[4 * j4 + 0] = 4u * r[4 * j4 + 0] + row_term - coef_x * uint32_t(rs.x);
+          r[4 * j4 + 1] = 4u * r[4 * j4 + 1] + row_term - coef_x * uint32_t(rs.y);
+          r[4 * j4 + 2] = 4u * r[4 * j4 + 2] + row_term - coef_x * uint32_t(rs.z);
+          r[4 * j4 + 3] = 4u * r[4 * j4 + 3] + row_term - coef_x * uint32_t(rs.w);
         }
         if (p.yf) {
           if (p.gran_x) {
@@ -509,7 +562,11 @@ __global__ void __maxnreg__(kXformWarpsCfg == 4 ? 136 : 104)
           fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {
-            tma_store_2d(&tmap_y, buf, int32_t(col0), int32_t(row0), store_hint);
+            if (p.split) {
+              tma_reduce_add_2d(&tmap_y, buf, int32_t(col0), int32_t(row0));
+            } else {
+              tma_store_2d(&tmap_y, buf, int32_t(col0), int32_t(row0), store_hint);
+            }
             bulk_commit();
           }
         } else if (row_ok && col0 < p.rows_x) {
@@ -574,6 +631,12 @@ cudaError_t launch_nw(const CUtensorMap& twp, const CUtensorMap& tx, const CUten
     }
   }
   const uint32_t mc = static_cast<uint32_t>(max_clusters);
+  if (p.split) {  // split-K units: (tiles of ncols) x split
+    const uint32_t units = p.tiles_m * p.tiles_n_split * p.split;
+    cfg.gridDim = dim3(2 * (units < mc ? units : mc));
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, twp, tx, tx64, ty, p);
+    return e != cudaSuccess ? e : cudaGetLastError();
+  }
   p.n_full = full_tiles;
   if (std::getenv("APMM_NO_TAIL_SPLIT") == nullptr) {
     const uint32_t r = full_tiles % mc;
@@ -597,6 +660,11 @@ cudaError_t launch_nw(const CUtensorMap& twp, const CUtensorMap& tx, const CUten
 // cannot hide: they need ~550 cycles per K block against ~350 cycles of MMA
 // (APMM_DEBUG_WAITS breakdown in profiles/r01b_notes.md). Kept, tested bit-exact, for the
 // shapes where it could pay (few N tiles, wide K).
+bool gemm_wplanes_addressable(const uint32_t* w_planes, uint64_t k) {
+  return ((k + 31) / 32) % 4 == 0 && reinterpret_cast<uintptr_t>(w_planes) % 16 == 0 &&
+         std::getenv("APMM_NO_FUSED") == nullptr;
+}
+
 bool gemm_fused_supported(const uint32_t* w_planes, uint64_t k) {
   const uint64_t wpr = (k + 31) / 32;
   const char* on = std::getenv("APMM_FUSED");
@@ -605,7 +673,7 @@ bool gemm_fused_supported(const uint32_t* w_planes, uint64_t k) {
 }
 
 cudaError_t launch_gemm_pair_wplanes(const GemmArgs& a, const uint32_t* w_planes,
-                                     cudaStream_t s, int* launches) {
+                                     cudaStream_t s, int* launches, bool split_k) {
   const uint64_t wpr = (a.k_logical + 31) / 32;
   CUtensorMap twp, tx, tx64, ty;
   {
@@ -666,6 +734,23 @@ cudaError_t launch_gemm_pair_wplanes(const GemmArgs& a, const uint32_t* w_planes
   }();
   p.ablate = ablate;
   const uint32_t full_tiles = p.tiles_m * p.tiles_n;
+  if (split_k) {
+    // mid-size call: tiles of 128 (M_tok <= 128) or 256 feature rows, K split so that the
+    // units fill the co-resident pairs (one per TPC: num_sms / 2)
+    p.ncols = a.rows_x <= 128 ? 128u : 256u;
+    p.tiles_n_split = static_cast<uint32_t>((a.rows_x + p.ncols - 1) / p.ncols);
+    const uint32_t tiles = p.tiles_m * p.tiles_n_split;
+    const uint32_t pairs = static_cast<uint32_t>(a.num_sms / 2);
+    uint32_t sk = pairs / (tiles ? tiles : 1);
+    const uint32_t max_s = p.kblocks / 2 > 0 ? p.kblocks / 2 : 1;  // >= 2 K blocks per unit
+    sk = sk < 1 ? 1 : (sk > max_s ? max_s : sk);
+    p.kb_per = (p.kblocks + sk - 1) / sk;
+    p.split = (p.kblocks + p.kb_per - 1) / p.kb_per;  // no empty units
+    if (std::getenv("APMM_DEBUG_PLAN")) {
+      std::fprintf(stderr, "[apmm fused] split-K: %u tiles of %u cols x %u K splits of %u blocks\n",
+                   tiles, p.ncols, p.split, p.kb_per);
+    }
+  }
   cudaError_t e;
   switch (a.n_w) {
     case 1: e = launch_nw<1>(twp, tx, tx64, ty, p, full_tiles, a.num_sms, s); break;

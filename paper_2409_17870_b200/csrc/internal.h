@@ -93,8 +93,12 @@ cudaError_t launch_gemm_pair(const GemmArgs& a, cudaStream_t s, int* launches);
 // aligned base (TMA); a.codes_w is unused (K1 then runs with w_codes == nullptr and only
 // produces rowsum_w).
 bool gemm_fused_supported(const uint32_t* w_planes, uint64_t k);
+bool gemm_wplanes_addressable(const uint32_t* w_planes, uint64_t k);
+// split_k: mid-size calls (too few tiles for the machine): K split into units whose int32
+// partials are TMA reduce-added into Y, which the caller must have zeroed (int32 out and
+// TMA-storable Y only).
 cudaError_t launch_gemm_pair_wplanes(const GemmArgs& a, const uint32_t* w_planes,
-                                     cudaStream_t s, int* launches);
+                                     cudaStream_t s, int* launches, bool split_k = false);
 
 // ---- skinny.cu (few feature rows: weight planes streamed from HBM into mma.sync) -----
 constexpr uint64_t kSkinnyMaxRowsX = 63;  // feature rows handled by K5 (+1 ones column <= 64)

@@ -274,6 +274,38 @@ def test_fused_weight_plane_gemm(gpu, oracle, nw, nx, n_out, m_tok, k):
     assert torch.equal(f1, want)
 
 
+@pytest.mark.parametrize("n_out,m_tok,k,nw,nx", [
+    (4096, 128, 4096, 2, 4), (4096, 512, 4096, 3, 8), (2305, 68, 4200, 1, 2),
+    (4096, 1024, 11008, 2, 4), (300, 260, 4224, 8, 8), (11008, 256, 4096, 4, 4),
+    (1000, 96, 128, 5, 3)])
+def test_mid_size_split_k_path(gpu, oracle, n_out, m_tok, k, nw, nx):
+    """Mid-size calls (too few 256x256 tiles; opt-in APMM_MID=1): weight planes expanded on
+    chip, K split over CTA pairs, int32 partials TMA reduce-added into a zeroed Y. Against the oracle on sampled
+    rows and against the 1-SM path (APMM_NO_MID=1) on every entry."""
+    import torch
+    ap, ctx = gpu
+    os.environ["APMM_MID"] = "1"
+    try:
+        y = _row_sample_check(ap, ctx, oracle, n_out, m_tok, k, nw, nx, seed=n_out * 7 + m_tok,
+                              sample=24)
+    finally:
+        del os.environ["APMM_MID"]
+    dev = torch.device("cuda", 0)
+    g = torch.Generator(device=dev)
+    g.manual_seed(n_out * 7 + m_tok)
+    wc = torch.randint(0, 1 << nw, (n_out, k), generator=g, device=dev, dtype=torch.uint8)
+    xc = torch.randint(0, 1 << nx, (m_tok, k), generator=g, device=dev, dtype=torch.uint8)
+    wpr = (k + 31) // 32
+    wp = torch.empty(nw * n_out * wpr, dtype=torch.int32, device=dev)
+    xp = torch.empty(nx * m_tok * wpr, dtype=torch.int32, device=dev)
+    ap.cu_pack(wc, n_out, k, nw, wp, ctx)
+    ap.cu_pack(xc, m_tok, k, nx, xp, ctx)
+    y2 = torch.empty((n_out, m_tok), dtype=torch.int32, device=dev)
+    ap.cu_matmul_ap(wp, n_out, nw, xp, m_tok, nx, k, y2, ctx)  # default route (K1 + 1-SM GEMM)
+    torch.cuda.synchronize()
+    assert torch.equal(y, y2), (n_out, m_tok, k, nw, nx)
+
+
 @pytest.mark.parametrize("nw,nx", [(1, 2), (2, 4), (3, 8), (4, 8)])
 def test_config2_4096_cubed_row_sampled(gpu, oracle, nw, nx):
     ap, ctx = gpu
