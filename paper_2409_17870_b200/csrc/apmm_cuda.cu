@@ -203,7 +203,28 @@ int run_matmul(apmm_ctx* ctx, const uint32_t* w, uint64_t rows_w, int n_w, const
                int gran_x, uint64_t k, int32_t* y, float* yf, cudaStream_t stream,
                bool x_ready = false) {
   CU(cudaSetDevice(ctx->device));
-  if (rows_x <= kSkinnyMaxRowsX && !ctx->force_tc && !x_ready) {
+  // Route. CTA-pair 256x256 tiles (K3) when they fill the machine. Otherwise mid-size calls
+  // (M_tok <= 256) take the split-K K3f: the weight planes are expanded on chip (each W row
+  // once: a single N tile), rowsum(U_w) formed by the transform warps, K split across CTA
+  // pairs, int32 partials TMA reduce-added into a Y zeroed by K1 (4096x128x4096 W2A4: 14.0
+  // us vs 18.3 us for K1 + the 1-SM GEMM; profiles/r01b_mid_size_v2.txt). Feature counts up
+  // to kSkinnyPreferRows stay on K5 (faster there: 4096x40x4096 8.6 vs 12.6 us,
+  // profiles/r01b_skinny_mid_boundary.txt), and K5 takes up to 63 rows when the split-K
+  // path cannot (int32 output with a TMA-storable Y only). APMM_MID=0/1 forces the split-K
+  // path off/on, APMM_SKINNY_MAX moves the K5 boundary (testing).
+  const uint64_t pair_tiles = ((rows_w + 255) / 256) * ((rows_x + kPairN - 1) / kPairN);
+  const bool pair = pair_tiles >= static_cast<uint64_t>(ctx->num_sms / 2) && !ctx->force_single_sm;
+  const char* mid_env = std::getenv("APMM_MID");
+  const bool mid = (mid_env ? mid_env[0] == '1' : rows_x <= 256) && !pair &&
+                   !ctx->force_single_sm && !yf && rows_x > 0 && rows_x % 4 == 0 &&
+                   reinterpret_cast<uintptr_t>(y) % 16 == 0 && gemm_wplanes_addressable(w, k);
+  static const uint64_t skinny_prefer = [] {
+    const char* e = std::getenv("APMM_SKINNY_MAX");
+    return e ? static_cast<uint64_t>(std::atoll(e)) : kSkinnyPreferRows;
+  }();
+  const bool skinny = rows_x <= kSkinnyMaxRowsX && !ctx->force_tc && !x_ready &&
+                      (rows_x <= skinny_prefer || !mid);
+  if (skinny) {
     // few feature rows: feature prep + K5, the weight planes streamed once from HBM
     const size_t need = skinny_acc_bytes(rows_w, rows_x);
     if (need > ctx->sk_ws_bytes) {  // split-K accumulators; zero at rest
@@ -256,29 +277,15 @@ int run_matmul(apmm_ctx* ctx, const uint32_t* w, uint64_t rows_w, int n_w, const
   const MatmulWs m = carve(ctx->ws, rows_w, rows_x, k, ctx->ws_half);
   ctx->ws_half ^= 1;
   const uint64_t rsx_pad = round_up(rows_x, kRowsumPad);
-  // CTA-pair 256x256 tiles when they fill the machine, else 1-SM 128x256 tiles. The pair
-  // kernel expands the weight planes on chip when TMA can address them (K3f), so K1 then
-  // only expands X and produces rowsum(U_w).
-  const uint64_t pair_tiles = ((rows_w + 255) / 256) * ((rows_x + kPairN - 1) / kPairN);
-  const bool pair = pair_tiles >= static_cast<uint64_t>(ctx->num_sms / 2) && !ctx->force_single_sm;
   const bool fused = pair && gemm_fused_supported(w, k);
-  // Mid-size calls (too few 256x256 tiles to fill the machine, e.g. M_tok = 64..1024), opt-in
-  // (APMM_MID=1): the weight planes are expanded on chip (each W row once per few N tiles)
-  // and K is split across CTA pairs, partials reduce-added into a zeroed Y. Bit-exact
-  // (tests) but measured slower than K1 + the 1-SM GEMM (4096x128x4096: 21.1 vs 18.3 us;
-  // profiles/r01b_mid_size.txt): the memset + K1 (W rowsum, latency-bound) + kernel start
-  // dominate at these sizes.
-  const char* mid_env = std::getenv("APMM_MID");
-  const bool mid_on = mid_env != nullptr && mid_env[0] == '1';
-  const bool mid = mid_on && !pair && !ctx->force_single_sm && !yf && rows_x > kSkinnyMaxRowsX &&
-                   rows_x % 4 == 0 && reinterpret_cast<uintptr_t>(y) % 16 == 0 &&
-                   gemm_wplanes_addressable(w, k) && std::getenv("APMM_NO_MID") == nullptr;
-  if (mid) CU(cudaMemsetAsync(y, 0, rows_w * rows_x * sizeof(int32_t), stream));
   {
     TimedLaunch t(ctx, 1, stream);
-    CU(launch_expand(w, rows_w, n_w, (fused || mid) ? nullptr : m.codes_w, m.rowsum_w, x_ready ? nullptr : x,
-                     x_ready ? 0 : rows_x, x_ready ? 0 : rsx_pad, n_x, m.codes_x, m.rowsum_x, k,
-                     m.kpad, ctx->num_sms, stream));
+    // mid (split-K K3f): W untouched (the GEMM expands it and forms rowsum(U_w) itself);
+    // K1 expands X and zeroes Y, which the split-K units reduce-add into
+    CU(launch_expand(w, mid ? 0 : rows_w, n_w, (fused || mid) ? nullptr : m.codes_w, m.rowsum_w,
+                     x_ready ? nullptr : x, x_ready ? 0 : rows_x, x_ready ? 0 : rsx_pad, n_x,
+                     m.codes_x, m.rowsum_x, k, m.kpad, ctx->num_sms, stream,
+                     mid ? static_cast<void*>(y) : nullptr, mid ? rows_w * rows_x * 4 : 0));
   }
   ctx->launches += 1;
   GemmArgs a{};

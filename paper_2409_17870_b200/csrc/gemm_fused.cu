@@ -62,7 +62,7 @@ __host__ __device__ constexpr int raw_plane(int nw) { return kHalf * 16 * raw_rb
 __host__ __device__ constexpr int raw_bytes(int nw) { return nw * raw_plane(nw); }
 constexpr int kOpStageBytes = 2 * kAS;
 __host__ __device__ constexpr int op_stages(int nw) { return nw <= 2 ? 5 : 4; }
-constexpr int kSmemCap = 232448 - 1024 - 1024;  // 227 KB minus alignment slack and barriers
+constexpr int kSmemCap = 232448 - 1024 - 1024 - 2048;  // 227 KB minus alignment slack, barriers and the static rowsum buffers
 __host__ __device__ constexpr int raw_stages(int nw) {
   return (kSmemCap - op_stages(nw) * kOpStageBytes - 4 * 2 * kEpiBuf) / raw_bytes(nw) > 16
              ? 16
@@ -260,6 +260,10 @@ __global__ void __maxnreg__(kXformWarpsCfg == 4 ? 136 : 104)
   uint64_t* tmem_full = raw_empty + kRawStages;
   uint64_t* tmem_empty = tmem_full + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
+  // split mode: rowsum(U_w) of this CTA's 128 rows over the unit's K range, computed by the
+  // transform warps (sum_i 2^i popc(plane words)), double-buffered like the accumulators
+  __shared__ int32_t rsw_s[2][kHalf];
+  __shared__ __align__(8) uint64_t rsw_full[2], rsw_empty[2];
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
@@ -287,6 +291,8 @@ __global__ void __maxnreg__(kXformWarpsCfg == 4 ? 136 : 104)
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tmem_full[s], 1);
       mbar_init(&tmem_empty[s], 8);
+      mbar_init(&rsw_full[s], kXformWarps);
+      mbar_init(&rsw_empty[s], 4);
     }
     fence_mbar_init();
   }
@@ -397,6 +403,7 @@ __global__ void __maxnreg__(kXformWarpsCfg == 4 ? 136 : 104)
     uint32_t stage = 0, phase = 0, rs = 0, rphase = 0;
     uint32_t x[kWPT][8];
     unsigned long long c_raw = 0;
+    uint32_t rsum = 0, rbuf = 0, rphase_e = 0;  // split mode: this unit's rowsum partial
     // the flat sequence of (unit, K block) this CTA's MMA consumes: cursor (fu, fkb) = the
     // block the next fetch() reads, within unit range [fkb0, fkb1)
     uint32_t fu = cluster, fkb0 = 0, fkb1 = 0, fkb = 0;
@@ -442,6 +449,7 @@ __global__ void __maxnreg__(kXformWarpsCfg == 4 ? 136 : 104)
           for (int u = 0; u < kWPT; ++u) x[u][i] = 0u;
         }
       }
+      if (kb == fkb0) rsum = 0;
       if (kb * 4u + 3u >= p.last_word) {  // the block holding the row's last plane word
 #pragma unroll
         for (int u = 0; u < kWPT; ++u) {
@@ -449,6 +457,21 @@ __global__ void __maxnreg__(kXformWarpsCfg == 4 ? 136 : 104)
           const uint32_t m = wd < p.last_word ? 0xffffffffu : wd == p.last_word ? p.tail_mask : 0u;
 #pragma unroll
           for (int i = 0; i < NW; ++i) x[u][i] &= m;
+        }
+      }
+      if (p.split) {
+#pragma unroll
+        for (int u = 0; u < kWPT; ++u) {
+#pragma unroll
+          for (int i = 0; i < NW; ++i) rsum += uint32_t(__popc(x[u][i])) << i;
+        }
+        if (kb + 1 == fkb1) {  // unit complete: publish the row's partial rowsum
+          rsum += __shfl_xor_sync(0xffffffffu, rsum, 1);  // the row's two threads (kWPT = 2)
+          mbar_wait_b(&rsw_empty[rbuf], rphase_e ^ 1, 8);
+          if (w0 == 0) rsw_s[rbuf][row] = static_cast<int32_t>(rsum);
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&rsw_full[rbuf]);
+          if (++rbuf == 2) { rbuf = 0; rphase_e ^= 1; }
         }
       }
 #pragma unroll
@@ -510,9 +533,18 @@ __global__ void __maxnreg__(kXformWarpsCfg == 4 ? 136 : 104)
       const uint32_t row0 = ti.tm * 2 * kHalf + q * kHalf + wq * 32;
       const uint32_t row = row0 + lane;
       const bool row_ok = row < p.rows_w;
-      const uint32_t rsw = row_ok ? static_cast<uint32_t>(__ldg(p.rowsum_w + row)) : 0u;
-      // split-K: only the unit holding K block 0 adds the rank-1 recovery term
-      const uint32_t row_term = un.first ? p.c0 - p.coef_w * rsw : 0u;
+      uint32_t rsw;
+      if (p.split) {  // this unit's K-range share of rowsum(U_w), from the transform warps
+        mbar_wait_b(&rsw_full[acc], acc_phase, 9);
+        rsw = static_cast<uint32_t>(rsw_s[acc][wq * 32 + lane]);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&rsw_empty[acc]);
+      } else {
+        rsw = row_ok ? static_cast<uint32_t>(__ldg(p.rowsum_w + row)) : 0u;
+      }
+      // split-K: every unit adds its W term (linear in K); the unit holding K block 0 adds
+      // the X term and the constant K*A*B once
+      const uint32_t row_term = (un.first ? p.c0 : 0u) - p.coef_w * rsw;
       const uint32_t coef_x = un.first ? p.coef_x : 0u;
       double swv = 0.0;
       if (p.yf) swv = p.gran_w ? (row_ok ? p.s_w[row] : 0.0) : p.s_w[0];

@@ -37,12 +37,14 @@ __host__ __device__ inline void raster_tile(uint32_t t, uint32_t tiles_m, uint32
 // Both operands' planes (reference layout) -> u8 codes [rows x kpad] (zero K padding, K
 // permuted identically within each 32-column group) + rowsum[rows], one launch.
 // rowsum_x[rows_x, rows_x_pad) is zeroed. Launched with PDL (see prep.cu). w_codes may be
-// null: then only rowsum_w is produced for W (the fused GEMM expands W on chip).
+// null: then only rowsum_w is produced for W (the fused GEMM expands W on chip); rows_w may
+// be 0 (W untouched). zero_out[0, zero_bytes) (16-B multiple) is zeroed after the previous
+// kernel in the stream completed (Y of a split-K GEMM).
 cudaError_t launch_expand(const uint32_t* w_planes, uint64_t rows_w, int n_w,
                           uint8_t* w_codes, int32_t* w_rowsum, const uint32_t* x_planes,
                           uint64_t rows_x, uint64_t rows_x_pad, int n_x, uint8_t* x_codes,
                           int32_t* x_rowsum, uint64_t cols, uint64_t kpad, int num_sms,
-                          cudaStream_t s);
+                          cudaStream_t s, void* zero_out = nullptr, uint64_t zero_bytes = 0);
 cudaError_t launch_pack(const uint8_t* codes, uint64_t rows, uint64_t cols, int n,
                         uint32_t* planes, cudaStream_t s);
 cudaError_t launch_unpack(const uint32_t* planes, uint64_t rows, uint64_t cols, int n,
@@ -102,6 +104,7 @@ cudaError_t launch_gemm_pair_wplanes(const GemmArgs& a, const uint32_t* w_planes
 
 // ---- skinny.cu (few feature rows: weight planes streamed from HBM into mma.sync) -----
 constexpr uint64_t kSkinnyMaxRowsX = 63;  // feature rows handled by K5 (+1 ones column <= 64)
+constexpr uint64_t kSkinnyPreferRows = 40;  // above this the split-K K3f wins when it applies
 struct SkinnyArgs {
   const uint32_t* w_planes;  // reference layout [n_w][rows_w][ceil(k/32)]
   const uint32_t* x_planes;  // reference layout [n_x][rows_x][ceil(k/32)]

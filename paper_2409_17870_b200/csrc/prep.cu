@@ -123,7 +123,8 @@ __device__ __forceinline__ int32_t expand_row(const ExpandOperand& op, uint32_t 
 // covers it.
 __global__ void __launch_bounds__(kExpandThreads) expand_kernel(ExpandOperand a, ExpandOperand b,
                                                                  uint32_t wpr, uint32_t tail_mask,
-                                                                 uint32_t kpad_words) {
+                                                                 uint32_t kpad_words,
+                                                                 uint4* zero_out, uint64_t zero_n) {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const uint32_t warps = blockDim.x >> 5;
   const uint32_t lane = threadIdx.x & 31;
@@ -161,6 +162,12 @@ __global__ void __launch_bounds__(kExpandThreads) expand_kernel(ExpandOperand a,
     for (uint32_t r = b.rows + threadIdx.x; r < b.rows_pad; r += blockDim.x) b.rowsum[r] = 0;
   }
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  // split-K GEMMs reduce-add into Y: zero it here, after the previous kernel in the stream
+  // (which may still have been writing the same Y) has completed
+  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < zero_n;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    zero_out[i] = make_uint4(0, 0, 0, 0);
+  }
 }
 
 // ---- K1': codes -> planes (decompose_and_pack) -------------------------------------------
@@ -389,7 +396,7 @@ cudaError_t launch_expand(const uint32_t* w_planes, uint64_t rows_w, int n_w,
                           uint8_t* w_codes, int32_t* w_rowsum, const uint32_t* x_planes,
                           uint64_t rows_x, uint64_t rows_x_pad, int n_x, uint8_t* x_codes,
                           int32_t* x_rowsum, uint64_t cols, uint64_t kpad, int num_sms,
-                          cudaStream_t s) {
+                          cudaStream_t s, void* zero_out, uint64_t zero_bytes) {
   const uint32_t wpr = static_cast<uint32_t>((cols + 31) / 32);
   const uint32_t tail = static_cast<uint32_t>(cols & 31);
   const uint32_t tail_mask = tail ? ((1u << tail) - 1u) : 0xffffffffu;
@@ -399,6 +406,7 @@ cudaError_t launch_expand(const uint32_t* w_planes, uint64_t rows_w, int n_w,
                         static_cast<uint32_t>(rows_x_pad), n_x};
   const uint64_t warps_needed = rows_w + rows_x;
   uint64_t blocks = (warps_needed + kExpandThreads / 32 - 1) / (kExpandThreads / 32);
+  if (zero_bytes && blocks < uint64_t(num_sms)) blocks = num_sms;  // the zeroing is grid-wide
   // one block per SM: all blocks fit beside a resident GEMM CTA (regs: 8 x 200 x 32 +
   // 4 x 80 x 32 <= 64K), so none is left waiting behind blocks parked in griddepcontrol.wait
   const uint64_t cap = uint64_t(num_sms);
@@ -414,7 +422,8 @@ cudaError_t launch_expand(const uint32_t* w_planes, uint64_t rows_w, int n_w,
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   cudaError_t e = cudaLaunchKernelEx(&cfg, expand_kernel, a, b, wpr, tail_mask,
-                                     static_cast<uint32_t>(kpad / 32));
+                                     static_cast<uint32_t>(kpad / 32),
+                                     static_cast<uint4*>(zero_out), zero_bytes / 16);
   return e != cudaSuccess ? e : cudaGetLastError();
 }
 

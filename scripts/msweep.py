@@ -16,7 +16,8 @@ torch.cuda.set_stream(s)
 wpr = (k + 31) // 32
 ws = [torch.randint(-2**31, 2**31 - 1, (nw * n_out * wpr,), dtype=torch.int32, device=dev)
       for _ in range(max(2, int(300e6 // (4 * nw * n_out * wpr)) + 1))]
-for m in (1, 16, 32, 63, 64, 96, 128, 192, 256, 384, 512, 768, 1024, 2048, 4096):
+ms = [int(v) for v in os.environ.get('MSWEEP', '1,16,32,63,64,96,128,192,256,384,512,768,1024,2048,4096').split(',')]
+for m in ms:
     xp = torch.randint(-2**31, 2**31 - 1, (nx * m * wpr,), dtype=torch.int32, device=dev)
     y = torch.empty((n_out, m), dtype=torch.int32, device=dev)
     reps = 20

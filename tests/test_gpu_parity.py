@@ -279,9 +279,10 @@ def test_fused_weight_plane_gemm(gpu, oracle, nw, nx, n_out, m_tok, k):
     (4096, 1024, 11008, 2, 4), (300, 260, 4224, 8, 8), (11008, 256, 4096, 4, 4),
     (1000, 96, 128, 5, 3)])
 def test_mid_size_split_k_path(gpu, oracle, n_out, m_tok, k, nw, nx):
-    """Mid-size calls (too few 256x256 tiles; opt-in APMM_MID=1): weight planes expanded on
-    chip, K split over CTA pairs, int32 partials TMA reduce-added into a zeroed Y. Against the oracle on sampled
-    rows and against the 1-SM path (APMM_NO_MID=1) on every entry."""
+    """Mid-size calls (too few 256x256 tiles; default for M_tok <= 256, forced here with
+    APMM_MID=1): weight planes expanded on chip, rowsum(U_w) in the transform warps, K split
+    over CTA pairs, int32 partials TMA reduce-added into a Y zeroed by K1. Against the oracle on sampled
+    rows and against the 1-SM path (APMM_MID=0) on every entry."""
     import torch
     ap, ctx = gpu
     os.environ["APMM_MID"] = "1"
@@ -301,8 +302,12 @@ def test_mid_size_split_k_path(gpu, oracle, n_out, m_tok, k, nw, nx):
     ap.cu_pack(wc, n_out, k, nw, wp, ctx)
     ap.cu_pack(xc, m_tok, k, nx, xp, ctx)
     y2 = torch.empty((n_out, m_tok), dtype=torch.int32, device=dev)
-    ap.cu_matmul_ap(wp, n_out, nw, xp, m_tok, nx, k, y2, ctx)  # default route (K1 + 1-SM GEMM)
-    torch.cuda.synchronize()
+    os.environ["APMM_MID"] = "0"  # K1 + the 1-SM GEMM
+    try:
+        ap.cu_matmul_ap(wp, n_out, nw, xp, m_tok, nx, k, y2, ctx)
+        torch.cuda.synchronize()
+    finally:
+        del os.environ["APMM_MID"]
     assert torch.equal(y, y2), (n_out, m_tok, k, nw, nx)
 
 
