@@ -586,8 +586,15 @@ def main():
     if world > 1:
         import torch
         import torch.distributed as dist
+        # APMM_BENCH_BACKEND=gloo (dev): exercise the multi-rank code path with several ranks
+        # sharing the GPUs that exist (NCCL needs one GPU per rank); numbers are not valid
+        backend = os.environ.get("APMM_BENCH_BACKEND", "nccl")
+        local_rank = local_rank % max(1, torch.cuda.device_count())
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:
+            dist.init_process_group(backend)
     try:
         run_ours(args, rank, world, local_rank)
     finally:
