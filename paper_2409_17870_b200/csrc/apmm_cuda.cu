@@ -278,6 +278,14 @@ int run_matmul(apmm_ctx* ctx, const uint32_t* w, uint64_t rows_w, int n_w, const
   ctx->ws_half ^= 1;
   const uint64_t rsx_pad = round_up(rows_x, kRowsumPad);
   const bool fused = pair && gemm_fused_supported(w, k);
+  // Opt-in (APMM_PSPLIT=1): the u8-code pair GEMM with K split over the pairs (partials
+  // reduce-added into a Y zeroed by K1) for calls with too few pair tiles. Bit-exact, but
+  // measured slower than the 1-SM kernel for 256 < M_tok <= 1024 (4096x512x4096: 32.4 vs
+  // 20.3 us; profiles/r01b_pair_split_sweep.txt).
+  const char* ps_env = std::getenv("APMM_PSPLIT");
+  const bool psplit = ps_env != nullptr && ps_env[0] == '1' && !pair && !mid &&
+                      !ctx->force_single_sm && !yf && rows_x % 4 == 0 &&
+                      reinterpret_cast<uintptr_t>(y) % 16 == 0;
   {
     TimedLaunch t(ctx, 1, stream);
     // mid (split-K K3f): W untouched (the GEMM expands it and forms rowsum(U_w) itself);
@@ -285,7 +293,8 @@ int run_matmul(apmm_ctx* ctx, const uint32_t* w, uint64_t rows_w, int n_w, const
     CU(launch_expand(w, mid ? 0 : rows_w, n_w, (fused || mid) ? nullptr : m.codes_w, m.rowsum_w,
                      x_ready ? nullptr : x, x_ready ? 0 : rows_x, x_ready ? 0 : rsx_pad, n_x,
                      m.codes_x, m.rowsum_x, k, m.kpad, ctx->num_sms, stream,
-                     mid ? static_cast<void*>(y) : nullptr, mid ? rows_w * rows_x * 4 : 0));
+                     (mid || psplit) ? static_cast<void*>(y) : nullptr,
+                     (mid || psplit) ? rows_w * rows_x * 4 : 0));
   }
   ctx->launches += 1;
   GemmArgs a{};
@@ -318,8 +327,8 @@ int run_matmul(apmm_ctx* ctx, const uint32_t* w, uint64_t rows_w, int n_w, const
     TimedLaunch t(ctx, 0, stream);
     if (fused || mid) {
       CU(launch_gemm_pair_wplanes(a, w, stream, &launches, /*split_k=*/mid));
-    } else if (pair) {
-      CU(launch_gemm_pair(a, stream, &launches));
+    } else if (pair || psplit) {
+      CU(launch_gemm_pair(a, stream, &launches, /*split_k=*/psplit));
     } else {
       CU(launch_gemm_tc(a, stream, &launches));
     }

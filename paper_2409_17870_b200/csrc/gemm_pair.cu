@@ -60,7 +60,26 @@ struct Params {
                        // last partial wave run as two 256 x 128 halves each (CL == 2 only)
   unsigned long long* dbg;  // optional wait-cycle counters (APMM_DEBUG_WAITS), else null
   uint32_t peak_probe;      // APMM_PEAK_PROBE=1 (measurement only): no operand reloads
+  // split-K (calls with too few tiles to fill the machine; CL == 2, int32 out): unit u =
+  // (tile u / split of `ncols` feature rows, K blocks [ks*kb_per, +kb_per)); int32 partials
+  // are TMA reduce-added into a Y zeroed by K1; the unit holding K block 0 adds the rank-1
+  // recovery terms. 0 = off.
+  uint32_t split, kb_per, ncols, tiles_n_split;
 };
+
+struct PUnit {
+  uint32_t tm, col0, ncols, kb0, kb1;
+  bool first;
+};
+
+// TMA reduce-add of a staged 32x32 int32 tile into Y (exact mod 2^32)
+APMM_DEV void tma_reduce_add_2d(const void* tmap, const void* smem_src, int32_t c0, int32_t c1) {
+  asm volatile(
+      "cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+          reinterpret_cast<uint64_t>(tmap)),
+      "r"(smem_u32(smem_src)), "r"(c0), "r"(c1)
+      : "memory");
+}
 
 __device__ __forceinline__ uint32_t dequant_bits(uint32_t v, double sw, double sx) {
   return __float_as_uint(static_cast<float>(__dmul_rn(__dmul_rn(double(int(v)), sw), sx)));
@@ -86,6 +105,19 @@ __device__ __forceinline__ TileInfo tile_info(uint32_t t, uint32_t tiles_m, uint
   const uint32_t h = t - n_full, f = n_full + (h >> 1);
   raster_tile(f, tiles_m, tiles_n, tm, tn);
   return {tm, tn * kPairN + (h & 1u) * (kPairN / 2), kPairN / 2};
+}
+
+__device__ __forceinline__ PUnit pair_unit(uint32_t t, const Params& p) {
+  if (!p.split) {
+    const TileInfo ti = tile_info(t, p.tiles_m, p.tiles_n, p.n_full);
+    return {ti.tm, ti.col0, ti.ncols, 0u, p.kblocks, true};
+  }
+  const uint32_t tile = t / p.split, ks = t - tile * p.split;
+  uint32_t tm, tn;
+  raster_tile(tile, p.tiles_m, p.tiles_n_split, tm, tn);
+  const uint32_t kb0 = ks * p.kb_per;
+  const uint32_t kb1 = kb0 + p.kb_per < p.kblocks ? kb0 + p.kb_per : p.kblocks;
+  return {tm, tn * p.ncols, p.ncols, kb0, kb1, ks == 0};
 }
 
 template <int CL>
@@ -117,7 +149,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr uint32_t kPairs = CL / 2;
   const uint32_t tiles_mc = (p.tiles_m + kPairs - 1) / kPairs;  // cluster tiles along W rows
   const uint32_t num_tiles =
-      CL == 2 ? p.n_full + 2 * (p.tiles_m * p.tiles_n - p.n_full) : tiles_mc * p.tiles_n;
+      CL == 2 ? (p.split ? p.tiles_m * p.tiles_n_split * p.split
+                         : p.n_full + 2 * (p.tiles_m * p.tiles_n - p.n_full))
+              : tiles_mc * p.tiles_n;
   constexpr uint16_t kAllMask = static_cast<uint16_t>((1u << CL) - 1u);
   const uint16_t pair_mask = static_cast<uint16_t>(0x3u << (2u * pr));
 
@@ -154,11 +188,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t hint = policy_evict_last();
       uint32_t stage = 0, phase = 0, loaded = 0;
       for (uint32_t t = cluster; t < num_tiles; t += nclusters) {
-        const TileInfo ti = CL == 2 ? tile_info(t, p.tiles_m, p.tiles_n, p.n_full)
-                                    : TileInfo{(t % tiles_mc) * kPairs + pr, (t / tiles_mc) * kPairN, kPairN};
+        const PUnit un = CL == 2 ? pair_unit(t, p)
+                                 : PUnit{(t % tiles_mc) * kPairs + pr, (t / tiles_mc) * kPairN,
+                                         kPairN, 0u, p.kblocks, true};
+        const TileInfo ti{un.tm, un.col0, un.ncols};
         const uint32_t tm = ti.tm;
         const bool half = ti.ncols != kPairN;
-        for (uint32_t kb = 0; kb < p.kblocks; ++kb) {
+        for (uint32_t kb = un.kb0; kb < un.kb1; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
           if (p.peak_probe && loaded >= kStages) {
             // measurement mode (APMM_PEAK_PROBE=1, results wrong): after one ring fill the
@@ -204,9 +240,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (p.dbg) w_tmem += clock64() - c0;
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * kPairN;
-        const uint32_t idesc =
-            (CL == 2 && tile_info(t, p.tiles_m, p.tiles_n, p.n_full).ncols != kPairN) ? kIdescHalf : kIdesc;
-        for (uint32_t kb = 0; kb < p.kblocks; ++kb) {
+        const PUnit un = CL == 2 ? pair_unit(t, p) : PUnit{0u, 0u, kPairN, 0u, p.kblocks, true};
+        const uint32_t idesc = un.ncols != kPairN ? kIdescHalf : kIdesc;
+        for (uint32_t kb = un.kb0; kb < un.kb1; ++kb) {
           c0 = p.dbg ? clock64() : 0;
           mbar_wait(&full_bar[stage], phase);
           if (p.dbg) w_full += clock64() - c0;
@@ -216,7 +252,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint64_t bdesc = umma_desc_sw128(st + kAS);
 #pragma unroll
           for (uint32_t k = 0; k < kBK / 32; ++k) {
-            mma_i8_pair(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) != 0);
+            mma_i8_pair(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb != un.kb0) || k != 0);
           }
           mma_commit_pair_mc(&empty_bar[stage], kAllMask);  // frees the slot in every CTA
           if (++stage == kStages) { stage = 0; phase ^= 1; }
@@ -238,14 +274,18 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t acc = 0, acc_phase = 0, nbuf = 0;
     const uint64_t store_hint = policy_evict_first();  // Y streams out; keep operands in L2
     for (uint32_t t = cluster; t < num_tiles; t += nclusters) {
-      const TileInfo ti = CL == 2 ? tile_info(t, p.tiles_m, p.tiles_n, p.n_full)
-                                  : TileInfo{(t % tiles_mc) * kPairs + pr, (t / tiles_mc) * kPairN, kPairN};
+      const PUnit un = CL == 2 ? pair_unit(t, p)
+                               : PUnit{(t % tiles_mc) * kPairs + pr, (t / tiles_mc) * kPairN,
+                                       kPairN, 0u, p.kblocks, true};
+      const TileInfo ti{un.tm, un.col0, un.ncols};
       const uint32_t tm = ti.tm;
       const uint32_t row0 = tm * 2 * kHalf + q * kHalf + wq * 32;
       const uint32_t row = row0 + lane;
       const bool row_ok = row < p.rows_w;
       const uint32_t rsw = row_ok ? static_cast<uint32_t>(__ldg(p.rowsum_w + row)) : 0u;
-      const uint32_t row_term = p.c0 - p.coef_w * rsw;
+      // split-K: the unit holding K block 0 adds the whole rank-1 term (full-K rowsums)
+      const uint32_t row_term = un.first ? p.c0 - p.coef_w * rsw : 0u;
+      const uint32_t coef_x = un.first ? p.coef_x : 0u;
       double sw = 0.0;
       if (p.yf) sw = p.gran_w ? (row_ok ? p.s_w[row] : 0.0) : p.s_w[0];
 
@@ -262,10 +302,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int j4 = 0; j4 < 8; ++j4) {
           const int4 rs = __ldg(rsx4 + j4);
-          r[4 * j4 + 0] = 4u * r[4 * j4 + 0] + row_term - p.coef_x * uint32_t(rs.x);
-          r[4 * j4 + 1] = 4u * r[4 * j4 + 1] + row_term - p.coef_x * uint32_t(rs.y);
-          r[4 * j4 + 2] = 4u * r[4 * j4 + 2] + row_term - p.coef_x * uint32_t(rs.z);
-          r[4 * j4 + 3] = 4u * r[4 * j4 + 3] + row_term - p.coef_x * uint32_t(rs.w);
+          r[4 * j4 + 0] = 4u * r[4 * j4 + 0] + row_term - coef_x * uint32_t(rs.x);
+          r[4 * j4 + 1] = 4u * r[4 * j4 + 1] + row_term - coef_x * uint32_t(rs.y);
+          r[4 * j4 + 2] = 4u * r[4 * j4 + 2] + row_term - coef_x * uint32_t(rs.z);
+          r[4 * j4 + 3] = 4u * r[4 * j4 + 3] + row_term - coef_x * uint32_t(rs.w);
         }
         if (p.yf) {
           if (p.gran_x) {
@@ -294,7 +334,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {
-            tma_store_2d(&tmap_y, buf, int32_t(col0), int32_t(row0), store_hint);
+            if (p.split) {
+              tma_reduce_add_2d(&tmap_y, buf, int32_t(col0), int32_t(row0));
+            } else {
+              tma_store_2d(&tmap_y, buf, int32_t(col0), int32_t(row0), store_hint);
+            }
             bulk_commit();
           }
         } else if (row_ok && col0 < p.rows_x) {
@@ -324,7 +368,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 }  // namespace
 
-cudaError_t launch_gemm_pair(const GemmArgs& a, cudaStream_t s, int* launches) {
+cudaError_t launch_gemm_pair(const GemmArgs& a, cudaStream_t s, int* launches, bool split_k) {
   CUtensorMap tw, tx, tx64, ty;
   if (encode_tmap_2d(&tw, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, a.codes_w, a.kpad, a.rows_w, a.kpad,
                      kBK, kHalf) != CUDA_SUCCESS ||
@@ -423,7 +467,24 @@ cudaError_t launch_gemm_pair(const GemmArgs& a, cudaStream_t s, int* launches) {
     const uint32_t r = full_tiles % max_clusters;
     if (r != 0 && 2 * r <= max_clusters) p.n_full = full_tiles - r;
   }
-  const uint32_t tiles = cl == 4 ? quad_tiles : p.n_full + 2 * (full_tiles - p.n_full);
+  uint32_t tiles = cl == 4 ? quad_tiles : p.n_full + 2 * (full_tiles - p.n_full);
+  if (split_k && cl == 2) {
+    // too few tiles for the machine: tiles of 128 (M_tok <= 128) or 256 feature rows, K split
+    // so that the units fill the co-resident pairs; Y was zeroed by K1
+    p.ncols = a.rows_x <= 128 ? 128u : 256u;
+    p.tiles_n_split = static_cast<uint32_t>((a.rows_x + p.ncols - 1) / p.ncols);
+    const uint32_t t2 = p.tiles_m * p.tiles_n_split;
+    uint32_t sk = max_clusters / (t2 ? t2 : 1);
+    const uint32_t max_s = p.kblocks / 4 > 0 ? p.kblocks / 4 : 1;  // >= 4 K blocks per unit
+    sk = sk < 1 ? 1 : (sk > max_s ? max_s : sk);
+    p.kb_per = (p.kblocks + sk - 1) / sk;
+    p.split = (p.kblocks + p.kb_per - 1) / p.kb_per;
+    tiles = t2 * p.split;
+    if (std::getenv("APMM_DEBUG_PLAN")) {
+      std::fprintf(stderr, "[apmm pair] split-K: %u tiles of %u cols x %u K splits of %u blocks\n",
+                   t2, p.ncols, p.split, p.kb_per);
+    }
+  }
   const uint32_t clusters = tiles < max_clusters ? tiles : max_clusters;
   cfg.gridDim = dim3(cl * clusters);
   cudaError_t e = cl == 4 ? cudaLaunchKernelEx(&cfg, gemm_u8_pair_kernel<4>, tw, tx, tx64, ty, p)

@@ -88,7 +88,9 @@ struct GemmArgs {
 // Returns the number of kernel launches it enqueued via *launches.
 cudaError_t launch_gemm_tc(const GemmArgs& a, cudaStream_t s, int* launches);
 // ---- gemm_pair.cu (CTA-pair, 256x256 tiles) -------------------------------------------
-cudaError_t launch_gemm_pair(const GemmArgs& a, cudaStream_t s, int* launches);
+// split_k: calls with too few 256x256 tiles: K split over the pairs, int32 partials TMA
+// reduce-added into a Y the caller zeroed (K1 zero_out); int32 output, TMA-storable Y only.
+cudaError_t launch_gemm_pair(const GemmArgs& a, cudaStream_t s, int* launches, bool split_k = false);
 
 // ---- gemm_fused.cu (CTA pair, weight planes expanded on chip by transform warps) -------
 // Needs the planes' row pitch (ceil(k/32) words) to be a multiple of 16 bytes and a 16-byte

@@ -311,6 +311,38 @@ def test_mid_size_split_k_path(gpu, oracle, n_out, m_tok, k, nw, nx):
     assert torch.equal(y, y2), (n_out, m_tok, k, nw, nx)
 
 
+@pytest.mark.parametrize("n_out,m_tok,k,nw,nx", [
+    (4096, 512, 4096, 2, 4), (2305, 300, 4200, 3, 8), (4096, 1024, 11008, 4, 4),
+    (1000, 96, 128, 5, 3)])
+def test_pair_split_k_path(gpu, oracle, n_out, m_tok, k, nw, nx):
+    """The u8-code pair GEMM with K split over the pairs (opt-in APMM_PSPLIT=1) == oracle on
+    sampled rows and == the default route on every entry."""
+    import torch
+    ap, ctx = gpu
+    os.environ["APMM_PSPLIT"] = "1"
+    os.environ["APMM_MID"] = "0"
+    try:
+        y = _row_sample_check(ap, ctx, oracle, n_out, m_tok, k, nw, nx, seed=n_out + 3 * m_tok,
+                              sample=24)
+    finally:
+        del os.environ["APMM_PSPLIT"]
+        del os.environ["APMM_MID"]
+    dev = torch.device("cuda", 0)
+    g = torch.Generator(device=dev)
+    g.manual_seed(n_out + 3 * m_tok)
+    wc = torch.randint(0, 1 << nw, (n_out, k), generator=g, device=dev, dtype=torch.uint8)
+    xc = torch.randint(0, 1 << nx, (m_tok, k), generator=g, device=dev, dtype=torch.uint8)
+    wpr = (k + 31) // 32
+    wp = torch.empty(nw * n_out * wpr, dtype=torch.int32, device=dev)
+    xp = torch.empty(nx * m_tok * wpr, dtype=torch.int32, device=dev)
+    ap.cu_pack(wc, n_out, k, nw, wp, ctx)
+    ap.cu_pack(xc, m_tok, k, nx, xp, ctx)
+    y2 = torch.empty((n_out, m_tok), dtype=torch.int32, device=dev)
+    ap.cu_matmul_ap(wp, n_out, nw, xp, m_tok, nx, k, y2, ctx)
+    torch.cuda.synchronize()
+    assert torch.equal(y, y2), (n_out, m_tok, k, nw, nx)
+
+
 @pytest.mark.parametrize("nw,nx", [(1, 2), (2, 4), (3, 8), (4, 8)])
 def test_config2_4096_cubed_row_sampled(gpu, oracle, nw, nx):
     ap, ctx = gpu
