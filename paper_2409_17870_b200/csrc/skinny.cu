@@ -177,9 +177,22 @@ APMM_DEV void swap_sel(uint32_t& a, uint32_t& b, uint32_t m, uint32_t mul_s) {
 // Codes of one 32-column word (x[i] = plane i word, zero for i >= N). SPLIT (N <= 4):
 // o[r] = codes of columns 8B+r, o[4+r] = 16x codes of columns 8B+4+r (r < 4). Otherwise
 // o[r] = codes of columns 8B+r (r < 8).
-template <int N, bool SPLIT>
+// EXT (N <= 2, few n-tiles): a single distance-1 swap leaves 2-bit codes; o[2s], o[2s+1]
+// = 4^s x codes of columns 8B+2s, 8B+2s+1 (s < 4), summed into four scaled accumulators --
+// 12 ops per word instead of ~22 for the nibble split.
+template <int N, bool SPLIT, bool EXT = false>
 APMM_DEV void codes_of_word(uint32_t (&x)[8], uint32_t (&o)[8], const SkinnyParams& p) {
-  if (SPLIT) {
+  if (EXT) {
+    swap_sel<1>(x[0], x[1], 0x55555555u, p.m2);  // x[0]: cols 8B+{0,2,4,6}, x[1]: 8B+{1,3,5,7}
+    o[0] = x[0] & 0x03030303u;
+    o[1] = x[1] & 0x03030303u;
+    o[2] = x[0] & 0x0C0C0C0Cu;
+    o[3] = x[1] & 0x0C0C0C0Cu;
+    o[4] = x[0] & 0x30303030u;
+    o[5] = x[1] & 0x30303030u;
+    o[6] = x[0] & 0xC0C0C0C0u;
+    o[7] = x[1] & 0xC0C0C0C0u;
+  } else if (SPLIT) {
     swap_sel<2>(x[0], x[2], 0x33333333u, p.m4);
     swap_sel<2>(x[1], x[3], 0x33333333u, p.m4);
     swap_sel<1>(x[0], x[1], 0x55555555u, p.m2);
@@ -426,11 +439,17 @@ __global__ void __launch_bounds__(sk_threads(N, NT), sk_ctas_per_sm(N, NT))
   }
 
 
-  uint32_t lo[NT][4], hi[NT][4];
+  // EXT: four accumulators scaled 1, 4, 16, 64 (lo, q4, hi, q64); else lo (+ hi = 16x)
+  constexpr bool EXT = SPLIT && N <= 2 && NT <= 2;
+  uint32_t lo[NT][4], hi[NT][4], q4[EXT ? NT : 1][4], q64[EXT ? NT : 1][4];
 #pragma unroll
   for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
     for (int e = 0; e < 4; ++e) lo[nt][e] = hi[nt][e] = 0u;
+#pragma unroll
+  for (int nt = 0; nt < (EXT ? NT : 1); ++nt)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) q4[nt][e] = q64[nt][e] = 0u;
 
   // B-fragment row of each n-tile for this lane: the feature row, else the zero row, or the
   // all-ones row for the rowsum(U_w) column
@@ -476,12 +495,19 @@ __global__ void __launch_bounds__(sk_threads(N, NT), sk_ctas_per_sm(N, NT))
               xa[pl] = xb[pl] = 0u;
             }
           }
-          codes_of_word<N, SPLIT>(xa, ca, p);
-          codes_of_word<N, SPLIT>(xb, cb, p);
+          codes_of_word<N, SPLIT, EXT>(xa, ca, p);
+          codes_of_word<N, SPLIT, EXT>(xb, cb, p);
 #pragma unroll
           for (int nt = 0; nt < NT; ++nt) {
             const uint4 x0 = xchunk[(w * 2u + 0u) * m4 + xrow[nt] * 4u + t];
             const uint4 x1 = xchunk[(w * 2u + 1u) * m4 + xrow[nt] * 4u + t];
+            if (EXT) {
+              mma_u8(lo[nt], ca[0], cb[0], ca[1], cb[1], x0.x, x0.y);
+              mma_u8(q4[EXT ? nt : 0], ca[2], cb[2], ca[3], cb[3], x0.z, x0.w);
+              mma_u8(hi[nt], ca[4], cb[4], ca[5], cb[5], x1.x, x1.y);
+              mma_u8(q64[EXT ? nt : 0], ca[6], cb[6], ca[7], cb[7], x1.z, x1.w);
+              continue;
+            }
             mma_u8(lo[nt], ca[0], cb[0], ca[1], cb[1], x0.x, x0.y);
             mma_u8(lo[nt], ca[2], cb[2], ca[3], cb[3], x0.z, x0.w);
             if (SPLIT) {
@@ -508,7 +534,11 @@ __global__ void __launch_bounds__(sk_threads(N, NT), sk_ctas_per_sm(N, NT))
         const uint32_t c = nt * 8u + 2u * t;
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-          const uint32_t v = lo[nt][e] + (SPLIT ? (hi[nt][e] >> 4) : 0u);
+          uint32_t v = lo[nt][e] + (SPLIT ? (hi[nt][e] >> 4) : 0u);
+          if (EXT) {  // exact: the host admits EXT only when 64 K A B < 2^32
+            v += (q4[EXT ? nt : 0][e] >> 2) + (q64[EXT ? nt : 0][e] >> 6);
+            q4[EXT ? nt : 0][e] = q64[EXT ? nt : 0][e] = 0u;
+          }
           atomicAdd(mine + (g + (e >= 2 ? 8u : 0u)) * M_PAD + c + (e & 1), v);
           lo[nt][e] = hi[nt][e] = 0u;
         }
@@ -710,7 +740,11 @@ cudaError_t launch_skinny(const SkinnyArgs& a, cudaStream_t s) {
   p.n_planes = static_cast<uint32_t>(a.n_w);
   p.chunks_total = (p.wpr + kChunkWords - 1) / kChunkWords;
   const uint32_t A = (1u << a.n_w) - 1u, B = (1u << a.n_x) - 1u;
-  const bool split = a.n_w <= 4 && static_cast<double>(a.k) * A * B < 268435456.0;
+  // SPLIT keeps a 16x accumulator (needs K A B < 2^28); its EXT form for n_w <= 2 and at
+  // most 2 n-tiles keeps a 64x one (needs K A B < 2^26)
+  const double kab = static_cast<double>(a.k) * A * B;
+  const bool ext_shape = a.n_w <= 2 && nt <= 2;
+  const bool split = a.n_w <= 4 && kab < (ext_shape ? 67108864.0 : 268435456.0);
   const int kn = kernel_n(a.n_w, split);
   // Ring depth 2 per warp: with deeper rings every warp requests its whole share at once,
   // HBM serves the requests in arbitrary order and warps wait for their first item while

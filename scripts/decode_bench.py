@@ -13,7 +13,7 @@ import paper_2409_17870_b200 as ap  # noqa: E402
 reps = int(sys.argv[1]) if len(sys.argv) > 1 else 30
 only = sys.argv[2].split(",") if len(sys.argv) > 2 else None  # e.g. "8192x1,8192x16"
 shapes = [(8192, 1, 8192, 3, 8), (8192, 8, 8192, 3, 8), (8192, 16, 8192, 3, 8),
-          (4096, 1, 4096, 2, 4), (4096, 16, 4096, 2, 4), (11008, 1, 4096, 2, 4),
+          (4096, 1, 4096, 2, 4), (4096, 8, 4096, 2, 4), (4096, 16, 4096, 2, 4), (11008, 8, 4096, 2, 4), (11008, 1, 4096, 2, 4),
           (11008, 16, 4096, 2, 4), (4096, 1, 11008, 2, 4), (4096, 16, 11008, 2, 4),
           (8192, 32, 8192, 3, 8), (8192, 63, 8192, 3, 8)]
 dev = torch.device("cuda", 0)
