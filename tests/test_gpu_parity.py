@@ -476,7 +476,8 @@ def test_host_api_row_block_pipeline(gpu, oracle):
     import torch
     ap, ctx = gpu
     rng = np.random.default_rng(5)
-    for (m, n, k, nw, nx) in [(4173, 1100, 256, 3, 4), (2300, 2049, 96, 2, 2), (700, 40, 4000, 4, 8)]:
+    for (m, n, k, nw, nx) in [(4173, 1100, 256, 3, 4), (2300, 2049, 96, 2, 2), (700, 40, 4000, 4, 8),
+                              (45000, 100, 256, 2, 4), (300, 44, 4096, 1, 8)]:
         wc = rng.integers(0, 1 << nw, size=(m, k), dtype=np.uint8)
         xc = rng.integers(0, 1 << nx, size=(n, k), dtype=np.uint8)
         wp, xp = oracle.pack(wc, nw), oracle.pack(xc, nx)
