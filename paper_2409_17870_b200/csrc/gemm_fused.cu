@@ -236,7 +236,7 @@ APMM_DEV void tma_reduce_add_2d(const void* tmap, const void* smem_src, int32_t 
 template <int NW>
 // Register cap: 384 x 136 leaves room for one K1 block (128 x 80) beside the resident CTA,
 // so the next call's K1 overlaps this GEMM (PDL) instead of queueing behind it.
-__global__ void __maxnreg__(kXformWarpsCfg == 4 ? 136 : 104)
+__global__ void __maxnreg__(kXformWarpsCfg == 4 ? 136 : 108)
     gemm_pair_wplanes_kernel(const __grid_constant__ CUtensorMap tmap_wp,
                              const __grid_constant__ CUtensorMap tmap_x,
                              const __grid_constant__ CUtensorMap tmap_x64,
@@ -549,6 +549,16 @@ __global__ void __maxnreg__(kXformWarpsCfg == 4 ? 136 : 104)
       double swv = 0.0;
       if (p.yf) swv = p.gran_w ? (row_ok ? p.s_w[row] : 0.0) : p.s_w[0];
 
+      // this tile's rowsum(U_x) into registers BEFORE waiting for the accumulator (lane l
+      // holds columns 8l..8l+7; chunk c's column j is a shuffle from lane 4c + j/8): the
+      // per-chunk global loads were serialised L2 round trips (~0.8 us each) exposed on a
+      // CTA's last tile (APMM_PAIR_TS timeline)
+      int4 rsx_lo = make_int4(0, 0, 0, 0), rsx_hi = make_int4(0, 0, 0, 0);
+      if (8u * lane < ti.ncols) {
+        const int4* src = reinterpret_cast<const int4*>(p.rowsum_x + ti.col0 + 8u * lane);
+        rsx_lo = __ldg(src);
+        rsx_hi = __ldg(src + 1);
+      }
       mbar_wait_b(&tmem_full[acc], acc_phase, 5);
       tc_fence_after();
       const uint32_t t_addr = tmem_base + ((wq * 32u) << 16) + acc * kPairN;
@@ -558,10 +568,16 @@ __global__ void __maxnreg__(kXformWarpsCfg == 4 ? 136 : 104)
         tmem_ld_32x32b_x32(t_addr + c * 32, r);
         tmem_ld_wait();
         const uint32_t col0 = ti.col0 + c * 32;
-        const int4* rsx4 = reinterpret_cast<const int4*>(p.rowsum_x + col0);
 #pragma unroll
         for (int j4 = 0; j4 < 8; ++j4) {
-          const int4 rs = __ldg(rsx4 + j4);
+          // columns 4 j4 .. 4 j4 + 3 of the chunk: lane 4c + j4/2, half (j4 & 1)
+          const uint32_t src_lane = 4u * c + (j4 >> 1);
+          const int4 mine = (j4 & 1) ? rsx_hi : rsx_lo;
+          int4 rs;
+          rs.x = __shfl_sync(0xffffffffu, mine.x, src_lane);
+          rs.y = __shfl_sync(0xffffffffu, mine.y, src_lane);
+          rs.z = __shfl_sync(0xffffffffu, mine.z, src_lane);
+          rs.w = __shfl_sync(0xffffffffu, mine.w, src_lane);
           r[4 * j4 + 0] = 4u * r[4 * j4 + 0] + row_term - coef_x * uint32_t(rs.x);
           r[4 * j4 + 1] = 4u * r[4 * j4 + 1] + row_term - coef_x * uint32_t(rs.y);
           r[4 * j4 + 2] = 4u * r[4 * j4 + 2] + row_term - coef_x * uint32_t(rs.z);

@@ -65,7 +65,14 @@ struct Params {
   // are TMA reduce-added into a Y zeroed by K1; the unit holding K block 0 adds the rank-1
   // recovery terms. 0 = off.
   uint32_t split, kb_per, ncols, tiles_n_split;
+  unsigned long long* ts;   // APMM_PAIR_TS=1 (dev only): per-CTA phase timestamps, else null
 };
+
+__device__ __forceinline__ unsigned long long gtime_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 struct PUnit {
   uint32_t tm, col0, ncols, kb0, kb1;
@@ -139,6 +146,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
+  if (p.ts && threadIdx.x == 0) p.ts[blockIdx.x * 8 + 0] = gtime_ns();
   const uint32_t rank = cluster_ctarank();
   const uint32_t q = rank & 1u;              // role within the pair (0 = MMA leader)
   const uint32_t pr = rank >> 1;             // pair index within the cluster
@@ -181,6 +189,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   // issue slots / registers of this SM while our tensor cores run.
   pdl_wait();
   if (threadIdx.x == 0) pdl_trigger();
+  if (p.ts && threadIdx.x == 0) p.ts[blockIdx.x * 8 + 1] = gtime_ns();
 
   if (warp == 0) {
     // ---------------- TMA producer (both CTAs) ----------------
@@ -246,6 +255,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           c0 = p.dbg ? clock64() : 0;
           mbar_wait(&full_bar[stage], phase);
           if (p.dbg) w_full += clock64() - c0;
+          if (p.ts && t == cluster && kb == un.kb0) p.ts[blockIdx.x * 8 + 2] = gtime_ns();
           tc_fence_after();
           const uint32_t st = smem_u32(stages + stage * kStageBytes);
           const uint64_t adesc = umma_desc_sw128(st);
@@ -258,6 +268,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
         mma_commit_pair_mc(&tmem_full[acc], pair_mask);
+        if (p.ts) p.ts[blockIdx.x * 8 + 3] = gtime_ns();  // last write = last unit issued
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
       if (p.dbg) {
@@ -289,6 +300,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       double sw = 0.0;
       if (p.yf) sw = p.gran_w ? (row_ok ? p.s_w[row] : 0.0) : p.s_w[0];
 
+      // this tile's rowsum(U_x) into registers BEFORE waiting for the accumulator (lane l
+      // holds columns 8l..8l+7; chunk c's column j is a shuffle from lane 4c + j/8): the
+      // per-chunk global loads were serialised L2 round trips (~0.8 us each) exposed on a
+      // CTA's last tile (APMM_PAIR_TS timeline)
+      int4 rsx_lo = make_int4(0, 0, 0, 0), rsx_hi = make_int4(0, 0, 0, 0);
+      if (8u * lane < ti.ncols) {
+        const int4* src = reinterpret_cast<const int4*>(p.rowsum_x + ti.col0 + 8u * lane);
+        rsx_lo = __ldg(src);
+        rsx_hi = __ldg(src + 1);
+      }
       mbar_wait(&tmem_full[acc], acc_phase);
       tc_fence_after();
       const uint32_t t_addr = tmem_base + ((wq * 32u) << 16) + acc * kPairN;
@@ -298,10 +319,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         tmem_ld_32x32b_x32(t_addr + c * 32, r);
         tmem_ld_wait();
         const uint32_t col0 = ti.col0 + c * 32;
-        const int4* rsx4 = reinterpret_cast<const int4*>(p.rowsum_x + col0);
 #pragma unroll
         for (int j4 = 0; j4 < 8; ++j4) {
-          const int4 rs = __ldg(rsx4 + j4);
+          // columns 4 j4 .. 4 j4 + 3 of the chunk: lane 4c + j4/2, half (j4 & 1)
+          const uint32_t src_lane = 4u * c + (j4 >> 1);
+          const int4 mine = (j4 & 1) ? rsx_hi : rsx_lo;
+          int4 rs;
+          rs.x = __shfl_sync(0xffffffffu, mine.x, src_lane);
+          rs.y = __shfl_sync(0xffffffffu, mine.y, src_lane);
+          rs.z = __shfl_sync(0xffffffffu, mine.z, src_lane);
+          rs.w = __shfl_sync(0xffffffffu, mine.w, src_lane);
           r[4 * j4 + 0] = 4u * r[4 * j4 + 0] + row_term - coef_x * uint32_t(rs.x);
           r[4 * j4 + 1] = 4u * r[4 * j4 + 1] + row_term - coef_x * uint32_t(rs.y);
           r[4 * j4 + 2] = 4u * r[4 * j4 + 2] + row_term - coef_x * uint32_t(rs.z);
@@ -358,6 +385,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     if (lane == 0) bulk_wait<0>();
     __syncwarp();
+    if (p.ts && lane == 0 && warp == 4) p.ts[blockIdx.x * 8 + 4] = gtime_ns();
   }
 
   tc_fence_before();
@@ -421,6 +449,13 @@ cudaError_t launch_gemm_pair(const GemmArgs& a, cudaStream_t s, int* launches, b
   p.dbg = a.dbg;
   static const uint32_t peak_probe = std::getenv("APMM_PEAK_PROBE") ? 1u : 0u;
   p.peak_probe = peak_probe;
+  static const bool want_ts = std::getenv("APMM_PAIR_TS") != nullptr;
+  static unsigned long long* ts_buf = nullptr;
+  if (want_ts) {
+    if (!ts_buf) cudaMalloc(&ts_buf, 512 * 8 * sizeof(unsigned long long));
+    cudaMemsetAsync(ts_buf, 0, 512 * 8 * sizeof(unsigned long long), s);
+    p.ts = ts_buf;
+  }
   // clusters of 4 (X multicast across two pairs) when there are enough cluster tiles to
   // fill the machine, else plain pairs. APMM_PAIR_CLUSTER=2|4 forces one (testing).
   static const int forced = [] {
@@ -490,6 +525,29 @@ cudaError_t launch_gemm_pair(const GemmArgs& a, cudaStream_t s, int* launches, b
   cudaError_t e = cl == 4 ? cudaLaunchKernelEx(&cfg, gemm_u8_pair_kernel<4>, tw, tx, tx64, ty, p)
                           : cudaLaunchKernelEx(&cfg, gemm_u8_pair_kernel<2>, tw, tx, tx64, ty, p);
   *launches += 1;
+  if (want_ts && e == cudaSuccess) {  // dev only: per-phase CTA timeline (us from first start)
+    unsigned long long h[512 * 8];
+    const unsigned g = cfg.gridDim.x;
+    cudaStreamSynchronize(s);
+    cudaMemcpy(h, ts_buf, g * 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+    unsigned long long t0 = ~0ull;
+    for (unsigned b = 0; b < g; ++b) t0 = h[b * 8] && h[b * 8] < t0 ? h[b * 8] : t0;
+    const char* names[5] = {"start", "pdl_wait", "first_full", "last_issue", "epi_done"};
+    for (int k = 0; k < 5; ++k) {
+      double mn = 1e30, mx = 0, sum = 0;
+      unsigned cnt = 0;
+      for (unsigned b = 0; b < g; ++b) {
+        if (!h[b * 8 + k]) continue;
+        const double v = (h[b * 8 + k] - t0) * 1e-3;
+        mn = v < mn ? v : mn;
+        mx = v > mx ? v : mx;
+        sum += v;
+        ++cnt;
+      }
+      std::fprintf(stderr, "[apmm pair ts] %-10s min %7.2f avg %7.2f max %7.2f us (%u CTAs)\n",
+                   names[k], cnt ? mn : 0.0, cnt ? sum / cnt : 0.0, mx, cnt);
+    }
+  }
   return e != cudaSuccess ? e : cudaGetLastError();
 }
 
