@@ -902,16 +902,6 @@ cudaError_t launch_skinny(const SkinnyArgs& a, cudaStream_t s) {
     }
   }
   return res;
-  switch (nt) {
-    case 1: return dispatch_n<1>(a.n_w, split, tm, p, pl.grid, pl.smem, s);
-    case 2: return dispatch_n<2>(a.n_w, split, tm, p, pl.grid, pl.smem, s);
-    case 3: return dispatch_n<3>(a.n_w, split, tm, p, pl.grid, pl.smem, s);
-    case 4: return dispatch_n<4>(a.n_w, split, tm, p, pl.grid, pl.smem, s);
-    case 5: return dispatch_n<5>(a.n_w, split, tm, p, pl.grid, pl.smem, s);
-    case 6: return dispatch_n<6>(a.n_w, split, tm, p, pl.grid, pl.smem, s);
-    case 7: return dispatch_n<7>(a.n_w, split, tm, p, pl.grid, pl.smem, s);
-    default: return dispatch_n<8>(a.n_w, split, tm, p, pl.grid, pl.smem, s);
-  }
 }
 
 }  // namespace apmm_b200
