@@ -1,6 +1,7 @@
 // skinny.cu -- K5: the WnAm bipolar-INT GEMM for few feature rows (decode / small-M LLM
 // shapes), HBM-bound on the packed weight planes. Two launches per matmul_ap call: a tiny
-// feature-prep kernel (X planes -> MMA fragment order, once) and the streaming kernel.
+// feature-prep kernel (X planes -> MMA fragment order, once) and the streaming kernel; for a
+// single feature row the streaming kernel builds its X slice itself (one launch).
 //
 // Why a separate path. With M_tok < 64 the GEMM does ~2*M ops per weight code, so the
 // roofline is the HBM read of the packed weight planes (n_w bits per weight). The large-M
@@ -10,9 +11,9 @@
 // fragments in registers by a partial 8x8 bit transpose, and feeds legacy-pipe mma.sync
 // m16n8k32 u8 x u8 -> s32 MMAs (measured ~1.1 POPS on this part, scripts/imma_probe.cu:
 // far above what M < 64 needs). What bounds it besides HBM is the instruction count per
-// weight code: the transpose costs ~0.7 ops/code for n_w <= 4 and is split evenly over the
-// ALU and FMA pipes (shifts as IMAD / IMAD.HI), rowsum(U_w) comes out of the MMA through
-// an all-ones feature column (no POPC), and the loop has no divisions.
+// weight code: the transpose costs ~0.7 ops/code for n_w <= 4 (~0.4 for n_w <= 2, see EXT)
+// and is split over the ALU and FMA pipes (shifts as IMAD / IMAD.HI), rowsum(U_w) comes out
+// of the MMA through an all-ones feature column (no POPC), and the loop has no divisions.
 //
 // The algebra is the same as the large-M path: one u8 x u8 MMA
 // of the unsigned codes performs the whole 2^(i+j)-weighted plane-pair recovery of the
