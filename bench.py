@@ -2,26 +2,35 @@
 """Benchmark of the B200 bipolar-INT WnAm GEMM (arXiv 2409.17870 hot path).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload sweep4096|w2a4_4096|llama7b|decode|ffn70b]
+                    [--workload ffn70b|sweep4096|w2a4_4096|llama7b|llama7b_small|decode]
 
-Default workload = BASELINE.json configs[1]: the precision sweep W1..W4 x A2/A4/A8 at
-M=N=K=4096 on one B200. One step = the 12 GEMMs of the sweep, each the full hot path
-through the C ABI (apmm_cu_matmul_ap: packed bit planes in HBM -> int32 Y in HBM).
-Metric = effective TOPS = sum(2*M*N*K) / device time (BASELINE.json `metric`).
+Default workload = BASELINE.json configs[4], the largest single-GPU configuration: the
+Llama-2-70B FFN projection W[28672 x 8192] W2A4 against X[4096 tokens x 8192] A4. One
+step = that GEMM through the C ABI (apmm_cu_matmul_ap: packed bit planes in HBM -> int32 Y
+in HBM). Metric = effective TOPS = 2*M*N*K / device time (BASELINE.json `metric`).
 
-Multi-GPU (torchrun, one process per GPU): every rank runs the same per-GPU sweep on its
-own GPU (independent GEMMs; no data-path collective) -> "scaling": "weak"; the reported
-value is all ranks' work / max-over-ranks device time.
+Multi-GPU: `--gpus N` (N > 1) re-launches itself under torch.distributed.run with one
+process per GPU unless it already runs under torchrun. ffn70b is N-sharded:
+rank p owns the contiguous W row block p of 28672/N rows, X is replicated, the GEMMs are
+independent ("scaling": "strong": the whole job is the one full GEMM), `value` is the full
+GEMM's ops / max-over-ranks compute time. The optional all-gather of the int32 row blocks
+(NCCL over NVLink, only where the consumer needs the full output) is timed separately and
+reported under "gather". Every other workload runs the same GEMMs on each rank as
+independent replicas ("scaling": "weak").
 
 `--impl reference` times the reference's own CPU matmul_ap (oracle/_ref, compiled from
-/root/reference/proj/src), row-sliced over all host threads, on a bounded row sample of the
-same workload; only rank 0 runs it.
+/root/reference/proj/src) on the same config, row-sliced over all host threads (legal per
+SPEC.md:266), plus the as-shipped 1-thread figure; only rank 0 runs it.
+
+After the timed region the GPU arm compares sampled rows of every Y it timed against the
+reference's matmul_ap (`"parity"` in the line); a mismatch exits non-zero.
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -31,6 +40,10 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+# One metric string, identical in both arms (BASELINE.json `metric`).
+METRIC = "effective TOPS (2MNK/s) of WnAm bipolar-INT GEMM vs roofline; decode HBM GB/s"
+UNIT = "TOPS"
+
 # ----------------------------------------------------------------------------- workloads
 SWEEP_BITS = [(nw, nx) for nw in (1, 2, 3, 4) for nx in (2, 4, 8)]
 
@@ -38,6 +51,8 @@ SWEEP_BITS = [(nw, nx) for nw in (1, 2, 3, 4) for nx in (2, 4, 8)]
 def workload_gemms(name: str):
     """List of (rows_w=N_out, rows_x=M_tok, K, n_w, n_x) in reference orientation
     matmul_ap(W[N_out x K], X[M_tok x K]) -> Y[N_out x M_tok]."""
+    if name == "ffn70b":
+        return [(28672, 4096, 8192, 2, 4)]
     if name == "sweep4096":
         return [(4096, 4096, 4096, nw, nx) for nw, nx in SWEEP_BITS]
     if name == "w2a4_4096":
@@ -48,21 +63,24 @@ def workload_gemms(name: str):
     if name == "llama7b_small":
         return [(n, m, k, 2, 4) for (n, k) in ((4096, 4096), (11008, 4096), (4096, 11008))
                 for m in (1, 16)]
+    if name == "llama7b_mid":
+        return [(n, m, k, 2, 4) for (n, k) in ((4096, 4096), (11008, 4096), (4096, 11008))
+                for m in (64, 128, 256, 512)]
     if name == "decode":
         return [(8192, m, 8192, 3, 8) for m in (1, 8, 16)]
-    if name == "ffn70b":
-        return [(28672, 4096, 8192, 2, 4)]
     raise SystemExit(f"unknown workload {name}")
 
 
 WORKLOAD_DESC = {
+    "ffn70b": "BASELINE configs[4]: Llama-2-70B FFN 28672x8192 W2A4, M=4096 tokens",
     "sweep4096": "BASELINE configs[1]: precision sweep W1-4 x A2/A4/A8, M=N=K=4096, 12 GEMMs/step",
     "w2a4_4096": "W2A4 M=N=K=4096",
     "llama7b": "BASELINE configs[2]: Llama-2-7B linear shapes W2A4, M=2048 tokens",
+    "llama7b_small": "BASELINE configs[2]: Llama-2-7B linear shapes W2A4, M in {1,16} tokens",
+    "llama7b_mid": "BASELINE configs[2]: Llama-2-7B linear shapes W2A4, M in {64,128,256,512}",
     "decode": "BASELINE configs[3]: decode W3A8 K=N=8192, M in {1,8,16}",
-    "llama7b_small": "BASELINE configs[3]: Llama-2-7B linear shapes W2A4, M in {1,16} tokens",
-    "ffn70b": "BASELINE configs[4]: Llama-2-70B FFN 28672x8192 W2A4, M=4096",
 }
+SHARDED = {"ffn70b"}  # workloads that N-shard one GEMM across the ranks
 
 
 def ops_of(g):
@@ -79,33 +97,48 @@ def algorithmic_bytes(g):
     return packed_bytes(n_out, k, nw) + packed_bytes(m_tok, k, nx) + 4 * n_out * m_tok
 
 
-def load_peaks():
-    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+def bench_config(workload: str, world: int) -> dict:
+    """The `config` object -- identical in both arms for the same workload and N."""
+    gemms = workload_gemms(workload)
+    sharded = workload in SHARDED and world > 1
+    return {
+        "workload": WORKLOAD_DESC[workload],
+        "shapes": [list(g) for g in gemms],
+        "shape_fields": "[N_out, M_tok, K, n_w, n_x]",
+        "gemms_per_step": len(gemms),
+        "orientation": "matmul_ap(W[N_out x K,n_w], X[M_tok x K,n_x]) -> int32 [N_out x M_tok]",
+        "parallelism": (f"N_out sharded x{world}: contiguous W row blocks, X replicated, "
+                        "no data-path collective (all-gather timed separately)" if sharded
+                        else ("N-sharded (1 GPU holds all rows)" if workload in SHARDED
+                              else f"replicas x{world}: independent GEMMs per GPU")),
+    }
+
+
+def load_json(rel):
     try:
-        with open(p) as f:
+        with open(os.path.join(ROOT, rel)) as f:
             return json.load(f)
     except Exception:
         return {}
 
 
-def load_i8_ceiling():
-    """The pair GEMM's own tcgen05 kind::i8 ceiling (scripts/i8_mma_peak.py: the real kernel
-    with operand reloads switched off), reported beside the contract's peak."""
-    p = os.path.join(ROOT, "profiles", "i8_mma_peak.json")
+def cpu_model() -> str:
     try:
-        with open(p) as f:
-            return json.load(f).get("i8_tops")
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
     except Exception:
-        return None
+        pass
+    import platform
+    return platform.processor() or "unknown"
 
 
-def load_traffic():
-    p = os.path.join(ROOT, "profiles", "traffic.json")
+def cpu_threads() -> int:
     try:
-        with open(p) as f:
-            return json.load(f)
+        return len(os.sched_getaffinity(0))
     except Exception:
-        return {}
+        return os.cpu_count() or 1
 
 
 # ------------------------------------------------------------------------------ clocks
@@ -165,18 +198,13 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------- CPU reference arm
-def cpu_threads() -> int:
-    try:
-        return len(os.sched_getaffinity(0))
-    except Exception:
-        return os.cpu_count() or 1
-
-
 class CpuReference:
-    """The reference's matmul_ap (oracle/_ref) -- or the C restatement when _ref is absent --
-    row-sliced over all host threads, on a row sample of each GEMM of the workload."""
+    """The reference's matmul_ap (oracle/_ref; the C restatement when _ref is absent),
+    row-sliced over `threads` host threads, on `rows[i]` W rows of each GEMM of a workload
+    (all rows = the full GEMM). Packing is done once, outside the timed calls, as in the
+    reference bench (apmm.cpp:163-172)."""
 
-    def __init__(self, gemms, budget_s: float, threads: int):
+    def __init__(self, gemms, threads: int, budget_s: float | None, seed: int = 1):
         import numpy as np
         from oracle import Oracle, Reference
         self.np = np
@@ -184,54 +212,95 @@ class CpuReference:
         self.kind = "reference" if Reference.available() else "port"
         self.ref = Reference() if self.kind == "reference" else None
         self.orc = Oracle()
-        rng = np.random.default_rng(1)
-        self.full = gemms
-        # calibrate: per-row cost of each GEMM at a small sample
-        self.ops_per_row = [2.0 * g[1] * g[2] for g in gemms]
-        cal_rows = max(2 * threads, 32)
-        self.inputs = []
+        self.gemms = gemms
+        rng = np.random.default_rng(seed)
+        self.x_planes, self.w_codes = [], []
         for (n_out, m_tok, k, nw, nx) in gemms:
-            wc = rng.integers(0, 1 << nw, size=(min(n_out, 4096), k), dtype=np.uint8)
             xc = rng.integers(0, 1 << nx, size=(m_tok, k), dtype=np.uint8)
-            self.inputs.append((wc, xc, nw, nx, k))
+            self.x_planes.append(self._pack(xc, nx))
+            self.w_codes.append(rng.integers(0, 1 << nw, size=(n_out, k), dtype=np.uint8))
+        # calibrate the per-W-row cost of each GEMM on a small slice
+        cal = max(2 * threads, 32)
         t_row = []
         for i, g in enumerate(gemms):
-            job = self._job(i, min(cal_rows, g[0]))
+            r = min(cal, g[0])
+            job = self._job(i, r, threads)
             job.run()
-            dt = job.run()
-            t_row.append(dt / min(cal_rows, g[0]))
-        per_step_full = sum(t * g[0] for t, g in zip(t_row, gemms))
-        frac = min(1.0, budget_s / max(per_step_full, 1e-9))
-        self.rows = [max(min(g[0], 4096), 1) for g in gemms]
-        self.rows = [max(min(r, int(round(g[0] * frac))), min(g[0], 2 * threads))
-                     for r, g in zip(self.rows, gemms)]
-        self.jobs = [self._job(i, r) for i, r in enumerate(self.rows)]
-        self.sample = ", ".join(f"{r}/{g[0]} W rows of W{g[3]}A{g[4]} {g[0]}x{g[1]}x{g[2]}"
-                                for r, g in zip(self.rows, gemms))
+            t_row.append(job.run() / r)
+        self.t_row = t_row
+        full = sum(t * g[0] for t, g in zip(t_row, gemms))
+        frac = 1.0 if budget_s is None else min(1.0, budget_s / max(full, 1e-9))
+        self.rows = [g[0] if frac >= 1.0 else max(min(g[0], 2 * threads), int(g[0] * frac))
+                     for g in gemms]
+        self.jobs = [self._job(i, r, threads) for i, r in enumerate(self.rows)]
+        self.full = all(r == g[0] for r, g in zip(self.rows, gemms))
+        self.sample = ("full GEMMs: " if self.full else "row sample: ") + ", ".join(
+            f"{r}/{g[0]} W rows of W{g[3]}A{g[4]} {g[0]}x{g[1]}x{g[2]}"
+            for r, g in zip(self.rows, gemms))
 
-    def _job(self, i, rows):
-        wc, xc, nw, nx, k = self.inputs[i]
-        wcs = self.np.ascontiguousarray(wc[:rows])
-        if self.kind == "reference":
-            wp = self.ref.pack(wcs, nw)
-            xp = self.ref.pack(xc, nx)
-            return self.ref.job(wp, rows, nw, xp, xc.shape[0], nx, k, self.threads)
-        wp = self.orc.pack(wcs, nw)
-        xp = self.orc.pack(xc, nx)
-        orc, th, mx = self.orc, self.threads, xc.shape[0]
+    def _pack(self, codes, n):
+        return self.ref.pack(codes, n) if self.ref else self.orc.pack(codes, n)
+
+    def _job(self, i, rows, threads):
+        n_out, m_tok, k, nw, nx = self.gemms[i]
+        wp = self._pack(self.np.ascontiguousarray(self.w_codes[i][:rows]), nw)
+        xp = self.x_planes[i]
+        if self.ref:
+            return self.ref.job(wp, rows, nw, xp, m_tok, nx, k, threads)
+        orc = self.orc
 
         class PortJob:
             def run(self_inner):
                 t0 = time.perf_counter()
-                orc.matmul_ap_mt(wp, rows, nw, xp, mx, nx, k, th)
+                orc.matmul_ap_mt(wp, rows, nw, xp, m_tok, nx, k, threads)
                 return time.perf_counter() - t0
         return PortJob()
 
     def step(self) -> tuple[float, float]:
-        """Run one sample step; returns (seconds, ops)."""
+        """One step (every GEMM's sample once); returns (seconds, ops)."""
         secs = sum(j.run() for j in self.jobs)
-        ops = sum(r * opr for r, opr in zip(self.rows, self.ops_per_row))
+        ops = sum(r * 2.0 * g[1] * g[2] for r, g in zip(self.rows, self.gemms))
         return secs, ops
+
+
+def single_thread_figure(gemms, budget_s: float = 6.0) -> dict:
+    """The reference as shipped: one thread, warmup 2 + mean of 10 (apmm.cpp:102-109,
+    :126-127) on a W-row sample of the first GEMM sized to ~budget_s in total."""
+    g = gemms[0]
+    import numpy as np
+    from oracle import Oracle, Reference
+    kind = "reference" if Reference.available() else "port"
+    n_out, m_tok, k, nw, nx = g
+    rng = np.random.default_rng(2)
+    xc = rng.integers(0, 1 << nx, size=(m_tok, k), dtype=np.uint8)
+    ref = Reference() if kind == "reference" else None
+    orc = Oracle()
+    pack = ref.pack if ref else orc.pack
+    xp = pack(xc, nx)
+
+    def make(rows):
+        wc = rng.integers(0, 1 << nw, size=(rows, k), dtype=np.uint8)
+        wp = pack(wc, nw)
+        if ref:
+            return ref.job(wp, rows, nw, xp, m_tok, nx, k, 1)
+
+        class PortJob:
+            def run(self_inner):
+                t0 = time.perf_counter()
+                orc.matmul_ap_mt(wp, rows, nw, xp, m_tok, nx, k, 1)
+                return time.perf_counter() - t0
+        return PortJob()
+    rows = min(n_out, 4)
+    t = make(rows).run()
+    rows = int(max(1, min(n_out, rows * (budget_s / 12.0) / max(t, 1e-6))))
+    job = make(rows)
+    for _ in range(2):
+        job.run()
+    ts = [job.run() for _ in range(10)]
+    mean = sum(ts) / len(ts)
+    return {"value": 2.0 * rows * m_tok * k / mean / 1e12, "unit": UNIT, "cores": 1, "kind": kind,
+            "sample": f"{rows}/{n_out} W rows of W{nw}A{nx} {n_out}x{m_tok}x{k}, warmup 2 + mean of 10 "
+                      "(as shipped, apmm.cpp:102-109)"}
 
 
 def run_reference_arm(args, rank, world):
@@ -239,8 +308,13 @@ def run_reference_arm(args, rank, world):
         return
     gemms = workload_gemms(args.workload)
     threads = cpu_threads()
-    budget = max(0.5, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
-    ref = CpuReference(gemms, budget, threads)
+    # every step is the full config when that fits ~8 min of CPU for the whole run,
+    # otherwise a W-row sample sized to that budget (stated in `sample`)
+    budget = 480.0 / max(1, args.steps + args.warmup)
+    ref = CpuReference(gemms, threads, None)
+    est_full = sum(t * g[0] for t, g in zip(ref.t_row, gemms))
+    if est_full > budget:
+        ref = CpuReference(gemms, threads, budget)
     for _ in range(args.warmup):
         ref.step()
     secs = ops = 0.0
@@ -250,17 +324,64 @@ def run_reference_arm(args, rank, world):
         ops += o
     tops = ops / secs / 1e12
     line = {
-        "impl": "reference", "metric": "effective TOPS (2MNK/s)", "value": tops, "unit": "TOPS",
-        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * secs / args.steps, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "int32 (bit-plane XOR-popcount)", "data": "synthetic",
-        "config": {"workload": WORKLOAD_DESC[args.workload], "gemms": len(gemms),
-                   "orientation": "matmul_ap(W[N_out x K], X[M_tok x K])"},
-        "cpu_baseline": {"value": tops, "unit": "TOPS", "cores": threads, "kind": ref.kind,
-                         "sample": ref.sample},
-        "e2e": {"value": tops, "unit": "TOPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "impl": "reference", "metric": METRIC, "value": tops, "unit": UNIT,
+        "n_gpus": world if world > 1 else args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * secs / args.steps, "higher_is_better": True,
+        "scaling": "strong" if args.workload in SHARDED else "weak", "vs_baseline": None,
+        "dtype": "int32 (bit-plane XOR-popcount, reference CPU kernel)",
+        "data": "synthetic (uniform bipolar codes, random_codes semantics)",
+        "config": bench_config(args.workload, world if world > 1 else args.gpus),
+        "cpu_baseline": {"value": tops, "unit": UNIT, "cores": threads, "kind": ref.kind,
+                         "sample": ref.sample, "cpu_model": cpu_model()},
+        "e2e": {"value": tops, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    try:
+        line["cpu_single_thread"] = single_thread_figure(gemms)
+    except Exception as e:
+        line["cpu_single_thread"] = {"value": None, "error": str(e)[:200]}
     print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------- parity check
+def parity_check(entries, threads):
+    """Sampled-row bit-exactness of the Y buffers the timed region produced.
+
+    entries: list of (g, w_planes_dev, x_planes_dev, y_dev). Two W rows per 256-row tile
+    (all tiles, all columns) are compared against the reference's matmul_ap (oracle/_ref,
+    or the C restatement when _ref is absent) on the same packed inputs."""
+    import numpy as np
+    import torch
+    from oracle import Oracle, Reference
+    kind = "reference" if Reference.available() else "port"
+    ref = Reference() if kind == "reference" else None
+    orc = Oracle()
+    gen = np.random.default_rng(7)
+    rows_checked = 0
+    for (g, wp, xp, y) in entries:
+        n_out, m_tok, k, nw, nx = g
+        wpr = (k + 31) // 32
+        rows = []
+        for t0 in range(0, n_out, 256):
+            span = min(256, n_out - t0)
+            rows.extend(sorted(set(int(t0 + r) for r in gen.integers(0, span, size=2))))
+        if n_out - 1 not in rows:
+            rows.append(n_out - 1)
+        idx = torch.tensor(rows, device=wp.device, dtype=torch.long)
+        w_rows = wp.view(nw, n_out, wpr).index_select(1, idx).contiguous().cpu().numpy().view(np.uint32)
+        x_h = xp.cpu().numpy().view(np.uint32)
+        y_rows = y.index_select(0, idx).cpu().numpy()
+        if ref:
+            job = ref.job(w_rows.reshape(-1), len(rows), nw, x_h, m_tok, nx, k, threads)
+            job.run()
+            want = job.result()
+        else:
+            want = orc.matmul_ap_mt(w_rows.reshape(-1), len(rows), nw, x_h, m_tok, nx, k, threads)
+        if not np.array_equal(y_rows, want):
+            bad = int((y_rows != want).sum())
+            return False, f"MISMATCH: {bad} entries differ in {len(rows)} sampled rows of {g}"
+        rows_checked += len(rows)
+    return True, (f"ok: {rows_checked} sampled W rows (2 per 256-row tile, all columns) of every "
+                  f"timed Y bit-exact vs the {kind} matmul_ap")
 
 
 # ---------------------------------------------------------------------------- GPU arm
@@ -275,62 +396,48 @@ def run_ours(args, rank, world, local_rank):
     ctx = ap.Context(local_rank)
     stream = torch.cuda.Stream(device=dev)  # every launch of the timed region goes here
     torch.cuda.set_stream(stream)
-    gemms = workload_gemms(args.workload)
-    # configs[4] (70B FFN): N_out sharded across the ranks (contiguous row blocks of W, X
-    # replicated; paper_2409_17870_b200/shard.py) -> strong scaling of one GEMM, optionally
-    # followed by the NCCL all-gather of the int32 row blocks (--gather). Every other
-    # workload runs the same per-GPU GEMMs on each rank (weak scaling, no collective).
-    sharded = args.workload == "ffn70b" and world > 1
-    full_gemms = gemms
-    if sharded:
+    full_gemms = workload_gemms(args.workload)
+    gemms = full_gemms
+    sharded = args.workload in SHARDED and world > 1
+    if sharded:  # rank p owns W rows [r0, r1) (paper_2409_17870_b200/shard.py)
         from paper_2409_17870_b200.shard import shard_bounds
-        n_out, m_tok, k, nw, nx = gemms[0]
+        n_out, m_tok, k, nw, nx = full_gemms[0]
         r0, r1 = shard_bounds(n_out, world, rank)
         gemms = [(r1 - r0, m_tok, k, nw, nx)]
 
-    # -- synthetic operands: uniform codes (like random_codes, verify.cpp:18-22), packed to
-    #    bit planes on device (packing excluded from timing, as in apmm.cpp:163-172)
+    # -- synthetic operands: uniform codes (random_codes, verify.cpp:18-22), packed to bit
+    #    planes on device (packing excluded from timing, as in apmm.cpp:163-172)
     gen = torch.Generator(device=dev)
     gen.manual_seed(1 + rank)
     ops_step = sum(ops_of(g) for g in gemms)
-    # L2 rule: when a step touches less than 2x the 126 MB L2, the weight planes rotate over
-    # `nrot` copies (step s uses copy s % nrot), so no step finds its weights in L2.
-    step_bytes = sum(packed_bytes(g[0], g[2], g[3]) + packed_bytes(g[1], g[2], g[4]) +
-                     4 * g[0] * g[1] for g in gemms)
-    nrot = max(1, -(-int(2 * 126e6) // int(step_bytes))) if step_bytes < 2 * 126e6 else 1
+    # L2 rule: when a step touches less than 2x the 126 MB L2, the inputs (W and X planes)
+    # rotate over `nrot` copies (step s uses copy s % nrot), so no step finds them in L2.
+    step_bytes = sum(algorithmic_bytes(g) for g in gemms)
+    nrot = 1 if step_bytes >= 2 * 126e6 else -(-int(2 * 126e6) // int(step_bytes))
     bufs = []
     for (n_out, m_tok, k, nw, nx) in gemms:
         wpr = (k + 31) // 32
-        wps = []
+        wps, xps = [], []
         for _ in range(nrot):
             wc = torch.randint(0, 1 << nw, (n_out, k), generator=gen, device=dev, dtype=torch.uint8)
             wp = torch.empty(nw * n_out * wpr, dtype=torch.int32, device=dev)
             ap.cu_pack(wc, n_out, k, nw, wp, ctx)
             wps.append(wp)
             del wc
-        xc = torch.randint(0, 1 << nx, (m_tok, k), generator=gen, device=dev, dtype=torch.uint8)
-        xp = torch.empty(nx * m_tok * wpr, dtype=torch.int32, device=dev)
-        ap.cu_pack(xc, m_tok, k, nx, xp, ctx)
+            xc = torch.randint(0, 1 << nx, (m_tok, k), generator=gen, device=dev, dtype=torch.uint8)
+            xp = torch.empty(nx * m_tok * wpr, dtype=torch.int32, device=dev)
+            ap.cu_pack(xc, m_tok, k, nx, xp, ctx)
+            xps.append(xp)
+            del xc
         y = torch.empty((n_out, m_tok), dtype=torch.int32, device=dev)
-        bufs.append((wps, xp, y))
-        del xc
+        bufs.append((wps, xps, y))
     torch.cuda.synchronize()
-    gather_out = None
-    if sharded and args.gather:
-        from paper_2409_17870_b200.shard import max_shard
-        n_full, m_full = full_gemms[0][0], full_gemms[0][1]
-        gather_send = torch.zeros((max_shard(n_full, world), m_full), dtype=torch.int32, device=dev)
-        gather_out = torch.empty((world * gather_send.shape[0], m_full), dtype=torch.int32, device=dev)
 
     def make_step(r):
         def step_r():
-            for (g, (wps, xp, y)) in zip(gemms, bufs):
+            for (g, (wps, xps, y)) in zip(gemms, bufs):
                 n_out, m_tok, k, nw, nx = g
-                ap.cu_matmul_ap(wps[r], n_out, nw, xp, m_tok, nx, k, y, ctx)
-            if gather_out is not None:  # full N_out x M_tok on every rank (NCCL over NVLink)
-                y = bufs[0][2]
-                gather_send[: y.shape[0]].copy_(y)
-                dist.all_gather_into_tensor(gather_out, gather_send)
+                ap.cu_matmul_ap(wps[r], n_out, nw, xps[r], m_tok, nx, k, y, ctx)
         return step_r
 
     step_fns = [make_step(r) for r in range(nrot)]
@@ -353,9 +460,8 @@ def run_ours(args, rank, world, local_rank):
     # launch overhead (Python + C ABI, ~10 us per call) leaves the timed region.
     # --no-graph times the eager launches instead.
     graph = None
-    eager_step = step
-    run_timed = None
-    if not args.no_graph and gather_out is None:
+    graph_launches = 0
+    if not args.no_graph:
         graph = torch.cuda.CUDAGraph()
         n0 = ctx.launch_count()
         with torch.cuda.graph(graph, stream=stream):
@@ -363,9 +469,6 @@ def run_ours(args, rank, world, local_rank):
                 step_fns[i % nrot]()
         graph_launches = (ctx.launch_count() - n0) // args.steps
         torch.cuda.synchronize()
-
-        def run_timed():
-            graph.replay()
 
         def step():  # noqa: F811  (heat phase: whole K-step replays)
             graph.replay()
@@ -387,11 +490,14 @@ def run_ours(args, rank, world, local_rank):
     barrier()
     torch.cuda.synchronize()
     ev0.record(stream)
-    if run_timed is not None:
-        run_timed()  # exactly K steps (one replay of the K-step graph)
+    if graph is not None:
+        graph.replay()  # exactly K steps
+        last_rot = (args.steps - 1) % nrot
     else:
+        step_i[0] = 0
         for _ in range(args.steps):
             step()
+        last_rot = (args.steps - 1) % nrot
     ev1.record(stream)
     torch.cuda.synchronize()
     barrier()
@@ -400,16 +506,36 @@ def run_ours(args, rank, world, local_rank):
         launches = graph_launches * args.steps
     clk = clocks.stop()
     ms = ev0.elapsed_time(ev1)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    # whole-job work per step: the full GEMM when sharded (strong), else every rank's GEMMs
+    job_ops_step = sum(ops_of(g) for g in full_gemms) if sharded else world * ops_step
+    value = args.steps * job_ops_step / (ms_max * 1e-3) / 1e12
+
+    # -- parity of exactly what was timed (sampled rows vs the reference), before anything
+    #    else touches the Y buffers
+    parity = None
+    if not args.no_parity and not args.profile:
+        entries = [(g, wps[last_rot], xps[last_rot], y) for g, (wps, xps, y) in zip(gemms, bufs)]
+        ok, msg = parity_check(entries, cpu_threads())
+        flag = torch.tensor([0 if ok else 1], dtype=torch.int32, device=dev)
+        if world > 1:
+            dist.all_reduce(flag, op=dist.ReduceOp.MAX)
+        parity_ok = int(flag.item()) == 0
+        parity = msg if (not ok or parity_ok) else "MISMATCH on another rank"
+
+
     # -- kernel pass (roofline): the same K steps again with every GEMM / expand launch
     #    bracketed by CUDA events on its launch stream (serialises expand and GEMM). In
     #    graph mode the bracketed steps are captured as a graph too, so the event pairs
-    #    time the kernels, not the host's launch gaps (decode kernels are shorter than the
-    #    ~10 us Python + C ABI call).
+    #    time the kernels, not the host's launch gaps.
     ctx.kernel_time(0)
     ctx.kernel_time(1)
     ek0, ek1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ctx.enable_timing(True)
     if graph is not None:
-        ctx.enable_timing(True)
         kgraph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(kgraph, stream=stream):
             for i in range(args.steps):
@@ -419,35 +545,74 @@ def run_ours(args, rank, world, local_rank):
         ek0.record(stream)
         kgraph.replay()
         ek1.record(stream)
-        torch.cuda.synchronize()
     else:
-        ctx.enable_timing(True)
         ek0.record(stream)
         for _ in range(args.steps):
             step()
         ek1.record(stream)
-        torch.cuda.synchronize()
-        ctx.enable_timing(False)
+    torch.cuda.synchronize()
+    ctx.enable_timing(False)
     ms_serial = ek0.elapsed_time(ek1)
     gemm_ms, gemm_n = ctx.kernel_time(0)
     exp_ms, exp_n = ctx.kernel_time(1)
-    t = torch.tensor([ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item())
-    # whole-job work per step: the full GEMM when sharded (strong), else every rank's GEMMs
-    job_ops_step = sum(ops_of(g) for g in full_gemms) if sharded else world * ops_step
-    value = args.steps * job_ops_step / (ms_max * 1e-3) / 1e12
+
+    if args.profile:
+        if rank == 0:
+            print(json.dumps({"profile_run": True, "ms_per_step": ms_max / args.steps}), flush=True)
+        return
+
+    # -- multi-GPU: the all-gather of the N-sharded int32 row blocks (NCCL over NVLink),
+    #    timed on its own (compute-only `value` above) and as compute + gather steps
+    gather = None
+    if sharded:
+        from paper_2409_17870_b200.shard import max_shard
+        n_full, m_full = full_gemms[0][0], full_gemms[0][1]
+        ms_blk = max_shard(n_full, world)
+        send = torch.zeros((ms_blk, m_full), dtype=torch.int32, device=dev)
+        recv = torch.empty((world * ms_blk, m_full), dtype=torch.int32, device=dev)
+        y0 = bufs[0][2]
+
+        def gather_only():
+            send[: y0.shape[0]].copy_(y0)
+            dist.all_gather_into_tensor(recv, send)
+
+        for _ in range(3):
+            gather_only()
+        torch.cuda.synchronize()
+
+        def timed(fn):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            barrier()
+            torch.cuda.synchronize()
+            e0.record(stream)
+            for _ in range(args.steps):
+                fn()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            barrier()
+            tt = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            return float(tt.item()) / args.steps
+
+        g_ms = timed(gather_only)
+
+        def compute_gather():
+            step_fns[0]()
+            gather_only()
+        cg_ms = timed(compute_gather)
+        recv_bytes = (world - 1) * ms_blk * m_full * 4
+        gather = {"format": "int32 Y row blocks", "collective": "all_gather_into_tensor (NCCL)",
+                  "ms_per_step": g_ms, "recv_bytes_per_rank": recv_bytes,
+                  "algbw_GBps": recv_bytes / (g_ms * 1e-3) / 1e9,
+                  "compute_plus_gather_ms_per_step": cg_ms,
+                  "compute_plus_gather_TOPS": job_ops_step / (cg_ms * 1e-3) / 1e12}
 
     # -- e2e through the public host API: pinned host planes -> H2D -> GEMM -> D2H int32
-    if args.profile:
-        print(json.dumps({"profile_run": True, "ms_per_step": ms_max / args.steps}), flush=True)
-        return
     e2e_steps = max(1, min(args.steps, 3))
     host = []
     h2d = d2h = 0
-    for (g, (wps, xp, y)) in zip(gemms, bufs):
-        wp = wps[0]
+    for (g, (wps, xps, y)) in zip(gemms, bufs):
+        wp, xp = wps[0], xps[0]
         hw = torch.empty(wp.shape, dtype=torch.int32, pin_memory=True)
         hx = torch.empty(xp.shape, dtype=torch.int32, pin_memory=True)
         hy = torch.empty(tuple(y.shape), dtype=torch.int32, pin_memory=True)
@@ -481,9 +646,11 @@ def run_ours(args, rank, world, local_rank):
     e2e_val = e2e_steps * job_ops_step / float(te.item()) / 1e12
 
     if rank != 0:
+        if parity is not None and not parity_ok:
+            sys.exit(1)
         return
-    peaks = load_peaks()
-    traffic = load_traffic()
+    peaks = load_json("MEASURED_PEAKS.json")
+    traffic = load_json("profiles/traffic.json")
     bf16 = peaks.get("bf16_tflops")
     i8_peak = 2.0 * bf16 if bf16 else 2.0 * 1590.0
     hbm_peak = peaks.get("hbm_gbs") or 7672.0
@@ -491,55 +658,61 @@ def run_ours(args, rank, world, local_rank):
     bytes_step = sum(algorithmic_bytes(g) for g in gemms)
     # which roofline bounds the dominant kernel: compare the two ideal times per step
     hbm_bound = bytes_step / (hbm_peak * 1e9) > ops_step / (i8_peak * 1e12)
-    skinny = all(g[1] <= 64 for g in gemms)
+    skinny = all(g[1] <= 40 for g in gemms)
     kname = ("skinny_kernel (weight planes -> mma.sync u8 fragments)" if skinny else
-             "gemm_u8_pair_kernel / gemm_u8_tc_kernel (tcgen05.mma kind::i8)")
+             "gemm_u8_pair_kernel / gemm_u8_tc_kernel / gemm_pair_wplanes_kernel "
+             "(tcgen05.mma kind::i8)")
+    per_rank_step_s = ms_max * 1e-3 / args.steps
     if hbm_bound:
         achieved = (args.steps * bytes_step / max(gemm_n, 1)) / (gemm_avg_ms * 1e-3) / 1e9
+        step_achieved = bytes_step / per_rank_step_s / 1e9
         peak, unit = hbm_peak, "GB/s"
         peak_src = ("MEASURED_PEAKS.json hbm_gbs (copy bandwidth)" if peaks.get("hbm_gbs")
                     else "B200_PROFILING.md fallback")
     else:
         achieved = (args.steps * ops_step / max(gemm_n, 1)) / (gemm_avg_ms * 1e-3) / 1e12
+        step_achieved = ops_step / per_rank_step_s / 1e12
         peak, unit = i8_peak, "TFLOP/s"
         peak_src = ("2 x measured bf16 burst (MEASURED_PEAKS.json bf16_tflops); "
                     "dense i8 = 2x dense bf16 on B200" if bf16 else
                     "2 x fallback bf16 1590 (B200_PROFILING.md)")
-    i8_ceiling = load_i8_ceiling()
-    tr_ent = traffic.get(args.workload) or {}
+    i8_ceiling = (load_json("profiles/i8_mma_peak.json") or {}).get("i8_tops")
+    tr_ent = traffic.get(args.workload if not sharded else f"{args.workload}_p{world}") or {}
     tr = tr_ent.get("bytes")  # dram read+write bytes per launch (ncu --set full), or None
     line = {
-        "metric": "effective TOPS (2MNK/s) of WnAm bipolar-INT GEMM",
-        "value": value, "unit": "TOPS", "n_gpus": world, "steps": args.steps,
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
-        "scaling": "strong" if sharded else "weak", "vs_baseline": None,
+        "scaling": "strong" if args.workload in SHARDED else "weak", "vs_baseline": None,
         "dtype": "u8 codes x u8 codes -> s32 (exact int)",
         "data": "synthetic (uniform bipolar codes, packed to bit planes on device)",
-        "config": {"workload": WORKLOAD_DESC[args.workload], "gemms_per_step": len(gemms),
-                   "shapes": [list(g) for g in gemms],
-                   "orientation": "matmul_ap(W[N_out x K,n_w], X[M_tok x K,n_x]) -> int32 [N_out x M_tok]",
-                   "parallelism": (f"N_out sharded x{world} (row blocks of W, X replicated)"
-                                   + (", NCCL all-gather of Y in the step" if gather_out is not None else "")
-                                   if sharded else f"replicas x{world} (N-independent GEMMs per GPU)"),
-                   "launch": "eager" if graph is None else "one cuda graph of the K timed steps",
-                   "l2": ("no flush: per-step packed inputs %.0f MB + outputs %.0f MB > 2 x 126 MB L2" % (
-                       sum(packed_bytes(g[0], g[2], g[3]) + packed_bytes(g[1], g[2], g[4]) for g in gemms) / 1e6,
-                       sum(4 * g[0] * g[1] for g in gemms) / 1e6) if nrot == 1 else
-                       "weight planes rotate over %d copies (step s uses copy s %% %d): %.0f MB "
-                       "between reuses > 2 x 126 MB L2" % (nrot, nrot, nrot * step_bytes / 1e6))},
+        "config": bench_config(args.workload, world),
+        "per_rank_shapes": [list(g) for g in gemms],
+        "launch": "eager" if graph is None else "one cuda graph of the K timed steps",
+        "l2": ("no flush: per-step packed inputs %.0f MB + outputs %.0f MB > 2 x 126 MB L2" % (
+            sum(packed_bytes(g[0], g[2], g[3]) + packed_bytes(g[1], g[2], g[4]) for g in gemms) / 1e6,
+            sum(4 * g[0] * g[1] for g in gemms) / 1e6) if nrot == 1 else
+            "W and X planes rotate over %d copies (step s uses copy s %% %d): %.0f MB "
+            "between reuses > 2 x 126 MB L2" % (nrot, nrot, nrot * step_bytes / 1e6)),
+        "parity": parity,
         "clocks": clk,
         "gpu_launches": int(launches),
-        "e2e": {"value": e2e_val, "unit": "TOPS", "h2d_bytes_per_step": int(h2d),
+        "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h), "api": "apmm_matmul_ap (host C ABI, pinned buffers)"},
         "roofline": {"bound": "hbm" if hbm_bound else "tensor", "achieved": achieved,
                      "peak": peak, "unit": unit, "frac": achieved / peak, "traffic": tr,
                      "traffic_source": tr_ent.get("kernel"),
+                     "kernel": kname, "peak_source": peak_src,
+                     "achieved_step": step_achieved, "frac_step": step_achieved / peak,
+                     "frac_note": ("frac = dominant kernel alone (event-timed launches); "
+                                   "frac_step = the whole pipelined step (expand + GEMM) per rank; "
+                                   "the north-star 60% target is read against `peak`"),
                      "i8_mma_ceiling_tops": None if hbm_bound else i8_ceiling,
                      "frac_of_i8_mma_ceiling": (achieved / i8_ceiling
                                                 if (i8_ceiling and not hbm_bound) else None),
+                     "frac_step_of_i8_mma_ceiling": (step_achieved / i8_ceiling
+                                                     if (i8_ceiling and not hbm_bound) else None),
                      "i8_mma_ceiling_source": None if hbm_bound else
                          "profiles/i8_mma_peak.json: this pair kernel with operand reloads off, 8192^3",
-                     "kernel": kname, "peak_source": peak_src,
                      "algorithmic_bytes_per_step": bytes_step,
                      "algorithmic_ops_per_step": ops_step,
                      "gemm_us_avg": 1e3 * gemm_avg_ms,
@@ -548,15 +721,26 @@ def run_ours(args, rank, world, local_rank):
                      "gemm_share_of_serialized_step": gemm_ms / ms_serial,
                      "expand_share_of_serialized_step": exp_ms / ms_serial},
     }
+    if gather is not None:
+        line["gather"] = gather
     if world == 1 and not args.no_cpu_baseline:
         try:
-            ref = CpuReference(gemms, 8.0, cpu_threads())
+            ref = CpuReference(gemms, cpu_threads(), 10.0)
             s, o = ref.step()
-            line["cpu_baseline"] = {"value": o / s / 1e12, "unit": "TOPS", "cores": ref.threads,
-                                    "kind": ref.kind, "sample": ref.sample}
+            line["cpu_baseline"] = {"value": o / s / 1e12, "unit": UNIT, "cores": ref.threads,
+                                    "kind": ref.kind, "sample": ref.sample,
+                                    "cpu_model": cpu_model()}
         except Exception as e:  # the baseline must never hide the GPU number
             line["cpu_baseline"] = {"value": None, "error": str(e)[:200]}
     print(json.dumps(line), flush=True)
+    if parity is not None and not parity_ok:
+        sys.exit(1)
+
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
 
 
 def main():
@@ -565,11 +749,10 @@ def main():
     ap_.add_argument("--steps", type=int, default=20)
     ap_.add_argument("--warmup", type=int, default=3)
     ap_.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap_.add_argument("--workload", default="sweep4096",
-                     choices=list(WORKLOAD_DESC))
+    ap_.add_argument("--workload", default="ffn70b", choices=list(WORKLOAD_DESC))
     ap_.add_argument("--no-cpu-baseline", action="store_true")
-    ap_.add_argument("--gather", action="store_true",
-                     help="ffn70b under torchrun: all-gather the N-sharded Y (NCCL) inside each step")
+    ap_.add_argument("--no-parity", action="store_true",
+                     help="skip the post-timing sampled-row parity check (dev only)")
     ap_.add_argument("--no-graph", action="store_true",
                      help="time eager launches instead of replaying the step as a CUDA graph")
     ap_.add_argument("--profile", action="store_true",
@@ -577,9 +760,18 @@ def main():
     args = ap_.parse_args()
     args.warmup = max(3, args.warmup)
 
+    in_torchrun = "WORLD_SIZE" in os.environ
+    if args.gpus > 1 and not in_torchrun and args.impl == "ours":
+        # one process per GPU: re-launch under torch.distributed.run (127.0.0.1 rendezvous)
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+               "--master-port", str(_free_port()), os.path.abspath(__file__)] + sys.argv[1:]
+        sys.exit(subprocess.call(cmd))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if in_torchrun and args.gpus not in (1, world):
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     if args.impl == "reference":
         run_reference_arm(args, rank, world)
         return

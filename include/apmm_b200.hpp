@@ -13,6 +13,8 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <filesystem>
+#include <span>
 #include <string>
 #include <vector>
 
@@ -21,6 +23,7 @@
 #include "apmm/error.hpp"
 #include "apmm/kernel.hpp"
 #include "apmm/matrix.hpp"
+#include "apmm/tensor_file.hpp"
 #include "apmm/verify.hpp"
 #include "apmm_cuda.h"
 
@@ -37,6 +40,8 @@ namespace apmm::b200 {
     case APMM_E_INDEX_OUT_OF_BOUNDS: throw IndexOutOfBounds(msg);
     case APMM_E_OVERFLOW: throw Overflow(msg);
     case APMM_E_OVERFLOW_BOUND: throw OverflowBound(msg);
+    case APMM_E_PARSE: throw ParseError(msg);
+    case APMM_E_IO: throw IoError(msg);
     default: throw Error(msg);
   }
 }
@@ -74,6 +79,33 @@ inline AccumMatrix matmul_ap(const PackedBitPlanes& weights, const PackedBitPlan
   check(apmm_matmul_ap(default_device().get(), weights.words().data(), weights.logical_rows(),
                        weights.width().n(), features.words().data(), features.logical_rows(),
                        features.width().n(), weights.logical_cols(), out.data.data()));
+  return out;
+}
+
+// kernel.hpp:61-62 -- k - 2 popc(a ^ b); OutOfRange for k == 0, LengthMismatch unless both
+// spans hold exactly ceil(k/32) words (kernel.cpp:117-121).
+inline std::int64_t dot_1bit_xor(std::span<const std::uint32_t> a,
+                                 std::span<const std::uint32_t> b, std::size_t k_logical) {
+  std::int64_t out = 0;
+  check(apmm_dot_1bit_xor(default_device().get(), a.data(), a.size(), b.data(), b.size(),
+                          k_logical, &out));
+  return out;
+}
+
+// kernel.hpp:66-67 -- one plane pair as a 1-bit x 1-bit GEMM on the device.
+inline IntMatrix matmul_plane_pair(const PackedBitPlanes& weights, unsigned weight_plane,
+                                   const PackedBitPlanes& features, unsigned feature_plane) {
+  if (weights.logical_cols() != features.logical_cols()) {  // kernel.cpp:127-130
+    throw DimensionMismatch("operands disagree on K: " + std::to_string(weights.logical_cols()) +
+                            " vs " + std::to_string(features.logical_cols()));
+  }
+  IntMatrix out(weights.logical_rows(), features.logical_rows());
+  check(apmm_matmul_plane_pair(default_device().get(), weights.words().data(),
+                               weights.logical_rows(), weights.width().n(),
+                               static_cast<int>(weight_plane), features.words().data(),
+                               features.logical_rows(), features.width().n(),
+                               static_cast<int>(feature_plane), weights.logical_cols(),
+                               out.data.data()));
   return out;
 }
 
@@ -173,6 +205,18 @@ inline RealMatrix matmul_ap_dequant(const PackedBitPlanes& weights, const std::v
   RealMatrix real(weights.logical_rows(), features.logical_rows());
   for (std::size_t e = 0; e < out.size(); ++e) real.data[e] = out[e];
   return real;
+}
+
+// tensor_file.hpp:61 + to_packed (tensor_file.cpp:124-130): parse a reference APMM v1
+// file straight into DEVICE buffers (planes in the PackedBitPlanes layout, scales; or a
+// float tensor widened to f64). Sizes from the returned header; buffers may be null.
+inline apmm_tensor_info load_tensor_file_to_device(const std::filesystem::path& path,
+                                                   std::uint32_t* dev_planes, double* dev_scales,
+                                                   double* dev_values) {
+  apmm_tensor_info info{};
+  check(apmm_tensor_file_load(default_device().get(), path.string().c_str(), &info, dev_planes,
+                              dev_scales, dev_values));
+  return info;
 }
 
 }  // namespace apmm::b200

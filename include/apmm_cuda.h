@@ -18,12 +18,27 @@
  *     bits zero. Device entry points take that layout in device memory unchanged.
  *   - apmm_cu_* entry points take DEVICE pointers and are stream-ordered: they enqueue
  *     work on `stream` (NULL = the legacy default stream) and return without
- *     synchronising. Scratch comes from the
- *     context's workspace, grown on first use for a shape and reused afterwards.
+ *     synchronising. Scratch comes from the context's workspace, grown (stream-ordered,
+ *     never with a device-wide synchronisation) on first use for a larger shape and reused
+ *     afterwards; apmm_ctx_reserve pre-sizes it. Growth is impossible while `stream` is
+ *     being captured into a CUDA graph: such a call fails with APMM_E_INVALID_ARGUMENT
+ *     and the caller reserves first.
  *   - apmm_* entry points without the cu_ prefix take HOST pointers and are
  *     synchronous (H2D, kernels, D2H on the context's stream). They are what a
  *     ctypes / cgo / JNI binding of the reference API calls.
- *   - A context is bound to one device and is not thread-safe; use one per thread.
+ *   - One context = one device, one stream, one thread. The workspace is not tied to a
+ *     stream by CUDA, so the context binds itself to the stream of its first device call
+ *     (or the one given to apmm_ctx_set_stream); a device call on any other stream fails
+ *     with APMM_E_INVALID_ARGUMENT instead of racing on the workspace. Use one context
+ *     per stream for concurrency. The bound stream must outlive its binding.
+ *   - Programmatic dependent launch: consecutive calls on the bound stream overlap (the
+ *     next call's weight expansion runs while the previous GEMM drains). Only WEIGHT
+ *     planes are read before the previous kernel in the stream has completed; feature
+ *     planes, scales and outputs are touched only after it. Weights therefore must not
+ *     be written by a kernel that triggers its dependents early
+ *     (griddepcontrol.launch_dependents) and is launched immediately before the call;
+ *     uploads (cudaMemcpy*) and ordinary kernels are always safe.
+ *     apmm_ctx_set_option(APMM_OPT_EARLY_WEIGHT_READ, 0) turns the early read off.
  */
 #ifndef APMM_CUDA_H_
 #define APMM_CUDA_H_
@@ -52,6 +67,8 @@ typedef enum apmm_status {
   APMM_E_OVERFLOW = 7,            /* apmm::Overflow          error.hpp:51-54 */
   APMM_E_OVERFLOW_BOUND = 8,      /* apmm::OverflowBound     error.hpp:57-60 */
   APMM_E_INVALID_ARGUMENT = 9,    /* null pointer / bad enum (reference: std::invalid_argument) */
+  APMM_E_PARSE = 10,              /* apmm::ParseError        error.hpp:62-65 */
+  APMM_E_IO = 11,                 /* apmm::IoError           error.hpp:67-70 */
   APMM_E_CUDA = 100,              /* CUDA runtime/driver error */
   APMM_E_NO_DEVICE = 101,         /* no usable device */
   APMM_E_UNSUPPORTED_DEVICE = 102 /* device is not sm_100 (B200) */
@@ -66,7 +83,10 @@ typedef struct CUstream_st* apmm_stream_t; /* == cudaStream_t */
 /* ---- context ------------------------------------------------------------------- */
 APMM_API int apmm_ctx_create(apmm_ctx** out, int device);
 APMM_API int apmm_ctx_destroy(apmm_ctx* ctx);
-/* Stream used by the synchronous host entry points (default: a private stream). */
+/* Bind the context to `stream`: the host entry points run on it and the device entry points
+ * must be given it (default: a private stream for the host entry points, and the stream of
+ * the first device call). The caller guarantees that work enqueued through the context on
+ * a previously bound stream is complete or ordered before work on the new one. */
 APMM_API int apmm_ctx_set_stream(apmm_ctx* ctx, apmm_stream_t stream);
 /* Human-readable message for the last failing call on this thread. */
 APMM_API const char* apmm_last_error(void);
@@ -75,6 +95,36 @@ APMM_API const char* apmm_status_name(int status);
 APMM_API const char* apmm_version(void);
 /* Number of kernel launches this context has enqueued (launch accounting for bench). */
 APMM_API uint64_t apmm_ctx_launch_count(const apmm_ctx* ctx);
+
+/* Pre-size the workspace for calls up to this shape (every route the shape can take), so
+ * that no later call grows it -- required before capturing such calls into a CUDA graph.
+ * rows_x = feature rows (tokens); n_w is the widest weight width that will be used. */
+APMM_API int apmm_ctx_reserve(apmm_ctx* ctx, uint64_t rows_w, uint64_t rows_x, uint64_t k,
+                              int n_w);
+
+/* Context options (apmm_ctx_set_option / apmm_ctx_get_option). */
+enum {
+  /* Kernel route for matmul calls. Routes are schedules only: every route returns the
+   * same bits (like TileConfig). AUTO picks by shape; the others
+   * force one route and make a call the route cannot serve fail with
+   * APMM_E_INVALID_ARGUMENT. Used by the parity tests to pin every kernel. */
+  APMM_OPT_ROUTE = 1,
+  /* 1 (default): PDL early read of the weight planes (see Conventions); 0: every operand
+   * is read after the previous kernel in the stream completed. */
+  APMM_OPT_EARLY_WEIGHT_READ = 2
+};
+enum {
+  APMM_ROUTE_AUTO = 0,         /* by shape */
+  APMM_ROUTE_SKINNY = 1,       /* K5: weight planes streamed into mma.sync (rows_x <= 63) */
+  APMM_ROUTE_MID_SPLITK = 2,   /* K3f split-K: on-chip weight expansion, K over CTA pairs */
+  APMM_ROUTE_PAIR = 3,         /* K1 + K3: tcgen05 cta_group::2 256x256 tiles */
+  APMM_ROUTE_PAIR_WPLANES = 4, /* K1(X) + K3f: pair tiles, weights expanded on chip */
+  APMM_ROUTE_PAIR_SPLITK = 5,  /* K1 + K3 with K split over the pairs */
+  APMM_ROUTE_SINGLE_SM = 6,    /* K1 + K3': 1-SM 128x256 tiles */
+  APMM_ROUTE_TENSOR_CORE = 7   /* AUTO without K5 (tcgen05 routes only) */
+};
+APMM_API int apmm_ctx_set_option(apmm_ctx* ctx, int option, int value);
+APMM_API int apmm_ctx_get_option(const apmm_ctx* ctx, int option, int* value);
 
 /* Kernel timing for measurement: when enabled, every launch of the given kernel class is
  * bracketed by CUDA events on the stream it is launched on. apmm_ctx_kernel_time
@@ -170,6 +220,80 @@ APMM_API int apmm_cu_quantize_matmul_ap_dequant(apmm_ctx* ctx, const uint32_t* w
                                        uint64_t rows_x, uint64_t k, int n_x, int x_granularity,
                                        double* x_scales, float* out, apmm_stream_t stream);
 
+/* dot_1bit_xor (kernel.hpp:61-62, kernel.cpp:115-123): k - 2 popc(a ^ b) over exactly
+ * ceil(k/32) words of each operand, into *out (device int64). k == 0 -> OutOfRange;
+ * a_words or b_words != ceil(k/32) -> LengthMismatch (checked on the host, before any
+ * device work). Padding bits are not masked, as in the reference. */
+APMM_API int apmm_cu_dot_1bit_xor(apmm_ctx* ctx, const uint32_t* a, uint64_t a_words,
+                                  const uint32_t* b, uint64_t b_words, uint64_t k, int64_t* out,
+                                  apmm_stream_t stream);
+
+/* Next-layer requantization fused behind the GEMM: matmul_ap with
+ * the dequant epilogue (tools/apmm.cpp:329-340) whose f32 output, read as the next layer's
+ * activation X' = dequant(Y)^T [rows_x tokens x rows_w features], is quantized
+ * (bipolar.cpp:72-100, fp64, per-tensor or per-token) and packed (bitplane.cpp:48-66) into
+ * X' planes [n_next][rows_x][ceil(rows_w/32)] + scales (1 or rows_x doubles). Bit-identical
+ * to apmm_cu_quantize_pack(transpose((double)apmm_cu_matmul_ap_dequant(...))). The GEMM
+ * epilogue also forms the per-token (or global) absmax of its tile, so the requantizer
+ * reads the f32 output once. `yf` (device, rows_w x rows_x f32) receives the dequantized
+ * output as well (it is the requantizer's input).
+ * `absmax` (device, rows_x doubles for per-token, 1 for per-tensor) may be NULL. When given
+ * the call stops after the GEMM: absmax receives the local maxima (for a cross-GPU
+ * max all-reduce of N-sharded layers) and apmm_cu_requant_pack finishes the job. */
+APMM_API int apmm_cu_matmul_ap_requant(apmm_ctx* ctx, const uint32_t* w_planes, uint64_t rows_w,
+                                       int n_w, const double* w_scales, int w_granularity,
+                                       const uint32_t* x_planes, uint64_t rows_x, int n_x,
+                                       const double* x_scales, int x_granularity, uint64_t k,
+                                       int n_next, int next_granularity, float* yf,
+                                       uint32_t* next_planes, double* next_scales,
+                                       double* absmax, apmm_stream_t stream);
+/* Second half of the split form: quantize + pack yf^T with the given (globally reduced)
+ * absmax (rows_x doubles per-token, 1 per-tensor) -> next_planes [n_next][rows_x]
+ * [ceil(rows_w/32)] / next_scales. An N-shard's block of the next-layer activation is a
+ * column block of whole words when its row count is a multiple of 32, so the blocks of all
+ * ranks all-gather into the full activation with one word-block re-layout. Non-finite
+ * input -> APMM_E_NON_FINITE after a stream synchronisation, as apmm_cu_quantize_pack. */
+APMM_API int apmm_cu_requant_pack(apmm_ctx* ctx, const float* yf, uint64_t rows_w,
+                                  uint64_t rows_x, const double* absmax, int n_next,
+                                  int next_granularity, uint32_t* next_planes,
+                                  double* next_scales, apmm_stream_t stream);
+
+/* ---- APMM v1 tensor files (tensor_file.hpp:12-64) --------------------------------- */
+typedef struct apmm_tensor_info {
+  int kind;           /* 0 float32 matrix, 1 quantized bipolar (TensorKind) */
+  int bit_width;      /* n (0 for float) */
+  int granularity;    /* APMM_PER_TENSOR / APMM_PER_ROW, -1 for float */
+  uint64_t rows, cols;
+  uint64_t scale_count;      /* 1 or rows (quantized), 0 (float) */
+  uint64_t payload_offset;   /* byte offset of the f32 values / packed words */
+  uint64_t payload_words;    /* rows*cols (float) or n*rows*ceil(cols/32) (quantized) */
+} apmm_tensor_info;
+/* parse_tensor (tensor_file.cpp:159-229): validates the header, the scales (finite,
+ * positive) and the exact payload length -> APMM_E_PARSE with the reference's messages;
+ * a quantized payload's padding bits are checked like to_packed -> PackedBitPlanes
+ * (bitplane.cpp:22-32, APMM_E_OUT_OF_RANGE). Host only, no device work. */
+APMM_API int apmm_tensor_parse(const uint8_t* bytes, uint64_t n_bytes, apmm_tensor_info* info);
+/* Parse + upload straight into device buffers (to_packed, tensor_file.cpp:124-130, without
+ * the host copy): quantized kind -> planes (n*rows*ceil(cols/32) u32, the PackedBitPlanes
+ * layout verbatim) and scales (scale_count doubles); float kind -> values (rows*cols
+ * doubles, widened from f32 on the device like to_real, tensor_file.cpp:115-120).
+ * Unused pointers may be NULL. Stream-ordered; `bytes` must stay valid until the stream
+ * reaches the copy (pinned memory makes it asynchronous). */
+APMM_API int apmm_cu_tensor_upload(apmm_ctx* ctx, const uint8_t* bytes, uint64_t n_bytes,
+                                   uint32_t* planes, double* scales, double* values,
+                                   apmm_stream_t stream);
+/* read_tensor_file (tensor_file.cpp:231-) + apmm_cu_tensor_upload, synchronous. A file
+ * that cannot be read -> APMM_E_IO. `info` may be NULL. */
+APMM_API int apmm_tensor_file_load(apmm_ctx* ctx, const char* path, apmm_tensor_info* info,
+                                   uint32_t* planes, double* scales, double* values);
+/* serialize_tensor (tensor_file.cpp:135-157) of a quantized tensor from host buffers:
+ * writes the exact byte image into out (capacity out_cap) and its length into *out_len.
+ * With out == NULL only *out_len is set. */
+APMM_API int apmm_tensor_serialize_quantized(uint64_t rows, uint64_t cols, int n,
+                                             int granularity, const double* scales,
+                                             const uint32_t* planes, uint8_t* out,
+                                             uint64_t out_cap, uint64_t* out_len);
+
 /* ---- host entry points (synchronous, host pointers) ------------------------------- */
 /* These mirror the reference functions one for one and add the H2D/D2H copies. */
 
@@ -197,6 +321,16 @@ APMM_API int apmm_compute_plane_products(apmm_ctx* ctx, const uint32_t* w_planes
 /* recover (kernel.cpp:159-181) with host buffers. */
 APMM_API int apmm_recover(apmm_ctx* ctx, const int32_t* stack, int n_w, int n_x, uint64_t k,
                  uint64_t rows, uint64_t cols, int32_t* y);
+
+/* dot_1bit_xor (kernel.cpp:115-123) with host buffers. */
+APMM_API int apmm_dot_1bit_xor(apmm_ctx* ctx, const uint32_t* a, uint64_t a_words,
+                               const uint32_t* b, uint64_t b_words, uint64_t k, int64_t* out);
+
+/* matmul_plane_pair (kernel.cpp:125-144) with host buffers; validates padding. */
+APMM_API int apmm_matmul_plane_pair(apmm_ctx* ctx, const uint32_t* w_planes, uint64_t rows_w,
+                                    int n_w, int weight_plane, const uint32_t* x_planes,
+                                    uint64_t rows_x, int n_x, int feature_plane, uint64_t k,
+                                    int32_t* y);
 
 /* matmul_ap (kernel.cpp:187-254). Validates padding like PackedBitPlanes
  * (bitplane.cpp:22-32), then K agreement and overflow_bound like kernel.cpp:189-199. */

@@ -29,7 +29,7 @@ PER_TENSOR, PER_ROW = 0, 1
 STATUS = {
     0: "OK", 1: "EvenValue", 2: "OutOfRange", 3: "NonFinite", 4: "LengthMismatch",
     5: "DimensionMismatch", 6: "IndexOutOfBounds", 7: "Overflow", 8: "OverflowBound",
-    9: "InvalidArgument",
+    9: "InvalidArgument", 10: "ParseError", 11: "IoError",
 }
 
 
@@ -258,6 +258,9 @@ class Reference:
                 "ref_job_result": (None, [vp, vp]),
                 "ref_job_free": (None, [vp]),
                 "ref_run_verify": (i32, [u64, i32, u64, u64, vp, i32]),
+                "ref_serialize_quantized": (i32, [vp, u64, u64, i32, i32, vp, u64, vp]),
+                "ref_serialize_float": (i32, [vp, u64, u64, vp, u64, vp]),
+                "ref_parse_to_packed": (i32, [vp, u64, vp, vp]),
                 "ref_last_error": (C.c_char_p, []),
             }
             for name, (res, args) in sig.items():
@@ -325,6 +328,33 @@ class Reference:
         out = np.zeros(1, dtype=np.int64)
         self._check(self.lib.ref_dot_1bit_xor(_p(a), a.size, _p(b), b.size, k, _p(out)))
         return int(out[0])
+
+    def serialize_quantized(self, x, n, gran) -> bytes:
+        """quantize -> TensorFile::from_quantized -> serialize_tensor (the reference's bytes)."""
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        ln = np.zeros(1, dtype=np.uint64)
+        self._check(self.lib.ref_serialize_quantized(_p(x), x.shape[0], x.shape[1], n, gran,
+                                                     None, 0, _p(ln)))
+        out = np.empty(int(ln[0]), dtype=np.uint8)
+        self._check(self.lib.ref_serialize_quantized(_p(x), x.shape[0], x.shape[1], n, gran,
+                                                     _p(out), out.size, _p(ln)))
+        return out.tobytes()
+
+    def serialize_float(self, x) -> bytes:
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        ln = np.zeros(1, dtype=np.uint64)
+        self._check(self.lib.ref_serialize_float(_p(x), x.shape[0], x.shape[1], None, 0, _p(ln)))
+        out = np.empty(int(ln[0]), dtype=np.uint8)
+        self._check(self.lib.ref_serialize_float(_p(x), x.shape[0], x.shape[1], _p(out), out.size,
+                                                 _p(ln)))
+        return out.tobytes()
+
+    def parse_to_packed(self, data: bytes, words: int, scales: int):
+        buf = np.frombuffer(bytes(data), dtype=np.uint8)
+        w = np.empty(words, dtype=np.uint32)
+        s = np.empty(scales, dtype=np.float64)
+        self._check(self.lib.ref_parse_to_packed(_p(buf), buf.size, _p(w), _p(s)))
+        return w, s
 
     def run_verify(self, seed=1, cases=1000, max_dim=32, max_k=200):
         passed = np.zeros(16, dtype=np.int32)

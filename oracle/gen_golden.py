@@ -70,6 +70,28 @@ def main():
     doc["plane_products"].append({"w_codes": wc.reshape(-1).tolist(), "x_codes": xc.reshape(-1).tolist(),
                                   "n_w": 2, "n_x": 2, "k": 2, "stack": stack.reshape(-1).tolist(),
                                   "y": y.reshape(-1).tolist()})
+    # APMM v1 tensor files written by the reference's serializer (tensor_file.cpp:135-157):
+    # the 1x4 W2 golden of test_tensor_file.cpp:21-26, a per-row W3 5x37 tensor (ragged
+    # words), a per-tensor W4 3x64 one and a float32 2x3 tensor; stored as files next to the
+    # JSON so the GPU box can upload them with no reference present.
+    gdir = os.path.dirname(OUT)
+    files = []
+    for name, x, n, gran in [("w2_1x4_tensor", np.array([[3.0, -1.0, 1.0, -3.0]]), 2, PER_TENSOR),
+                             ("w3_5x37_row", rng.uniform(-8, 8, size=(5, 37)), 3, PER_ROW),
+                             ("w4_3x64_tensor", rng.uniform(-2, 2, size=(3, 64)), 4, PER_TENSOR)]:
+        data = ref.serialize_quantized(x, n, gran)
+        codes, scales = ref.quantize(x, n, gran)
+        with open(os.path.join(gdir, name + ".apmm"), "wb") as f:
+            f.write(data)
+        files.append({"file": name + ".apmm", "kind": 1, "rows": x.shape[0], "cols": x.shape[1],
+                      "n": n, "gran": gran, "words": ref.pack(codes, n).tolist(),
+                      "scales": hexd(scales)})
+    xf = np.array([[0.5, -1.25, 3.0], [1e10, -7.5e-3, 0.0]])  # test_tensor_file.cpp:56
+    with open(os.path.join(gdir, "f32_2x3.apmm"), "wb") as f:
+        f.write(ref.serialize_float(xf))
+    files.append({"file": "f32_2x3.apmm", "kind": 0, "rows": 2, "cols": 3,
+                  "values": hexd(xf.astype(np.float32).astype(np.float64))})
+    doc["tensor_files"] = files
     os.makedirs(os.path.dirname(OUT), exist_ok=True)
     with open(OUT, "w") as f:
         json.dump(doc, f, separators=(",", ":"))

@@ -22,6 +22,7 @@
 #include "apmm/kernel.hpp"
 #include "apmm/oracle.hpp"
 #include "apmm/rng.hpp"
+#include "apmm/tensor_file.hpp"
 #include "apmm/verify.hpp"
 
 #include "../include/apmm_cuda.h"
@@ -42,6 +43,8 @@ int status_of(const std::exception& e) {
   if (dynamic_cast<const IndexOutOfBounds*>(&e)) return APMM_E_INDEX_OUT_OF_BOUNDS;
   if (dynamic_cast<const OverflowBound*>(&e)) return APMM_E_OVERFLOW_BOUND;
   if (dynamic_cast<const Overflow*>(&e)) return APMM_E_OVERFLOW;
+  if (dynamic_cast<const ParseError*>(&e)) return APMM_E_PARSE;
+  if (dynamic_cast<const IoError*>(&e)) return APMM_E_IO;
   return APMM_E_INVALID_ARGUMENT;
 }
 
@@ -153,6 +156,42 @@ int ref_dot_1bit_xor(const uint32_t* a, uint64_t a_words, const uint32_t* b, uin
   GUARD({
     *out = dot_1bit_xor(std::span<const uint32_t>(a, a_words),
                         std::span<const uint32_t>(b, b_words), k);
+  })
+}
+
+// ---- APMM v1 tensor files (tensor_file.cpp): the reference's own serializer / parser ----
+// quantize (bipolar.cpp:72-100) -> TensorFile::from_quantized -> serialize_tensor; with
+// out == nullptr only *len is set.
+int ref_serialize_quantized(const double* x, uint64_t rows, uint64_t cols, int n, int gran,
+                            uint8_t* out, uint64_t cap, uint64_t* len) {
+  GUARD({
+    const QuantizedTensor q =
+        quantize(RealMatrix(rows, cols, std::vector<double>(x, x + rows * cols)), BitWidth(n),
+                 gran == APMM_PER_ROW ? Granularity::PerRow : Granularity::PerTensor);
+    const std::vector<uint8_t> b = serialize_tensor(TensorFile::from_quantized(q));
+    *len = b.size();
+    if (out && cap >= b.size()) std::memcpy(out, b.data(), b.size());
+  })
+}
+
+// RealMatrix -> TensorFile::from_real (f32) -> serialize_tensor.
+int ref_serialize_float(const double* x, uint64_t rows, uint64_t cols, uint8_t* out, uint64_t cap,
+                        uint64_t* len) {
+  GUARD({
+    const std::vector<uint8_t> b = serialize_tensor(
+        TensorFile::from_real(RealMatrix(rows, cols, std::vector<double>(x, x + rows * cols))));
+    *len = b.size();
+    if (out && cap >= b.size()) std::memcpy(out, b.data(), b.size());
+  })
+}
+
+// parse_tensor + to_packed (quantized) -> words, scales; status as the reference throws.
+int ref_parse_to_packed(const uint8_t* bytes, uint64_t n, uint32_t* words, double* scales) {
+  GUARD({
+    const TensorFile t = parse_tensor(std::span<const uint8_t>(bytes, n));
+    const PackedBitPlanes p = t.to_packed();
+    std::memcpy(words, p.words().data(), p.words().size() * sizeof(uint32_t));
+    std::memcpy(scales, t.scales.data(), t.scales.size() * sizeof(double));
   })
 }
 

@@ -71,6 +71,40 @@ int main(int argc, char** argv) {
                   ref_threw == gpu_threw && gpu_threw ? "PASS" : "FAIL", ref_threw, gpu_threw);
       if (!(ref_threw && gpu_threw)) rc = 1;
     }
+    {  // dot_1bit_xor / matmul_plane_pair through the drop-in (kernel.hpp:61-69): the
+       // xor_identity property (verify.cpp:142-157) on the device, plus the error classes
+      int bad = 0;
+      for (int c = 0; c < 200; ++c) {
+        const std::size_t k = 1 + gen() % 2000, words = (k + 31) / 32;
+        std::vector<std::uint32_t> a(words), b(words);
+        for (auto& v : a) v = static_cast<std::uint32_t>(gen());
+        for (auto& v : b) v = static_cast<std::uint32_t>(gen());
+        if (k % 32) {
+          a.back() &= (1u << (k % 32)) - 1u;
+          b.back() &= (1u << (k % 32)) - 1u;
+        }
+        if (apmm::b200::dot_1bit_xor(a, b, k) != apmm::dot_1bit_xor(a, b, k)) ++bad;
+      }
+      bool len_ok = false, k_ok = false;
+      const std::vector<std::uint32_t> one(1), two(2);
+      try { apmm::b200::dot_1bit_xor(one, two, 32); } catch (const apmm::LengthMismatch&) { len_ok = true; }
+      try { apmm::b200::dot_1bit_xor(one, one, 0); } catch (const apmm::OutOfRange&) { k_ok = true; }
+      for (int c = 0; c < 20; ++c) {
+        const std::size_t m = 1 + gen() % 30, n = 1 + gen() % 30, k = 1 + gen() % 400;
+        const int nw = 1 + static_cast<int>(gen() % 8), nx = 1 + static_cast<int>(gen() % 8);
+        std::vector<std::uint8_t> wb(m * k), xb(n * k);
+        for (auto& v : wb) v = static_cast<std::uint8_t>(gen() % (1u << nw));
+        for (auto& v : xb) v = static_cast<std::uint8_t>(gen() % (1u << nx));
+        const auto w = apmm::decompose_and_pack(apmm::CodeMatrix(m, k, apmm::BitWidth(nw), wb));
+        const auto x = apmm::decompose_and_pack(apmm::CodeMatrix(n, k, apmm::BitWidth(nx), xb));
+        const unsigned i = static_cast<unsigned>(gen() % nw), j = static_cast<unsigned>(gen() % nx);
+        if (!(apmm::b200::matmul_plane_pair(w, i, x, j) == apmm::matmul_plane_pair(w, i, x, j))) ++bad;
+      }
+      const bool ok = bad == 0 && len_ok && k_ok;
+      std::printf("%s xor_identity / dot_1bit_xor / matmul_plane_pair through the drop-in "
+                  "(200 dots, 20 plane pairs, errors %d%d)\n", ok ? "PASS" : "FAIL", len_ok, k_ok);
+      if (!ok) rc = 1;
+    }
     apmm::VerifyOptions mopt = opt;
     mopt.cases = 50;
     const apmm::VerifyReport bad = apmm::run_verify(mopt, mutant);

@@ -11,6 +11,8 @@ from .apmm import (  # noqa: F401
     decompose_and_pack, unpack, quantize, matmul_ap, matmul_ap_dequant, overflow_bound,
     kernel_fn, cu_matmul_ap, cu_matmul_ap_dequant, cu_pack, cu_unpack, cu_quantize_pack,
     PlaneProductStack, matmul_plane_pair, compute_plane_products, recover,
-    cu_quantize_matmul_ap_dequant,
+    cu_quantize_matmul_ap_dequant, Route, dot_1bit_xor, cu_dot_1bit_xor, cu_matmul_ap_requant,
+    cu_requant_pack, ParseError, IoError, TensorKind, TensorFile, parse_tensor, read_tensor_file,
+    serialize_tensor, load_tensor_file,
     version,
 )

@@ -24,6 +24,9 @@ _SIGNATURES = {
     "apmm_ctx_launch_count": (u64, [vp]),
     "apmm_ctx_enable_timing": (i32, [vp, i32]),
     "apmm_ctx_kernel_time": (i32, [vp, i32, C.POINTER(C.c_double), C.POINTER(u64)]),
+    "apmm_ctx_reserve": (i32, [vp, u64, u64, u64, i32]),
+    "apmm_ctx_set_option": (i32, [vp, i32, i32]),
+    "apmm_ctx_get_option": (i32, [vp, i32, C.POINTER(i32)]),
     "apmm_overflow_bound": (i32, [i32, i32, u64, C.POINTER(i64)]),
     "apmm_packed_words": (u64, [i32, u64, u64]),
     "apmm_cu_pack": (i32, [vp, vp, u64, u64, i32, vp, vp]),
@@ -37,6 +40,17 @@ _SIGNATURES = {
     "apmm_cu_matmul_plane_pair": (i32, [vp, vp, u64, i32, i32, vp, u64, i32, i32, u64, vp, vp]),
     "apmm_cu_compute_plane_products": (i32, [vp, vp, u64, i32, vp, u64, i32, u64, vp, vp]),
     "apmm_cu_recover": (i32, [vp, vp, i32, i32, u64, u64, u64, vp, vp]),
+    "apmm_cu_dot_1bit_xor": (i32, [vp, vp, u64, vp, u64, u64, vp, vp]),
+    "apmm_cu_matmul_ap_requant": (i32, [vp, vp, u64, i32, vp, i32, vp, u64, i32, vp, i32, u64, i32,
+                                        i32, vp, vp, vp, vp, vp]),
+    "apmm_cu_requant_pack": (i32, [vp, vp, u64, u64, vp, i32, i32, vp, vp, vp]),
+    "apmm_tensor_parse": (i32, [vp, u64, vp]),
+    "apmm_cu_tensor_upload": (i32, [vp, vp, u64, vp, vp, vp, vp]),
+    "apmm_tensor_file_load": (i32, [vp, C.c_char_p, vp, vp, vp, vp]),
+    "apmm_tensor_serialize_quantized": (i32, [u64, u64, i32, i32, vp, vp, vp, u64,
+                                              C.POINTER(u64)]),
+    "apmm_dot_1bit_xor": (i32, [vp, vp, u64, vp, u64, u64, vp]),
+    "apmm_matmul_plane_pair": (i32, [vp, vp, u64, i32, i32, vp, u64, i32, i32, u64, vp]),
     "apmm_compute_plane_products": (i32, [vp, vp, u64, i32, vp, u64, i32, u64, vp]),
     "apmm_recover": (i32, [vp, vp, i32, i32, u64, u64, u64, vp]),
     "apmm_decompose_and_pack": (i32, [vp, vp, u64, u64, i32, vp]),

@@ -49,6 +49,8 @@ class IndexOutOfBounds(Error): pass
 class Overflow(Error): pass
 class OverflowBound(Error): pass
 class InvalidArgument(Error): pass
+class ParseError(Error): pass
+class IoError(Error): pass
 class CudaError(Error): pass
 class NoDevice(Error): pass
 class UnsupportedDevice(Error): pass
@@ -56,7 +58,8 @@ class UnsupportedDevice(Error): pass
 
 _STATUS_TO_ERROR = {
     1: EvenValue, 2: OutOfRange, 3: NonFinite, 4: LengthMismatch, 5: DimensionMismatch,
-    6: IndexOutOfBounds, 7: Overflow, 8: OverflowBound, 9: InvalidArgument, 100: CudaError,
+    6: IndexOutOfBounds, 7: Overflow, 8: OverflowBound, 9: InvalidArgument, 10: ParseError,
+    11: IoError, 100: CudaError,
     101: NoDevice, 102: UnsupportedDevice,
 }
 
@@ -186,8 +189,24 @@ class QuantizedTensor:
 
 
 # ---- device context -------------------------------------------------------------------------
+class Route(enum.IntEnum):
+    """Kernel routes (apmm_cuda.h APMM_ROUTE_*): schedules only, every route returns the same
+    bits. AUTO picks by shape; the others pin one kernel (tests)."""
+    AUTO = 0
+    SKINNY = 1
+    MID_SPLITK = 2
+    PAIR = 3
+    PAIR_WPLANES = 4
+    PAIR_SPLITK = 5
+    SINGLE_SM = 6
+    TENSOR_CORE = 7
+
+
+OPT_ROUTE, OPT_EARLY_WEIGHT_READ = 1, 2
+
+
 class Context:
-    """Owns an apmm_ctx (one device, private stream, reusable workspace)."""
+    """Owns an apmm_ctx (one device, one bound stream, reusable workspace)."""
 
     def __init__(self, device: int = 0):
         self.lib = _lib.load()
@@ -210,6 +229,26 @@ class Context:
     def launch_count(self) -> int:
         return int(self.lib.apmm_ctx_launch_count(self.h))
 
+    def set_route(self, route: "Route") -> None:
+        _check(self.lib.apmm_ctx_set_option(self.h, OPT_ROUTE, int(route)))
+
+    def route(self) -> "Route":
+        v = C.c_int()
+        _check(self.lib.apmm_ctx_get_option(self.h, OPT_ROUTE, C.byref(v)))
+        return Route(v.value)
+
+    def set_early_weight_read(self, on: bool) -> None:
+        _check(self.lib.apmm_ctx_set_option(self.h, OPT_EARLY_WEIGHT_READ, int(bool(on))))
+
+    def reserve(self, rows_w: int, rows_x: int, k: int, n_w: int = 8) -> None:
+        """Pre-size the workspace for calls up to this shape (before CUDA-graph capture)."""
+        _check(self.lib.apmm_ctx_reserve(self.h, int(rows_w), int(rows_x), int(k), int(n_w)))
+
+    def set_stream(self, stream) -> None:
+        """Bind to a torch.cuda.Stream (or raw handle); see apmm_ctx_set_stream."""
+        handle = getattr(stream, "cuda_stream", stream)
+        _check(self.lib.apmm_ctx_set_stream(self.h, C.c_void_p(handle)))
+
     def enable_timing(self, enable: bool = True) -> None:
         _check(self.lib.apmm_ctx_enable_timing(self.h, int(bool(enable))))
 
@@ -223,13 +262,17 @@ class Context:
 _tls = threading.local()
 
 
-def default_context(device: int = 0) -> Context:
+def default_context(device: int = 0, stream: int | None = None) -> Context:
+    """Per-thread context for (device, stream). A context binds to one stream (its workspace
+    is shared by its calls), so the device wrappers key theirs by the stream they enqueue
+    on; the host API (stream None) uses the context's private stream."""
     ctxs = getattr(_tls, "ctxs", None)
     if ctxs is None:
         ctxs = _tls.ctxs = {}
-    if device not in ctxs:
-        ctxs[device] = Context(device)
-    return ctxs[device]
+    key = (device, stream)
+    if key not in ctxs:
+        ctxs[key] = Context(device)
+    return ctxs[key]
 
 
 def _ptr(a: np.ndarray):
@@ -345,17 +388,24 @@ def matmul_plane_pair(weights: PackedBitPlanes, weight_plane: int, features: Pac
     if weights.logical_cols() != features.logical_cols():
         raise DimensionMismatch(f"operands disagree on K: {weights.logical_cols()} vs "
                                 f"{features.logical_cols()}")
-    import torch
-    k = weights.logical_cols()
-    dev = torch.device("cuda", ctx.device)
-    w = torch.from_numpy(weights.words().view(np.int32)).to(dev)
-    x = torch.from_numpy(features.words().view(np.int32)).to(dev)
-    y = torch.empty((weights.logical_rows(), features.logical_rows()), dtype=torch.int32, device=dev)
-    _check(ctx.lib.apmm_cu_matmul_plane_pair(
-        ctx.h, C.c_void_p(w.data_ptr()), weights.logical_rows(), weights.width().n(),
-        int(weight_plane), C.c_void_p(x.data_ptr()), features.logical_rows(),
-        features.width().n(), int(feature_plane), k, C.c_void_p(y.data_ptr()), None))
-    return y.cpu().numpy()
+    y = np.empty((weights.logical_rows(), features.logical_rows()), dtype=np.int32)
+    _check(ctx.lib.apmm_matmul_plane_pair(
+        ctx.h, _ptr(weights.words()), weights.logical_rows(), weights.width().n(),
+        int(weight_plane), _ptr(features.words()), features.logical_rows(),
+        features.width().n(), int(feature_plane), weights.logical_cols(), _ptr(y)))
+    return y
+
+
+def dot_1bit_xor(a, b, k_logical: int, ctx: Context | None = None) -> int:
+    """kernel.cpp:115-123 on the GPU: k - 2 popc(a ^ b); OutOfRange for k == 0,
+    LengthMismatch unless both hold exactly ceil(k/32) words."""
+    ctx = ctx or default_context()
+    a = np.ascontiguousarray(a, dtype=np.uint32)
+    b = np.ascontiguousarray(b, dtype=np.uint32)
+    out = C.c_int64()
+    _check(ctx.lib.apmm_dot_1bit_xor(ctx.h, _ptr(a), a.size, _ptr(b), b.size, int(k_logical),
+                                     C.byref(out)))
+    return int(out.value)
 
 
 def compute_plane_products(weights: PackedBitPlanes, features: PackedBitPlanes,
@@ -421,10 +471,18 @@ def _stream_ptr(stream=None):
     return C.c_void_p(s.cuda_stream)
 
 
+def _dctx(ctx, t, stream):
+    """The context for a device call: the given one, else the thread's context for
+    (device of t, the stream the call enqueues on)."""
+    if ctx is not None:
+        return ctx
+    return default_context(t.device.index or 0, _stream_ptr(stream).value or 0)
+
+
 def cu_matmul_ap(w_planes, rows_w: int, n_w: int, x_planes, rows_x: int, n_x: int, k: int,
                  y, ctx: Context | None = None, stream=None) -> None:
     """apmm_cu_matmul_ap on device buffers (torch tensors); y: int32 [rows_w, rows_x]."""
-    ctx = ctx or default_context(w_planes.device.index or 0)
+    ctx = _dctx(ctx, w_planes, stream)
     _check(ctx.lib.apmm_cu_matmul_ap(ctx.h, C.c_void_p(w_planes.data_ptr()), rows_w, n_w,
                                      C.c_void_p(x_planes.data_ptr()), rows_x, n_x, k,
                                      C.c_void_p(y.data_ptr()), _stream_ptr(stream)))
@@ -433,7 +491,7 @@ def cu_matmul_ap(w_planes, rows_w: int, n_w: int, x_planes, rows_x: int, n_x: in
 def cu_matmul_ap_dequant(w_planes, rows_w, n_w, w_scales, w_gran, x_planes, rows_x, n_x,
                          x_scales, x_gran, k, out, ctx: Context | None = None,
                          stream=None) -> None:
-    ctx = ctx or default_context(w_planes.device.index or 0)
+    ctx = _dctx(ctx, w_planes, stream)
     _check(ctx.lib.apmm_cu_matmul_ap_dequant(
         ctx.h, C.c_void_p(w_planes.data_ptr()), rows_w, n_w, C.c_void_p(w_scales.data_ptr()),
         int(w_gran), C.c_void_p(x_planes.data_ptr()), rows_x, n_x,
@@ -446,7 +504,7 @@ def cu_quantize_matmul_ap_dequant(w_planes, rows_w, n_w, w_scales, w_gran, x_val
                                   stream=None) -> None:
     """quantize(X) -> matmul_ap -> dequant in one call (apmm.cpp:275-340), the quantizer
     writing the GEMM operand directly; x_scales receives X's scales (torch CUDA tensors)."""
-    ctx = ctx or default_context(w_planes.device.index or 0)
+    ctx = _dctx(ctx, w_planes, stream)
     _check(ctx.lib.apmm_cu_quantize_matmul_ap_dequant(
         ctx.h, C.c_void_p(w_planes.data_ptr()), rows_w, n_w, C.c_void_p(w_scales.data_ptr()),
         int(w_gran), C.c_void_p(x_values.data_ptr()), rows_x, k, n_x, int(x_gran),
@@ -454,21 +512,183 @@ def cu_quantize_matmul_ap_dequant(w_planes, rows_w, n_w, w_scales, w_gran, x_val
 
 
 def cu_pack(codes, rows, cols, n, planes, ctx: Context | None = None, stream=None) -> None:
-    ctx = ctx or default_context(codes.device.index or 0)
+    ctx = _dctx(ctx, codes, stream)
     _check(ctx.lib.apmm_cu_pack(ctx.h, C.c_void_p(codes.data_ptr()), rows, cols, n,
                                 C.c_void_p(planes.data_ptr()), _stream_ptr(stream)))
 
 
 def cu_unpack(planes, rows, cols, n, codes, ctx: Context | None = None, stream=None) -> None:
-    ctx = ctx or default_context(planes.device.index or 0)
+    ctx = _dctx(ctx, planes, stream)
     _check(ctx.lib.apmm_cu_unpack(ctx.h, C.c_void_p(planes.data_ptr()), rows, cols, n,
                                   C.c_void_p(codes.data_ptr()), _stream_ptr(stream)))
 
 
 def cu_quantize_pack(values, rows, cols, n, gran, planes, scales, codes=None,
                      ctx: Context | None = None, stream=None) -> None:
-    ctx = ctx or default_context(values.device.index or 0)
+    ctx = _dctx(ctx, values, stream)
     _check(ctx.lib.apmm_cu_quantize_pack(
         ctx.h, C.c_void_p(values.data_ptr()), rows, cols, n, int(gran),
         C.c_void_p(planes.data_ptr()), C.c_void_p(scales.data_ptr()),
         C.c_void_p(codes.data_ptr() if codes is not None else 0), _stream_ptr(stream)))
+
+
+def cu_dot_1bit_xor(a, b, k_logical: int, out, ctx: Context | None = None, stream=None) -> None:
+    """apmm_cu_dot_1bit_xor: out (int64 device tensor, 1 element) <- k - 2 popc(a ^ b)."""
+    ctx = _dctx(ctx, a, stream)
+    _check(ctx.lib.apmm_cu_dot_1bit_xor(ctx.h, C.c_void_p(a.data_ptr()), a.numel(),
+                                        C.c_void_p(b.data_ptr()), b.numel(), int(k_logical),
+                                        C.c_void_p(out.data_ptr()), _stream_ptr(stream)))
+
+
+def cu_matmul_ap_requant(w_planes, rows_w, n_w, w_scales, w_gran, x_planes, rows_x, n_x, x_scales,
+                         x_gran, k, n_next, next_gran, yf, next_planes=None, next_scales=None,
+                         absmax=None, ctx: Context | None = None, stream=None) -> None:
+    """matmul_ap -> dequant -> the next layer's quantize + pack (apmm_cu_matmul_ap_requant).
+    With `absmax` (device f64, rows_x or 1) the call stops after the GEMM and leaves the local
+    maxima there (N-sharded layers reduce them across ranks, then cu_requant_pack)."""
+    ctx = _dctx(ctx, w_planes, stream)
+
+    def p(t):
+        return C.c_void_p(t.data_ptr() if t is not None else 0)
+    _check(ctx.lib.apmm_cu_matmul_ap_requant(
+        ctx.h, p(w_planes), rows_w, n_w, p(w_scales), int(w_gran), p(x_planes), rows_x, n_x,
+        p(x_scales), int(x_gran), k, n_next, int(next_gran), p(yf), p(next_planes),
+        p(next_scales), p(absmax), _stream_ptr(stream)))
+
+
+def cu_requant_pack(yf, rows_w, rows_x, absmax, n_next, next_gran, next_planes, next_scales,
+                    ctx: Context | None = None, stream=None) -> None:
+    """apmm_cu_requant_pack: quantize + pack X' = yf^T with the given absmax."""
+    ctx = _dctx(ctx, yf, stream)
+    _check(ctx.lib.apmm_cu_requant_pack(
+        ctx.h, C.c_void_p(yf.data_ptr()), rows_w, rows_x, C.c_void_p(absmax.data_ptr()), n_next,
+        int(next_gran), C.c_void_p(next_planes.data_ptr()), C.c_void_p(next_scales.data_ptr()),
+        _stream_ptr(stream)))
+
+
+# ---- APMM v1 tensor files (tensor_file.hpp:12-64) -------------------------------------------
+class TensorKind(enum.IntEnum):
+    Float32 = 0
+    QuantizedBipolar = 1
+
+
+class _TensorInfo(C.Structure):
+    _fields_ = [("kind", C.c_int), ("bit_width", C.c_int), ("granularity", C.c_int),
+                ("rows", C.c_uint64), ("cols", C.c_uint64), ("scale_count", C.c_uint64),
+                ("payload_offset", C.c_uint64), ("payload_words", C.c_uint64)]
+
+
+@dataclass
+class TensorFile:
+    """tensor_file.hpp:41-64. Header validation and parsing run in the C library
+    (apmm_tensor_parse, the reference's checks and messages); the arrays are views of the
+    file bytes."""
+    kind: TensorKind
+    bit_width: int
+    granularity: int  # 0 per-tensor, 1 per-row, 0xFF for float
+    rows: int
+    cols: int
+    scales: np.ndarray
+    float_data: np.ndarray
+    packed: np.ndarray
+    _bytes: bytes = b""
+
+    def to_packed(self) -> PackedBitPlanes:
+        if self.kind != TensorKind.QuantizedBipolar:
+            raise ParseError("tensor file is not the quantized kind")
+        return PackedBitPlanes(self.rows, self.cols, BitWidth(self.bit_width), self.packed)
+
+    def to_real(self) -> np.ndarray:
+        if self.kind != TensorKind.Float32:
+            raise ParseError("tensor file is not the float32 kind")
+        return self.float_data.astype(np.float64).reshape(self.rows, self.cols)
+
+    def granularity_enum(self) -> Granularity:
+        if self.granularity in (0, 1):
+            return Granularity(self.granularity)
+        raise ParseError("tensor file carries no quantization granularity")
+
+    def cu_upload(self, ctx: Context | None = None, stream=None):
+        """Device copies straight from the file bytes (apmm_cu_tensor_upload): quantized ->
+        (planes int32 tensor, scales f64 tensor); float -> f64 values [rows, cols]."""
+        import torch
+        ctx = ctx or default_context(torch.cuda.current_device(), _stream_ptr(stream).value or 0)
+        dev = torch.device("cuda", ctx.device)
+        buf = np.frombuffer(self._bytes, dtype=np.uint8)
+        if self.kind == TensorKind.QuantizedBipolar:
+            planes = torch.empty(self.packed.size, dtype=torch.int32, device=dev)
+            scales = torch.empty(self.scales.size, dtype=torch.float64, device=dev)
+            _check(ctx.lib.apmm_cu_tensor_upload(ctx.h, _ptr(buf), buf.size,
+                                                 C.c_void_p(planes.data_ptr()),
+                                                 C.c_void_p(scales.data_ptr()), None,
+                                                 _stream_ptr(stream)))
+            return planes, scales
+        values = torch.empty((self.rows, self.cols), dtype=torch.float64, device=dev)
+        _check(ctx.lib.apmm_cu_tensor_upload(ctx.h, _ptr(buf), buf.size, None, None,
+                                             C.c_void_p(values.data_ptr()), _stream_ptr(stream)))
+        return values
+
+
+def parse_tensor(data: bytes) -> TensorFile:
+    """tensor_file.cpp:159-229 (validation in the C library)."""
+    data = bytes(data)
+    buf = np.frombuffer(data, dtype=np.uint8)
+    info = _TensorInfo()
+    _check(_lib.load().apmm_tensor_parse(_ptr(buf) if buf.size else None, buf.size,
+                                         C.byref(info)))
+    off = info.payload_offset
+    if info.kind == 1:
+        scales = np.frombuffer(data, dtype="<f8", count=info.scale_count, offset=16).copy()
+        packed = np.frombuffer(data, dtype="<u4", count=info.payload_words, offset=off).copy()
+        return TensorFile(TensorKind.QuantizedBipolar, info.bit_width, info.granularity,
+                          info.rows, info.cols, scales, np.empty(0, np.float32), packed, data)
+    floats = np.frombuffer(data, dtype="<f4", count=info.payload_words, offset=off).copy()
+    return TensorFile(TensorKind.Float32, 0, 0xFF, info.rows, info.cols, np.empty(0),
+                      floats, np.empty(0, np.uint32), data)
+
+
+def read_tensor_file(path) -> TensorFile:
+    """tensor_file.cpp:231- (IoError when unreadable)."""
+    try:
+        with open(path, "rb") as f:
+            data = f.read()
+    except OSError as e:
+        raise IoError(f"cannot open {path} for reading") from e
+    return parse_tensor(data)
+
+
+def serialize_tensor(t: TensorFile) -> bytes:
+    """tensor_file.cpp:135-157 for the quantized kind (apmm_tensor_serialize_quantized)."""
+    if t.kind != TensorKind.QuantizedBipolar:
+        raise InvalidArgument("only the quantized kind is serialized by this library")
+    lib = _lib.load()
+    sc = np.ascontiguousarray(t.scales, dtype=np.float64)
+    pk = np.ascontiguousarray(t.packed, dtype=np.uint32)
+    n = C.c_uint64()
+    _check(lib.apmm_tensor_serialize_quantized(t.rows, t.cols, t.bit_width, t.granularity,
+                                               _ptr(sc), _ptr(pk), None, 0, C.byref(n)))
+    out = np.empty(n.value, dtype=np.uint8)
+    _check(lib.apmm_tensor_serialize_quantized(t.rows, t.cols, t.bit_width, t.granularity,
+                                               _ptr(sc), _ptr(pk), _ptr(out), out.size,
+                                               C.byref(n)))
+    return out.tobytes()
+
+
+def load_tensor_file(path, ctx: Context | None = None):
+    """apmm_tensor_file_load: read + validate + upload into fresh device tensors (synchronous).
+    Returns (TensorKind, tensors...) like TensorFile.cu_upload."""
+    import torch
+    ctx = ctx or default_context(torch.cuda.current_device())
+    t = read_tensor_file(path)
+    dev = torch.device("cuda", ctx.device)
+    if t.kind == TensorKind.QuantizedBipolar:
+        planes = torch.empty(t.packed.size, dtype=torch.int32, device=dev)
+        scales = torch.empty(t.scales.size, dtype=torch.float64, device=dev)
+        _check(ctx.lib.apmm_tensor_file_load(ctx.h, str(path).encode(), None,
+                                             C.c_void_p(planes.data_ptr()),
+                                             C.c_void_p(scales.data_ptr()), None))
+        return t, planes, scales
+    values = torch.empty((t.rows, t.cols), dtype=torch.float64, device=dev)
+    _check(ctx.lib.apmm_tensor_file_load(ctx.h, str(path).encode(), None, None, None,
+                                         C.c_void_p(values.data_ptr())))
+    return t, values

@@ -1,8 +1,11 @@
 """Build libapmm_b200.so in-tree with nvcc for sm_100a (no JIT, no torch extension).
 
-    python -m paper_2409_17870_b200.build [--force] [--verbose]
+    python -m paper_2409_17870_b200.build [--force] [--verbose] [--dev]
 
-The shared library exports exactly the C ABI declared in include/apmm_cuda.h.
+The shared library exports exactly the C ABI declared in include/apmm_cuda.h. The release
+build reads no environment variables. `--dev` builds the same sources with
+-DAPMM_DEVTOOLS (plan dumps, per-phase timelines, ablations; csrc/internal.h) into
+devlib/libapmm_b200_dev.so, for the scripts/ probes via APMM_LIB -- never the product.
 """
 from __future__ import annotations
 
@@ -43,16 +46,21 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(d) <= t for d in deps())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and up_to_date():
+DEV_LIB = os.path.join(ROOT, "devlib", "libapmm_b200_dev.so")
+
+
+def build(force: bool = False, verbose: bool = False, dev: bool = False) -> str:
+    lib = DEV_LIB if dev else LIB
+    if not force and not dev and up_to_date():
         return LIB
-    objdir = os.path.join(PKG, "build")
+    objdir = os.path.join(PKG, "build_dev" if dev else "build")
+    os.makedirs(os.path.dirname(lib), exist_ok=True)
     os.makedirs(objdir, exist_ok=True)
     from concurrent.futures import ThreadPoolExecutor
 
     def compile_one(src):
         obj = os.path.join(objdir, os.path.basename(src) + ".o")
-        cmd = [NVCC] + NVCC_FLAGS + ["-c", src, "-o", obj]
+        cmd = [NVCC] + NVCC_FLAGS + (["-DAPMM_DEVTOOLS"] if dev else []) + ["-c", src, "-o", obj]
         return src, obj, subprocess.run(cmd, capture_output=True, text=True)
 
     objs = []
@@ -70,14 +78,15 @@ def build(force: bool = False, verbose: bool = False) -> str:
     vscript = os.path.join(objdir, "exports.map")
     with open(vscript, "w") as f:
         f.write("{ global: apmm_*; local: *; };\n")
-    cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", LIB] + objs + [
+    cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", lib] + objs + [
         "-Xlinker", f"--version-script={vscript}", "-lcudart_static", "-lrt", "-ldl", "-lpthread"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
         raise RuntimeError("nvcc link failed")
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="--verbose" in sys.argv))
+    print(build(force="--force" in sys.argv, verbose="--verbose" in sys.argv,
+                dev="--dev" in sys.argv))

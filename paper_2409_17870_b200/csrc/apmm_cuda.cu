@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -32,18 +33,24 @@ struct apmm_ctx {
   uint64_t launches = 0;
   // measurement: event pairs around launches of kernel class 0 (GEMM) / 1 (expand)
   bool timing = false;
-  bool force_single_sm = false;
+  int route = APMM_ROUTE_AUTO;  // APMM_OPT_ROUTE
+  bool early_w = true;          // APMM_OPT_EARLY_WEIGHT_READ
+  // stream binding (apmm_cuda.h, Conventions): the device entry points' stream
+  bool bound = false;
+  cudaStream_t bound_stream = nullptr;
+  int host_depth = 0;  // > 0 inside a synchronous host entry point
   int ws_half = 0;  // which half of the ping-pong workspace the next matmul uses
   void* sk_ws = nullptr;  // K5 split-K accumulators (zero between calls)
   size_t sk_ws_bytes = 0;
   void* sk_scratch = nullptr;  // K5 feature fragments (ping-pong halves) + weight repack
   size_t sk_scratch_bytes = 0;
-  bool force_tc = false;  // APMM_FORCE_TC=1: never use K5 (testing)
   bool dbg_waits = false;  // APMM_DEBUG_WAITS=1: MMA-issuer wait-cycle counters (dev only)
   void* dbg = nullptr;  // APMM_DEBUG_WAITS counters (dev only)
-  int* flags = nullptr;  // recover's device error flags (2 ints)
+  int* flags = nullptr;  // device error flags (recover: 2 ints; quantize / requant: 1)
   void* qx = nullptr;  // fused quantize: feature planes (skinny) / absmax + flag scratch
   size_t qx_bytes = 0;
+  void* rq = nullptr;  // requant: absmax scratch (ordered u32 bits, rows_x + 1)
+  size_t rq_bytes = 0;
   // host entry points' transfer pipeline: H2D / D2H copy streams and their events
   cudaStream_t s_in = nullptr, s_out = nullptr;
   cudaEvent_t pipe_ev[16] = {};
@@ -114,17 +121,32 @@ int check_matmul(int n_w, int n_x, uint64_t rows_w, uint64_t rows_x, uint64_t k)
   return APMM_OK;
 }
 
-int ensure(void** buf, size_t* have, size_t need, int device) {
+bool capturing(cudaStream_t s) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  return cudaStreamIsCapturing(s, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone;
+}
+
+// Grow a workspace buffer, stream-ordered on `s` (the only stream that uses it, by the
+// context's stream binding): the old buffer is released with cudaFreeAsync after the work
+// already enqueued on `s`, the new one comes from cudaMallocAsync -- no host or device-wide
+// synchronisation. Growth inside a stream capture is refused (reserve first).
+int ensure(void** buf, size_t* have, size_t need, int device, cudaStream_t s, bool zero = false) {
   if (need <= *have) return APMM_OK;
+  if (capturing(s)) {
+    return fail(APMM_E_INVALID_ARGUMENT,
+                "workspace must grow from %zu to %zu bytes while the stream is being captured; "
+                "call apmm_ctx_reserve with the largest shape before capturing",
+                *have, need);
+  }
   CU(cudaSetDevice(device));
   if (*buf) {
-    CU(cudaDeviceSynchronize());  // growth only: previous users of the buffer must finish
-    CU(cudaFree(*buf));
+    CU(cudaFreeAsync(*buf, s));
     *buf = nullptr;
     *have = 0;
   }
   const size_t sz = need + need / 4;
-  CU(cudaMalloc(buf, sz));
+  CU(cudaMallocAsync(buf, sz, s));
+  if (zero) CU(cudaMemsetAsync(*buf, 0, sz, s));
   *have = sz;
   return APMM_OK;
 }
@@ -196,52 +218,108 @@ struct TimedLaunch {
   }
 };
 
+// Kernel routes (apmm_cuda.h APMM_ROUTE_*). Every route computes the same bits.
+enum class Route { Skinny, Mid, Pair, PairW, PairSplit, Single };
+
+const char* route_name(Route r) {
+  switch (r) {
+    case Route::Skinny: return "skinny (K5)";
+    case Route::Mid: return "mid split-K (K3f)";
+    case Route::Pair: return "pair (K1 + K3)";
+    case Route::PairW: return "pair weight-planes (K3f)";
+    case Route::PairSplit: return "pair split-K (K1 + K3)";
+    default: return "single-SM (K1 + K3')";
+  }
+}
+
+// Which routes can serve a call (their layout / output constraints).
+struct RouteCaps {
+  bool skinny, mid, pair_w, pair_split;
+};
+RouteCaps caps_of(const uint32_t* w, uint64_t rows_x, uint64_t k, const void* y, bool dequant,
+                  bool x_ready) {
+  const bool splitk_out = !dequant && rows_x % 4 == 0 && reinterpret_cast<uintptr_t>(y) % 16 == 0;
+  RouteCaps c;
+  c.skinny = rows_x <= kSkinnyMaxRowsX && !x_ready;
+  c.mid = splitk_out && gemm_wplanes_addressable(w, k);
+  c.pair_w = gemm_wplanes_addressable(w, k);
+  c.pair_split = splitk_out;
+  return c;
+}
+
+// AUTO. CTA-pair 256x256 tiles (K3) when they fill the machine. Otherwise mid-size calls
+// (M_tok <= 256) take the split-K K3f: the weight planes are expanded on chip (each W row
+// once: a single N tile), rowsum(U_w) formed by the transform warps, K split across CTA
+// pairs, int32 partials TMA reduce-added into a Y zeroed by K1 (4096x128x4096 W2A4: 14.0 us
+// vs 18.3 us for K1 + the 1-SM GEMM; profiles/r01b_mid_size_v2.txt). Feature counts up to
+// kSkinnyPreferRows stay on K5 (faster there: 4096x40x4096 8.6 vs 12.6 us,
+// profiles/r01b_skinny_mid_boundary.txt), and K5 takes up to 63 rows when the split-K path
+// cannot (int32 output with a TMA-storable Y only). TENSOR_CORE = the same without K5.
+int pick_route(const apmm_ctx* ctx, const RouteCaps& c, uint64_t rows_w, uint64_t rows_x,
+               Route* out) {
+  const uint64_t pair_tiles = ((rows_w + 255) / 256) * ((rows_x + kPairN - 1) / kPairN);
+  const bool pair = pair_tiles >= static_cast<uint64_t>(ctx->num_sms / 2);
+  const bool mid = c.mid && !pair && rows_x <= 256;
+  auto forced = [&](bool ok, Route r) {
+    if (!ok) {
+      return fail(APMM_E_INVALID_ARGUMENT, "forced route %s cannot serve this call "
+                  "(%llu x %llu)", route_name(r), (unsigned long long)rows_w,
+                  (unsigned long long)rows_x);
+    }
+    *out = r;
+    return int(APMM_OK);
+  };
+  switch (ctx->route) {
+    case APMM_ROUTE_SKINNY: return forced(c.skinny, Route::Skinny);
+    case APMM_ROUTE_MID_SPLITK: return forced(c.mid, Route::Mid);
+    case APMM_ROUTE_PAIR: return forced(true, Route::Pair);
+    case APMM_ROUTE_PAIR_WPLANES: return forced(c.pair_w, Route::PairW);
+    case APMM_ROUTE_PAIR_SPLITK: return forced(c.pair_split, Route::PairSplit);
+    case APMM_ROUTE_SINGLE_SM: return forced(true, Route::Single);
+    default: break;
+  }
+  const bool allow_skinny = ctx->route != APMM_ROUTE_TENSOR_CORE;
+  if (allow_skinny && c.skinny && (rows_x <= kSkinnyPreferRows || !mid)) {
+    *out = Route::Skinny;
+  } else if (pair) {
+    *out = Route::Pair;
+  } else if (mid) {
+    *out = Route::Mid;
+  } else {
+    *out = Route::Single;
+  }
+  return APMM_OK;
+}
+
+// requant absmax scratch: rows_x u32 (+ 1 for the global max), 16-byte multiple (K1 zeroes it)
+uint64_t colmax_bytes(uint64_t rows_x) { return round_up((rows_x + 1) * 4, 16); }
+
+// Workspace a route needs for a call (growth is stream-ordered; see ensure()).
+int reserve_skinny(apmm_ctx* ctx, uint64_t rows_w, uint64_t rows_x, uint64_t k, int n_w,
+                   const void* w, cudaStream_t s) {
+  int st = ensure(&ctx->sk_ws, &ctx->sk_ws_bytes, skinny_acc_bytes(rows_w, rows_x), ctx->device,
+                  s, /*zero=*/true);  // split-K accumulators: zero at rest
+  if (st) return st;
+  return ensure(&ctx->sk_scratch, &ctx->sk_scratch_bytes,
+                skinny_scratch_bytes(rows_w, rows_x, k, n_w, w), ctx->device, s);
+}
+
 // x_ready: the feature operand is already in this call's workspace half as u8 codes +
 // rowsum (written by the fused quantize, K2 -> K3); then K1 expands W only and x is unused.
+// colmax (dequant only): per-column absmax of the f32 output (requant), or null.
 int run_matmul(apmm_ctx* ctx, const uint32_t* w, uint64_t rows_w, int n_w, const double* s_w,
                int gran_w, const uint32_t* x, uint64_t rows_x, int n_x, const double* s_x,
                int gran_x, uint64_t k, int32_t* y, float* yf, cudaStream_t stream,
-               bool x_ready = false) {
+               bool x_ready = false, unsigned* colmax = nullptr, bool colmax_global = false) {
   CU(cudaSetDevice(ctx->device));
-  // Route. CTA-pair 256x256 tiles (K3) when they fill the machine. Otherwise mid-size calls
-  // (M_tok <= 256) take the split-K K3f: the weight planes are expanded on chip (each W row
-  // once: a single N tile), rowsum(U_w) formed by the transform warps, K split across CTA
-  // pairs, int32 partials TMA reduce-added into a Y zeroed by K1 (4096x128x4096 W2A4: 14.0
-  // us vs 18.3 us for K1 + the 1-SM GEMM; profiles/r01b_mid_size_v2.txt). Feature counts up
-  // to kSkinnyPreferRows stay on K5 (faster there: 4096x40x4096 8.6 vs 12.6 us,
-  // profiles/r01b_skinny_mid_boundary.txt), and K5 takes up to 63 rows when the split-K
-  // path cannot (int32 output with a TMA-storable Y only). APMM_MID=0/1 forces the split-K
-  // path off/on, APMM_SKINNY_MAX moves the K5 boundary (testing).
-  const uint64_t pair_tiles = ((rows_w + 255) / 256) * ((rows_x + kPairN - 1) / kPairN);
-  const bool pair = pair_tiles >= static_cast<uint64_t>(ctx->num_sms / 2) && !ctx->force_single_sm;
-  const char* mid_env = std::getenv("APMM_MID");
-  const bool mid = (mid_env ? mid_env[0] == '1' : rows_x <= 256) && !pair &&
-                   !ctx->force_single_sm && !yf && rows_x > 0 && rows_x % 4 == 0 &&
-                   reinterpret_cast<uintptr_t>(y) % 16 == 0 && gemm_wplanes_addressable(w, k);
-  static const uint64_t skinny_prefer = [] {
-    const char* e = std::getenv("APMM_SKINNY_MAX");
-    return e ? static_cast<uint64_t>(std::atoll(e)) : kSkinnyPreferRows;
-  }();
-  const bool skinny = rows_x <= kSkinnyMaxRowsX && !ctx->force_tc && !x_ready &&
-                      (rows_x <= skinny_prefer || !mid);
-  if (skinny) {
+  const RouteCaps caps = caps_of(w, rows_x, k, yf ? static_cast<const void*>(yf) : y, yf != nullptr,
+                                 x_ready);
+  Route route;
+  int st = pick_route(ctx, caps, rows_w, rows_x, &route);
+  if (st) return st;
+  if (route == Route::Skinny) {
     // few feature rows: feature prep + K5, the weight planes streamed once from HBM
-    const size_t need = skinny_acc_bytes(rows_w, rows_x);
-    if (need > ctx->sk_ws_bytes) {  // split-K accumulators; zero at rest
-      if (ctx->sk_ws) {
-        CU(cudaDeviceSynchronize());
-        CU(cudaFree(ctx->sk_ws));
-        ctx->sk_ws = nullptr;
-        ctx->sk_ws_bytes = 0;
-      }
-      const size_t sz = need + need / 4;
-      CU(cudaMalloc(&ctx->sk_ws, sz));
-      CU(cudaMemset(ctx->sk_ws, 0, sz));
-      ctx->sk_ws_bytes = sz;
-    }
-    int st = ensure(&ctx->sk_scratch, &ctx->sk_scratch_bytes,
-                    skinny_scratch_bytes(rows_w, rows_x, k, n_w, w), ctx->device);
-    if (st) return st;
+    if ((st = reserve_skinny(ctx, rows_w, rows_x, k, n_w, w, stream))) return st;
     SkinnyArgs s{};
     s.w_planes = w;
     s.x_planes = x;
@@ -260,6 +338,7 @@ int run_matmul(apmm_ctx* ctx, const uint32_t* w, uint64_t rows_w, int n_w, const
     s.acc_ws = ctx->sk_ws;
     s.scratch_ws = ctx->sk_scratch;
     s.ws_half = ctx->ws_half;
+    s.early_w = ctx->early_w;
     ctx->ws_half ^= 1;
     {
       // kernel timing brackets the streaming kernel alone (not the feature-prep launch)
@@ -270,31 +349,33 @@ int run_matmul(apmm_ctx* ctx, const uint32_t* w, uint64_t rows_w, int n_w, const
       CU(launch_skinny(s, stream));
     }
     ctx->launches += rows_x <= 1 ? 1 : 2;  // (feature prep +) streaming kernel
+    if (colmax) {  // K5's epilogue does not form the column absmax: one pass over yf
+      CU(cudaMemsetAsync(colmax, 0, colmax_bytes(rows_x), stream));
+      CU(launch_colmax(yf, rows_w, rows_x, colmax, colmax_global, ctx->num_sms, stream));
+      ctx->launches += 1;
+    }
     return APMM_OK;
   }
-  int st = ensure(&ctx->ws, &ctx->ws_bytes, matmul_ws_bytes(rows_w, rows_x, k), ctx->device);
-  if (st) return st;
+  if ((st = ensure(&ctx->ws, &ctx->ws_bytes, matmul_ws_bytes(rows_w, rows_x, k), ctx->device,
+                   stream))) {
+    return st;
+  }
   const MatmulWs m = carve(ctx->ws, rows_w, rows_x, k, ctx->ws_half);
   ctx->ws_half ^= 1;
   const uint64_t rsx_pad = round_up(rows_x, kRowsumPad);
-  const bool fused = pair && gemm_fused_supported(w, k);
-  // Opt-in (APMM_PSPLIT=1): the u8-code pair GEMM with K split over the pairs (partials
-  // reduce-added into a Y zeroed by K1) for calls with too few pair tiles. Bit-exact, but
-  // measured slower than the 1-SM kernel for 256 < M_tok <= 1024 (4096x512x4096: 32.4 vs
-  // 20.3 us; profiles/r01b_pair_split_sweep.txt).
-  const char* ps_env = std::getenv("APMM_PSPLIT");
-  const bool psplit = ps_env != nullptr && ps_env[0] == '1' && !pair && !mid &&
-                      !ctx->force_single_sm && !yf && rows_x % 4 == 0 &&
-                      reinterpret_cast<uintptr_t>(y) % 16 == 0;
+  const bool wplanes = route == Route::Mid || route == Route::PairW;  // K3f expands W on chip
+  const bool zero_y = route == Route::Mid || route == Route::PairSplit;  // split-K reduce-adds
   {
     TimedLaunch t(ctx, 1, stream);
-    // mid (split-K K3f): W untouched (the GEMM expands it and forms rowsum(U_w) itself);
-    // K1 expands X and zeroes Y, which the split-K units reduce-add into
-    CU(launch_expand(w, mid ? 0 : rows_w, n_w, (fused || mid) ? nullptr : m.codes_w, m.rowsum_w,
-                     x_ready ? nullptr : x, x_ready ? 0 : rows_x, x_ready ? 0 : rsx_pad, n_x,
-                     m.codes_x, m.rowsum_x, k, m.kpad, ctx->num_sms, stream,
-                     (mid || psplit) ? static_cast<void*>(y) : nullptr,
-                     (mid || psplit) ? rows_w * rows_x * 4 : 0));
+    // K3f: W untouched by K1 except for rowsum(U_w) on the pair route (the split-K mid route
+    // forms it in the GEMM); split-K: K1 also zeroes Y, which the units reduce-add into
+    CU(launch_expand(w, route == Route::Mid ? 0 : rows_w, n_w, wplanes ? nullptr : m.codes_w,
+                     m.rowsum_w, x_ready ? nullptr : x, x_ready ? 0 : rows_x,
+                     x_ready ? 0 : rsx_pad, n_x, m.codes_x, m.rowsum_x, k, m.kpad, ctx->num_sms,
+                     stream,
+                     zero_y ? static_cast<void*>(y) : static_cast<void*>(colmax),
+                     zero_y ? rows_w * rows_x * 4 : (colmax ? colmax_bytes(rows_x) : 0),
+                     ctx->early_w));
   }
   ctx->launches += 1;
   GemmArgs a{};
@@ -315,6 +396,8 @@ int run_matmul(apmm_ctx* ctx, const uint32_t* w, uint64_t rows_w, int n_w, const
   a.s_x = s_x;
   a.gran_x = gran_x;
   a.num_sms = ctx->num_sms;
+  a.colmax = route == Route::PairW ? nullptr : colmax;
+  a.colmax_global = colmax_global;
   if (ctx->dbg_waits) {
     if (!ctx->dbg) {
       CU(cudaMalloc(&ctx->dbg, 128));
@@ -325,21 +408,74 @@ int run_matmul(apmm_ctx* ctx, const uint32_t* w, uint64_t rows_w, int n_w, const
   int launches = 0;
   {
     TimedLaunch t(ctx, 0, stream);
-    if (fused || mid) {
-      CU(launch_gemm_pair_wplanes(a, w, stream, &launches, /*split_k=*/mid));
-    } else if (pair || psplit) {
-      CU(launch_gemm_pair(a, stream, &launches, /*split_k=*/psplit));
-    } else {
-      CU(launch_gemm_tc(a, stream, &launches));
+    switch (route) {
+      case Route::Mid: CU(launch_gemm_pair_wplanes(a, w, stream, &launches, /*split_k=*/true)); break;
+      case Route::PairW: CU(launch_gemm_pair_wplanes(a, w, stream, &launches, false)); break;
+      case Route::Pair: CU(launch_gemm_pair(a, stream, &launches, false)); break;
+      case Route::PairSplit: CU(launch_gemm_pair(a, stream, &launches, /*split_k=*/true)); break;
+      default: CU(launch_gemm_tc(a, stream, &launches)); break;
     }
   }
   ctx->launches += static_cast<uint64_t>(launches);
+  if (colmax && route == Route::PairW) {  // K3f's epilogue does not form the column absmax
+    CU(launch_colmax(yf, rows_w, rows_x, colmax, colmax_global, ctx->num_sms, stream));
+    ctx->launches += 1;
+  }
   return APMM_OK;
 }
 
 // Device entry points run on exactly the stream they are given (NULL = the legacy default
-// stream, as everywhere in CUDA); only the host entry points use the context's stream.
-cudaStream_t pick(apmm_ctx* /*ctx*/, apmm_stream_t s) { return reinterpret_cast<cudaStream_t>(s); }
+// stream, as everywhere in CUDA), which must be the context's bound stream: the workspace
+// is shared by every call of the context, so two streams would race on it
+// (apmm_cuda.h, Conventions). The first device call binds; the host entry points run on
+// ctx->stream after draining the bound stream, and skip the check for their inner calls.
+int bind(apmm_ctx* ctx, apmm_stream_t st, cudaStream_t* out) {
+  const cudaStream_t s = reinterpret_cast<cudaStream_t>(st);
+  *out = s;
+  if (ctx->host_depth > 0) return APMM_OK;
+  if (!ctx->bound) {
+    ctx->bound = true;
+    ctx->bound_stream = s;
+    return APMM_OK;
+  }
+  if (ctx->bound_stream != s) {
+    return fail(APMM_E_INVALID_ARGUMENT,
+                "context is bound to stream %p but was called on stream %p: use one context per "
+                "stream, or rebind with apmm_ctx_set_stream once the old stream's work is ordered",
+                static_cast<void*>(ctx->bound_stream), static_cast<void*>(s));
+  }
+  return APMM_OK;
+}
+
+// Scope of a synchronous host entry point: drains device work enqueued on the bound stream
+// (it shares the workspace) and runs the inner device calls on ctx->stream.
+struct HostCall {
+  apmm_ctx* ctx;
+  int status = APMM_OK;
+  explicit HostCall(apmm_ctx* c) : ctx(c) {
+    if (!ctx) return;
+    ++ctx->host_depth;
+    cudaSetDevice(ctx->device);
+    if (ctx->bound && ctx->bound_stream != ctx->stream) {
+      const cudaError_t e = cudaStreamSynchronize(ctx->bound_stream);
+      if (e != cudaSuccess) status = cuda_fail(e, "cudaStreamSynchronize(bound stream)");
+    }
+  }
+  ~HostCall() {
+    if (ctx) --ctx->host_depth;
+  }
+};
+
+#define HOST_CALL(ctx)                          \
+  HostCall host_call_(ctx);                     \
+  if (host_call_.status) return host_call_.status
+
+// Small per-context device scratch (ctx->flags, 64 bytes): [0..1] recover flags,
+// [2] quantize non-finite flag, bytes 32..39 the per-tensor absmax bits.
+int* quant_flag(apmm_ctx* ctx) { return ctx->flags + 2; }
+unsigned long long* quant_amax(apmm_ctx* ctx) {
+  return reinterpret_cast<unsigned long long*>(reinterpret_cast<uint8_t*>(ctx->flags) + 32);
+}
 
 // Host-side PackedBitPlanes invariants (bitplane.cpp:17-32).
 int check_padding(const uint32_t* planes, uint64_t rows, uint64_t cols, int n) {
@@ -405,13 +541,13 @@ int apmm_ctx_create(apmm_ctx** out, int device) {
   auto* ctx = new apmm_ctx();
   ctx->device = device;
   ctx->num_sms = prop.multiProcessorCount;
-  if (const char* f = std::getenv("APMM_FORCE_1SM")) ctx->force_single_sm = f[0] == '1';
-  if (const char* f = std::getenv("APMM_DEBUG_WAITS")) ctx->dbg_waits = f[0] == '1';
-  if (const char* f = std::getenv("APMM_FORCE_TC")) ctx->force_tc = f[0] == '1';
+  if (const char* f = APMM_DEV_ENV("APMM_DEBUG_WAITS")) ctx->dbg_waits = f[0] == '1';
   cudaError_t e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaMalloc(&ctx->flags, 64);
   if (e != cudaSuccess) {
+    if (ctx->stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
-    return cuda_fail(e, "cudaStreamCreate");
+    return cuda_fail(e, "context setup");
   }
   ctx->own_stream = true;
   *out = ctx;
@@ -421,7 +557,9 @@ int apmm_ctx_create(apmm_ctx** out, int device) {
 int apmm_ctx_destroy(apmm_ctx* ctx) {
   if (!ctx) return APMM_OK;
   cudaSetDevice(ctx->device);
-  cudaDeviceSynchronize();
+  // the context's work is on its bound stream and its own streams
+  if (ctx->bound) cudaStreamSynchronize(ctx->bound_stream);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   if (ctx->dbg) {
     unsigned long long h[16] = {};
     cudaMemcpy(h, ctx->dbg, sizeof(h), cudaMemcpyDeviceToHost);
@@ -442,6 +580,7 @@ int apmm_ctx_destroy(apmm_ctx* ctx) {
   }
   if (ctx->flags) cudaFree(ctx->flags);
   if (ctx->qx) cudaFree(ctx->qx);
+  if (ctx->rq) cudaFree(ctx->rq);
   if (ctx->ws) cudaFree(ctx->ws);
   if (ctx->sk_ws) cudaFree(ctx->sk_ws);
   if (ctx->sk_scratch) cudaFree(ctx->sk_scratch);
@@ -464,9 +603,67 @@ int apmm_ctx_destroy(apmm_ctx* ctx) {
 
 int apmm_ctx_set_stream(apmm_ctx* ctx, apmm_stream_t stream) {
   if (!ctx) return fail(APMM_E_INVALID_ARGUMENT, "null context");
-  if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+  CU(cudaSetDevice(ctx->device));
+  if (ctx->own_stream && ctx->stream) {
+    CU(cudaStreamSynchronize(ctx->stream));
+    cudaStreamDestroy(ctx->stream);
+  }
   ctx->stream = reinterpret_cast<cudaStream_t>(stream);
   ctx->own_stream = false;
+  ctx->bound = true;
+  ctx->bound_stream = ctx->stream;
+  return APMM_OK;
+}
+
+int apmm_ctx_set_option(apmm_ctx* ctx, int option, int value) {
+  if (!ctx) return fail(APMM_E_INVALID_ARGUMENT, "null context");
+  switch (option) {
+    case APMM_OPT_ROUTE:
+      if (value < APMM_ROUTE_AUTO || value > APMM_ROUTE_TENSOR_CORE) {
+        return fail(APMM_E_INVALID_ARGUMENT, "unknown route %d", value);
+      }
+      ctx->route = value;
+      return APMM_OK;
+    case APMM_OPT_EARLY_WEIGHT_READ:
+      ctx->early_w = value != 0;
+      return APMM_OK;
+    default:
+      return fail(APMM_E_INVALID_ARGUMENT, "unknown option %d", option);
+  }
+}
+
+int apmm_ctx_get_option(const apmm_ctx* ctx, int option, int* value) {
+  if (!ctx || !value) return fail(APMM_E_INVALID_ARGUMENT, "null argument");
+  switch (option) {
+    case APMM_OPT_ROUTE: *value = ctx->route; return APMM_OK;
+    case APMM_OPT_EARLY_WEIGHT_READ: *value = ctx->early_w ? 1 : 0; return APMM_OK;
+    default: return fail(APMM_E_INVALID_ARGUMENT, "unknown option %d", option);
+  }
+}
+
+int apmm_ctx_reserve(apmm_ctx* ctx, uint64_t rows_w, uint64_t rows_x, uint64_t k, int n_w) {
+  int st;
+  if (!ctx) return fail(APMM_E_INVALID_ARGUMENT, "null context");
+  if ((st = check_width(n_w)) || (st = check_dims(rows_w, k, "weights")) ||
+      (st = check_dims(rows_x, k, "features"))) {
+    return st;
+  }
+  const cudaStream_t s = ctx->bound ? ctx->bound_stream : ctx->stream;
+  if ((st = ensure(&ctx->ws, &ctx->ws_bytes, matmul_ws_bytes(rows_w, rows_x, k), ctx->device, s))) {
+    return st;
+  }
+  if (rows_x <= kSkinnyMaxRowsX) {
+    // worst case: a weight buffer that needs the 16-byte repack
+    if ((st = reserve_skinny(ctx, rows_w, rows_x, k, n_w, reinterpret_cast<const void*>(4), s))) {
+      return st;
+    }
+  }
+  if ((st = ensure(&ctx->qx, &ctx->qx_bytes, apmm_packed_words(8, rows_x, k) * 4 + 64, ctx->device,
+                   s))) {
+    return st;
+  }
+  if ((st = ensure(&ctx->rq, &ctx->rq_bytes, (rows_x + 1) * 4, ctx->device, s))) return st;
+  CU(cudaStreamSynchronize(s));
   return APMM_OK;
 }
 
@@ -515,8 +712,10 @@ int apmm_cu_pack(apmm_ctx* ctx, const uint8_t* codes, uint64_t rows, uint64_t co
   int st;
   if (!ctx || !codes || !planes) return fail(APMM_E_INVALID_ARGUMENT, "null argument");
   if ((st = check_width(n)) || (st = check_dims(rows, cols, "CodeMatrix"))) return st;
+  cudaStream_t s;
+  if ((st = bind(ctx, stream, &s))) return st;
   CU(cudaSetDevice(ctx->device));
-  CU(launch_pack(codes, rows, cols, n, planes, pick(ctx, stream)));
+  CU(launch_pack(codes, rows, cols, n, planes, s));
   ctx->launches += 1;
   return APMM_OK;
 }
@@ -526,8 +725,10 @@ int apmm_cu_unpack(apmm_ctx* ctx, const uint32_t* planes, uint64_t rows, uint64_
   int st;
   if (!ctx || !codes || !planes) return fail(APMM_E_INVALID_ARGUMENT, "null argument");
   if ((st = check_width(n)) || (st = check_dims(rows, cols, "PackedBitPlanes"))) return st;
+  cudaStream_t s;
+  if ((st = bind(ctx, stream, &s))) return st;
   CU(cudaSetDevice(ctx->device));
-  CU(launch_unpack(planes, rows, cols, n, codes, pick(ctx, stream)));
+  CU(launch_unpack(planes, rows, cols, n, codes, s));
   ctx->launches += 1;
   return APMM_OK;
 }
@@ -539,12 +740,11 @@ int apmm_cu_quantize_pack(apmm_ctx* ctx, const double* values, uint64_t rows, ui
   if (!ctx || !values || !planes || !scales) return fail(APMM_E_INVALID_ARGUMENT, "null argument");
   if (!valid_gran(granularity)) return fail(APMM_E_INVALID_ARGUMENT, "bad granularity");
   if ((st = check_width(n)) || (st = check_dims(rows, cols, "RealMatrix"))) return st;
-  // scratch: amax bits + flag live past the matmul region of the workspace
-  if ((st = ensure(&ctx->ws, &ctx->ws_bytes, 64, ctx->device))) return st;
+  cudaStream_t s;
+  if ((st = bind(ctx, stream, &s))) return st;
   CU(cudaSetDevice(ctx->device));
-  auto* amax = static_cast<unsigned long long*>(ctx->ws);
-  int* flag = reinterpret_cast<int*>(static_cast<uint8_t*>(ctx->ws) + 16);
-  const cudaStream_t s = pick(ctx, stream);
+  unsigned long long* amax = quant_amax(ctx);
+  int* flag = quant_flag(ctx);
   CU(launch_quantize_pack(values, rows, cols, n, granularity, planes, scales, codes, amax, flag, s));
   ctx->launches += granularity == APMM_PER_ROW ? 1 : 2;
   int h_flag = 0;
@@ -560,8 +760,10 @@ int apmm_cu_matmul_ap(apmm_ctx* ctx, const uint32_t* w_planes, uint64_t rows_w, 
   if (!ctx || !w_planes || !x_planes || !y) return fail(APMM_E_INVALID_ARGUMENT, "null argument");
   int st = check_matmul(n_w, n_x, rows_w, rows_x, k);
   if (st) return st;
+  cudaStream_t s;
+  if ((st = bind(ctx, stream, &s))) return st;
   return run_matmul(ctx, w_planes, rows_w, n_w, nullptr, 0, x_planes, rows_x, n_x, nullptr, 0, k,
-                    y, nullptr, pick(ctx, stream));
+                    y, nullptr, s);
 }
 
 int apmm_cu_matmul_ap_dequant(apmm_ctx* ctx, const uint32_t* w_planes, uint64_t rows_w,
@@ -577,8 +779,10 @@ int apmm_cu_matmul_ap_dequant(apmm_ctx* ctx, const uint32_t* w_planes, uint64_t 
   }
   int st = check_matmul(n_w, n_x, rows_w, rows_x, k);
   if (st) return st;
+  cudaStream_t s;
+  if ((st = bind(ctx, stream, &s))) return st;
   return run_matmul(ctx, w_planes, rows_w, n_w, w_scales, w_granularity, x_planes, rows_x, n_x,
-                    x_scales, x_granularity, k, nullptr, out, pick(ctx, stream));
+                    x_scales, x_granularity, k, nullptr, out, s);
 }
 
 int apmm_cu_matmul_plane_pair(apmm_ctx* ctx, const uint32_t* w_planes, uint64_t rows_w, int n_w,
@@ -595,10 +799,12 @@ int apmm_cu_matmul_plane_pair(apmm_ctx* ctx, const uint32_t* w_planes, uint64_t 
   // one plane of a packed buffer is itself a 1-bit packed buffer; a 1-bit x 1-bit matmul_ap
   // is exactly the XOR dot  K - 2 popc(a ^ b)  of kernel.cpp:115-144 (v = 2u - 1 = +-1)
   if ((st = check_matmul(1, 1, rows_w, rows_x, k))) return st;
+  cudaStream_t s;
+  if ((st = bind(ctx, stream, &s))) return st;
   const uint64_t wpr = (k + 31) / 32;
   return run_matmul(ctx, w_planes + uint64_t(weight_plane) * rows_w * wpr, rows_w, 1, nullptr, 0,
                     x_planes + uint64_t(feature_plane) * rows_x * wpr, rows_x, 1, nullptr, 0, k,
-                    y, nullptr, pick(ctx, stream));
+                    y, nullptr, s);
 }
 
 int apmm_cu_compute_plane_products(apmm_ctx* ctx, const uint32_t* w_planes, uint64_t rows_w,
@@ -622,9 +828,9 @@ int apmm_cu_recover(apmm_ctx* ctx, const int32_t* stack, int n_w, int n_x, uint6
   int st;
   if (!ctx || !stack || !y) return fail(APMM_E_INVALID_ARGUMENT, "null argument");
   if ((st = check_width(n_w)) || (st = check_width(n_x))) return st;
+  cudaStream_t s;
+  if ((st = bind(ctx, stream, &s))) return st;
   CU(cudaSetDevice(ctx->device));
-  if (!ctx->flags) CU(cudaMalloc(&ctx->flags, 2 * sizeof(int)));
-  const cudaStream_t s = pick(ctx, stream);
   CU(cudaMemsetAsync(ctx->flags, 0, 2 * sizeof(int), s));
   CU(launch_recover(stack, n_w, n_x, rows * cols, k, y, ctx->flags, s));
   ctx->launches += 1;
@@ -650,13 +856,15 @@ int apmm_cu_quantize_matmul_ap_dequant(apmm_ctx* ctx, const uint32_t* w_planes, 
   }
   if ((st = check_width(n_w)) || (st = check_width(n_x))) return st;
   if ((st = check_dims(rows_x, k, "RealMatrix")) || (st = check_dims(rows_w, k, "weights"))) return st;
+  cudaStream_t s;
+  if ((st = bind(ctx, stream, &s))) return st;
   CU(cudaSetDevice(ctx->device));
-  const cudaStream_t s = pick(ctx, stream);
-  if (rows_x <= kSkinnyMaxRowsX && !ctx->force_tc) {
+  if (rows_x <= kSkinnyMaxRowsX && ctx->route != APMM_ROUTE_TENSOR_CORE &&
+      (ctx->route == APMM_ROUTE_AUTO || ctx->route == APMM_ROUTE_SKINNY)) {
     // few feature rows: the skinny kernel consumes planes -> quantize_pack into a scratch
     // plane buffer, then the ordinary device matmul (both stream-ordered)
     const size_t words = apmm_packed_words(n_x, rows_x, k);
-    if ((st = ensure(&ctx->qx, &ctx->qx_bytes, words * 4 + 64, ctx->device))) return st;
+    if ((st = ensure(&ctx->qx, &ctx->qx_bytes, words * 4 + 64, ctx->device, s))) return st;
     uint32_t* xp = static_cast<uint32_t*>(ctx->qx);
     if ((st = apmm_cu_quantize_pack(ctx, x_values, rows_x, k, n_x, x_granularity, xp, x_scales,
                                     nullptr, stream))) {
@@ -668,11 +876,13 @@ int apmm_cu_quantize_matmul_ap_dequant(apmm_ctx* ctx, const uint32_t* w_planes, 
   }
   // K2 -> K3: quantize straight into this call's workspace half (u8 codes in K1's layout +
   // rowsum(U_x)); K1 then expands W only. The feature planes never exist.
-  if ((st = ensure(&ctx->ws, &ctx->ws_bytes, matmul_ws_bytes(rows_w, rows_x, k), ctx->device))) return st;
-  if ((st = ensure(&ctx->qx, &ctx->qx_bytes, 64, ctx->device))) return st;
+  if ((st = ensure(&ctx->ws, &ctx->ws_bytes, matmul_ws_bytes(rows_w, rows_x, k), ctx->device,
+                   s))) {
+    return st;
+  }
   const MatmulWs m = carve(ctx->ws, rows_w, rows_x, k, ctx->ws_half);
-  auto* amax = static_cast<unsigned long long*>(ctx->qx);
-  int* flag = reinterpret_cast<int*>(static_cast<uint8_t*>(ctx->qx) + 16);
+  unsigned long long* amax = quant_amax(ctx);
+  int* flag = quant_flag(ctx);
   CU(launch_quantize_pack(x_values, rows_x, k, n_x, x_granularity, nullptr, x_scales, nullptr,
                           amax, flag, s, m.codes_x, m.rowsum_x, m.kpad, round_up(rows_x, kRowsumPad)));
   ctx->launches += x_granularity == APMM_PER_ROW ? 1 : 2;
@@ -685,18 +895,106 @@ int apmm_cu_quantize_matmul_ap_dequant(apmm_ctx* ctx, const uint32_t* w_planes, 
                     x_scales, x_granularity, k, nullptr, out, s, /*x_ready=*/true);
 }
 
+int apmm_cu_dot_1bit_xor(apmm_ctx* ctx, const uint32_t* a, uint64_t a_words, const uint32_t* b,
+                         uint64_t b_words, uint64_t k, int64_t* out, apmm_stream_t stream) {
+  if (!ctx || !a || !b || !out) return fail(APMM_E_INVALID_ARGUMENT, "null argument");
+  // kernel.cpp:117-121, same order and messages
+  if (k == 0) return fail(APMM_E_OUT_OF_RANGE, "k_logical must be positive");
+  const uint64_t need = (k + 31) / 32;
+  if (a_words != need || b_words != need) {
+    return fail(APMM_E_LENGTH_MISMATCH, "word sequences must hold exactly ceil(k/32) words");
+  }
+  int st;
+  cudaStream_t s;
+  if ((st = bind(ctx, stream, &s))) return st;
+  CU(cudaSetDevice(ctx->device));
+  CU(launch_dot_xor(a, b, need, k, out, s));
+  ctx->launches += 1;
+  return APMM_OK;
+}
+
+int apmm_cu_matmul_ap_requant(apmm_ctx* ctx, const uint32_t* w_planes, uint64_t rows_w, int n_w,
+                              const double* w_scales, int w_granularity, const uint32_t* x_planes,
+                              uint64_t rows_x, int n_x, const double* x_scales, int x_granularity,
+                              uint64_t k, int n_next, int next_granularity, float* yf,
+                              uint32_t* next_planes, double* next_scales, double* absmax,
+                              apmm_stream_t stream) {
+  if (!ctx || !w_planes || !x_planes || !w_scales || !x_scales || !yf) {
+    return fail(APMM_E_INVALID_ARGUMENT, "null argument");
+  }
+  if (!absmax && (!next_planes || !next_scales)) return fail(APMM_E_INVALID_ARGUMENT, "null argument");
+  if (!valid_gran(w_granularity) || !valid_gran(x_granularity) || !valid_gran(next_granularity)) {
+    return fail(APMM_E_INVALID_ARGUMENT, "bad granularity");
+  }
+  int st;
+  if ((st = check_width(n_next))) return st;
+  if ((st = check_matmul(n_w, n_x, rows_w, rows_x, k))) return st;
+  cudaStream_t s;
+  if ((st = bind(ctx, stream, &s))) return st;
+  CU(cudaSetDevice(ctx->device));
+  if ((st = ensure(&ctx->rq, &ctx->rq_bytes, colmax_bytes(rows_x), ctx->device, s))) return st;
+  const bool global = next_granularity == APMM_PER_TENSOR;
+  unsigned* colmax = static_cast<unsigned*>(ctx->rq);
+  if ((st = run_matmul(ctx, w_planes, rows_w, n_w, w_scales, w_granularity, x_planes, rows_x, n_x,
+                       x_scales, x_granularity, k, nullptr, yf, s, false, colmax, global))) {
+    return st;
+  }
+  if (absmax) {  // split form: hand out the local maxima (as doubles) for a cross-GPU max
+    CU(launch_bits_to_double(colmax, global ? 1 : rows_x, absmax, s));
+    ctx->launches += 1;
+    return APMM_OK;
+  }
+  CU(cudaMemsetAsync(quant_flag(ctx), 0, sizeof(int), s));
+  CU(launch_requant_pack(yf, rows_w, rows_x, colmax, global, n_next, next_planes, next_scales,
+                         quant_flag(ctx), s));
+  ctx->launches += 1;
+  int h_flag = 0;  // the reference's quantize throws NonFinite (bipolar.cpp:73-75)
+  CU(cudaMemcpyAsync(&h_flag, quant_flag(ctx), sizeof(int), cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  if (h_flag) return fail(APMM_E_NON_FINITE, "input contains NaN or infinity");
+  return APMM_OK;
+}
+
+int apmm_cu_requant_pack(apmm_ctx* ctx, const float* yf, uint64_t rows_w, uint64_t rows_x,
+                         const double* absmax, int n_next, int next_granularity,
+                         uint32_t* next_planes, double* next_scales, apmm_stream_t stream) {
+  if (!ctx || !yf || !absmax || !next_planes || !next_scales) {
+    return fail(APMM_E_INVALID_ARGUMENT, "null argument");
+  }
+  if (!valid_gran(next_granularity)) return fail(APMM_E_INVALID_ARGUMENT, "bad granularity");
+  int st;
+  if ((st = check_width(n_next)) || (st = check_dims(rows_x, rows_w, "RealMatrix"))) return st;
+  cudaStream_t s;
+  if ((st = bind(ctx, stream, &s))) return st;
+  CU(cudaSetDevice(ctx->device));
+  if ((st = ensure(&ctx->rq, &ctx->rq_bytes, colmax_bytes(rows_x), ctx->device, s))) return st;
+  const bool global = next_granularity == APMM_PER_TENSOR;
+  unsigned* colmax = static_cast<unsigned*>(ctx->rq);
+  CU(launch_double_to_bits(absmax, global ? 1 : rows_x, colmax, s));
+  CU(cudaMemsetAsync(quant_flag(ctx), 0, sizeof(int), s));
+  CU(launch_requant_pack(yf, rows_w, rows_x, colmax, global, n_next, next_planes, next_scales,
+                         quant_flag(ctx), s));
+  ctx->launches += 2;
+  int h_flag = 0;
+  CU(cudaMemcpyAsync(&h_flag, quant_flag(ctx), sizeof(int), cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  if (h_flag) return fail(APMM_E_NON_FINITE, "input contains NaN or infinity");
+  return APMM_OK;
+}
+
 // ---- host entry points ------------------------------------------------------------------
 int apmm_decompose_and_pack(apmm_ctx* ctx, const uint8_t* codes, uint64_t rows, uint64_t cols,
                             int n, uint32_t* planes) {
   int st;
   if (!ctx || !codes || !planes) return fail(APMM_E_INVALID_ARGUMENT, "null argument");
+  HOST_CALL(ctx);
   if ((st = check_width(n)) || (st = check_dims(rows, cols, "CodeMatrix"))) return st;
   const uint32_t limit = 1u << n;
   for (uint64_t e = 0; e < rows * cols; ++e) {  // CodeMatrix ctor (bipolar.cpp:33-36)
     if (codes[e] >= limit) return fail(APMM_E_OUT_OF_RANGE, "code has bits above position n-1");
   }
   const size_t in_b = align_up(rows * cols), out_b = apmm_packed_words(n, rows, cols) * 4;
-  if ((st = ensure(&ctx->io, &ctx->io_bytes, in_b + out_b, ctx->device))) return st;
+  if ((st = ensure(&ctx->io, &ctx->io_bytes, in_b + out_b, ctx->device, ctx->stream))) return st;
   uint8_t* d_codes = static_cast<uint8_t*>(ctx->io);
   uint32_t* d_planes = reinterpret_cast<uint32_t*>(d_codes + in_b);
   CU(cudaMemcpyAsync(d_codes, codes, rows * cols, cudaMemcpyHostToDevice, ctx->stream));
@@ -710,10 +1008,11 @@ int apmm_unpack(apmm_ctx* ctx, const uint32_t* planes, uint64_t rows, uint64_t c
                 uint8_t* codes) {
   int st;
   if (!ctx || !codes || !planes) return fail(APMM_E_INVALID_ARGUMENT, "null argument");
+  HOST_CALL(ctx);
   if ((st = check_width(n)) || (st = check_dims(rows, cols, "PackedBitPlanes"))) return st;
   if ((st = check_padding(planes, rows, cols, n))) return st;
   const size_t in_b = align_up(apmm_packed_words(n, rows, cols) * 4), out_b = rows * cols;
-  if ((st = ensure(&ctx->io, &ctx->io_bytes, in_b + out_b, ctx->device))) return st;
+  if ((st = ensure(&ctx->io, &ctx->io_bytes, in_b + out_b, ctx->device, ctx->stream))) return st;
   uint32_t* d_planes = static_cast<uint32_t*>(ctx->io);
   uint8_t* d_codes = static_cast<uint8_t*>(ctx->io) + in_b;
   CU(cudaMemcpyAsync(d_planes, planes, apmm_packed_words(n, rows, cols) * 4,
@@ -728,12 +1027,13 @@ int apmm_quantize_pack(apmm_ctx* ctx, const double* values, uint64_t rows, uint6
                        int granularity, uint8_t* codes, uint32_t* planes, double* scales) {
   int st;
   if (!ctx || !values || !planes || !scales) return fail(APMM_E_INVALID_ARGUMENT, "null argument");
+  HOST_CALL(ctx);
   if (!valid_gran(granularity)) return fail(APMM_E_INVALID_ARGUMENT, "bad granularity");
   if ((st = check_width(n)) || (st = check_dims(rows, cols, "RealMatrix"))) return st;
   const uint64_t n_scales = granularity == APMM_PER_ROW ? rows : 1;
   const size_t x_b = align_up(rows * cols * 8), p_b = align_up(apmm_packed_words(n, rows, cols) * 4);
   const size_t s_b = align_up(n_scales * 8), c_b = align_up(rows * cols);
-  if ((st = ensure(&ctx->io, &ctx->io_bytes, x_b + p_b + s_b + c_b, ctx->device))) return st;
+  if ((st = ensure(&ctx->io, &ctx->io_bytes, x_b + p_b + s_b + c_b, ctx->device, ctx->stream))) return st;
   uint8_t* base = static_cast<uint8_t*>(ctx->io);
   double* d_x = reinterpret_cast<double*>(base);
   uint32_t* d_p = reinterpret_cast<uint32_t*>(base + x_b);
@@ -761,6 +1061,7 @@ static int host_matmul(apmm_ctx* ctx, const uint32_t* w, uint64_t rows_w, int n_
                        const double* s_w, int gran_w, const uint32_t* x, uint64_t rows_x,
                        int n_x, const double* s_x, int gran_x, uint64_t k, int32_t* y,
                        float* yf) {
+  HOST_CALL(ctx);
   int st;
   if ((st = check_width(n_w)) || (st = check_width(n_x))) return st;
   if ((st = check_dims(rows_w, k, "weights")) || (st = check_dims(rows_x, k, "features"))) {
@@ -776,7 +1077,7 @@ static int host_matmul(apmm_ctx* ctx, const uint32_t* w, uint64_t rows_w, int n_
   const size_t y_b = align_up(rows_w * rows_x * 4);
   const size_t sw_n = gran_w == APMM_PER_ROW ? rows_w : 1, sx_n = gran_x == APMM_PER_ROW ? rows_x : 1;
   const size_t sw_b = yf ? align_up(sw_n * 8) : 0, sx_b = yf ? align_up(sx_n * 8) : 0;
-  if ((st = ensure(&ctx->io, &ctx->io_bytes, w_b + x_b + y_b + sw_b + sx_b, ctx->device))) return st;
+  if ((st = ensure(&ctx->io, &ctx->io_bytes, w_b + x_b + y_b + sw_b + sx_b, ctx->device, ctx->stream))) return st;
   CU(cudaSetDevice(ctx->device));
   if (!ctx->s_in) {
     CU(cudaStreamCreateWithFlags(&ctx->s_in, cudaStreamNonBlocking));
@@ -837,6 +1138,7 @@ int apmm_compute_plane_products(apmm_ctx* ctx, const uint32_t* w_planes, uint64_
                                 uint64_t k, int32_t* stack) {
   int st;
   if (!ctx || !w_planes || !x_planes || !stack) return fail(APMM_E_INVALID_ARGUMENT, "null argument");
+  HOST_CALL(ctx);
   if ((st = check_width(n_w)) || (st = check_width(n_x))) return st;
   if ((st = check_dims(rows_w, k, "weights")) || (st = check_dims(rows_x, k, "features"))) return st;
   if ((st = check_padding(w_planes, rows_w, k, n_w)) || (st = check_padding(x_planes, rows_x, k, n_x))) {
@@ -846,7 +1148,7 @@ int apmm_compute_plane_products(apmm_ctx* ctx, const uint32_t* w_planes, uint64_
   const size_t w_words = apmm_packed_words(n_w, rows_w, k), x_words = apmm_packed_words(n_x, rows_x, k);
   const size_t w_b = align_up(w_words * 4), x_b = align_up(x_words * 4);
   const size_t s_n = size_t(n_w) * n_x * rows_w * rows_x;
-  if ((st = ensure(&ctx->io, &ctx->io_bytes, w_b + x_b + align_up(s_n * 4), ctx->device))) return st;
+  if ((st = ensure(&ctx->io, &ctx->io_bytes, w_b + x_b + align_up(s_n * 4), ctx->device, ctx->stream))) return st;
   CU(cudaSetDevice(ctx->device));
   uint8_t* base = static_cast<uint8_t*>(ctx->io);
   uint32_t* d_w = reinterpret_cast<uint32_t*>(base);
@@ -867,10 +1169,11 @@ int apmm_recover(apmm_ctx* ctx, const int32_t* stack, int n_w, int n_x, uint64_t
                  uint64_t rows, uint64_t cols, int32_t* y) {
   int st;
   if (!ctx || !stack || !y) return fail(APMM_E_INVALID_ARGUMENT, "null argument");
+  HOST_CALL(ctx);
   if ((st = check_width(n_w)) || (st = check_width(n_x))) return st;
   const size_t s_n = size_t(n_w) * n_x * rows * cols;
   const size_t s_b = align_up(s_n * 4);
-  if ((st = ensure(&ctx->io, &ctx->io_bytes, s_b + align_up(rows * cols * 4), ctx->device))) return st;
+  if ((st = ensure(&ctx->io, &ctx->io_bytes, s_b + align_up(rows * cols * 4), ctx->device, ctx->stream))) return st;
   CU(cudaSetDevice(ctx->device));
   int32_t* d_s = static_cast<int32_t*>(ctx->io);
   int32_t* d_y = reinterpret_cast<int32_t*>(static_cast<uint8_t*>(ctx->io) + s_b);
@@ -903,6 +1206,252 @@ int apmm_matmul_ap_dequant(apmm_ctx* ctx, const uint32_t* w_planes, uint64_t row
   }
   return host_matmul(ctx, w_planes, rows_w, n_w, w_scales, w_granularity, x_planes, rows_x, n_x,
                      x_scales, x_granularity, k, nullptr, out);
+}
+
+int apmm_dot_1bit_xor(apmm_ctx* ctx, const uint32_t* a, uint64_t a_words, const uint32_t* b,
+                      uint64_t b_words, uint64_t k, int64_t* out) {
+  if (!ctx || !a || !b || !out) return fail(APMM_E_INVALID_ARGUMENT, "null argument");
+  if (k == 0) return fail(APMM_E_OUT_OF_RANGE, "k_logical must be positive");
+  const uint64_t need = (k + 31) / 32;
+  if (a_words != need || b_words != need) {
+    return fail(APMM_E_LENGTH_MISMATCH, "word sequences must hold exactly ceil(k/32) words");
+  }
+  HOST_CALL(ctx);
+  int st;
+  const size_t w_b = align_up(need * 4);
+  if ((st = ensure(&ctx->io, &ctx->io_bytes, 2 * w_b + 64, ctx->device, ctx->stream))) return st;
+  uint8_t* base = static_cast<uint8_t*>(ctx->io);
+  uint32_t* d_a = reinterpret_cast<uint32_t*>(base);
+  uint32_t* d_b = reinterpret_cast<uint32_t*>(base + w_b);
+  int64_t* d_o = reinterpret_cast<int64_t*>(base + 2 * w_b);
+  CU(cudaMemcpyAsync(d_a, a, need * 4, cudaMemcpyHostToDevice, ctx->stream));
+  CU(cudaMemcpyAsync(d_b, b, need * 4, cudaMemcpyHostToDevice, ctx->stream));
+  if ((st = apmm_cu_dot_1bit_xor(ctx, d_a, need, d_b, need, k, d_o,
+                                 reinterpret_cast<apmm_stream_t>(ctx->stream)))) {
+    return st;
+  }
+  CU(cudaMemcpyAsync(out, d_o, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  return APMM_OK;
+}
+
+int apmm_matmul_plane_pair(apmm_ctx* ctx, const uint32_t* w_planes, uint64_t rows_w, int n_w,
+                           int weight_plane, const uint32_t* x_planes, uint64_t rows_x, int n_x,
+                           int feature_plane, uint64_t k, int32_t* y) {
+  int st;
+  if (!ctx || !w_planes || !x_planes || !y) return fail(APMM_E_INVALID_ARGUMENT, "null argument");
+  HOST_CALL(ctx);
+  if ((st = check_width(n_w)) || (st = check_width(n_x))) return st;
+  if ((st = check_dims(rows_w, k, "weights")) || (st = check_dims(rows_x, k, "features"))) return st;
+  if ((st = check_padding(w_planes, rows_w, k, n_w)) || (st = check_padding(x_planes, rows_x, k, n_x))) {
+    return st;
+  }
+  if (weight_plane < 0 || weight_plane >= n_w || feature_plane < 0 || feature_plane >= n_x) {
+    return fail(APMM_E_INDEX_OUT_OF_BOUNDS, "plane pair (%d, %d) out of range", weight_plane,
+                feature_plane);
+  }
+  const uint64_t wpr = (k + 31) / 32;
+  const size_t w_b = align_up(rows_w * wpr * 4), x_b = align_up(rows_x * wpr * 4);
+  if ((st = ensure(&ctx->io, &ctx->io_bytes, w_b + x_b + align_up(rows_w * rows_x * 4), ctx->device,
+                   ctx->stream))) {
+    return st;
+  }
+  uint8_t* base = static_cast<uint8_t*>(ctx->io);
+  uint32_t* d_w = reinterpret_cast<uint32_t*>(base);
+  uint32_t* d_x = reinterpret_cast<uint32_t*>(base + w_b);
+  int32_t* d_y = reinterpret_cast<int32_t*>(base + w_b + x_b);
+  // only the two planes travel (plane_row offsets, bitplane.cpp:44)
+  CU(cudaMemcpyAsync(d_w, w_planes + uint64_t(weight_plane) * rows_w * wpr, rows_w * wpr * 4,
+                     cudaMemcpyHostToDevice, ctx->stream));
+  CU(cudaMemcpyAsync(d_x, x_planes + uint64_t(feature_plane) * rows_x * wpr, rows_x * wpr * 4,
+                     cudaMemcpyHostToDevice, ctx->stream));
+  if ((st = apmm_cu_matmul_plane_pair(ctx, d_w, rows_w, 1, 0, d_x, rows_x, 1, 0, k, d_y,
+                                      reinterpret_cast<apmm_stream_t>(ctx->stream)))) {
+    return st;
+  }
+  CU(cudaMemcpyAsync(y, d_y, rows_w * rows_x * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  return APMM_OK;
+}
+
+// ---- APMM v1 tensor files (tensor_file.hpp:12-64) --------------------------------------
+static uint32_t rd_u32(const uint8_t* p) {
+  return uint32_t(p[0]) | (uint32_t(p[1]) << 8) | (uint32_t(p[2]) << 16) | (uint32_t(p[3]) << 24);
+}
+static uint64_t rd_u64(const uint8_t* p) {
+  uint64_t v = 0;
+  for (int i = 0; i < 8; ++i) v |= uint64_t(p[i]) << (8 * i);
+  return v;
+}
+
+// parse_tensor (tensor_file.cpp:159-229): same checks, same order, same messages.
+int apmm_tensor_parse(const uint8_t* bytes, uint64_t n, apmm_tensor_info* info) {
+  if (!bytes || !info) return fail(APMM_E_INVALID_ARGUMENT, "null argument");
+  if (n < 16) return fail(APMM_E_PARSE, "truncated tensor header");
+  if (std::memcmp(bytes, "APMM", 4) != 0) return fail(APMM_E_PARSE, "bad magic bytes");
+  if (bytes[4] != 0x01) return fail(APMM_E_PARSE, "unsupported tensor version %d", int(bytes[4]));
+  apmm_tensor_info t{};
+  t.bit_width = bytes[6];
+  const int gran = bytes[7];
+  t.rows = rd_u32(bytes + 8);
+  t.cols = rd_u32(bytes + 12);
+  if (t.rows == 0 || t.cols == 0) return fail(APMM_E_PARSE, "tensor dimensions must be positive");
+  const uint64_t elems = t.rows * t.cols;
+  uint64_t off = 16;
+  if (bytes[5] == 0x00) {
+    t.kind = 0;
+    t.granularity = -1;
+    if (t.bit_width != 0) return fail(APMM_E_PARSE, "float tensor must carry bit width 0");
+    if (gran != 0xFF) return fail(APMM_E_PARSE, "float tensor granularity must be 0xFF");
+    if (n != off + elems * 4) {
+      return fail(APMM_E_PARSE, "float payload length mismatch: file holds %llu bytes, expected %llu",
+                  (unsigned long long)(n - off), (unsigned long long)(elems * 4));
+    }
+    t.payload_offset = off;
+    t.payload_words = elems;
+    *info = t;
+    return APMM_OK;
+  }
+  if (bytes[5] != 0x01) return fail(APMM_E_PARSE, "unknown tensor kind %d", int(bytes[5]));
+  t.kind = 1;
+  if (t.bit_width < 1 || t.bit_width > 8) return fail(APMM_E_PARSE, "quantized bit width must be in [1, 8]");
+  if (gran == 0x00) {
+    t.scale_count = 1;
+  } else if (gran == 0x01) {
+    t.scale_count = t.rows;
+  } else {
+    return fail(APMM_E_PARSE, "quantized granularity must be 0x00 or 0x01");
+  }
+  t.granularity = gran;
+  if (n < off + t.scale_count * 8) return fail(APMM_E_PARSE, "truncated scale block");
+  for (uint64_t i = 0; i < t.scale_count; ++i) {
+    const uint64_t b = rd_u64(bytes + off + i * 8);
+    double v;
+    std::memcpy(&v, &b, 8);
+    if (!std::isfinite(v) || v <= 0.0) return fail(APMM_E_PARSE, "scales must be finite and positive");
+  }
+  off += t.scale_count * 8;
+  const uint64_t words = apmm_packed_words(t.bit_width, t.rows, t.cols);
+  if (n != off + words * 4) {
+    return fail(APMM_E_PARSE, "packed payload length mismatch: file holds %llu bytes, expected %llu",
+                (unsigned long long)(n - off), (unsigned long long)(words * 4));
+  }
+  t.payload_offset = off;
+  t.payload_words = words;
+  // to_packed -> PackedBitPlanes constructor: padding bits must be zero (bitplane.cpp:22-32)
+  const uint32_t tail = static_cast<uint32_t>(t.cols & 31);
+  if (tail) {
+    const uint32_t pad = ~((1u << tail) - 1u);
+    const uint64_t wpr = (t.cols + 31) / 32;
+    for (uint64_t pr = 0; pr < uint64_t(t.bit_width) * t.rows; ++pr) {
+      if (rd_u32(bytes + off + ((pr + 1) * wpr - 1) * 4) & pad) {
+        return fail(APMM_E_OUT_OF_RANGE, "packed buffer has nonzero padding bits");
+      }
+    }
+  }
+  *info = t;
+  return APMM_OK;
+}
+
+int apmm_cu_tensor_upload(apmm_ctx* ctx, const uint8_t* bytes, uint64_t n, uint32_t* planes,
+                          double* scales, double* values, apmm_stream_t stream) {
+  if (!ctx) return fail(APMM_E_INVALID_ARGUMENT, "null context");
+  apmm_tensor_info t;
+  int st = apmm_tensor_parse(bytes, n, &t);
+  if (st) return st;
+  cudaStream_t s;
+  if ((st = bind(ctx, stream, &s))) return st;
+  CU(cudaSetDevice(ctx->device));
+  if (t.kind == 1) {
+    // the payload IS the PackedBitPlanes buffer (tensor_file.cpp:218-228): one copy, no relayout
+    if (planes) {
+      CU(cudaMemcpyAsync(planes, bytes + t.payload_offset, t.payload_words * 4,
+                         cudaMemcpyHostToDevice, s));
+    }
+    if (scales) {
+      CU(cudaMemcpyAsync(scales, bytes + 16, t.scale_count * 8, cudaMemcpyHostToDevice, s));
+    }
+    return APMM_OK;
+  }
+  if (values) {  // f32 payload -> device staging -> widened to f64 on device (to_real)
+    if ((st = ensure(&ctx->qx, &ctx->qx_bytes, t.payload_words * 4, ctx->device, s))) return st;
+    CU(cudaMemcpyAsync(ctx->qx, bytes + t.payload_offset, t.payload_words * 4,
+                       cudaMemcpyHostToDevice, s));
+    CU(launch_widen(static_cast<const float*>(ctx->qx), t.payload_words, values, s));
+    ctx->launches += 1;
+  }
+  return APMM_OK;
+}
+
+int apmm_tensor_file_load(apmm_ctx* ctx, const char* path, apmm_tensor_info* info,
+                          uint32_t* planes, double* scales, double* values) {
+  if (!ctx || !path) return fail(APMM_E_INVALID_ARGUMENT, "null argument");
+  // read_tensor_file (tensor_file.cpp:231-): IoError when the file cannot be read
+  FILE* f = std::fopen(path, "rb");
+  if (!f) return fail(APMM_E_IO, "cannot open %s for reading", path);
+  std::vector<uint8_t> bytes;
+  uint8_t buf[1 << 16];
+  size_t got;
+  while ((got = std::fread(buf, 1, sizeof(buf), f)) > 0) bytes.insert(bytes.end(), buf, buf + got);
+  const bool bad = std::ferror(f) != 0;
+  std::fclose(f);
+  if (bad) return fail(APMM_E_IO, "short read from %s", path);
+  HOST_CALL(ctx);
+  apmm_tensor_info t;
+  int st = apmm_tensor_parse(bytes.data(), bytes.size(), &t);
+  if (st) return st;
+  if (info) *info = t;
+  if ((st = apmm_cu_tensor_upload(ctx, bytes.data(), bytes.size(), planes, scales, values,
+                                  reinterpret_cast<apmm_stream_t>(ctx->stream)))) {
+    return st;
+  }
+  CU(cudaStreamSynchronize(ctx->stream));
+  return APMM_OK;
+}
+
+// serialize_tensor (tensor_file.cpp:135-157) for the quantized kind, with the consistency
+// checks of check_consistent (tensor_file.cpp:47-85).
+int apmm_tensor_serialize_quantized(uint64_t rows, uint64_t cols, int n, int granularity,
+                                    const double* scales, const uint32_t* planes, uint8_t* out,
+                                    uint64_t out_cap, uint64_t* out_len) {
+  if (!scales || !planes || !out_len) return fail(APMM_E_INVALID_ARGUMENT, "null argument");
+  if (rows == 0 || cols == 0) return fail(APMM_E_OUT_OF_RANGE, "tensor dimensions must be positive");
+  if (rows > 0xFFFFFFFFull || cols > 0xFFFFFFFFull) {
+    return fail(APMM_E_OUT_OF_RANGE, "matrix too large for tensor file");
+  }
+  if (n < 1 || n > 8) return fail(APMM_E_OUT_OF_RANGE, "quantized bit width must be in [1, 8]");
+  if (!valid_gran(granularity)) {
+    return fail(APMM_E_OUT_OF_RANGE, "quantized granularity must be per-tensor or per-row");
+  }
+  const uint64_t sc = granularity == APMM_PER_ROW ? rows : 1;
+  for (uint64_t i = 0; i < sc; ++i) {
+    if (!std::isfinite(scales[i]) || scales[i] <= 0.0) {
+      return fail(APMM_E_OUT_OF_RANGE, "scales must be finite and positive");
+    }
+  }
+  const uint64_t words = apmm_packed_words(n, rows, cols);
+  const uint64_t len = 16 + sc * 8 + words * 4;
+  *out_len = len;
+  if (!out) return APMM_OK;
+  if (out_cap < len) return fail(APMM_E_LENGTH_MISMATCH, "output buffer holds %llu bytes, need %llu",
+                                 (unsigned long long)out_cap, (unsigned long long)len);
+  std::memcpy(out, "APMM", 4);
+  out[4] = 0x01;
+  out[5] = 0x01;
+  out[6] = static_cast<uint8_t>(n);
+  out[7] = static_cast<uint8_t>(granularity);
+  for (int i = 0; i < 4; ++i) out[8 + i] = static_cast<uint8_t>(rows >> (8 * i));
+  for (int i = 0; i < 4; ++i) out[12 + i] = static_cast<uint8_t>(cols >> (8 * i));
+  uint8_t* p = out + 16;
+  for (uint64_t i = 0; i < sc; ++i) {
+    uint64_t b;
+    std::memcpy(&b, &scales[i], 8);
+    for (int j = 0; j < 8; ++j) *p++ = static_cast<uint8_t>(b >> (8 * j));
+  }
+  for (uint64_t w = 0; w < words; ++w) {
+    for (int j = 0; j < 4; ++j) *p++ = static_cast<uint8_t>(planes[w] >> (8 * j));
+  }
+  return APMM_OK;
 }
 
 }  // extern "C"

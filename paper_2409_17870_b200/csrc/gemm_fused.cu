@@ -647,7 +647,8 @@ cudaError_t launch_nw(const CUtensorMap& twp, const CUtensorMap& tx, const CUten
                       const CUtensorMap& ty, Params p, uint32_t full_tiles, int num_sms,
                       cudaStream_t s) {
   auto kern = gemm_pair_wplanes_kernel<NW>;
-  static int max_clusters = 0;
+  static int max_clusters_dev[kMaxDevices] = {};
+  int& max_clusters = max_clusters_dev[current_device()];
   cudaLaunchConfig_t cfg{};
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = smem_bytes(NW);
@@ -673,7 +674,7 @@ cudaError_t launch_nw(const CUtensorMap& twp, const CUtensorMap& tx, const CUten
     int n = 0;
     e = cudaOccupancyMaxActiveClusters(&n, kern, &cfg);
     max_clusters = (e == cudaSuccess && n > 0) ? n : num_sms / 2;
-    if (std::getenv("APMM_DEBUG_PLAN")) {
+    if (APMM_DEV_ENV("APMM_DEBUG_PLAN")) {
       std::fprintf(stderr, "[apmm fused] NW=%d operand stages=%d raw stages=%d smem=%d: %d co-resident pairs\n",
                    NW, op_stages(NW), raw_stages(NW), smem_bytes(NW), max_clusters);
     }
@@ -686,7 +687,7 @@ cudaError_t launch_nw(const CUtensorMap& twp, const CUtensorMap& tx, const CUten
     return e != cudaSuccess ? e : cudaGetLastError();
   }
   p.n_full = full_tiles;
-  if (std::getenv("APMM_NO_TAIL_SPLIT") == nullptr) {
+  if (APMM_DEV_ENV("APMM_NO_TAIL_SPLIT") == nullptr) {
     const uint32_t r = full_tiles % mc;
     if (r != 0 && 2 * r <= mc) p.n_full = full_tiles - r;
   }
@@ -703,21 +704,13 @@ cudaError_t launch_nw(const CUtensorMap& twp, const CUtensorMap& tx, const CUten
 
 }  // namespace
 
-// Opt-in (APMM_FUSED=1): measured slower than K1 + K3 on B200 (4096^3 W2A4: 66-68 us vs
+// Opt-in (APMM_ROUTE_PAIR_WPLANES): measured slower than K1 + K3 on B200 (4096^3 W2A4: 66-68 us vs
 // 51 us). The per-tile re-expansion of W (16x at 4096^3) is ALU work the transform warps
 // cannot hide: they need ~550 cycles per K block against ~350 cycles of MMA
 // (APMM_DEBUG_WAITS breakdown in profiles/r01b_notes.md). Kept, tested bit-exact, for the
 // shapes where it could pay (few N tiles, wide K).
 bool gemm_wplanes_addressable(const uint32_t* w_planes, uint64_t k) {
-  return ((k + 31) / 32) % 4 == 0 && reinterpret_cast<uintptr_t>(w_planes) % 16 == 0 &&
-         std::getenv("APMM_NO_FUSED") == nullptr;
-}
-
-bool gemm_fused_supported(const uint32_t* w_planes, uint64_t k) {
-  const uint64_t wpr = (k + 31) / 32;
-  const char* on = std::getenv("APMM_FUSED");
-  return on != nullptr && on[0] == '1' && std::getenv("APMM_NO_FUSED") == nullptr &&
-         wpr % 4 == 0 && reinterpret_cast<uintptr_t>(w_planes) % 16 == 0;
+  return ((k + 31) / 32) % 4 == 0 && reinterpret_cast<uintptr_t>(w_planes) % 16 == 0;
 }
 
 cudaError_t launch_gemm_pair_wplanes(const GemmArgs& a, const uint32_t* w_planes,
@@ -777,7 +770,7 @@ cudaError_t launch_gemm_pair_wplanes(const GemmArgs& a, const uint32_t* w_planes
   p.tail_mask = tail ? ((1u << tail) - 1u) : 0xffffffffu;
   p.dbg = a.dbg;
   static const uint32_t ablate = [] {
-    const char* e = std::getenv("APMM_FUSED_ABLATE");
+    const char* e = APMM_DEV_ENV("APMM_FUSED_ABLATE");
     return e ? static_cast<uint32_t>(std::atoi(e)) : 0u;
   }();
   p.ablate = ablate;
@@ -794,7 +787,7 @@ cudaError_t launch_gemm_pair_wplanes(const GemmArgs& a, const uint32_t* w_planes
     sk = sk < 1 ? 1 : (sk > max_s ? max_s : sk);
     p.kb_per = (p.kblocks + sk - 1) / sk;
     p.split = (p.kblocks + p.kb_per - 1) / p.kb_per;  // no empty units
-    if (std::getenv("APMM_DEBUG_PLAN")) {
+    if (APMM_DEV_ENV("APMM_DEBUG_PLAN")) {
       std::fprintf(stderr, "[apmm fused] split-K: %u tiles of %u cols x %u K splits of %u blocks\n",
                    tiles, p.ncols, p.split, p.kb_per);
     }

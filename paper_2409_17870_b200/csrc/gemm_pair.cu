@@ -66,6 +66,8 @@ struct Params {
   // recovery terms. 0 = off.
   uint32_t split, kb_per, ncols, tiles_n_split;
   unsigned long long* ts;   // APMM_PAIR_TS=1 (dev only): per-CTA phase timestamps, else null
+  unsigned* colmax;         // dequant: per-column (or global) |v| max for the requantizer
+  uint32_t colmax_global;
 };
 
 __device__ __forceinline__ unsigned long long gtime_ns() {
@@ -346,6 +348,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int j = 0; j < 32; ++j) r[j] = dequant_bits(r[j], sw, sx);
           }
+          if (p.colmax) {
+            uint32_t f[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) f[j] = row_ok && col0 + j < p.rows_x ? r[j] : 0u;
+            colmax_warp(f, lane, col0, p.rows_x, p.colmax, p.colmax_global != 0);
+          }
         }
         if (p.tma_store) {
           uint8_t* buf = staging + (wq * 2 + nbuf) * kEpiBuf;
@@ -416,8 +424,9 @@ cudaError_t launch_gemm_pair(const GemmArgs& a, cudaStream_t s, int* launches, b
   } else {
     ty = tw;  // unused
   }
-  static bool attr_set = false;
-  if (!attr_set) {
+  static DeviceBits attr_set;
+  const int dev = current_device();
+  if (!attr_set.test(dev)) {
     cudaError_t e = cudaFuncSetAttribute(gemm_u8_pair_kernel<2>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
     if (e == cudaSuccess) {
@@ -425,7 +434,7 @@ cudaError_t launch_gemm_pair(const GemmArgs& a, cudaStream_t s, int* launches, b
                                kSmemBytes);
     }
     if (e != cudaSuccess) return e;
-    attr_set = true;
+    attr_set.set(dev);
   }
   Params p{};
   p.rowsum_w = a.rowsum_w;
@@ -447,9 +456,11 @@ cudaError_t launch_gemm_pair(const GemmArgs& a, cudaStream_t s, int* launches, b
   p.c0 = static_cast<uint32_t>(a.k_logical) * A * B;
   p.tma_store = tma_store ? 1u : 0u;
   p.dbg = a.dbg;
-  static const uint32_t peak_probe = std::getenv("APMM_PEAK_PROBE") ? 1u : 0u;
+  p.colmax = a.colmax;
+  p.colmax_global = a.colmax_global ? 1u : 0u;
+  static const uint32_t peak_probe = APMM_DEV_ENV("APMM_PEAK_PROBE") ? 1u : 0u;
   p.peak_probe = peak_probe;
-  static const bool want_ts = std::getenv("APMM_PAIR_TS") != nullptr;
+  static const bool want_ts = APMM_DEV_ENV("APMM_PAIR_TS") != nullptr;
   static unsigned long long* ts_buf = nullptr;
   if (want_ts) {
     if (!ts_buf) cudaMalloc(&ts_buf, 512 * 8 * sizeof(unsigned long long));
@@ -459,7 +470,7 @@ cudaError_t launch_gemm_pair(const GemmArgs& a, cudaStream_t s, int* launches, b
   // clusters of 4 (X multicast across two pairs) when there are enough cluster tiles to
   // fill the machine, else plain pairs. APMM_PAIR_CLUSTER=2|4 forces one (testing).
   static const int forced = [] {
-    const char* f = std::getenv("APMM_PAIR_CLUSTER");
+    const char* f = APMM_DEV_ENV("APMM_PAIR_CLUSTER");
     return f ? std::atoi(f) : 0;
   }();
   const uint32_t quad_tiles = ((p.tiles_m + 1) / 2) * p.tiles_n;
@@ -484,21 +495,22 @@ cudaError_t launch_gemm_pair(const GemmArgs& a, cudaStream_t s, int* launches, b
   cfg.numAttrs = 2;
   // persistent grid = the clusters that can be co-resident (clusters cannot straddle GPCs,
   // so for 4-CTA clusters this can be fewer than num_sms / 4)
-  static int max_active[5] = {0, 0, 0, 0, 0};
+  static int max_active_dev[kMaxDevices][5] = {};
+  int* max_active = max_active_dev[dev];
   if (!max_active[cl]) {
     cfg.gridDim = dim3(static_cast<unsigned>(a.num_sms / cl * cl));
     int n = 0;
     cudaError_t oe = cl == 4 ? cudaOccupancyMaxActiveClusters(&n, gemm_u8_pair_kernel<4>, &cfg)
                              : cudaOccupancyMaxActiveClusters(&n, gemm_u8_pair_kernel<2>, &cfg);
     max_active[cl] = (oe == cudaSuccess && n > 0) ? n : a.num_sms / cl;
-    if (std::getenv("APMM_DEBUG_PLAN")) {
+    if (APMM_DEV_ENV("APMM_DEBUG_PLAN")) {
       std::fprintf(stderr, "[apmm pair] cluster %d: %d co-resident clusters\n", cl, max_active[cl]);
     }
   }
   const uint32_t max_clusters = static_cast<uint32_t>(max_active[cl]);
   // last-wave split (pairs only): r = T mod P tiles become 2r half-width tiles if r <= P/2
   p.n_full = full_tiles;
-  if (cl == 2 && std::getenv("APMM_NO_TAIL_SPLIT") == nullptr) {
+  if (cl == 2 && APMM_DEV_ENV("APMM_NO_TAIL_SPLIT") == nullptr) {
     const uint32_t r = full_tiles % max_clusters;
     if (r != 0 && 2 * r <= max_clusters) p.n_full = full_tiles - r;
   }
@@ -515,7 +527,7 @@ cudaError_t launch_gemm_pair(const GemmArgs& a, cudaStream_t s, int* launches, b
     p.kb_per = (p.kblocks + sk - 1) / sk;
     p.split = (p.kblocks + p.kb_per - 1) / p.kb_per;
     tiles = t2 * p.split;
-    if (std::getenv("APMM_DEBUG_PLAN")) {
+    if (APMM_DEV_ENV("APMM_DEBUG_PLAN")) {
       std::fprintf(stderr, "[apmm pair] split-K: %u tiles of %u cols x %u K splits of %u blocks\n",
                    t2, p.ncols, p.split, p.kb_per);
     }

@@ -55,6 +55,8 @@ struct Params {
   uint32_t coef_w;  // 2*(2^n_x - 1): multiplies rowsum_w
   uint32_t coef_x;  // 2*(2^n_w - 1): multiplies rowsum_x
   uint32_t c0;      // K*(2^n_w-1)*(2^n_x-1) mod 2^32
+  unsigned* colmax;         // dequant: per-column (or global) |v| max for the requantizer
+  uint32_t colmax_global;
 };
 
 __global__ void __launch_bounds__(kThreads, 1)
@@ -197,12 +199,20 @@ __global__ void __launch_bounds__(kThreads, 1)
             float* dst = p.yf + off;
 #pragma unroll
             for (uint32_t j = 0; j < 32; ++j) {
-              if (col0 + j < p.rows_x) {
-                const double sx = p.gran_x ? p.s_x[col0 + j] : p.s_x[0];
-                dst[j] = static_cast<float>(__dmul_rn(__dmul_rn(double(int(v[j])), sw), sx));
-              }
+              const double sx = p.gran_x ? p.s_x[col0 + j < p.rows_x ? col0 + j : 0] : p.s_x[0];
+              const float fv = static_cast<float>(__dmul_rn(__dmul_rn(double(int(v[j])), sw), sx));
+              v[j] = col0 + j < p.rows_x ? __float_as_uint(fv) : 0u;
+              if (col0 + j < p.rows_x) dst[j] = fv;
             }
           }
+        }
+        __syncwarp();
+        if (p.colmax) {
+          if (!(row_ok && col0 < p.rows_x)) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = 0u;
+          }
+          colmax_warp(v, lane, col0, p.rows_x, p.colmax, p.colmax_global != 0);
         }
         __syncwarp();  // reconverge before the next .sync.aligned tcgen05.ld
       }
@@ -229,12 +239,13 @@ cudaError_t launch_gemm_tc(const GemmArgs& a, cudaStream_t s, int* launches) {
                      kBK, kBN) != CUDA_SUCCESS) {
     return cudaErrorInvalidValue;
   }
-  static bool attr_set = false;
-  if (!attr_set) {
+  static DeviceBits attr_set;
+  const int dev = current_device();
+  if (!attr_set.test(dev)) {
     cudaError_t e = cudaFuncSetAttribute(gemm_u8_tc_kernel,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
     if (e != cudaSuccess) return e;
-    attr_set = true;
+    attr_set.set(dev);
   }
   Params p{};
   p.rowsum_w = a.rowsum_w;
@@ -254,6 +265,8 @@ cudaError_t launch_gemm_tc(const GemmArgs& a, cudaStream_t s, int* launches) {
   p.coef_w = 2u * B;
   p.coef_x = 2u * A;
   p.c0 = static_cast<uint32_t>(a.k_logical) * A * B;  // wraps mod 2^32 by design
+  p.colmax = a.colmax;
+  p.colmax_global = a.colmax_global ? 1u : 0u;
   const uint32_t tiles = p.tiles_m * p.tiles_n;
   const uint32_t grid = tiles < uint32_t(a.num_sms) ? tiles : uint32_t(a.num_sms);
   cudaLaunchConfig_t cfg{};

@@ -3,9 +3,35 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
+#include <cstdlib>
+
+// Development instrumentation (plan dumps, per-phase CTA timelines, wait-cycle counters,
+// ablations and route/stage overrides read from the environment) is compiled only with
+// -DAPMM_DEVTOOLS (python -m paper_2409_17870_b200.build --dev). The release library never
+// reads the environment: APMM_DEV_ENV is a null constant and the names are not in the .so.
+#ifdef APMM_DEVTOOLS
+#define APMM_DEV_ENV(name) std::getenv(name)
+#else
+#define APMM_DEV_ENV(name) (static_cast<const char*>(nullptr))
+#endif
 
 namespace apmm_b200 {
+
+// cudaFuncSetAttribute and occupancy queries are per device; a process may drive several
+// devices through several contexts. One bit / slot per device ordinal.
+constexpr int kMaxDevices = 64;
+inline int current_device() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return d & (kMaxDevices - 1);
+}
+struct DeviceBits {
+  std::atomic<uint64_t> bits{0};
+  bool test(int dev) const { return (bits.load(std::memory_order_acquire) >> dev) & 1u; }
+  void set(int dev) { bits.fetch_or(uint64_t(1) << dev, std::memory_order_acq_rel); }
+};
 
 // Geometry of the tensor-core GEMM (gemm_tc.cu).
 constexpr int kBM = 128;        // weight rows per CTA tile (MMA M, TMEM lanes)
@@ -40,11 +66,14 @@ __host__ __device__ inline void raster_tile(uint32_t t, uint32_t tiles_m, uint32
 // null: then only rowsum_w is produced for W (the fused GEMM expands W on chip); rows_w may
 // be 0 (W untouched). zero_out[0, zero_bytes) (16-B multiple) is zeroed after the previous
 // kernel in the stream completed (Y of a split-K GEMM).
+// PDL: W rows are expanded before griddepcontrol.wait when early_w (weights may be read
+// while the previous kernel in the stream drains), X rows and the zeroing only after it.
 cudaError_t launch_expand(const uint32_t* w_planes, uint64_t rows_w, int n_w,
                           uint8_t* w_codes, int32_t* w_rowsum, const uint32_t* x_planes,
                           uint64_t rows_x, uint64_t rows_x_pad, int n_x, uint8_t* x_codes,
                           int32_t* x_rowsum, uint64_t cols, uint64_t kpad, int num_sms,
-                          cudaStream_t s, void* zero_out = nullptr, uint64_t zero_bytes = 0);
+                          cudaStream_t s, void* zero_out = nullptr, uint64_t zero_bytes = 0,
+                          bool early_w = true);
 cudaError_t launch_pack(const uint8_t* codes, uint64_t rows, uint64_t cols, int n,
                         uint32_t* planes, cudaStream_t s);
 cudaError_t launch_unpack(const uint32_t* planes, uint64_t rows, uint64_t cols, int n,
@@ -60,6 +89,25 @@ cudaError_t launch_quantize_pack(const double* x, uint64_t rows, uint64_t cols, 
                                  cudaStream_t s, uint8_t* gemm_codes = nullptr,
                                  int32_t* gemm_rowsum = nullptr, uint64_t kpad = 0,
                                  uint64_t rowsum_pad = 0);
+
+// dot_1bit_xor (kernel.cpp:115-123) into *out (device int64), one block.
+cudaError_t launch_dot_xor(const uint32_t* a, const uint32_t* b, uint64_t words, uint64_t k,
+                           int64_t* out, cudaStream_t s);
+// f32 -> f64 (tensor file float payload, to_real).
+cudaError_t launch_widen(const float* src, uint64_t n, double* dst, cudaStream_t s);
+// Column (per-token) or global absmax of yf [rows_w x rows_x] f32 as ordered u32 bits of |v|
+// (atomicMax into colmax, which the caller zeroes).
+cudaError_t launch_colmax(const float* yf, uint64_t rows_w, uint64_t rows_x, unsigned* colmax,
+                          bool global, int num_sms, cudaStream_t s);
+// quantize + pack of X' = yf^T with absmax `colmax` -> planes [n][rows_x][ceil(rows_w/32)],
+// scales (rows_x or 1); flag[0] <- 1 on a non-finite absmax.
+cudaError_t launch_requant_pack(const float* yf, uint64_t rows_w, uint64_t rows_x,
+                                const unsigned* colmax, bool global, int n, uint32_t* planes,
+                                double* scales, int* flag, cudaStream_t s);
+
+// absmax bits (u32 of |float|) <-> doubles, for the split (multi-GPU) requant form
+cudaError_t launch_bits_to_double(const unsigned* bits, uint64_t n, double* out, cudaStream_t s);
+cudaError_t launch_double_to_bits(const double* in, uint64_t n, unsigned* bits, cudaStream_t s);
 
 // recover (kernel.cpp:159-181) over a device plane-product stack [n_w*n_x][m*n] int32:
 // y = sum 2^(i+j) stack[i][j] in int64, narrowed to int32. flags[0] <- 1 if an entry lies
@@ -84,6 +132,10 @@ struct GemmArgs {
   int gran_x;
   int num_sms;
   unsigned long long* dbg = nullptr;  // optional wait-cycle counters (dev instrumentation)
+  // dequant epilogue only: per-column (per-token) absmax of the f32 output as ordered u32
+  // bits of |v| (atomicMax), or one global max when colmax_global; null = off
+  unsigned* colmax = nullptr;
+  bool colmax_global = false;
 };
 // Returns the number of kernel launches it enqueued via *launches.
 cudaError_t launch_gemm_tc(const GemmArgs& a, cudaStream_t s, int* launches);
@@ -122,6 +174,7 @@ struct SkinnyArgs {
   void* acc_ws;      // skinny_acc_bytes(): split-K accumulators, zero on entry, left zero
   void* scratch_ws;  // skinny_scratch_bytes(): feature fragments (2 halves) + weight repack
   int ws_half;       // ping-pong half for the feature fragments (PDL overlap of calls)
+  bool early_w = true;  // PDL: stream weight planes before the previous kernel completes
   // measurement (bench kernel pass): when non-null, recorded right before / after the
   // streaming kernel's launch (after the feature-prep kernel), with `ev_flags`
   cudaEvent_t ev_start = nullptr, ev_stop = nullptr;

@@ -116,52 +116,60 @@ __device__ __forceinline__ int32_t expand_row(const ExpandOperand& op, uint32_t 
   return sum;
 }
 
-// PDL protocol (see gemm_pair.cu): this kernel may start while the previous call's GEMM
-// still runs -- it only reads the caller's planes and writes the workspace half that the
-// GEMM two calls ago used (complete by construction) -- and it completes only after that
-// previous GEMM (griddepcontrol.wait at the end), so the next GEMM's wait on us also
-// covers it.
+__device__ __forceinline__ void expand_one(const ExpandOperand& op, uint32_t r, uint32_t wpr,
+                                           uint32_t tail_mask, uint32_t kpad_words,
+                                           uint32_t lane) {
+  int32_t sum = 0;
+  if (op.codes == nullptr) {
+    switch (op.n) {
+      case 1: sum = rowsum_row<1>(op, r, wpr, tail_mask, lane); break;
+      case 2: sum = rowsum_row<2>(op, r, wpr, tail_mask, lane); break;
+      case 3: sum = rowsum_row<3>(op, r, wpr, tail_mask, lane); break;
+      case 4: sum = rowsum_row<4>(op, r, wpr, tail_mask, lane); break;
+      default: sum = rowsum_row<8>(op, r, wpr, tail_mask, lane); break;
+    }
+  } else switch (op.n) {
+    case 1: sum = expand_row<1>(op, r, wpr, tail_mask, kpad_words, lane); break;
+    case 2: sum = expand_row<2>(op, r, wpr, tail_mask, kpad_words, lane); break;
+    case 3: sum = expand_row<3>(op, r, wpr, tail_mask, kpad_words, lane); break;
+    case 4: sum = expand_row<4>(op, r, wpr, tail_mask, kpad_words, lane); break;
+    case 5: sum = expand_row<5>(op, r, wpr, tail_mask, kpad_words, lane); break;
+    case 6: sum = expand_row<6>(op, r, wpr, tail_mask, kpad_words, lane); break;
+    case 7: sum = expand_row<7>(op, r, wpr, tail_mask, kpad_words, lane); break;
+    default: sum = expand_row<8>(op, r, wpr, tail_mask, kpad_words, lane); break;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+  if (lane == 0) op.rowsum[r] = sum;
+}
+
+// PDL protocol (see gemm_pair.cu). This kernel may start while the previous kernel in the
+// stream (normally the previous call's GEMM) still runs. Before griddepcontrol.wait it
+// touches only the WEIGHT planes (when early_w: weights are not produced by the kernel
+// immediately before the call -- apmm_cuda.h, Conventions) and the workspace half that the
+// GEMM two calls ago used (complete by construction). The feature planes -- possibly the
+// previous kernel's output -- and the zeroing of Y are read / written only after the wait.
+// It completes only after the previous kernel, so the next GEMM's wait on us covers both.
 __global__ void __launch_bounds__(kExpandThreads) expand_kernel(ExpandOperand a, ExpandOperand b,
                                                                  uint32_t wpr, uint32_t tail_mask,
                                                                  uint32_t kpad_words,
-                                                                 uint4* zero_out, uint64_t zero_n) {
+                                                                 uint4* zero_out, uint64_t zero_n,
+                                                                 uint32_t early_w) {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  if (!early_w) asm volatile("griddepcontrol.wait;" ::: "memory");
   const uint32_t warps = blockDim.x >> 5;
   const uint32_t lane = threadIdx.x & 31;
-  const uint32_t total = a.rows + b.rows;
-  for (uint32_t gr = blockIdx.x * warps + (threadIdx.x >> 5); gr < total;
-       gr += gridDim.x * warps) {
-    const bool is_a = gr < a.rows;
-    const ExpandOperand& op = is_a ? a : b;
-    const uint32_t r = is_a ? gr : gr - a.rows;
-    int32_t sum = 0;
-    if (op.codes == nullptr) {
-      switch (op.n) {
-        case 1: sum = rowsum_row<1>(op, r, wpr, tail_mask, lane); break;
-        case 2: sum = rowsum_row<2>(op, r, wpr, tail_mask, lane); break;
-        case 3: sum = rowsum_row<3>(op, r, wpr, tail_mask, lane); break;
-        case 4: sum = rowsum_row<4>(op, r, wpr, tail_mask, lane); break;
-        default: sum = rowsum_row<8>(op, r, wpr, tail_mask, lane); break;
-      }
-    } else switch (op.n) {
-      case 1: sum = expand_row<1>(op, r, wpr, tail_mask, kpad_words, lane); break;
-      case 2: sum = expand_row<2>(op, r, wpr, tail_mask, kpad_words, lane); break;
-      case 3: sum = expand_row<3>(op, r, wpr, tail_mask, kpad_words, lane); break;
-      case 4: sum = expand_row<4>(op, r, wpr, tail_mask, kpad_words, lane); break;
-      case 5: sum = expand_row<5>(op, r, wpr, tail_mask, kpad_words, lane); break;
-      case 6: sum = expand_row<6>(op, r, wpr, tail_mask, kpad_words, lane); break;
-      case 7: sum = expand_row<7>(op, r, wpr, tail_mask, kpad_words, lane); break;
-      default: sum = expand_row<8>(op, r, wpr, tail_mask, kpad_words, lane); break;
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-    if (lane == 0) op.rowsum[r] = sum;
-  }
+  const uint32_t gwarp = blockIdx.x * warps + (threadIdx.x >> 5), nwarps = gridDim.x * warps;
+  for (uint32_t r = gwarp; r < a.rows; r += nwarps) expand_one(a, r, wpr, tail_mask, kpad_words, lane);
   if (blockIdx.x == 0) {
     for (uint32_t r = a.rows + threadIdx.x; r < a.rows_pad; r += blockDim.x) a.rowsum[r] = 0;
     for (uint32_t r = b.rows + threadIdx.x; r < b.rows_pad; r += blockDim.x) b.rowsum[r] = 0;
   }
-  asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (early_w) asm volatile("griddepcontrol.wait;" ::: "memory");
+  // X rows continue the W rows' round robin, so a grid-stride pass over both stays balanced
+  for (uint32_t r = (gwarp + nwarps - a.rows % nwarps) % nwarps; r < b.rows; r += nwarps) {
+    expand_one(b, r, wpr, tail_mask, kpad_words, lane);
+  }
   // split-K GEMMs reduce-add into Y: zero it here, after the previous kernel in the stream
   // (which may still have been writing the same Y) has completed
   for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < zero_n;
@@ -386,6 +394,132 @@ __global__ void __launch_bounds__(kThreads) recover_kernel(const int32_t* __rest
   y[e] = static_cast<int32_t>(acc);
 }
 
+// ---- dot_1bit_xor (kernel.cpp:115-123): k - 2 popc(a ^ b), one block -----------------
+__global__ void __launch_bounds__(kThreads) dot_xor_kernel(const uint32_t* __restrict__ a,
+                                                            const uint32_t* __restrict__ b,
+                                                            uint64_t words, uint64_t k,
+                                                            int64_t* out) {
+  uint64_t pc = 0;
+  for (uint64_t w = threadIdx.x; w < words; w += blockDim.x) pc += __popc(__ldg(a + w) ^ __ldg(b + w));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) pc += __shfl_xor_sync(0xffffffffu, pc, o);
+  __shared__ uint64_t part[kThreads / 32];
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = pc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint64_t t = 0;
+    for (int i = 0; i < kThreads / 32; ++i) t += part[i];
+    *out = static_cast<int64_t>(k) - 2 * static_cast<int64_t>(t);
+  }
+}
+
+// ---- to_real (tensor_file.cpp:115-120): f32 payload -> f64 values -------------------------
+__global__ void __launch_bounds__(kThreads) widen_kernel(const float* __restrict__ src,
+                                                          uint64_t n, double* __restrict__ dst) {
+  for (uint64_t e = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < n;
+       e += uint64_t(gridDim.x) * blockDim.x) {
+    dst[e] = static_cast<double>(src[e]);
+  }
+}
+
+// ---- next-layer requantization -------------------------------------
+// yf: the dequantized GEMM output [rows_w][rows_x] f32 (rows = output features, columns =
+// tokens); the next layer's activation is X' = yf^T [rows_x tokens][rows_w features].
+// Column absmax when the GEMM epilogue did not form it (skinny / weight-plane routes):
+// thread per column over a slab of rows, one atomicMax per (thread, slab).
+__global__ void __launch_bounds__(kThreads) colmax_kernel(const float* __restrict__ yf,
+                                                           uint64_t rows_w, uint64_t rows_x,
+                                                           uint64_t rows_per_slab,
+                                                           unsigned* colmax, int global) {
+  const uint64_t c = uint64_t(blockIdx.x) * 32 + (threadIdx.x & 31);
+  const uint64_t r0 = uint64_t(blockIdx.y) * rows_per_slab;
+  const uint64_t r1 = r0 + rows_per_slab < rows_w ? r0 + rows_per_slab : rows_w;
+  uint32_t m = 0;
+  if (c < rows_x) {
+    for (uint64_t r = r0 + (threadIdx.x >> 5); r < r1; r += blockDim.x / 32) {
+      const uint32_t b = __float_as_uint(__ldg(yf + r * rows_x + c)) & 0x7fffffffu;
+      m = b > m ? b : m;
+    }
+  }
+  if (global) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const uint32_t t = __shfl_xor_sync(0xffffffffu, m, o);
+      m = t > m ? t : m;
+    }
+    if ((threadIdx.x & 31) == 0) atomicMax(colmax, m);
+  } else if (c < rows_x) {
+    atomicMax(colmax + c, m);
+  }
+}
+
+// quantize (bipolar.cpp:72-100) of X' with the reduced absmax, then decompose_and_pack
+// (bitplane.cpp:48-66): block = 8 warps x (32 tokens, 8 consecutive plane words). Warp q
+// reads yf rows 32(w0+q) .. +31 for 32 tokens (coalesced 128-B rows), lane = token, and
+// builds its token's n plane words bit by bit; the words go through shared memory so each
+// (plane, token) row receives 8 consecutive words (32-B sectors) per block.
+__global__ void bits_to_double_kernel(const unsigned* bits, uint64_t n, double* out) {
+  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    out[i] = static_cast<double>(__uint_as_float(bits[i]));
+  }
+}
+// inverse (absmax values of the f32 output, exactly representable as float); a non-finite
+// value maps to the inf/NaN bit patterns so the pack kernel reports it
+__global__ void double_to_bits_kernel(const double* in, uint64_t n, unsigned* bits) {
+  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    bits[i] = __float_as_uint(fabsf(static_cast<float>(in[i])));
+  }
+}
+
+constexpr int kRqWords = 8;
+__global__ void __launch_bounds__(kThreads) requant_pack_kernel(
+    const float* __restrict__ yf, uint64_t rows_w, uint64_t rows_x, const unsigned* colmax,
+    int global, int n, uint32_t* __restrict__ planes, double* __restrict__ scales, int* flag) {
+  __shared__ uint32_t sw[8][32][kRqWords + 1];
+  const uint32_t lane = threadIdx.x & 31, q = threadIdx.x >> 5;
+  const uint64_t wpr = (rows_w + 31) / 32;
+  const uint64_t t = uint64_t(blockIdx.y) * 32 + lane;
+  const uint64_t w = uint64_t(blockIdx.x) * kRqWords + q;
+  const int maxv = (1 << n) - 1;
+  const uint32_t mbits = global ? colmax[0] : (t < rows_x ? colmax[t] : 0u);
+  const double m = static_cast<double>(__uint_as_float(mbits));
+  const bool finite = mbits < 0x7f800000u;
+  if (!finite && t < rows_x) atomicOr(flag, 1);
+  const double s = m == 0.0 ? 1.0 : __ddiv_rn(m, double(maxv));  // bipolar.cpp:91
+  if (blockIdx.x == 0 && q == 0 && finite) {
+    if (global) {
+      if (blockIdx.y == 0 && lane == 0) scales[0] = s;
+    } else if (t < rows_x) {
+      scales[t] = s;
+    }
+  }
+  uint32_t word[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  if (t < rows_x && w < wpr && finite) {
+    const uint64_t r0 = w * 32;
+    const uint32_t nr = rows_w - r0 < 32 ? static_cast<uint32_t>(rows_w - r0) : 32u;
+    for (uint32_t j = 0; j < nr; ++j) {
+      const double v = static_cast<double>(__ldg(yf + (r0 + j) * rows_x + t));
+      const uint32_t c = quantize_code(v, s, maxv);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) word[i] |= ((c >> i) & 1u) << j;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    if (i < n) sw[i][lane][q] = word[i];
+  }
+  __syncthreads();
+  // write out: thread = (plane i, token, word) with the word index fastest
+  const uint64_t w0 = uint64_t(blockIdx.x) * kRqWords;
+  for (uint32_t e = threadIdx.x; e < uint32_t(n) * 32u * kRqWords; e += blockDim.x) {
+    const uint32_t qq = e % kRqWords, tok = (e / kRqWords) % 32, i = e / (kRqWords * 32);
+    const uint64_t tt = uint64_t(blockIdx.y) * 32 + tok, ww = w0 + qq;
+    if (tt < rows_x && ww < wpr) planes[(uint64_t(i) * rows_x + tt) * wpr + ww] = sw[i][tok][qq];
+  }
+}
+
 unsigned blocks_for(uint64_t threads) {
   return static_cast<unsigned>((threads + kThreads - 1) / kThreads);
 }
@@ -396,7 +530,7 @@ cudaError_t launch_expand(const uint32_t* w_planes, uint64_t rows_w, int n_w,
                           uint8_t* w_codes, int32_t* w_rowsum, const uint32_t* x_planes,
                           uint64_t rows_x, uint64_t rows_x_pad, int n_x, uint8_t* x_codes,
                           int32_t* x_rowsum, uint64_t cols, uint64_t kpad, int num_sms,
-                          cudaStream_t s, void* zero_out, uint64_t zero_bytes) {
+                          cudaStream_t s, void* zero_out, uint64_t zero_bytes, bool early_w) {
   const uint32_t wpr = static_cast<uint32_t>((cols + 31) / 32);
   const uint32_t tail = static_cast<uint32_t>(cols & 31);
   const uint32_t tail_mask = tail ? ((1u << tail) - 1u) : 0xffffffffu;
@@ -423,7 +557,8 @@ cudaError_t launch_expand(const uint32_t* w_planes, uint64_t rows_w, int n_w,
   cfg.numAttrs = 1;
   cudaError_t e = cudaLaunchKernelEx(&cfg, expand_kernel, a, b, wpr, tail_mask,
                                      static_cast<uint32_t>(kpad / 32),
-                                     static_cast<uint4*>(zero_out), zero_bytes / 16);
+                                     static_cast<uint4*>(zero_out), zero_bytes / 16,
+                                     early_w ? 1u : 0u);
   return e != cudaSuccess ? e : cudaGetLastError();
 }
 
@@ -521,6 +656,57 @@ CUresult encode_tmap_3d_u32(CUtensorMap* map, const void* base, const uint64_t (
   return encode(map, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, const_cast<void*>(base), d, st, b, es,
                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+}
+
+cudaError_t launch_dot_xor(const uint32_t* a, const uint32_t* b, uint64_t words, uint64_t k,
+                           int64_t* out, cudaStream_t s) {
+  dot_xor_kernel<<<1, kThreads, 0, s>>>(a, b, words, k, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_widen(const float* src, uint64_t n, double* dst, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  uint64_t blocks = (n + kThreads - 1) / kThreads;
+  if (blocks > 4096) blocks = 4096;
+  widen_kernel<<<static_cast<unsigned>(blocks), kThreads, 0, s>>>(src, n, dst);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_colmax(const float* yf, uint64_t rows_w, uint64_t rows_x, unsigned* colmax,
+                          bool global, int num_sms, cudaStream_t s) {
+  const uint64_t cblocks = (rows_x + 31) / 32;
+  uint64_t slabs = (uint64_t(4) * num_sms + cblocks - 1) / cblocks;
+  const uint64_t max_slabs = (rows_w + 63) / 64;
+  if (slabs > max_slabs) slabs = max_slabs;
+  if (slabs < 1) slabs = 1;
+  if (slabs > 65535) slabs = 65535;
+  const uint64_t per = (rows_w + slabs - 1) / slabs;
+  colmax_kernel<<<dim3(static_cast<unsigned>(cblocks), static_cast<unsigned>(slabs)), kThreads, 0,
+                  s>>>(yf, rows_w, rows_x, per, colmax, global ? 1 : 0);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_bits_to_double(const unsigned* bits, uint64_t n, double* out, cudaStream_t s) {
+  const unsigned blocks = static_cast<unsigned>(n / kThreads + 1 < 1024 ? n / kThreads + 1 : 1024);
+  bits_to_double_kernel<<<blocks, kThreads, 0, s>>>(bits, n, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_double_to_bits(const double* in, uint64_t n, unsigned* bits, cudaStream_t s) {
+  const unsigned blocks = static_cast<unsigned>(n / kThreads + 1 < 1024 ? n / kThreads + 1 : 1024);
+  double_to_bits_kernel<<<blocks, kThreads, 0, s>>>(in, n, bits);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_requant_pack(const float* yf, uint64_t rows_w, uint64_t rows_x,
+                                const unsigned* colmax, bool global, int n, uint32_t* planes,
+                                double* scales, int* flag, cudaStream_t s) {
+  const uint64_t wpr = (rows_w + 31) / 32;
+  const dim3 grid(static_cast<unsigned>((wpr + kRqWords - 1) / kRqWords),
+                  static_cast<unsigned>((rows_x + 31) / 32));
+  requant_pack_kernel<<<grid, kThreads, 0, s>>>(yf, rows_w, rows_x, colmax, global ? 1 : 0, n,
+                                                planes, scales, flag);
+  return cudaGetLastError();
 }
 
 }  // namespace apmm_b200

@@ -251,4 +251,39 @@ __host__ __device__ constexpr uint32_t idesc_i8_u8u8(uint32_t M, uint32_t N) {
          | ((M >> 4) << 24);  // m_dim
 }
 
+// ---- epilogue helpers -------------------------------------------------------------
+// Column absmax of a warp's 32 x 32 output block (lane = row, f[j] = float bits of column
+// col0 + j, 0 for masked entries) for the next layer's quantizer. |v| as u32 bits orders
+// like |v| (NaN above inf, so a non-finite output is visible in the max). Transpose-reduce
+// in 31 shuffles: after the step with offset o each lane keeps the half of its columns
+// selected by lane bit o, so lane l ends up with column l's maximum over the 32 rows. Then
+// one atomicMax per column (or one per warp into colmax[0] when global).
+APMM_DEV void colmax_warp(uint32_t (&f)[32], uint32_t lane, uint32_t col0, uint32_t rows_x,
+                          unsigned* colmax, bool global) {
+#pragma unroll
+  for (int j = 0; j < 32; ++j) f[j] &= 0x7fffffffu;
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {
+    const bool upper = (lane & uint32_t(o)) != 0;
+#pragma unroll
+    for (int j = 0; j < o; ++j) {
+      const uint32_t keep = upper ? f[j + o] : f[j];
+      const uint32_t send = upper ? f[j] : f[j + o];
+      const uint32_t recv = __shfl_xor_sync(0xffffffffu, send, o);
+      f[j] = keep > recv ? keep : recv;
+    }
+  }
+  uint32_t m = f[0];
+  if (global) {
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+      const uint32_t r = __shfl_xor_sync(0xffffffffu, m, o);
+      m = m > r ? m : r;
+    }
+    if (lane == 0) atomicMax(colmax, m);
+  } else if (col0 + lane < rows_x) {
+    atomicMax(colmax + col0 + lane, m);
+  }
+}
+
 }  // namespace apmm_ptx

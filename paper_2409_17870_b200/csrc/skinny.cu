@@ -113,6 +113,7 @@ struct SkinnyParams {
   // multipliers kept in the parameter bank so ptxas emits IMAD (FMA pipe), not SHF/IADD
   uint32_t m2, m4, m16, neg1;
   unsigned long long* ts;    // APMM_SKINNY_TS=1 (dev only): per-CTA phase timestamps, else null
+  uint32_t early_w;          // PDL: weight loads may start before the previous kernel completes
 };
 
 APMM_DEV unsigned long long gtime() {
@@ -238,15 +239,16 @@ APMM_DEV void transpose8(uint32_t (&x)[8]) {
 
 // ---- feature prep: X planes -> fragment-order codes + rowsum(U_x) -----------------------
 // grid (ceil(chunks_total*16 / 256), rows_x); thread = (feature row, 32-column word).
-// PDL: reads only the caller's X planes before griddepcontrol.wait; writes its workspace
-// half (last read by the call before the previous one, complete by construction) and
-// completes only after the previous kernel in the stream, like the expand kernel.
+// PDL: triggers its dependents at once (the streaming kernel's weight loads may start),
+// but reads the caller's X planes and writes its workspace half only after
+// griddepcontrol.wait: X may be the output of the previous kernel in the stream.
 __global__ void __launch_bounds__(kPrepThreads) prep_x_kernel(const uint32_t* __restrict__ x,
                                                               uint32_t rows_x, uint32_t wpr,
                                                               int n_x, uint32_t words_pad,
                                                               uint8_t* __restrict__ xfrag,
                                                               int32_t* __restrict__ rsx_part) {
   apmm_ptx::pdl_trigger();
+  apmm_ptx::pdl_wait();
   const uint32_t tok = blockIdx.y, W = blockIdx.x * kPrepThreads + threadIdx.x;
   const uint32_t xr = frag_rows(rows_x);
   uint32_t v[8];
@@ -260,7 +262,6 @@ __global__ void __launch_bounds__(kPrepThreads) prep_x_kernel(const uint32_t* __
     if (real && i < n_x) rs += __popc(v[i]) << i;
   }
   if (real) transpose8(v);
-  apmm_ptx::pdl_wait();  // the workspace half may be written only now
   if (W < words_pad) {
     const uint32_t cl = W / kChunkWords, t = (W % kChunkWords) >> 2, w = W & 3u;
     uint4* dst = reinterpret_cast<uint4*>(xfrag + uint64_t(cl) * chunk_bytes_m(xr)) +
@@ -364,6 +365,7 @@ __global__ void __launch_bounds__(sk_threads(N, NT), sk_ctas_per_sm(N, NT))
   // The weight planes are inputs of this call, so their loads may overlap the prep kernel
   // still running ahead of us (PDL); X, the workspace and Y only after pdl_wait.
   if (p.ts && tid == 0) p.ts[blockIdx.x * 8 + 6] = gtime();
+  if (!p.early_w) apmm_ptx::pdl_wait();  // weights may be produced by the previous kernel
   for (uint32_t i = 0; i < stages - 1 + p.prefetch; ++i) prefetch_next();
   for (uint32_t s = 0; s + 1 < stages; ++s) issue();
   if (p.ts && tid == 0) p.ts[blockIdx.x * 8 + 7] = gtime();
@@ -604,13 +606,14 @@ template <int N, int NT, bool SPLIT>
 cudaError_t launch_t(const CUtensorMap& tm, const SkinnyParams& p, unsigned grid, uint32_t smem,
                      cudaStream_t s) {
   auto kern = skinny_kernel<N, NT, SPLIT>;
-  static bool attr_set = false;  // one per instantiation
+  static DeviceBits attr_set;  // one per instantiation
+  const int dev = current_device();
   cudaError_t e;
-  if (!attr_set) {
+  if (!attr_set.test(dev)) {
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(sk_smem_budget(N, NT)));
     if (e != cudaSuccess) return e;
-    attr_set = true;
+    attr_set.set(dev);
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
@@ -753,11 +756,11 @@ cudaError_t launch_skinny(const SkinnyArgs& a, cudaStream_t s) {
   // profiles/r01b_skinny_stage_sweep.txt). 16 warps x 2 slots still keep ~100 KB per SM in
   // flight, above what HBM latency x bandwidth needs. APMM_SK_STAGES overrides (dev).
   static const int stage_cap = [] {
-    const char* e = std::getenv("APMM_SK_STAGES");
+    const char* e = APMM_DEV_ENV("APMM_SK_STAGES");
     return e ? std::atoi(e) : 2;
   }();
   static const int inprep_env = [] {
-    const char* e = std::getenv("APMM_SK_INPREP");
+    const char* e = APMM_DEV_ENV("APMM_SK_INPREP");
     return e ? std::atoi(e) : -1;
   }();
   const Plan pl = plan_for(a.rows_w, a.rows_x, p.chunks_total, kn, static_cast<int>(nt), a.num_sms,
@@ -766,7 +769,7 @@ cudaError_t launch_skinny(const SkinnyArgs& a, cudaStream_t s) {
   // PDL round trip; for more rows the redundant per-CTA transposes cost more).
   const bool inprep = inprep_env >= 0 ? inprep_env != 0 : a.rows_x <= 1;
   if (pl.grid == 0) return cudaErrorInvalidConfiguration;
-  static const bool show = std::getenv("APMM_DEBUG_PLAN") != nullptr;
+  static const bool show = APMM_DEV_ENV("APMM_DEBUG_PLAN") != nullptr;
 
   // scratch: [half 0 | half 1] feature fragments + rowsum(U_x) parts, then the repack
   uint8_t* scratch = static_cast<uint8_t*>(a.scratch_ws);
@@ -811,8 +814,9 @@ cudaError_t launch_skinny(const SkinnyArgs& a, cudaStream_t s) {
   p.xfrag = xfrag;
   p.x_planes = a.x_planes;
   p.inprep = inprep ? 1u : 0u;
+  p.early_w = a.early_w ? 1u : 0u;
   static const uint32_t prefetch = [] {
-    const char* e = std::getenv("APMM_SK_PREFETCH");
+    const char* e = APMM_DEV_ENV("APMM_SK_PREFETCH");
     return e ? static_cast<uint32_t>(std::atoi(e)) : 0u;  // measured no gain (r01b_skinny_prefetch_sweep.txt)
   }();
   p.prefetch = prefetch;
@@ -840,7 +844,7 @@ cudaError_t launch_skinny(const SkinnyArgs& a, cudaStream_t s) {
   p.m4 = 4u;
   p.m16 = 16u;
   p.neg1 = 0xFFFFFFFFu;
-  static const bool want_ts = std::getenv("APMM_SKINNY_TS") != nullptr;
+  static const bool want_ts = APMM_DEV_ENV("APMM_SKINNY_TS") != nullptr;
   static unsigned long long* ts_buf = nullptr;
   if (want_ts) {
     if (!ts_buf) cudaMalloc(&ts_buf, 1024 * 8 * sizeof(unsigned long long));
@@ -849,10 +853,11 @@ cudaError_t launch_skinny(const SkinnyArgs& a, cudaStream_t s) {
   }
 
   if (!inprep) {  // feature prep (same shared-memory carveout as the streaming kernel: no reconfig)
-    static bool carve_set = false;
-    if (!carve_set) {
+    static DeviceBits carve_set;
+    const int dev = current_device();
+    if (!carve_set.test(dev)) {
       cudaFuncSetAttribute(prep_x_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-      carve_set = true;
+      carve_set.set(dev);
     }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(prep_blocks, frag_rows(p.rows_x));

@@ -90,3 +90,86 @@ def sharded_matmul_ap(w_planes_full, n_out: int, n_w: int, x_planes, m_tok: int,
     if not gather:
         return y
     return gather_rows(y, n_out, m_tok, group)
+
+
+# ---- next-layer activations: requantize, then gather packed planes
+def word_shard_bounds(n_out: int, world: int, rank: int) -> tuple[int, int]:
+    """Row block [r0, r1) of rank `rank` with both ends on 32-row (one plane word)
+    boundaries, so each rank's block of the next layer's activation X' = Y^T is a block of
+    whole plane words in every X' row (the last rank takes the ragged end)."""
+    words = -(-n_out // 32)
+    w0, w1 = shard_bounds(words, world, rank)
+    return min(32 * w0, n_out), min(32 * w1, n_out)
+
+
+def gather_packed_planes(local_planes, n_next: int, m_tok: int, n_out: int, group=None):
+    """All-gather every rank's X' plane block ([n_next][m_tok][words_p] u32, rows of its
+    word_shard_bounds block) into the full next-layer activation planes
+    [n_next][m_tok][ceil(n_out/32)] (the PackedBitPlanes layout) on every rank: one
+    all_gather_into_tensor of padded blocks, then one word-block re-layout."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    spans = [word_shard_bounds(n_out, world, p) for p in range(world)]
+    wps = [-(-(r1 - r0) // 32) for r0, r1 in spans]
+    wmax = max(wps)
+    mine = wps[rank]
+    if local_planes.numel() != n_next * m_tok * mine:
+        raise ValueError("local plane block has the wrong size")
+    send = local_planes.reshape(n_next, m_tok, mine)
+    if mine != wmax:
+        pad = torch.zeros((n_next, m_tok, wmax), dtype=local_planes.dtype, device=local_planes.device)
+        pad[:, :, :mine] = send
+        send = pad
+    out = torch.empty((world * n_next, m_tok, wmax), dtype=local_planes.dtype,
+                      device=local_planes.device)
+    dist.all_gather_into_tensor(out, send.contiguous(), group=group)
+    out = out.view(world, n_next, m_tok, wmax)
+    if all(w == wmax for w in wps):
+        return out.permute(1, 2, 0, 3).reshape(n_next, m_tok, world * wmax).reshape(-1)
+    blocks = [out[p, :, :, :wps[p]] for p in range(world)]
+    return torch.cat(blocks, dim=2).reshape(-1)
+
+
+def sharded_matmul_requant(w_planes_full, n_out: int, n_w: int, w_scales_full, w_gran: int,
+                           x_planes, m_tok: int, n_x: int, x_scales, x_gran: int, k: int,
+                           n_next: int, next_gran: int, group=None, local_ops=None):
+    """One N-sharded layer whose consumer needs the full output as the NEXT layer's packed
+    activation: per rank matmul_ap -> dequant (+ column absmax in the GEMM epilogue), a MAX
+    all-reduce of the per-token (or global) absmax, the rank's quantize + pack of its word
+    block, then the all-gather of packed planes -- n_next/32 of the int32 gather's bytes.
+    Returns (planes [n_next * m_tok * ceil(n_out/32)] int32, scales f64) on every rank,
+    bit-identical to quantize_pack(dequant(Y_full)^T).
+
+    `local_ops` = (gemm_absmax, requant_pack) replaces the B200 calls (CPU tests):
+    gemm_absmax(w_shard, rows, w_scales_shard) -> (yf [rows, m_tok] f32, absmax f64);
+    requant_pack(yf, rows, absmax) -> (planes, scales)."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    r0, r1 = word_shard_bounds(n_out, world, rank)
+    rows = r1 - r0
+    w_shard = slice_plane_rows(w_planes_full, n_out, k, n_w, r0, r1)
+    ws = w_scales_full[r0:r1] if w_gran == 1 else w_scales_full
+    n_scales = m_tok if next_gran == 1 else 1
+    if local_ops is None:
+        from .apmm import cu_matmul_ap_requant, cu_requant_pack
+        dev = x_planes.device
+        yf = torch.empty((rows, m_tok), dtype=torch.float32, device=dev)
+        absmax = torch.empty(n_scales, dtype=torch.float64, device=dev)
+        cu_matmul_ap_requant(w_shard, rows, n_w, ws.contiguous(), w_gran, x_planes, m_tok, n_x,
+                             x_scales, x_gran, k, n_next, next_gran, yf, absmax=absmax)
+        dist.all_reduce(absmax, op=dist.ReduceOp.MAX, group=group)
+        planes = torch.empty(n_next * m_tok * (-(-rows // 32)), dtype=torch.int32, device=dev)
+        scales = torch.empty(n_scales, dtype=torch.float64, device=dev)
+        cu_requant_pack(yf, rows, m_tok, absmax, n_next, next_gran, planes, scales)
+    else:
+        gemm_absmax, requant_pack = local_ops
+        yf, absmax = gemm_absmax(w_shard, rows, ws)
+        dist.all_reduce(absmax, op=dist.ReduceOp.MAX, group=group)
+        planes, scales = requant_pack(yf, rows, absmax)
+    return gather_packed_planes(planes, n_next, m_tok, n_out, group), scales

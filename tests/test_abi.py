@@ -104,3 +104,22 @@ def test_product_never_imports_the_oracle():
                 src = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in src and "from oracle" not in src, f
                 assert "apmm_oracle" not in src and "liboracle" not in src, f
+
+
+def test_release_library_reads_no_environment():
+    """Dev instrumentation (route overrides, ablations that change results, timelines that
+    synchronise inside a launch) is compiled only with -DAPMM_DEVTOOLS: the release .so holds
+    none of those environment names (build.py, csrc/internal.h APMM_DEV_ENV)."""
+    so = os.path.join(ROOT, "paper_2409_17870_b200", "libapmm_b200.so")
+    data = open(so, "rb").read()
+    for name in (b"APMM_PEAK_PROBE", b"APMM_FUSED_ABLATE", b"APMM_PAIR_TS", b"APMM_SKINNY_TS",
+                 b"APMM_DEBUG_WAITS", b"APMM_MID", b"APMM_PSPLIT", b"APMM_FUSED",
+                 b"APMM_FORCE_TC", b"APMM_FORCE_1SM", b"APMM_SK_STAGES", b"APMM_DEBUG_PLAN"):
+        assert name not in data, name
+
+
+def test_option_validation_without_device(lib):
+    assert lib.apmm_ctx_set_option(None, 1, 0) == 9
+    v = C.c_int()
+    assert lib.apmm_ctx_get_option(None, 1, C.byref(v)) == 9
+    assert lib.apmm_ctx_reserve(None, 1, 1, 1, 1) == 9
