@@ -400,7 +400,7 @@ def run_ours(args, rank, world, local_rank):
     gemms = full_gemms
     sharded = args.workload in SHARDED and world > 1
     if sharded:  # rank p owns W rows [r0, r1) (paper_2409_17870_b200/shard.py)
-        from paper_2409_17870_b200.shard import shard_bounds
+        from paper_2409_17870_b200.shard import word_shard_bounds as shard_bounds
         n_out, m_tok, k, nw, nx = full_gemms[0]
         r0, r1 = shard_bounds(n_out, world, rank)
         gemms = [(r1 - r0, m_tok, k, nw, nx)]
@@ -565,9 +565,9 @@ def run_ours(args, rank, world, local_rank):
     #    timed on its own (compute-only `value` above) and as compute + gather steps
     gather = None
     if sharded:
-        from paper_2409_17870_b200.shard import max_shard
-        n_full, m_full = full_gemms[0][0], full_gemms[0][1]
-        ms_blk = max_shard(n_full, world)
+        n_full, m_full, k, nw, nx = full_gemms[0]
+        wpr = (k + 31) // 32
+        ms_blk = max(b - a for a, b in (shard_bounds(n_full, world, p) for p in range(world)))
         send = torch.zeros((ms_blk, m_full), dtype=torch.int32, device=dev)
         recv = torch.empty((world * ms_blk, m_full), dtype=torch.int32, device=dev)
         y0 = bufs[0][2]
@@ -606,6 +606,34 @@ def run_ours(args, rank, world, local_rank):
                   "algbw_GBps": recv_bytes / (g_ms * 1e-3) / 1e9,
                   "compute_plus_gather_ms_per_step": cg_ms,
                   "compute_plus_gather_TOPS": job_ops_step / (cg_ms * 1e-3) / 1e12}
+        # the consumer's view: the next layer needs X' = dequant(Y)^T as
+        # A4 packed planes. Per rank: GEMM + dequant epilogue (+ per-token absmax), a MAX
+        # all-reduce of 4096 doubles, quantize + pack of the rank's word block, all-gather of
+        # the packed planes (+ one word-block re-layout) -- instead of the int32 gather.
+        from paper_2409_17870_b200.shard import sharded_matmul_requant
+        n_next = 4
+        wfull = torch.empty(nw * n_full * wpr, dtype=torch.int32, device=dev)
+        r0, r1 = shard_bounds(n_full, world, rank)
+        wfull.view(nw, n_full, wpr)[:, r0:r1].copy_(bufs[0][0][0].view(nw, r1 - r0, wpr))
+        sw_full = torch.rand(n_full, dtype=torch.float64, device=dev, generator=gen) + 0.5
+        sx = torch.rand(m_full, dtype=torch.float64, device=dev, generator=gen) + 0.5
+        xq = bufs[0][1][0]
+
+        def layer_packed():
+            return sharded_matmul_requant(wfull, n_full, nw, sw_full, 1, xq, m_full, nx, sx, 1,
+                                          k, n_next, 1)
+        for _ in range(2):
+            layer_packed()
+        torch.cuda.synchronize()
+        lp_ms = timed(layer_packed)
+        wps_ = -(-n_full // 32)
+        packed_recv = (world - 1) * n_next * m_full * (-(-wps_ // world)) * 4
+        gather["next_layer_packed"] = {
+            "format": f"A{n_next} packed planes of X' = dequant(Y)^T + per-token scales",
+            "ms_per_step": lp_ms, "recv_bytes_per_rank": packed_recv,
+            "bytes_vs_int32": packed_recv / recv_bytes,
+            "note": ("GEMM + dequant/absmax epilogue + absmax all-reduce + requant/pack + packed "
+                     "all-gather, per step; W rows split on 32-row word boundaries")}
 
     # -- e2e through the public host API: pinned host planes -> H2D -> GEMM -> D2H int32
     e2e_steps = max(1, min(args.steps, 3))

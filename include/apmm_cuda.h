@@ -111,7 +111,12 @@ enum {
   APMM_OPT_ROUTE = 1,
   /* 1 (default): PDL early read of the weight planes (see Conventions); 0: every operand
    * is read after the previous kernel in the stream completed. */
-  APMM_OPT_EARLY_WEIGHT_READ = 2
+  APMM_OPT_EARLY_WEIGHT_READ = 2,
+  /* 0 (default): feature planes are read only after the previous kernel in the stream has
+   * completed. 1: they are read early too (more overlap of consecutive calls) -- only for
+   * callers whose features are never produced by an early-triggering kernel launched
+   * immediately before the call (e.g. several projections of one resident activation). */
+  APMM_OPT_EARLY_FEATURE_READ = 3
 };
 enum {
   APMM_ROUTE_AUTO = 0,         /* by shape */

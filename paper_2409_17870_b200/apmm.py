@@ -202,7 +202,7 @@ class Route(enum.IntEnum):
     TENSOR_CORE = 7
 
 
-OPT_ROUTE, OPT_EARLY_WEIGHT_READ = 1, 2
+OPT_ROUTE, OPT_EARLY_WEIGHT_READ, OPT_EARLY_FEATURE_READ = 1, 2, 3
 
 
 class Context:
@@ -239,6 +239,11 @@ class Context:
 
     def set_early_weight_read(self, on: bool) -> None:
         _check(self.lib.apmm_ctx_set_option(self.h, OPT_EARLY_WEIGHT_READ, int(bool(on))))
+
+    def set_early_feature_read(self, on: bool) -> None:
+        """APMM_OPT_EARLY_FEATURE_READ: only when features are never produced by an
+        early-triggering kernel launched right before a call (apmm_cuda.h)."""
+        _check(self.lib.apmm_ctx_set_option(self.h, OPT_EARLY_FEATURE_READ, int(bool(on))))
 
     def reserve(self, rows_w: int, rows_x: int, k: int, n_w: int = 8) -> None:
         """Pre-size the workspace for calls up to this shape (before CUDA-graph capture)."""

@@ -5,7 +5,8 @@
 The shared library exports exactly the C ABI declared in include/apmm_cuda.h. The release
 build reads no environment variables. `--dev` builds the same sources with
 -DAPMM_DEVTOOLS (plan dumps, per-phase timelines, ablations; csrc/internal.h) into
-devlib/libapmm_b200_dev.so, for the scripts/ probes via APMM_LIB -- never the product.
+abtest/libapmm_b200_dev.so (git-ignored), for the scripts/ probes via APMM_LIB -- never
+the product.
 """
 from __future__ import annotations
 
@@ -46,7 +47,7 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(d) <= t for d in deps())
 
 
-DEV_LIB = os.path.join(ROOT, "devlib", "libapmm_b200_dev.so")
+DEV_LIB = os.path.join(ROOT, "abtest", "libapmm_b200_dev.so")
 
 
 def build(force: bool = False, verbose: bool = False, dev: bool = False) -> str:

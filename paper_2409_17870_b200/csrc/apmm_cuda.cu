@@ -35,6 +35,7 @@ struct apmm_ctx {
   bool timing = false;
   int route = APMM_ROUTE_AUTO;  // APMM_OPT_ROUTE
   bool early_w = true;          // APMM_OPT_EARLY_WEIGHT_READ
+  bool early_x = false;         // APMM_OPT_EARLY_FEATURE_READ
   // stream binding (apmm_cuda.h, Conventions): the device entry points' stream
   bool bound = false;
   cudaStream_t bound_stream = nullptr;
@@ -51,6 +52,12 @@ struct apmm_ctx {
   size_t qx_bytes = 0;
   void* rq = nullptr;  // requant: absmax scratch (ordered u32 bits, rows_x + 1)
   size_t rq_bytes = 0;
+  // dev launch trace (APMM_TRACE=<slots>, -DAPMM_DEVTOOLS builds only): per launch a slot of
+  // [1024 CTAs][8] globaltimer stamps, round robin; trace_kind[slot] = kernel kind
+  unsigned long long* trace = nullptr;
+  int trace_slots = 0;
+  int trace_seq = 0;
+  std::vector<int> trace_kind;
   // host entry points' transfer pipeline: H2D / D2H copy streams and their events
   cudaStream_t s_in = nullptr, s_out = nullptr;
   cudaEvent_t pipe_ev[16] = {};
@@ -291,6 +298,18 @@ int pick_route(const apmm_ctx* ctx, const RouteCaps& c, uint64_t rows_w, uint64_
   return APMM_OK;
 }
 
+// dev launch trace: the next slot (kind 1 expand, 2 pair GEMM, 3 weight-plane GEMM, 5 skinny)
+unsigned long long* trace_slot(apmm_ctx* ctx, int kind) {
+  if (!ctx->trace) return nullptr;
+  const int slot = ctx->trace_seq++ % ctx->trace_slots;
+  ctx->trace_kind[slot] = kind;
+  return ctx->trace + uint64_t(slot) * 1024 * 8;
+}
+
+// blocks per SM of an expansion launch that runs after the previous kernel completed
+// (4 x 128 threads x 80 registers: one wave on every SM)
+constexpr int kK1xBlocksPerSm = 4;
+
 // requant absmax scratch: rows_x u32 (+ 1 for the global max), 16-byte multiple (K1 zeroes it)
 uint64_t colmax_bytes(uint64_t rows_x) { return round_up((rows_x + 1) * 4, 16); }
 
@@ -339,6 +358,8 @@ int run_matmul(apmm_ctx* ctx, const uint32_t* w, uint64_t rows_w, int n_w, const
     s.scratch_ws = ctx->sk_scratch;
     s.ws_half = ctx->ws_half;
     s.early_w = ctx->early_w;
+    s.early_x = ctx->early_w && ctx->early_x;
+    s.trace = trace_slot(ctx, 5);
     ctx->ws_half ^= 1;
     {
       // kernel timing brackets the streaming kernel alone (not the feature-prep launch)
@@ -367,15 +388,33 @@ int run_matmul(apmm_ctx* ctx, const uint32_t* w, uint64_t rows_w, int n_w, const
   const bool zero_y = route == Route::Mid || route == Route::PairSplit;  // split-K reduce-adds
   {
     TimedLaunch t(ctx, 1, stream);
-    // K3f: W untouched by K1 except for rowsum(U_w) on the pair route (the split-K mid route
-    // forms it in the GEMM); split-K: K1 also zeroes Y, which the units reduce-add into
-    CU(launch_expand(w, route == Route::Mid ? 0 : rows_w, n_w, wplanes ? nullptr : m.codes_w,
-                     m.rowsum_w, x_ready ? nullptr : x, x_ready ? 0 : rows_x,
-                     x_ready ? 0 : rsx_pad, n_x, m.codes_x, m.rowsum_x, k, m.kpad, ctx->num_sms,
-                     stream,
-                     zero_y ? static_cast<void*>(y) : static_cast<void*>(colmax),
-                     zero_y ? rows_w * rows_x * 4 : (colmax ? colmax_bytes(rows_x) : 0),
-                     ctx->early_w));
+    // K1. K3f: W untouched except for rowsum(U_w) on the pair route (the split-K mid route
+    // forms it in the GEMM); split-K: K1 also zeroes Y, which the units reduce-add into.
+    // Work that must wait for the previous kernel (features unless the caller allows early
+    // reads, the zeroing) runs in a second launch with the whole machine (K1x) when there
+    // is also early work (weights) for a first, GEMM-co-resident launch (K1w).
+    const uint64_t w_rows = route == Route::Mid ? 0 : rows_w;
+    const bool early_x = ctx->early_w && ctx->early_x;
+    void* zero_ptr = zero_y ? static_cast<void*>(y) : static_cast<void*>(colmax);
+    const uint64_t zero_bytes = zero_y ? rows_w * rows_x * 4 : (colmax ? colmax_bytes(rows_x) : 0);
+    const uint64_t x_rows = x_ready ? 0 : rows_x;
+    const bool split_x = ctx->early_w && w_rows > 0 && !early_x && (x_rows > 0 || zero_bytes > 0);
+    if (split_x) {
+      CU(launch_expand(w, w_rows, n_w, wplanes ? nullptr : m.codes_w, m.rowsum_w, nullptr, 0,
+                       x_ready ? 0 : rsx_pad, n_x, m.codes_x, m.rowsum_x, k, m.kpad,
+                       ctx->num_sms, stream, nullptr, 0, true, false, trace_slot(ctx, 1)));
+      CU(launch_expand(w, 0, n_w, nullptr, m.rowsum_w, x_ready ? nullptr : x, x_rows,
+                       x_ready ? 0 : rsx_pad, n_x, m.codes_x, m.rowsum_x, k, m.kpad,
+                       ctx->num_sms, stream, zero_ptr, zero_bytes, false, false,
+                       trace_slot(ctx, 1), kK1xBlocksPerSm));
+      ctx->launches += 1;
+    } else {
+      CU(launch_expand(w, w_rows, n_w, wplanes ? nullptr : m.codes_w, m.rowsum_w,
+                       x_ready ? nullptr : x, x_rows, x_ready ? 0 : rsx_pad, n_x, m.codes_x,
+                       m.rowsum_x, k, m.kpad, ctx->num_sms, stream, zero_ptr, zero_bytes,
+                       ctx->early_w, early_x, trace_slot(ctx, 1),
+                       w_rows == 0 || !ctx->early_w ? kK1xBlocksPerSm : 1));
+    }
   }
   ctx->launches += 1;
   GemmArgs a{};
@@ -396,7 +435,10 @@ int run_matmul(apmm_ctx* ctx, const uint32_t* w, uint64_t rows_w, int n_w, const
   a.s_x = s_x;
   a.gran_x = gran_x;
   a.num_sms = ctx->num_sms;
+  a.trace = route == Route::Single ? nullptr
+                                    : trace_slot(ctx, route == Route::Mid || route == Route::PairW ? 3 : 2);
   a.colmax = route == Route::PairW ? nullptr : colmax;
+  a.early_w = ctx->early_w;
   a.colmax_global = colmax_global;
   if (ctx->dbg_waits) {
     if (!ctx->dbg) {
@@ -542,6 +584,14 @@ int apmm_ctx_create(apmm_ctx** out, int device) {
   ctx->device = device;
   ctx->num_sms = prop.multiProcessorCount;
   if (const char* f = APMM_DEV_ENV("APMM_DEBUG_WAITS")) ctx->dbg_waits = f[0] == '1';
+  if (const char* f = APMM_DEV_ENV("APMM_TRACE")) {
+    ctx->trace_slots = std::max(1, std::atoi(f));
+    const size_t b = size_t(ctx->trace_slots) * 1024 * 8 * 8;
+    if (cudaMalloc(&ctx->trace, b) != cudaSuccess || cudaMemset(ctx->trace, 0, b) != cudaSuccess) {
+      ctx->trace = nullptr;
+    }
+    ctx->trace_kind.assign(ctx->trace_slots, 0);
+  }
   cudaError_t e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaMalloc(&ctx->flags, 64);
   if (e != cudaSuccess) {
@@ -581,6 +631,7 @@ int apmm_ctx_destroy(apmm_ctx* ctx) {
   if (ctx->flags) cudaFree(ctx->flags);
   if (ctx->qx) cudaFree(ctx->qx);
   if (ctx->rq) cudaFree(ctx->rq);
+  if (ctx->trace) cudaFree(ctx->trace);
   if (ctx->ws) cudaFree(ctx->ws);
   if (ctx->sk_ws) cudaFree(ctx->sk_ws);
   if (ctx->sk_scratch) cudaFree(ctx->sk_scratch);
@@ -627,6 +678,9 @@ int apmm_ctx_set_option(apmm_ctx* ctx, int option, int value) {
     case APMM_OPT_EARLY_WEIGHT_READ:
       ctx->early_w = value != 0;
       return APMM_OK;
+    case APMM_OPT_EARLY_FEATURE_READ:
+      ctx->early_x = value != 0;
+      return APMM_OK;
     default:
       return fail(APMM_E_INVALID_ARGUMENT, "unknown option %d", option);
   }
@@ -637,6 +691,7 @@ int apmm_ctx_get_option(const apmm_ctx* ctx, int option, int* value) {
   switch (option) {
     case APMM_OPT_ROUTE: *value = ctx->route; return APMM_OK;
     case APMM_OPT_EARLY_WEIGHT_READ: *value = ctx->early_w ? 1 : 0; return APMM_OK;
+    case APMM_OPT_EARLY_FEATURE_READ: *value = ctx->early_x ? 1 : 0; return APMM_OK;
     default: return fail(APMM_E_INVALID_ARGUMENT, "unknown option %d", option);
   }
 }
@@ -1453,5 +1508,23 @@ int apmm_tensor_serialize_quantized(uint64_t rows, uint64_t cols, int n, int gra
   }
   return APMM_OK;
 }
+
+#ifdef APMM_DEVTOOLS
+// dev only (not in the release .so): copy the launch trace out and clear it. out holds
+// slots x 1024 x 8 u64, kinds `slots` ints; returns the number of launches recorded so far.
+__attribute__((visibility("default"))) int apmm_dev_trace_read(apmm_ctx* ctx, unsigned long long* out,
+                                                            int* kinds) {
+  if (!ctx || !ctx->trace) return -1;
+  cudaSetDevice(ctx->device);
+  cudaDeviceSynchronize();
+  const size_t b = size_t(ctx->trace_slots) * 1024 * 8 * 8;
+  cudaMemcpy(out, ctx->trace, b, cudaMemcpyDeviceToHost);
+  cudaMemset(ctx->trace, 0, b);
+  for (int i = 0; i < ctx->trace_slots; ++i) kinds[i] = ctx->trace_kind[i];
+  const int n = ctx->trace_seq;
+  ctx->trace_seq = 0;
+  return n;
+}
+#endif
 
 }  // extern "C"

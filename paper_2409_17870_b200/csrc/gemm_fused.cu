@@ -97,6 +97,8 @@ struct Params {
   uint32_t kb_per, ncols, tiles_n_split;
   uint32_t ablate;  // dev only (APMM_FUSED_ABLATE, results wrong): 1 skip A stores, 2 skip B loads
   unsigned long long* dbg;  // APMM_DEBUG_WAITS=1: wait-cycle counters per role, else null
+  unsigned long long* ts;   // dev launch trace (APMM_TRACE): [0] start [1] pdl_wait [4] end
+  uint32_t early_w;         // PDL: weight-plane loads + transforms before the previous kernel ends
 };
 
 // Bounded mbarrier waits: a wait that does not complete within ~4 s of clock64 cycles
@@ -267,6 +269,14 @@ __global__ void __maxnreg__(kXformWarpsCfg == 4 ? 136 : 108)
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
+  auto stamp = [&](int k) {
+    if (p.ts && threadIdx.x == 0) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      p.ts[blockIdx.x * 8 + k] = t;
+    }
+  };
+  stamp(0);
   const uint32_t q = cluster_ctarank() & 1u;  // 0 = MMA leader
   const uint32_t lead_rank = 0;
   const bool leader = q == 0;
@@ -301,8 +311,14 @@ __global__ void __maxnreg__(kXformWarpsCfg == 4 ? 136 : 108)
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  pdl_wait();
+  // PDL. The weight planes are inputs of the call (apmm_cuda.h: readable before the previous
+  // kernel completes), so with early_w the raw-plane producer, the transform warps and the
+  // MMA issuer start at once: the first operand stages fill while the previous kernel (K1,
+  // expanding X) drains. The feature-code producer (K1's output) and the epilogue (rowsum(U_x),
+  // Y) wait for it.
+  if (!p.early_w || warp == 0 || (warp >= 4 && warp < kXformWarp0)) pdl_wait();
   if (threadIdx.x == 0) pdl_trigger();
+  stamp(1);
 
   if (warp == 0) {
     // ---------------- TMA producer (both CTAs) ----------------
@@ -349,6 +365,11 @@ __global__ void __maxnreg__(kXformWarpsCfg == 4 ? 136 : 108)
         const uint32_t idesc = un.ti.ncols != kPairN ? kIdescHalf : kIdesc;
         for (uint32_t kb = un.kb0; kb < un.kb1; ++kb) {
           mbar_wait_b<true>(&full_bar[stage], phase, 3, af);
+          if (p.ts && t == cluster && kb == un.kb0) {  // first operand stage ready
+            unsigned long long tt;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt));
+            p.ts[blockIdx.x * 8 + 2] = tt;
+          }
           tc_fence_after();
           const uint32_t st = smem_u32(stages + stage * kStageBytes);
           const uint64_t adesc = umma_desc_sw128(st);
@@ -361,6 +382,11 @@ __global__ void __maxnreg__(kXformWarpsCfg == 4 ? 136 : 108)
           if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
         mma_commit_pair_mc(&tmem_full[acc], 0x3);
+        if (p.ts) {  // last write = the last unit's MMAs issued
+          unsigned long long tt;
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt));
+          p.ts[blockIdx.x * 8 + 3] = tt;
+        }
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
       if (p.dbg) {
@@ -632,7 +658,14 @@ __global__ void __maxnreg__(kXformWarpsCfg == 4 ? 136 : 108)
       if (lane == 0) mbar_arrive_cluster(mapa(smem_u32(&tmem_empty[acc]), lead_rank));
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
-    if (lane == 0) bulk_wait<0>();
+    // the staging buffers must have been read before the CTA exits; the stores themselves
+    // complete with the grid (as CUTLASS's tma_store_wait), so no write round trip here
+    if (lane == 0) bulk_wait_read<0>();
+    if (p.ts && lane == 0 && warp == 4) {  // epilogue drained
+      unsigned long long tt;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt));
+      p.ts[blockIdx.x * 8 + 5] = tt;
+    }
     __syncwarp();
   }
 
@@ -640,6 +673,7 @@ __global__ void __maxnreg__(kXformWarpsCfg == 4 ? 136 : 108)
   cluster_sync();
   tc_fence_after();
   if (warp == 2) tmem_dealloc_pair<kTmemCols>(tmem_base);
+  stamp(4);
 }
 
 template <int NW>
@@ -769,6 +803,8 @@ cudaError_t launch_gemm_pair_wplanes(const GemmArgs& a, const uint32_t* w_planes
   const uint32_t tail = static_cast<uint32_t>(a.k_logical & 31);
   p.tail_mask = tail ? ((1u << tail) - 1u) : 0xffffffffu;
   p.dbg = a.dbg;
+  p.ts = a.trace;
+  p.early_w = a.early_w ? 1u : 0u;
   static const uint32_t ablate = [] {
     const char* e = APMM_DEV_ENV("APMM_FUSED_ABLATE");
     return e ? static_cast<uint32_t>(std::atoi(e)) : 0u;

@@ -391,7 +391,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (lane == 0) mbar_arrive_cluster(mapa(smem_u32(&tmem_empty[acc]), lead_rank));
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
-    if (lane == 0) bulk_wait<0>();
+    // the staging buffers must have been read before the CTA exits; the stores themselves
+    // complete with the grid (as CUTLASS's tma_store_wait), so no write round trip here
+    if (lane == 0) bulk_wait_read<0>();
     __syncwarp();
     if (p.ts && lane == 0 && warp == 4) p.ts[blockIdx.x * 8 + 4] = gtime_ns();
   }
@@ -467,6 +469,7 @@ cudaError_t launch_gemm_pair(const GemmArgs& a, cudaStream_t s, int* launches, b
     cudaMemsetAsync(ts_buf, 0, 512 * 8 * sizeof(unsigned long long), s);
     p.ts = ts_buf;
   }
+  if (a.trace) p.ts = a.trace;  // dev launch trace (APMM_TRACE)
   // clusters of 4 (X multicast across two pairs) when there are enough cluster tiles to
   // fill the machine, else plain pairs. APMM_PAIR_CLUSTER=2|4 forces one (testing).
   static const int forced = [] {

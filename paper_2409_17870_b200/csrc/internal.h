@@ -67,13 +67,15 @@ __host__ __device__ inline void raster_tile(uint32_t t, uint32_t tiles_m, uint32
 // be 0 (W untouched). zero_out[0, zero_bytes) (16-B multiple) is zeroed after the previous
 // kernel in the stream completed (Y of a split-K GEMM).
 // PDL: W rows are expanded before griddepcontrol.wait when early_w (weights may be read
-// while the previous kernel in the stream drains), X rows and the zeroing only after it.
+// while the previous kernel in the stream drains), X rows too when early_x (caller's
+// promise, APMM_OPT_EARLY_FEATURE_READ), the zeroing always after it.
 cudaError_t launch_expand(const uint32_t* w_planes, uint64_t rows_w, int n_w,
                           uint8_t* w_codes, int32_t* w_rowsum, const uint32_t* x_planes,
                           uint64_t rows_x, uint64_t rows_x_pad, int n_x, uint8_t* x_codes,
                           int32_t* x_rowsum, uint64_t cols, uint64_t kpad, int num_sms,
                           cudaStream_t s, void* zero_out = nullptr, uint64_t zero_bytes = 0,
-                          bool early_w = true);
+                          bool early_w = true, bool early_x = false,
+                          unsigned long long* trace = nullptr, int blocks_per_sm = 1);
 cudaError_t launch_pack(const uint8_t* codes, uint64_t rows, uint64_t cols, int n,
                         uint32_t* planes, cudaStream_t s);
 cudaError_t launch_unpack(const uint32_t* planes, uint64_t rows, uint64_t cols, int n,
@@ -136,6 +138,8 @@ struct GemmArgs {
   // bits of |v| (atomicMax), or one global max when colmax_global; null = off
   unsigned* colmax = nullptr;
   bool colmax_global = false;
+  unsigned long long* trace = nullptr;  // dev (APMM_TRACE): per-CTA globaltimer stamps [grid][8]
+  bool early_w = true;  // PDL: the weight-plane GEMM may read W before the previous kernel ends
 };
 // Returns the number of kernel launches it enqueued via *launches.
 cudaError_t launch_gemm_tc(const GemmArgs& a, cudaStream_t s, int* launches);
@@ -175,6 +179,8 @@ struct SkinnyArgs {
   void* scratch_ws;  // skinny_scratch_bytes(): feature fragments (2 halves) + weight repack
   int ws_half;       // ping-pong half for the feature fragments (PDL overlap of calls)
   bool early_w = true;  // PDL: stream weight planes before the previous kernel completes
+  bool early_x = false;  // PDL: feature prep may read X before it (APMM_OPT_EARLY_FEATURE_READ)
+  unsigned long long* trace = nullptr;  // dev (APMM_TRACE): per-CTA stamps [grid][8]
   // measurement (bench kernel pass): when non-null, recorded right before / after the
   // streaming kernel's launch (after the feature-prep kernel), with `ev_flags`
   cudaEvent_t ev_start = nullptr, ev_stop = nullptr;

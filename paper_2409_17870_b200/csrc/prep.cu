@@ -13,6 +13,7 @@
 
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 
 #include "internal.h"
 
@@ -39,6 +40,7 @@ struct ExpandOperand {
   uint32_t rows;
   uint32_t rows_pad;  // rowsum[rows, rows_pad) is zeroed (GEMM epilogue reads whole tiles)
   int n;
+  int stream_store;   // 1: codes stored evict-first (st.global.cs), see launch_expand
 };
 
 constexpr int kExpandThreads = 128;  // small blocks: fit beside a resident GEMM CTA
@@ -108,8 +110,13 @@ __device__ __forceinline__ int32_t expand_row(const ExpandOperand& op, uint32_t 
       transpose8(x[u]);
       if (w < kpad_words) {
         uint4* d = reinterpret_cast<uint4*>(dst_row + uint64_t(w) * 32u);
-        d[0] = make_uint4(x[u][0], x[u][1], x[u][2], x[u][3]);
-        d[1] = make_uint4(x[u][4], x[u][5], x[u][6], x[u][7]);
+        if (op.stream_store) {
+          __stcs(d, make_uint4(x[u][0], x[u][1], x[u][2], x[u][3]));
+          __stcs(d + 1, make_uint4(x[u][4], x[u][5], x[u][6], x[u][7]));
+        } else {
+          d[0] = make_uint4(x[u][0], x[u][1], x[u][2], x[u][3]);
+          d[1] = make_uint4(x[u][4], x[u][5], x[u][6], x[u][7]);
+        }
       }
     }
   }
@@ -154,21 +161,37 @@ __global__ void __launch_bounds__(kExpandThreads) expand_kernel(ExpandOperand a,
                                                                  uint32_t wpr, uint32_t tail_mask,
                                                                  uint32_t kpad_words,
                                                                  uint4* zero_out, uint64_t zero_n,
-                                                                 uint32_t early_w) {
+                                                                 uint32_t early_w, uint32_t early_x,
+                                                                 unsigned long long* ts) {
+  // dev trace (APMM_TRACE): [0] start [1] W rows done [2] wait returned [3] end
+  auto stamp = [&](int k) {
+    if (ts && threadIdx.x == 0) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      ts[blockIdx.x * 8 + k] = t;
+    }
+  };
+  stamp(0);
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (!early_w) asm volatile("griddepcontrol.wait;" ::: "memory");
   const uint32_t warps = blockDim.x >> 5;
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t gwarp = blockIdx.x * warps + (threadIdx.x >> 5), nwarps = gridDim.x * warps;
   for (uint32_t r = gwarp; r < a.rows; r += nwarps) expand_one(a, r, wpr, tail_mask, kpad_words, lane);
+  // X rows continue the W rows' round robin, so a grid-stride pass over both stays balanced
+  const uint32_t xr0 = (gwarp + nwarps - a.rows % nwarps) % nwarps;
+  if (early_x) {
+    for (uint32_t r = xr0; r < b.rows; r += nwarps) expand_one(b, r, wpr, tail_mask, kpad_words, lane);
+  }
   if (blockIdx.x == 0) {
     for (uint32_t r = a.rows + threadIdx.x; r < a.rows_pad; r += blockDim.x) a.rowsum[r] = 0;
     for (uint32_t r = b.rows + threadIdx.x; r < b.rows_pad; r += blockDim.x) b.rowsum[r] = 0;
   }
+  stamp(1);
   if (early_w) asm volatile("griddepcontrol.wait;" ::: "memory");
-  // X rows continue the W rows' round robin, so a grid-stride pass over both stays balanced
-  for (uint32_t r = (gwarp + nwarps - a.rows % nwarps) % nwarps; r < b.rows; r += nwarps) {
-    expand_one(b, r, wpr, tail_mask, kpad_words, lane);
+  stamp(2);
+  if (!early_x) {
+    for (uint32_t r = xr0; r < b.rows; r += nwarps) expand_one(b, r, wpr, tail_mask, kpad_words, lane);
   }
   // split-K GEMMs reduce-add into Y: zero it here, after the previous kernel in the stream
   // (which may still have been writing the same Y) has completed
@@ -176,6 +199,8 @@ __global__ void __launch_bounds__(kExpandThreads) expand_kernel(ExpandOperand a,
        i += uint64_t(gridDim.x) * blockDim.x) {
     zero_out[i] = make_uint4(0, 0, 0, 0);
   }
+  __syncthreads();
+  stamp(3);
 }
 
 // ---- K1': codes -> planes (decompose_and_pack) -------------------------------------------
@@ -530,20 +555,33 @@ cudaError_t launch_expand(const uint32_t* w_planes, uint64_t rows_w, int n_w,
                           uint8_t* w_codes, int32_t* w_rowsum, const uint32_t* x_planes,
                           uint64_t rows_x, uint64_t rows_x_pad, int n_x, uint8_t* x_codes,
                           int32_t* x_rowsum, uint64_t cols, uint64_t kpad, int num_sms,
-                          cudaStream_t s, void* zero_out, uint64_t zero_bytes, bool early_w) {
+                          cudaStream_t s, void* zero_out, uint64_t zero_bytes, bool early_w,
+                          bool early_x, unsigned long long* trace, int blocks_per_sm) {
   const uint32_t wpr = static_cast<uint32_t>((cols + 31) / 32);
   const uint32_t tail = static_cast<uint32_t>(cols & 31);
   const uint32_t tail_mask = tail ? ((1u << tail) - 1u) : 0xffffffffu;
+  // Weight codes are written while the previous GEMM runs (PDL) and are far larger than its
+  // L2 working set at large shapes (70B FFN: 235 MB): streaming stores keep them from
+  // evicting the running GEMM's operand tiles. APMM_K1_CS (dev builds) overrides: bit 0 =
+  // weights, bit 1 = features.
+  static const int cs_env = [] {
+    const char* e = APMM_DEV_ENV("APMM_K1_CS");
+    return e ? std::atoi(e) : -1;
+  }();
+  const int cs_w = cs_env >= 0 ? (cs_env & 1) : 1, cs_x = cs_env >= 0 ? ((cs_env >> 1) & 1) : 0;
   const ExpandOperand a{w_planes, w_codes, w_rowsum, static_cast<uint32_t>(rows_w),
-                        static_cast<uint32_t>(rows_w), n_w};
+                        static_cast<uint32_t>(rows_w), n_w, cs_w};
   const ExpandOperand b{x_planes, x_codes, x_rowsum, static_cast<uint32_t>(rows_x),
-                        static_cast<uint32_t>(rows_x_pad), n_x};
+                        static_cast<uint32_t>(rows_x_pad), n_x, cs_x};
   const uint64_t warps_needed = rows_w + rows_x;
   uint64_t blocks = (warps_needed + kExpandThreads / 32 - 1) / (kExpandThreads / 32);
   if (zero_bytes && blocks < uint64_t(num_sms)) blocks = num_sms;  // the zeroing is grid-wide
-  // one block per SM: all blocks fit beside a resident GEMM CTA (regs: 8 x 200 x 32 +
-  // 4 x 80 x 32 <= 64K), so none is left waiting behind blocks parked in griddepcontrol.wait
-  const uint64_t cap = uint64_t(num_sms);
+  // one block per SM when the launch overlaps a running GEMM (early reads): every block fits
+  // beside the resident GEMM CTA (regs: 8 x 192 x 32 + 4 x 80 x 32 <= 64K), so none is left
+  // waiting behind blocks parked in griddepcontrol.wait. A launch that only works after the
+  // previous kernel completed (blocks_per_sm > 1) has the whole machine: more warps, more
+  // loads in flight (the expansion is latency bound at one 4-warp block per SM).
+  const uint64_t cap = uint64_t(num_sms) * uint64_t(blocks_per_sm < 1 ? 1 : blocks_per_sm);
   if (blocks > cap) blocks = cap;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(static_cast<unsigned>(blocks));
@@ -558,7 +596,7 @@ cudaError_t launch_expand(const uint32_t* w_planes, uint64_t rows_w, int n_w,
   cudaError_t e = cudaLaunchKernelEx(&cfg, expand_kernel, a, b, wpr, tail_mask,
                                      static_cast<uint32_t>(kpad / 32),
                                      static_cast<uint4*>(zero_out), zero_bytes / 16,
-                                     early_w ? 1u : 0u);
+                                     early_w ? 1u : 0u, early_x ? 1u : 0u, trace);
   return e != cudaSuccess ? e : cudaGetLastError();
 }
 

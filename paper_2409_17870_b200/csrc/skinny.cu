@@ -239,16 +239,18 @@ APMM_DEV void transpose8(uint32_t (&x)[8]) {
 
 // ---- feature prep: X planes -> fragment-order codes + rowsum(U_x) -----------------------
 // grid (ceil(chunks_total*16 / 256), rows_x); thread = (feature row, 32-column word).
-// PDL: triggers its dependents at once (the streaming kernel's weight loads may start),
-// but reads the caller's X planes and writes its workspace half only after
-// griddepcontrol.wait: X may be the output of the previous kernel in the stream.
+// PDL: triggers its dependents at once (the streaming kernel's weight loads may start). It
+// reads the caller's X planes only after griddepcontrol.wait (X may be the output of the
+// previous kernel in the stream) unless early_x (APMM_OPT_EARLY_FEATURE_READ), and writes
+// its workspace half only after it.
 __global__ void __launch_bounds__(kPrepThreads) prep_x_kernel(const uint32_t* __restrict__ x,
                                                               uint32_t rows_x, uint32_t wpr,
                                                               int n_x, uint32_t words_pad,
                                                               uint8_t* __restrict__ xfrag,
-                                                              int32_t* __restrict__ rsx_part) {
+                                                              int32_t* __restrict__ rsx_part,
+                                                              uint32_t early_x) {
   apmm_ptx::pdl_trigger();
-  apmm_ptx::pdl_wait();
+  if (!early_x) apmm_ptx::pdl_wait();
   const uint32_t tok = blockIdx.y, W = blockIdx.x * kPrepThreads + threadIdx.x;
   const uint32_t xr = frag_rows(rows_x);
   uint32_t v[8];
@@ -262,6 +264,7 @@ __global__ void __launch_bounds__(kPrepThreads) prep_x_kernel(const uint32_t* __
     if (real && i < n_x) rs += __popc(v[i]) << i;
   }
   if (real) transpose8(v);
+  if (early_x) apmm_ptx::pdl_wait();  // the workspace half may be written only now
   if (W < words_pad) {
     const uint32_t cl = W / kChunkWords, t = (W % kChunkWords) >> 2, w = W & 3u;
     uint4* dst = reinterpret_cast<uint4*>(xfrag + uint64_t(cl) * chunk_bytes_m(xr)) +
@@ -851,6 +854,7 @@ cudaError_t launch_skinny(const SkinnyArgs& a, cudaStream_t s) {
     cudaMemsetAsync(ts_buf, 0, 1024 * 8 * sizeof(unsigned long long), s);
     p.ts = ts_buf;
   }
+  if (a.trace) p.ts = a.trace;  // dev launch trace (APMM_TRACE)
 
   if (!inprep) {  // feature prep (same shared-memory carveout as the streaming kernel: no reconfig)
     static DeviceBits carve_set;
@@ -869,7 +873,8 @@ cudaError_t launch_skinny(const SkinnyArgs& a, cudaStream_t s) {
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     cudaError_t e = cudaLaunchKernelEx(&cfg, prep_x_kernel, a.x_planes, p.rows_x, p.wpr, a.n_x,
-                                       p.chunks_total * kChunkWords, xfrag, rsx);
+                                       p.chunks_total * kChunkWords, xfrag, rsx,
+                                       a.early_x ? 1u : 0u);
     if (e != cudaSuccess) return e;
   }
   if (a.ev_start) cudaEventRecordWithFlags(a.ev_start, s, a.ev_flags);

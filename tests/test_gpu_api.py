@@ -202,9 +202,10 @@ def test_context_is_bound_to_one_stream(gpu):
     torch.cuda.synchronize()
 
 
-def test_early_weight_read_off_is_bit_identical(gpu, oracle):
-    """APMM_OPT_EARLY_WEIGHT_READ = 0 (every operand read after the previous kernel) gives
-    the same bits on the expand + GEMM and skinny routes."""
+def test_early_read_options_are_bit_identical(gpu, oracle):
+    """APMM_OPT_EARLY_WEIGHT_READ = 0 (every operand read after the previous kernel) and
+    APMM_OPT_EARLY_FEATURE_READ = 1 (features read early too) give the same bits on the
+    expand + GEMM and skinny routes."""
     import torch
     ap, _ = gpu
     ctx = ap.Context(0)
@@ -218,5 +219,10 @@ def test_early_weight_read_off_is_bit_identical(gpu, oracle):
         ctx.set_early_weight_read(False)
         ap.cu_matmul_ap(wp, n_out, 2, xp, m_tok, 4, k, y2, ctx)
         ctx.set_early_weight_read(True)
+        y3 = torch.empty_like(y1)
+        ctx.set_early_feature_read(True)
+        ap.cu_matmul_ap(wp, n_out, 2, xp, m_tok, 4, k, y3, ctx)
+        ap.cu_matmul_ap(wp, n_out, 2, xp, m_tok, 4, k, y3, ctx)
+        ctx.set_early_feature_read(False)
         torch.cuda.synchronize()
-        assert torch.equal(y1, y2)
+        assert torch.equal(y1, y2) and torch.equal(y1, y3)

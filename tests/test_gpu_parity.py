@@ -532,8 +532,9 @@ def test_reference_run_verify_with_gpu_kernel():
     for seed in ("1", "2"):
         r = subprocess.run([exe, seed, "1000"], capture_output=True, text=True, timeout=600)
         assert r.returncode == 0, r.stdout + r.stderr
-        assert r.stdout.count("PASS") == 11 and "mutant kernel caught" in r.stdout
+        assert r.stdout.count("PASS") == 12 and "mutant kernel caught" in r.stdout
         assert "PASS compute_plane_products + recover on the device" in r.stdout
+        assert "PASS xor_identity / dot_1bit_xor / matmul_plane_pair through the drop-in" in r.stdout
 
 
 def test_host_api_row_block_pipeline(gpu, oracle):
