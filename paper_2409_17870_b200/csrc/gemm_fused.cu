@@ -364,7 +364,11 @@ __global__ void __maxnreg__(kXformWarpsCfg == 4 ? 136 : 108)
         const Unit un = unit_info(t, p);
         const uint32_t idesc = un.ti.ncols != kPairN ? kIdescHalf : kIdesc;
         for (uint32_t kb = un.kb0; kb < un.kb1; ++kb) {
-          mbar_wait_b<true>(&full_bar[stage], phase, 3, af);
+          // CTA-scope acquire (as CUTLASS's ClusterBarrier::wait): the stage is read by the
+          // tensor core (async proxy); the writers fenced their generic stores to the async
+          // proxy before arriving. The cluster-scope form invalidated L1 (CCTL.IVALL) on every
+          // poll (ncu source view, profiles/r02_ncu_mid_wplanes.txt).
+          mbar_wait_b(&full_bar[stage], phase, 3, af);
           if (p.ts && t == cluster && kb == un.kb0) {  // first operand stage ready
             unsigned long long tt;
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt));
@@ -427,7 +431,7 @@ __global__ void __maxnreg__(kXformWarpsCfg == 4 ? 136 : 108)
     const uint32_t sw = row & 7u;
     const uint32_t fb0 = mapa(smem_u32(&full_bar[0]), lead_rank);
     uint32_t stage = 0, phase = 0, rs = 0, rphase = 0;
-    uint32_t x[kWPT][8];
+    uint32_t xa[kWPT][8];
     unsigned long long c_raw = 0;
     uint32_t rsum = 0, rbuf = 0, rphase_e = 0;  // split mode: this unit's rowsum partial
     // the flat sequence of (unit, K block) this CTA's MMA consumes: cursor (fu, fkb) = the
@@ -448,7 +452,7 @@ __global__ void __maxnreg__(kXformWarpsCfg == 4 ? 136 : 108)
         cursor_load();
       }
     };
-    auto fetch = [&](uint32_t kb) {  // raw planes of K block kb -> codes in x
+    auto fetch = [&](uint32_t kb, uint32_t (&x)[kWPT][8]) {  // raw planes of block kb -> codes
       const uint32_t j = (kb - fkb0) % kRB;  // K block within the raw stage (stages start at kb0)
       if (j == 0) {
         const unsigned long long r0 = p.dbg ? clock64() : 0;
@@ -511,7 +515,7 @@ __global__ void __maxnreg__(kXformWarpsCfg == 4 ? 136 : 108)
     unsigned long long c_empty = 0, c_fetch = 0, c_pub = 0;
     const unsigned long long t_loop = clock64();
     bool have = fu < num_tiles;
-    if (have) fetch(fkb);
+    if (have) fetch(fkb, xa);
     while (have) {
       const unsigned long long t0 = p.dbg ? clock64() : 0;
       mbar_wait_b(&empty_bar[stage], phase ^ 1, 7);  // the MMA is done with this A slot
@@ -521,13 +525,14 @@ __global__ void __maxnreg__(kXformWarpsCfg == 4 ? 136 : 108)
       for (int u = 0; u < kWPT; ++u) {
         if (p.ablate & 1) break;
         const uint32_t c = 2u * (w0 + u);  // word w -> 16-B chunks 2w, 2w+1 of the 128-B row
-        st_shared_v4(arow + ((c ^ sw) << 4), x[u][0], x[u][1], x[u][2], x[u][3]);
-        st_shared_v4(arow + (((c + 1u) ^ sw) << 4), x[u][4], x[u][5], x[u][6], x[u][7]);
+        st_shared_v4(arow + ((c ^ sw) << 4), xa[u][0], xa[u][1], xa[u][2], xa[u][3]);
+        st_shared_v4(arow + (((c + 1u) ^ sw) << 4), xa[u][4], xa[u][5], xa[u][6], xa[u][7]);
       }
-      // next block's codes while the stores drain; then publish this stage
+      // next block's codes while the stores drain; then publish this stage (a two-block
+      // variant with both blocks in flight per iteration measured ~3% slower, r02 notes)
       cursor_next();
       have = fu < num_tiles;
-      if (have) fetch(fkb);
+      if (have) fetch(fkb, xa);
       const unsigned long long t2 = p.dbg ? clock64() : 0;
       if (!(p.ablate & 4)) fence_proxy_async_smem();  // generic stores -> async proxy (MMA)
       __syncwarp();
@@ -587,6 +592,11 @@ __global__ void __maxnreg__(kXformWarpsCfg == 4 ? 136 : 108)
       }
       mbar_wait_b(&tmem_full[acc], acc_phase, 5);
       tc_fence_after();
+      if (p.ts && lane == 0 && warp == 4) {  // accumulator ready (last write = last unit)
+        unsigned long long tt;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt));
+        p.ts[blockIdx.x * 8 + 6] = tt;
+      }
       const uint32_t t_addr = tmem_base + ((wq * 32u) << 16) + acc * kPairN;
 #pragma unroll 1
       for (uint32_t c = 0; c < ti.ncols / 32; ++c) {
@@ -657,6 +667,11 @@ __global__ void __maxnreg__(kXformWarpsCfg == 4 ? 136 : 108)
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(mapa(smem_u32(&tmem_empty[acc]), lead_rank));
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      if (p.ts && lane == 0 && warp == 4) {  // chunks issued (last write = last unit)
+        unsigned long long tt;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt));
+        p.ts[blockIdx.x * 8 + 7] = tt;
+      }
     }
     // the staging buffers must have been read before the CTA exits; the stores themselves
     // complete with the grid (as CUTLASS's tma_store_wait), so no write round trip here

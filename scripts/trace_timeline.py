@@ -50,7 +50,8 @@ n = fn(ctx.h, buf.ctypes.data, kinds.ctypes.data)
 t = buf.reshape(slots, 1024, 8).astype(np.float64)
 names = {1: ("expand", ["start", "w_done", "waited", "end"]),
          2: ("pair", ["start", "pdl_wait", "first_full", "last_issue", "end"]),
-         3: ("wplanes", ["start", "pdl_wait", "first_full", "last_issue", "end", "epi_done"]),
+         3: ("wplanes", ["start", "pdl_wait", "first_full", "last_issue", "end", "epi_done",
+                         "acc_ready", "chunks_out"]),
          5: ("skinny", ["start", "pdl_wait", "x_ready", "item0", "tile0", "end", "inited", "issued"])}
 t0 = min(t[i][t[i] > 0].min() for i in range(slots) if (t[i] > 0).any())
 print(f"{n_out}x{m}x{k} W{nw}A{nx}: {calls} calls, {1e3 * e0.elapsed_time(e1) / calls:.2f} us/call (graph)")
