@@ -635,6 +635,42 @@ def run_ours(args, rank, world, local_rank):
             "note": ("GEMM + dequant/absmax epilogue + absmax all-reduce + requant/pack + packed "
                      "all-gather, per step; W rows split on 32-row word boundaries")}
 
+    # -- single GPU: the layer form the next layer consumes, timed on its
+    #    own: GEMM + dequant epilogue with the per-token absmax fused in + requantize/pack of
+    #    X' = dequant(Y)^T to A4 planes (apmm_cu_matmul_ap_requant), vs the int32 GEMM above
+    requant = None
+    if not sharded and args.workload in SHARDED:
+        g0 = gemms[0]
+        n_out, m_tok, k, nw, nx = g0
+        wps, xps, _ = bufs[0]
+        sw = torch.rand(n_out, dtype=torch.float64, device=dev, generator=gen) + 0.5
+        sx = torch.rand(m_tok, dtype=torch.float64, device=dev, generator=gen) + 0.5
+        yf = torch.empty((n_out, m_tok), dtype=torch.float32, device=dev)
+        n_next = 4
+        nplanes = torch.empty(n_next * m_tok * (-(-n_out // 32)), dtype=torch.int32, device=dev)
+        nscales = torch.empty(m_tok, dtype=torch.float64, device=dev)
+
+        def rq_step():
+            ap.cu_matmul_ap_requant(wps[0], n_out, nw, sw, 1, xps[0], m_tok, nx, sx, 1, k, n_next,
+                                    1, yf, nplanes, nscales, ctx=ctx, stream=stream)
+        for _ in range(2):
+            rq_step()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = max(3, min(args.steps, 10))
+        e0.record(stream)
+        for _ in range(reps):
+            rq_step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        rq_ms = e0.elapsed_time(e1) / reps
+        requant = {"api": "apmm_cu_matmul_ap_requant (W2A4 GEMM -> dequant + absmax -> A4 planes)",
+                   "ms_per_step": rq_ms, "TOPS": ops_step / (rq_ms * 1e-3) / 1e12,
+                   "out_bytes": int(nplanes.numel() * 4 + nscales.numel() * 8),
+                   "out_bytes_int32_Y": int(4 * n_out * m_tok),
+                   "note": "eager launches, includes the NonFinite check's stream sync per call"}
+        del yf
+
     # -- e2e through the public host API: pinned host planes -> H2D -> GEMM -> D2H int32
     e2e_steps = max(1, min(args.steps, 3))
     host = []
@@ -751,6 +787,8 @@ def run_ours(args, rank, world, local_rank):
     }
     if gather is not None:
         line["gather"] = gather
+    if requant is not None:
+        line["next_layer_requant"] = requant
     if world == 1 and not args.no_cpu_baseline:
         try:
             ref = CpuReference(gemms, cpu_threads(), 10.0)

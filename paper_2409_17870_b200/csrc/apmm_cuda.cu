@@ -307,8 +307,8 @@ unsigned long long* trace_slot(apmm_ctx* ctx, int kind) {
 }
 
 // blocks per SM of an expansion launch that runs after the previous kernel completed
-// (4 x 128 threads x 80 registers: one wave on every SM)
-constexpr int kK1xBlocksPerSm = 4;
+// (6 x 128 threads x 80 registers = 61440 <= 64K: one wave on every SM)
+constexpr int kK1xBlocksPerSm = 6;
 
 // requant absmax scratch: rows_x u32 (+ 1 for the global max), 16-byte multiple (K1 zeroes it)
 uint64_t colmax_bytes(uint64_t rows_x) { return round_up((rows_x + 1) * 4, 16); }
