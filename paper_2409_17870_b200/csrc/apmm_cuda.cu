@@ -437,7 +437,10 @@ int run_matmul(apmm_ctx* ctx, const uint32_t* w, uint64_t rows_w, int n_w, const
   a.num_sms = ctx->num_sms;
   a.trace = route == Route::Single ? nullptr
                                     : trace_slot(ctx, route == Route::Mid || route == Route::PairW ? 3 : 2);
-  a.colmax = route == Route::PairW ? nullptr : colmax;
+  // dev A/B (APMM_COLMAX_PASS=1): the absmax as a separate pass over yf on every route
+  static const bool colmax_pass = APMM_DEV_ENV("APMM_COLMAX_PASS") != nullptr;
+  const bool epi_colmax = route != Route::PairW && !colmax_pass;
+  a.colmax = epi_colmax ? colmax : nullptr;
   a.early_w = ctx->early_w;
   a.colmax_global = colmax_global;
   if (ctx->dbg_waits) {
@@ -459,7 +462,7 @@ int run_matmul(apmm_ctx* ctx, const uint32_t* w, uint64_t rows_w, int n_w, const
     }
   }
   ctx->launches += static_cast<uint64_t>(launches);
-  if (colmax && route == Route::PairW) {  // K3f's epilogue does not form the column absmax
+  if (colmax && !epi_colmax) {  // K3f's epilogue does not form the column absmax
     CU(launch_colmax(yf, rows_w, rows_x, colmax, colmax_global, ctx->num_sms, stream));
     ctx->launches += 1;
   }

@@ -251,6 +251,53 @@ __device__ __forceinline__ uint32_t quantize_code(double x, double s, int maxv) 
   return static_cast<uint32_t>((qi + maxv) / 2);
 }
 
+// Same result as quantize_code without the fp64 division and without fp64 conversions
+// (cvt runs on a slow pipe) on almost every element. The code depends on x / s only through
+// h = floor(RN(x/s) / 2) = floor(RN(x / (2s))) (halving is exact). With r2 = RN(1 / (2s)),
+// u = RN(x * r2) is within ~2 ulps of RN(x / (2s)), |u| <= 2^8 for every admissible code, so
+// |u - RN(x/(2s))| < 2^-43. floor(u) comes from the 1.5 * 2^52 rounding trick (two DADDs,
+// integer bits). If u lies farther than 2^-40 from an integer, floor(u) is the reference's
+// floor; otherwise (values on a grid boundary, subnormal quotients) the exact division
+// decides. Zero maps to q = 1 directly (x / s = +-0).
+// r2 = RN(1 / (2s)) for the fast paths, or 0 (u = 0 lands in the guard band, so every element
+// takes the exact division) when it would not be a normal double with margin
+__device__ __forceinline__ double fast_recip(double s) {
+  const double r2 = __ddiv_rn(1.0, __dmul_rn(2.0, s));
+  return (r2 >= 0x1p-1000 && r2 <= 0x1p1000) ? r2 : 0.0;
+}
+__device__ __forceinline__ uint32_t code_of_q(int q, int maxv) {
+  q = q > maxv ? maxv : (q < -maxv ? -maxv : q);
+  return static_cast<uint32_t>((q + maxv) / 2);
+}
+__device__ __forceinline__ uint32_t quantize_code_fast(double x, double s, double r2, int maxv) {
+  if (x == 0.0) return static_cast<uint32_t>((1 + maxv) / 2);
+  const double u = __dmul_rn(x, r2);
+  if (fabs(u) < 0x1p40) {
+    const double t = __dadd_rn(u, 6755399441055744.0);  // 1.5 * 2^52: RN(u) in the low bits
+    const double back = __dsub_rn(t, 6755399441055744.0);
+    int n = __double2loint(t);
+    const bool above = back > u;
+    const double frac = __dsub_rn(u, above ? __dsub_rn(back, 1.0) : back);
+    if (frac > 0x1p-40 && frac < 1.0 - 0x1p-40) return code_of_q(2 * (n - (above ? 1 : 0)) + 1, maxv);
+  }
+  return quantize_code(x, s, maxv);
+}
+// f32 input (the dequantized GEMM output): the approximation in FP32 (error < 2^-15 for
+// |u| <= 2^8) with a 2^-14 guard band, the exact fp64 path otherwise.
+__device__ __forceinline__ uint32_t quantize_code_f32(float v, double s, float r2f, int maxv) {
+  if (v == 0.0f) return static_cast<uint32_t>((1 + maxv) / 2);
+  const float u = __fmul_rn(v, r2f);
+  if (fabsf(u) < 4194304.0f) {
+    const float t = __fadd_rn(u, 12582912.0f);  // 1.5 * 2^23: RN(u) in the low bits
+    const float back = __fsub_rn(t, 12582912.0f);
+    const int n = __float_as_int(t) - 0x4B400000;
+    const bool above = back > u;
+    const float frac = __fsub_rn(u, above ? __fsub_rn(back, 1.0f) : back);
+    if (frac > 0x1p-14f && frac < 1.0f - 0x1p-14f) return code_of_q(2 * (n - (above ? 1 : 0)) + 1, maxv);
+  }
+  return quantize_code(static_cast<double>(v), s, maxv);
+}
+
 // Optional GEMM-operand output (K2 feeding K3 without planes): `codes` = u8 codes
 // [rows][kpad] in K1's permuted order (column 8b + c of each 32-column group at byte 4c + b).
 struct GemmCodesOut {
@@ -263,7 +310,7 @@ struct GemmCodesOut {
 __device__ __forceinline__ uint32_t quantize_pack_word(const double* __restrict__ xrow,
                                                        uint64_t r, uint64_t rows, uint64_t cols,
                                                        uint64_t w, int n, int maxv, double s,
-                                                       uint32_t* __restrict__ planes,
+                                                       double r2, uint32_t* __restrict__ planes,
                                                        uint8_t* __restrict__ codes,
                                                        const GemmCodesOut& g) {
   const uint32_t lane = threadIdx.x & 31;
@@ -271,7 +318,7 @@ __device__ __forceinline__ uint32_t quantize_pack_word(const double* __restrict_
   const uint64_t col = w * 32 + lane;
   uint32_t c = 0;
   if (col < cols) {
-    c = quantize_code(xrow[col], s, maxv);
+    c = quantize_code_fast(xrow[col], s, r2, maxv);
     if (codes) codes[r * cols + col] = static_cast<uint8_t>(c);
   }
   if (g.codes) {
@@ -326,11 +373,12 @@ __global__ void __launch_bounds__(kThreads)
     return;
   }
   const double s = m == 0.0 ? 1.0 : __ddiv_rn(m, double(maxv));  // bipolar.cpp:91
+  const double r2 = fast_recip(s);  // quantize_code_fast
   if (threadIdx.x == 0) scales[r] = s;
   const uint64_t wpr = (cols + 31) / 32;
   int32_t rsum = 0;
   for (uint64_t w = threadIdx.x >> 5; w < wpr; w += blockDim.x / 32) {
-    rsum += static_cast<int32_t>(quantize_pack_word(xrow, r, rows, cols, w, n, maxv, s, planes,
+    rsum += static_cast<int32_t>(quantize_pack_word(xrow, r, rows, cols, w, n, maxv, s, r2, planes,
                                                     codes, g));
   }
   if (g.codes) {
@@ -383,13 +431,14 @@ __global__ void __launch_bounds__(kThreads)
   const int maxv = (1 << n) - 1;
   const double m = __longlong_as_double(static_cast<long long>(*amax_bits));
   const double s = m == 0.0 ? 1.0 : __ddiv_rn(m, double(maxv));
+  const double r2 = fast_recip(s);  // quantize_code_fast
   if (blockIdx.x == 0 && threadIdx.x == 0) scales[0] = s;
   const uint64_t wpr = (cols + 31) / 32;
   const uint64_t gw = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   if (gw >= rows * wpr) return;
   const uint64_t r = gw / wpr, w = gw % wpr;
   int32_t c = static_cast<int32_t>(
-      quantize_pack_word(x + r * cols, r, rows, cols, w, n, maxv, s, planes, codes, g));
+      quantize_pack_word(x + r * cols, r, rows, cols, w, n, maxv, s, r2, planes, codes, g));
   if (g.codes) {  // one atomic per (row, word) into the zeroed rowsum
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
@@ -461,7 +510,16 @@ __global__ void __launch_bounds__(kThreads) colmax_kernel(const float* __restric
   const uint64_t r1 = r0 + rows_per_slab < rows_w ? r0 + rows_per_slab : rows_w;
   uint32_t m = 0;
   if (c < rows_x) {
-    for (uint64_t r = r0 + (threadIdx.x >> 5); r < r1; r += blockDim.x / 32) {
+    const uint64_t step = blockDim.x / 32;
+    uint64_t r = r0 + (threadIdx.x >> 5);
+    for (; r + 7 * step < r1; r += 8 * step) {  // 8 loads in flight per thread
+      uint32_t b[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) b[u] = __float_as_uint(__ldg(yf + (r + u * step) * rows_x + c));
+#pragma unroll
+      for (int u = 0; u < 8; ++u) m = (b[u] & 0x7fffffffu) > m ? (b[u] & 0x7fffffffu) : m;
+    }
+    for (; r < r1; r += step) {
       const uint32_t b = __float_as_uint(__ldg(yf + r * rows_x + c)) & 0x7fffffffu;
       m = b > m ? b : m;
     }
@@ -499,23 +557,32 @@ __global__ void double_to_bits_kernel(const double* in, uint64_t n, unsigned* bi
 }
 
 constexpr int kRqWords = 8;
+template <int N>
 __global__ void __launch_bounds__(kThreads) requant_pack_kernel(
     const float* __restrict__ yf, uint64_t rows_w, uint64_t rows_x, const unsigned* colmax,
-    int global, int n, uint32_t* __restrict__ planes, double* __restrict__ scales, int* flag) {
+    int global, uint32_t* __restrict__ planes, double* __restrict__ scales, int* flag) {
+  constexpr int n = N;  // planes of the next layer's activation (compile time: the bit
+                        // inserts below run for live planes only)
   __shared__ uint32_t sw[8][32][kRqWords + 1];
   const uint32_t lane = threadIdx.x & 31, q = threadIdx.x >> 5;
   const uint64_t wpr = (rows_w + 31) / 32;
-  const uint64_t t = uint64_t(blockIdx.y) * 32 + lane;
-  const uint64_t w = uint64_t(blockIdx.x) * kRqWords + q;
+  // blockIdx.x = token block (fastest): the resident blocks read whole rows of yf (all
+  // tokens) at once, so DRAM pages are used fully (word groups first read 128 B per row)
+  const uint64_t t = uint64_t(blockIdx.x) * 32 + lane;
+  const uint64_t w = uint64_t(blockIdx.y) * kRqWords + q;
   const int maxv = (1 << n) - 1;
   const uint32_t mbits = global ? colmax[0] : (t < rows_x ? colmax[t] : 0u);
   const double m = static_cast<double>(__uint_as_float(mbits));
   const bool finite = mbits < 0x7f800000u;
   if (!finite && t < rows_x) atomicOr(flag, 1);
   const double s = m == 0.0 ? 1.0 : __ddiv_rn(m, double(maxv));  // bipolar.cpp:91
-  if (blockIdx.x == 0 && q == 0 && finite) {
+  const double r2 = fast_recip(s);
+  // fast FP32 path only where RN(1/(2s)) is a normal float with margin (else r2f = 0: every
+  // element takes the exact path, see quantize_code_f32)
+  const float r2f = (r2 >= 0x1p-120 && r2 <= 0x1p120) ? static_cast<float>(r2) : 0.0f;
+  if (blockIdx.y == 0 && q == 0 && finite) {
     if (global) {
-      if (blockIdx.y == 0 && lane == 0) scales[0] = s;
+      if (blockIdx.x == 0 && lane == 0) scales[0] = s;
     } else if (t < rows_x) {
       scales[t] = s;
     }
@@ -524,23 +591,25 @@ __global__ void __launch_bounds__(kThreads) requant_pack_kernel(
   if (t < rows_x && w < wpr && finite) {
     const uint64_t r0 = w * 32;
     const uint32_t nr = rows_w - r0 < 32 ? static_cast<uint32_t>(rows_w - r0) : 32u;
-    for (uint32_t j = 0; j < nr; ++j) {
-      const double v = static_cast<double>(__ldg(yf + (r0 + j) * rows_x + t));
-      const uint32_t c = quantize_code(v, s, maxv);
+    // all 32 loads first (one memory round trip per thread, not 32 dependent ones)
+    float v[32];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) word[i] |= ((c >> i) & 1u) << j;
+    for (uint32_t j = 0; j < 32; ++j) v[j] = j < nr ? __ldg(yf + (r0 + j) * rows_x + t) : 0.0f;
+#pragma unroll
+    for (uint32_t j = 0; j < 32; ++j) {
+      const uint32_t c = j < nr ? quantize_code_f32(v[j], s, r2f, maxv) : 0u;
+#pragma unroll
+      for (int i = 0; i < N; ++i) word[i] |= ((c >> i) & 1u) << j;
     }
   }
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    if (i < n) sw[i][lane][q] = word[i];
-  }
+  for (int i = 0; i < N; ++i) sw[i][lane][q] = word[i];
   __syncthreads();
   // write out: thread = (plane i, token, word) with the word index fastest
-  const uint64_t w0 = uint64_t(blockIdx.x) * kRqWords;
+  const uint64_t w0 = uint64_t(blockIdx.y) * kRqWords;
   for (uint32_t e = threadIdx.x; e < uint32_t(n) * 32u * kRqWords; e += blockDim.x) {
     const uint32_t qq = e % kRqWords, tok = (e / kRqWords) % 32, i = e / (kRqWords * 32);
-    const uint64_t tt = uint64_t(blockIdx.y) * 32 + tok, ww = w0 + qq;
+    const uint64_t tt = uint64_t(blockIdx.x) * 32 + tok, ww = w0 + qq;
     if (tt < rows_x && ww < wpr) planes[(uint64_t(i) * rows_x + tt) * wpr + ww] = sw[i][tok][qq];
   }
 }
@@ -740,10 +809,18 @@ cudaError_t launch_requant_pack(const float* yf, uint64_t rows_w, uint64_t rows_
                                 const unsigned* colmax, bool global, int n, uint32_t* planes,
                                 double* scales, int* flag, cudaStream_t s) {
   const uint64_t wpr = (rows_w + 31) / 32;
-  const dim3 grid(static_cast<unsigned>((wpr + kRqWords - 1) / kRqWords),
-                  static_cast<unsigned>((rows_x + 31) / 32));
-  requant_pack_kernel<<<grid, kThreads, 0, s>>>(yf, rows_w, rows_x, colmax, global ? 1 : 0, n,
-                                                planes, scales, flag);
+  const dim3 grid(static_cast<unsigned>((rows_x + 31) / 32),
+                  static_cast<unsigned>((wpr + kRqWords - 1) / kRqWords));
+  switch (n) {
+#define APMM_RQ(NN) \
+  case NN: \
+    requant_pack_kernel<NN><<<grid, kThreads, 0, s>>>(yf, rows_w, rows_x, colmax, global ? 1 : 0, \
+                                                      planes, scales, flag); \
+    break;
+    APMM_RQ(1) APMM_RQ(2) APMM_RQ(3) APMM_RQ(4) APMM_RQ(5) APMM_RQ(6) APMM_RQ(7) APMM_RQ(8)
+#undef APMM_RQ
+    default: return cudaErrorInvalidValue;
+  }
   return cudaGetLastError();
 }
 

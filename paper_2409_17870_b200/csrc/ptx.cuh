@@ -252,6 +252,7 @@ __host__ __device__ constexpr uint32_t idesc_i8_u8u8(uint32_t M, uint32_t N) {
 }
 
 // ---- epilogue helpers -------------------------------------------------------------
+
 // Column absmax of a warp's 32 x 32 output block (lane = row, f[j] = float bits of column
 // col0 + j, 0 for masked entries) for the next layer's quantizer. |v| as u32 bits orders
 // like |v| (NaN above inf, so a non-finite output is visible in the max). Transpose-reduce

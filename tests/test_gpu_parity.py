@@ -476,6 +476,25 @@ def test_quantize_bit_exact(gpu, oracle, golden):
             q = ap.quantize(x, ap.BitWidth(n), ap.Granularity(gran), ctx)
             c, s = oracle.quantize(x, n, gran)
             assert np.array_equal(q.codes, c) and np.array_equal(q.scales, s)
+    # grid-boundary inputs: values at and within a few ulps of every multiple of the scale
+    # (where floor(x / (2s)) flips), exact zeros, tiny and huge magnitudes -- the quantizer's
+    # reciprocal fast path must hand every such element to the exact division
+    for n in (1, 2, 3, 4, 8):
+        maxv = (1 << n) - 1
+        for amax in (float(maxv), 1.0, 3.0e-300, 7.25e250, 0.1):
+            sc = amax / maxv
+            ks = np.arange(-maxv - 1, maxv + 2, dtype=np.float64)
+            base = ks * sc
+            x = np.concatenate([base, np.nextafter(base, np.inf), np.nextafter(base, -np.inf),
+                                np.nextafter(np.nextafter(base, np.inf), np.inf),
+                                np.nextafter(np.nextafter(base, -np.inf), -np.inf), [0.0, -0.0]])
+            x = np.clip(x, -amax, amax)
+            x[0] = amax  # the absmax (and so the scale) is exactly `amax`
+            x = np.ascontiguousarray(np.tile(x, (3, 1)))
+            for gran in (PER_TENSOR, PER_ROW):
+                q = ap.quantize(x, ap.BitWidth(n), ap.Granularity(gran), ctx)
+                c, sref = oracle.quantize(x, n, gran)
+                assert np.array_equal(q.codes, c) and np.array_equal(q.scales, sref), (n, amax)
     with pytest.raises(ap.NonFinite):
         ap.quantize(np.array([[1.0, np.nan]]), ap.BitWidth(2), ap.Granularity.PerTensor, ctx)
     with pytest.raises(ap.NonFinite):
