@@ -114,9 +114,11 @@ struct SkinnyParams {
   uint32_t m2, m4, m16, neg1;
   unsigned long long* ts;    // APMM_SKINNY_TS=1 (dev only): per-CTA phase timestamps, else null
   uint32_t early_w;          // PDL: weight loads may start before the previous kernel completes
+  uint32_t ts_clock;         // dev: stamps are the SM's clock64 (cycle resolution, per CTA) instead
+  uint32_t l2_prefetch;      // 1: L2-prefetch each warp's next item ahead of its TMA load
 };
 
-APMM_DEV unsigned long long gtime() {
+APMM_DEV unsigned long long gtime_ns() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
@@ -300,7 +302,11 @@ __global__ void __launch_bounds__(sk_threads(N, NT), sk_ctas_per_sm(N, NT))
 
   const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t g = lane >> 2, t = lane & 3;
-  if (p.ts && tid == 0) p.ts[blockIdx.x * 8 + 0] = gtime();
+  if (p.ts && tid == 0) p.ts[blockIdx.x * 8 + 0] = (p.ts_clock ? static_cast<unsigned long long>(clock64()) : gtime_ns());
+  // dev (APMM_TRACE_CLOCK): cycle stamps of the individual prologue steps, thread 0 only
+  auto fine = [&](int k) {
+    if (p.ts && p.ts_clock && tid == 0) p.ts[blockIdx.x * 8 + k] = clock64();
+  };
   const uint32_t warps_k = WARPS / p.rgroups;
   const uint32_t wr = warp / warps_k, wk = warp % warps_k;
   const uint32_t tile_rows = 16u * p.rgroups;
@@ -325,14 +331,18 @@ __global__ void __launch_bounds__(sk_threads(N, NT), sk_ctas_per_sm(N, NT))
     if (warp == 0) {
       for (int i = 0; i < kXPieces; ++i) apmm_ptx::mbar_init(&xbars[i], 1);
     }
+    fine(1);
     // mbarrier inits -> visible to the TMA unit (async proxy). A non-cluster launch needs
     // no cluster-scope release (fence.mbarrier_init.release.cluster cost ~0.8 us per CTA at
     // kernel start, profiles/r01b_skinny_phase_ts2.txt).
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    fine(2);
     apmm_ptx::tma_prefetch_desc(&tmap_w);
+    fine(3);
   }
   __syncwarp();
   const uint64_t hint = apmm_ptx::policy_evict_first();  // weights are read exactly once
+  fine(4);
 
   // ---- per-warp TMA ring: item cursor (tile index, chunk step) ----
   // L2 prefetch cursor, kPrefetch items ahead of the ring: the weight stream runs at HBM
@@ -340,7 +350,7 @@ __global__ void __launch_bounds__(sk_threads(N, NT), sk_ctas_per_sm(N, NT))
   // HBM serves it) while the shallow shared-memory ring refills from L2.
   uint32_t pf_tile = 0, pf_c = 0;
   auto prefetch_next = [&]() {
-    if (pf_tile < my_tiles) {
+    if (p.l2_prefetch && pf_tile < my_tiles) {
       const uint32_t chunk = s_begin + pf_c * warps_k + wk;
       if (chunk < s_end && lane == 0) {
         const uint32_t row0 = (j0 + pf_tile * gs) * tile_rows + wr * 16u;
@@ -367,13 +377,16 @@ __global__ void __launch_bounds__(sk_threads(N, NT), sk_ctas_per_sm(N, NT))
 
   // The weight planes are inputs of this call, so their loads may overlap the prep kernel
   // still running ahead of us (PDL); X, the workspace and Y only after pdl_wait.
-  if (p.ts && tid == 0) p.ts[blockIdx.x * 8 + 6] = gtime();
+  if (p.ts && !p.ts_clock && tid == 0) p.ts[blockIdx.x * 8 + 6] = gtime_ns();
   if (!p.early_w) apmm_ptx::pdl_wait();  // weights may be produced by the previous kernel
   for (uint32_t i = 0; i < stages - 1 + p.prefetch; ++i) prefetch_next();
+  fine(5);
   for (uint32_t s = 0; s + 1 < stages; ++s) issue();
-  if (p.ts && tid == 0) p.ts[blockIdx.x * 8 + 7] = gtime();
+  fine(6);
+  if (p.ts && !p.ts_clock && tid == 0) p.ts[blockIdx.x * 8 + 7] = gtime_ns();
   apmm_ptx::pdl_wait();
-  if (p.ts && tid == 0) p.ts[blockIdx.x * 8 + 1] = gtime();
+  fine(7);
+  if (p.ts && !p.ts_clock && tid == 0) p.ts[blockIdx.x * 8 + 1] = gtime_ns();
   __syncthreads();  // xbars initialised
   const uint32_t xpc = (p.slice_chunks + kXPieces - 1) / kXPieces;  // chunks per X piece
   if (p.inprep) {
@@ -434,7 +447,7 @@ __global__ void __launch_bounds__(sk_threads(N, NT), sk_ctas_per_sm(N, NT))
     for (uint32_t q = tid; q < tile_rows * M_PAD; q += THREADS) red[q] = 0u;
     __syncthreads();
   }
-  if (p.ts && tid == 0) p.ts[blockIdx.x * 8 + 2] = gtime();
+  if (p.ts && !p.ts_clock && tid == 0) p.ts[blockIdx.x * 8 + 2] = gtime_ns();
   // The terms are linear in K: with the prep kernel, slice 0 adds the X term and the whole
   // constant; with in-kernel prep every slice adds its own X term and K_slice * A * B.
   uint32_t cterm = slice == 0 ? p.c0 : 0u;
@@ -527,9 +540,9 @@ __global__ void __launch_bounds__(sk_threads(N, NT), sk_ctas_per_sm(N, NT))
         }
       }
       if (++cs_slot == stages) cs_slot = 0;
-      if (p.ts && tid == 0 && ti == 0 && c == 0) p.ts[blockIdx.x * 8 + 3] = gtime();
+      if (p.ts && !p.ts_clock && tid == 0 && ti == 0 && c == 0) p.ts[blockIdx.x * 8 + 3] = gtime_ns();
     }
-    if (p.ts && tid == 0 && ti == 0) p.ts[blockIdx.x * 8 + 4] = gtime();
+    if (p.ts && !p.ts_clock && tid == 0 && ti == 0) p.ts[blockIdx.x * 8 + 4] = gtime_ns();
 
     // ---------------- end of tile: combine the K groups, epilogue ----------------
     if (ti + 1 == my_tiles) apmm_ptx::pdl_trigger();  // last tile: the next call may start
@@ -602,7 +615,7 @@ __global__ void __launch_bounds__(sk_threads(N, NT), sk_ctas_per_sm(N, NT))
     // s_last is next written after the next tile's first barrier
   }
   if (my_tiles == 0) apmm_ptx::pdl_trigger();
-  if (p.ts && tid == 0) p.ts[blockIdx.x * 8 + 5] = gtime();
+  if (p.ts && !p.ts_clock && tid == 0) p.ts[blockIdx.x * 8 + 5] = gtime_ns();
 }
 
 template <int N, int NT, bool SPLIT>
@@ -855,6 +868,16 @@ cudaError_t launch_skinny(const SkinnyArgs& a, cudaStream_t s) {
     p.ts = ts_buf;
   }
   if (a.trace) p.ts = a.trace;  // dev launch trace (APMM_TRACE)
+  static const bool ts_clock = APMM_DEV_ENV("APMM_TRACE_CLOCK") != nullptr;
+  p.ts_clock = ts_clock ? 1u : 0u;
+  // Off: the L2 prefetch ahead of each TMA load doubled the TMA instructions a warp issues
+  // at kernel start (~1000 cycles of the prologue, cycle trace) and the stream gained nothing:
+  // 8192^2 W3A8 M=1 9.67 -> 9.15 us, 4096x1x11008 W2A4 7.54 -> 7.00 us (r02/r2_sk_l2pf.txt).
+  static const int l2pf = [] {  // dev A/B (APMM_SK_L2PF=0/1)
+    const char* e = APMM_DEV_ENV("APMM_SK_L2PF");
+    return e ? std::atoi(e) : 0;
+  }();
+  p.l2_prefetch = l2pf ? 1u : 0u;
 
   if (!inprep) {  // feature prep (same shared-memory carveout as the streaming kernel: no reconfig)
     static DeviceBits carve_set;
