@@ -298,6 +298,11 @@ int pick_route(const apmm_ctx* ctx, const RouteCaps& c, uint64_t rows_w, uint64_
   return APMM_OK;
 }
 
+// bytes 48..63: the split-K weight-plane GEMM's grid barrier (count, generation)
+unsigned long long* grid_barrier(apmm_ctx* ctx) {
+  return reinterpret_cast<unsigned long long*>(reinterpret_cast<uint8_t*>(ctx->flags) + 48);
+}
+
 // dev launch trace: the next slot (kind 1 expand, 2 pair GEMM, 3 weight-plane GEMM, 5 skinny)
 unsigned long long* trace_slot(apmm_ctx* ctx, int kind) {
   if (!ctx->trace) return nullptr;
@@ -386,7 +391,10 @@ int run_matmul(apmm_ctx* ctx, const uint32_t* w, uint64_t rows_w, int n_w, const
   const uint64_t rsx_pad = round_up(rows_x, kRowsumPad);
   const bool wplanes = route == Route::Mid || route == Route::PairW;  // K3f expands W on chip
   const bool zero_y = route == Route::Mid || route == Route::PairSplit;  // split-K reduce-adds
-  {
+  // the mid route expands its features and zeroes Y itself (in-kernel prep + grid barrier):
+  // no K1 launch at all (the K1x launch + gap cost ~3 us of a ~12 us call, r02 notes)
+  const bool xprep = route == Route::Mid && !x_ready;
+  if (!xprep) {
     TimedLaunch t(ctx, 1, stream);
     // K1. K3f: W untouched except for rowsum(U_w) on the pair route (the split-K mid route
     // forms it in the GEMM); split-K: K1 also zeroes Y, which the units reduce-add into.
@@ -415,8 +423,8 @@ int run_matmul(apmm_ctx* ctx, const uint32_t* w, uint64_t rows_w, int n_w, const
                        ctx->early_w, early_x, trace_slot(ctx, 1),
                        w_rows == 0 || !ctx->early_w ? kK1xBlocksPerSm : 1));
     }
+    ctx->launches += 1;
   }
-  ctx->launches += 1;
   GemmArgs a{};
   a.codes_w = m.codes_w;
   a.codes_x = m.codes_x;
@@ -442,6 +450,11 @@ int run_matmul(apmm_ctx* ctx, const uint32_t* w, uint64_t rows_w, int n_w, const
   const bool epi_colmax = route != Route::PairW && !colmax_pass;
   a.colmax = epi_colmax ? colmax : nullptr;
   a.early_w = ctx->early_w;
+  if (xprep) {
+    a.xprep_planes = x;
+    a.xprep_rows_pad = rsx_pad;
+    a.grid_bar = grid_barrier(ctx);
+  }
   a.colmax_global = colmax_global;
   if (ctx->dbg_waits) {
     if (!ctx->dbg) {
@@ -515,12 +528,14 @@ struct HostCall {
   HostCall host_call_(ctx);                     \
   if (host_call_.status) return host_call_.status
 
-// Small per-context device scratch (ctx->flags, 64 bytes): [0..1] recover flags,
-// [2] quantize non-finite flag, bytes 32..39 the per-tensor absmax bits.
+// Small per-context device scratch (ctx->flags, 64 bytes, zeroed at creation): [0..1]
+// recover flags, [2] quantize non-finite flag, bytes 32..39 the per-tensor absmax bits,
+// bytes 48..63 the grid barrier (count, generation).
 int* quant_flag(apmm_ctx* ctx) { return ctx->flags + 2; }
 unsigned long long* quant_amax(apmm_ctx* ctx) {
   return reinterpret_cast<unsigned long long*>(reinterpret_cast<uint8_t*>(ctx->flags) + 32);
 }
+
 
 // Host-side PackedBitPlanes invariants (bitplane.cpp:17-32).
 int check_padding(const uint32_t* planes, uint64_t rows, uint64_t cols, int n) {
@@ -597,6 +612,7 @@ int apmm_ctx_create(apmm_ctx** out, int device) {
   }
   cudaError_t e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaMalloc(&ctx->flags, 64);
+  if (e == cudaSuccess) e = cudaMemset(ctx->flags, 0, 64);  // incl. the grid-barrier counter
   if (e != cudaSuccess) {
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
     delete ctx;

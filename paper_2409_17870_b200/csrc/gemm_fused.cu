@@ -27,6 +27,7 @@
 #include <cstdio>
 #include <cstdlib>
 
+#include "expand.cuh"
 #include "internal.h"
 #include "ptx.cuh"
 
@@ -99,6 +100,18 @@ struct Params {
   unsigned long long* dbg;  // APMM_DEBUG_WAITS=1: wait-cycle counters per role, else null
   unsigned long long* ts;   // dev launch trace (APMM_TRACE): [0] start [1] pdl_wait [4] end
   uint32_t early_w;         // PDL: weight-plane loads + transforms before the previous kernel ends
+  // In-kernel feature prep (split mode; replaces the K1x launch): after griddepcontrol.wait
+  // the epilogue warps of all CTAs expand X planes -> u8 codes + rowsum(U_x) (the layout K1
+  // writes, read back by the B operand's TMA) and zero Y, then meet at a grid-wide barrier
+  // (sense-reversing: count + generation) before B loads and reduce-adds.
+  uint32_t xprep;
+  const uint32_t* x_planes;
+  uint8_t* x_codes;
+  int32_t* x_rowsum;
+  uint32_t rows_x_pad, n_x, wpr, kpad_words;
+  uint4* y_zero;
+  uint64_t y_zero_n;               // 16-byte units
+  unsigned long long* grid_bar;    // [count, generation], zero-initialised once per context
 };
 
 // Bounded mbarrier waits: a wait that does not complete within ~4 s of clock64 cycles
@@ -266,6 +279,7 @@ __global__ void __maxnreg__(kXformWarpsCfg == 4 ? 136 : 108)
   // transform warps (sum_i 2^i popc(plane words)), double-buffered like the accumulators
   __shared__ int32_t rsw_s[2][kHalf];
   __shared__ __align__(8) uint64_t rsw_full[2], rsw_empty[2];
+  __shared__ __align__(8) uint64_t x_ready;  // xprep: the grid-wide feature prep is done
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
@@ -304,6 +318,7 @@ __global__ void __maxnreg__(kXformWarpsCfg == 4 ? 136 : 108)
       mbar_init(&rsw_full[s], kXformWarps);
       mbar_init(&rsw_empty[s], 4);
     }
+    mbar_init(&x_ready, 1);
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc_pair<kTmemCols>(tmem_slot);
@@ -325,6 +340,10 @@ __global__ void __maxnreg__(kXformWarpsCfg == 4 ? 136 : 108)
     if (elect_one()) {
       const uint64_t hint = policy_evict_last();
       uint32_t stage = 0, phase = 0;
+      if (p.xprep) {  // the feature codes are written by this grid (every CTA's epilogue warps)
+        mbar_wait_b(&x_ready, 0, 10);
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+      }
       for (uint32_t t = cluster; t < num_tiles; t += nclusters) {
         const Unit un = unit_info(t, p);
         const TileInfo ti = un.ti;
@@ -556,6 +575,54 @@ __global__ void __maxnreg__(kXformWarpsCfg == 4 ? 136 : 108)
   } else if (warp >= 4) {
     // ---------------- epilogue (both CTAs); identical to gemm_pair.cu ----------------
     const uint32_t wq = warp & 3;
+    if (p.xprep) {
+      // feature prep for the whole grid (rows round-robin over every CTA's 4 epilogue warps),
+      // Y zeroed for the reduce-adds, then the grid-wide barrier
+      const xpd::ExpandOperand xo{p.x_planes, p.x_codes, p.x_rowsum, p.rows_x, p.rows_x_pad,
+                                  static_cast<int>(p.n_x), 0};
+      const uint32_t nwarps = gridDim.x * 4u;
+      for (uint32_t r = blockIdx.x * 4u + wq; r < p.rows_x; r += nwarps) {
+        xpd::expand_one(xo, r, p.wpr, p.tail_mask, p.kpad_words, lane);
+      }
+      const uint32_t te = wq * 32u + lane;
+      if (blockIdx.x == 0) {
+        for (uint32_t r = p.rows_x + te; r < p.rows_x_pad; r += 128u) p.x_rowsum[r] = 0;
+      }
+      for (uint64_t i = uint64_t(blockIdx.x) * 128u + te; i < p.y_zero_n; i += uint64_t(gridDim.x) * 128u) {
+        p.y_zero[i] = make_uint4(0, 0, 0, 0);
+      }
+      // generic-proxy writes -> visible to the async proxy (other CTAs' TMA loads / reduce-adds)
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+      __threadfence();
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (wq == 0 && lane == 0) {
+        // sense-reversing grid barrier (grid sizes differ between calls): count at
+        // grid_bar[0], generation at grid_bar[1]; the last arriver resets the count and
+        // advances the generation. A launch starts only after the previous one completed
+        // (griddepcontrol.wait above), so barriers of consecutive calls never overlap.
+        unsigned long long* count = p.grid_bar;
+        unsigned long long* gen = p.grid_bar + 1;
+        unsigned long long g0, old;
+        asm volatile("ld.acquire.gpu.u64 %0, [%1];" : "=l"(g0) : "l"(gen) : "memory");
+        asm volatile("atom.add.acq_rel.gpu.u64 %0, [%1], 1;" : "=l"(old) : "l"(count) : "memory");
+        if (old + 1 == gridDim.x) {
+          asm volatile("st.relaxed.gpu.u64 [%0], 0;" ::"l"(count) : "memory");
+          asm volatile("st.release.gpu.u64 [%0], %1;" ::"l"(gen), "l"(g0 + 1) : "memory");
+        } else {
+          unsigned long long now;
+          const long long t0 = clock64();
+          do {
+            asm volatile("ld.acquire.gpu.u64 %0, [%1];" : "=l"(now) : "l"(gen) : "memory");
+            if (clock64() - t0 > 8000000000ll) {
+              printf("[apmm fused] grid barrier timeout: block %d\n", blockIdx.x);
+              __trap();
+            }
+          } while (now == g0);
+        }
+        mbar_arrive(&x_ready);  // the B producer may load feature codes now
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+    }
     uint32_t acc = 0, acc_phase = 0, nbuf = 0;
     const uint64_t store_hint = policy_evict_first();
     for (uint32_t t = cluster; t < num_tiles; t += nclusters) {
@@ -587,8 +654,10 @@ __global__ void __maxnreg__(kXformWarpsCfg == 4 ? 136 : 108)
       int4 rsx_lo = make_int4(0, 0, 0, 0), rsx_hi = make_int4(0, 0, 0, 0);
       if (8u * lane < ti.ncols) {
         const int4* src = reinterpret_cast<const int4*>(p.rowsum_x + ti.col0 + 8u * lane);
-        rsx_lo = __ldg(src);
-        rsx_hi = __ldg(src + 1);
+        // written by this grid's feature prep (xprep): coherent L2 loads, never the
+        // read-only path (ld.global.nc may serve data cached before the grid barrier)
+        rsx_lo = p.xprep ? __ldcg(src) : __ldg(src);
+        rsx_hi = p.xprep ? __ldcg(src + 1) : __ldg(src + 1);
       }
       mbar_wait_b(&tmem_full[acc], acc_phase, 5);
       tc_fence_after();
@@ -820,6 +889,19 @@ cudaError_t launch_gemm_pair_wplanes(const GemmArgs& a, const uint32_t* w_planes
   p.dbg = a.dbg;
   p.ts = a.trace;
   p.early_w = a.early_w ? 1u : 0u;
+  if (a.xprep_planes) {
+    p.xprep = 1u;
+    p.x_planes = a.xprep_planes;
+    p.x_codes = const_cast<uint8_t*>(a.codes_x);
+    p.x_rowsum = const_cast<int32_t*>(a.rowsum_x);
+    p.rows_x_pad = static_cast<uint32_t>(a.xprep_rows_pad);
+    p.n_x = static_cast<uint32_t>(a.n_x);
+    p.wpr = static_cast<uint32_t>(wpr);
+    p.kpad_words = static_cast<uint32_t>(a.kpad / 32);
+    p.y_zero = reinterpret_cast<uint4*>(a.y);
+    p.y_zero_n = a.rows_w * a.rows_x * 4 / 16;
+    p.grid_bar = a.grid_bar;
+  }
   static const uint32_t ablate = [] {
     const char* e = APMM_DEV_ENV("APMM_FUSED_ABLATE");
     return e ? static_cast<uint32_t>(std::atoi(e)) : 0u;

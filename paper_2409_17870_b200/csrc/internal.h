@@ -140,6 +140,11 @@ struct GemmArgs {
   bool colmax_global = false;
   unsigned long long* trace = nullptr;  // dev (APMM_TRACE): per-CTA globaltimer stamps [grid][8]
   bool early_w = true;  // PDL: the weight-plane GEMM may read W before the previous kernel ends
+  // split-K weight-plane GEMM only: expand the feature planes and zero Y inside the kernel
+  // (grid-wide barrier) instead of a K1x launch; null = K1x did it
+  const uint32_t* xprep_planes = nullptr;
+  uint64_t xprep_rows_pad = 0;
+  unsigned long long* grid_bar = nullptr;
 };
 // Returns the number of kernel launches it enqueued via *launches.
 cudaError_t launch_gemm_tc(const GemmArgs& a, cudaStream_t s, int* launches);
