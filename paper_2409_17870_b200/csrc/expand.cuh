@@ -132,6 +132,19 @@ __device__ __forceinline__ void expand_one(const ExpandOperand& op, uint32_t r, 
   if (lane == 0) op.rowsum[r] = sum;
 }
 
+// The same with the plane count fixed at compile time (single-operand expansion launches:
+// a fraction of expand_one's code, which matters for short launches -- instruction-cache
+// misses were their top stall, profiles/r02_notes.md).
+template <int N>
+__device__ __forceinline__ void expand_one_n(const ExpandOperand& op, uint32_t r, uint32_t wpr,
+                                             uint32_t tail_mask, uint32_t kpad_words,
+                                             uint32_t lane) {
+  int32_t sum = op.codes == nullptr ? rowsum_row<N>(op, r, wpr, tail_mask, lane)
+                                    : expand_row<N>(op, r, wpr, tail_mask, kpad_words, lane);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+  if (lane == 0) op.rowsum[r] = sum;
+}
 
 }  // namespace xpd
 }  // namespace apmm_b200

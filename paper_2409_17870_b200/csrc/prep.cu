@@ -46,6 +46,20 @@ using xpd::transpose8;
 // GEMM two calls ago used (complete by construction). The feature planes -- possibly the
 // previous kernel's output -- and the zeroing of Y are read / written only after the wait.
 // It completes only after the previous kernel, so the next GEMM's wait on us covers both.
+// NA / NB: the operands' plane counts at compile time (0: dispatched at run time, -1: the
+// operand is absent). Single-operand launches (K1w weights, K1x features) use fixed counts.
+template <int NA, int NB>
+__device__ __forceinline__ void expand_sel(const ExpandOperand& op, uint32_t r, uint32_t wpr,
+                                           uint32_t tail_mask, uint32_t kpad_words,
+                                           uint32_t lane) {
+  if constexpr (NA > 0) {
+    xpd::expand_one_n<NA>(op, r, wpr, tail_mask, kpad_words, lane);
+  } else {
+    expand_one(op, r, wpr, tail_mask, kpad_words, lane);
+  }
+}
+
+template <int NA, int NB>
 __global__ void __launch_bounds__(kExpandThreads) expand_kernel(ExpandOperand a, ExpandOperand b,
                                                                  uint32_t wpr, uint32_t tail_mask,
                                                                  uint32_t kpad_words,
@@ -66,11 +80,19 @@ __global__ void __launch_bounds__(kExpandThreads) expand_kernel(ExpandOperand a,
   const uint32_t warps = blockDim.x >> 5;
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t gwarp = blockIdx.x * warps + (threadIdx.x >> 5), nwarps = gridDim.x * warps;
-  for (uint32_t r = gwarp; r < a.rows; r += nwarps) expand_one(a, r, wpr, tail_mask, kpad_words, lane);
+  if constexpr (NA >= 0) {
+    for (uint32_t r = gwarp; r < a.rows; r += nwarps) {
+      expand_sel<NA, 0>(a, r, wpr, tail_mask, kpad_words, lane);
+    }
+  }
   // X rows continue the W rows' round robin, so a grid-stride pass over both stays balanced
-  const uint32_t xr0 = (gwarp + nwarps - a.rows % nwarps) % nwarps;
-  if (early_x) {
-    for (uint32_t r = xr0; r < b.rows; r += nwarps) expand_one(b, r, wpr, tail_mask, kpad_words, lane);
+  const uint32_t xr0 = NA >= 0 ? (gwarp + nwarps - a.rows % nwarps) % nwarps : gwarp;
+  if constexpr (NB >= 0) {
+    if (early_x) {
+      for (uint32_t r = xr0; r < b.rows; r += nwarps) {
+        expand_sel<NB, 0>(b, r, wpr, tail_mask, kpad_words, lane);
+      }
+    }
   }
   if (blockIdx.x == 0) {
     for (uint32_t r = a.rows + threadIdx.x; r < a.rows_pad; r += blockDim.x) a.rowsum[r] = 0;
@@ -79,8 +101,12 @@ __global__ void __launch_bounds__(kExpandThreads) expand_kernel(ExpandOperand a,
   stamp(1);
   if (early_w) asm volatile("griddepcontrol.wait;" ::: "memory");
   stamp(2);
-  if (!early_x) {
-    for (uint32_t r = xr0; r < b.rows; r += nwarps) expand_one(b, r, wpr, tail_mask, kpad_words, lane);
+  if constexpr (NB >= 0) {
+    if (!early_x) {
+      for (uint32_t r = xr0; r < b.rows; r += nwarps) {
+        expand_sel<NB, 0>(b, r, wpr, tail_mask, kpad_words, lane);
+      }
+    }
   }
   // split-K GEMMs reduce-add into Y: zero it here, after the previous kernel in the stream
   // (which may still have been writing the same Y) has completed
@@ -551,10 +577,42 @@ cudaError_t launch_expand(const uint32_t* w_planes, uint64_t rows_w, int n_w,
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, expand_kernel, a, b, wpr, tail_mask,
-                                     static_cast<uint32_t>(kpad / 32),
-                                     static_cast<uint4*>(zero_out), zero_bytes / 16,
-                                     early_w ? 1u : 0u, early_x ? 1u : 0u, trace);
+  // single-operand launches (one side has no rows) get a kernel specialised on its plane
+  // count; the combined launch dispatches per row at run time
+  const uint32_t kw = static_cast<uint32_t>(kpad / 32);
+  uint4* zo = static_cast<uint4*>(zero_out);
+  const uint64_t zn = zero_bytes / 16;
+  const uint32_t ew = early_w ? 1u : 0u, ex = early_x ? 1u : 0u;
+  cudaError_t e;
+#define APMM_K1_ONE(KA, KB) \
+  cudaLaunchKernelEx(&cfg, expand_kernel<KA, KB>, a, b, wpr, tail_mask, kw, zo, zn, ew, ex, trace)
+  // (the absent side keeps its rowsum padding zeroing, done by block 0 for both operands)
+  if (rows_x == 0 && w_codes != nullptr && n_w >= 1 && n_w <= 8) {
+    switch (n_w) {
+      case 1: e = APMM_K1_ONE(1, -1); break;
+      case 2: e = APMM_K1_ONE(2, -1); break;
+      case 3: e = APMM_K1_ONE(3, -1); break;
+      case 4: e = APMM_K1_ONE(4, -1); break;
+      case 5: e = APMM_K1_ONE(5, -1); break;
+      case 6: e = APMM_K1_ONE(6, -1); break;
+      case 7: e = APMM_K1_ONE(7, -1); break;
+      default: e = APMM_K1_ONE(8, -1); break;
+    }
+  } else if (rows_w == 0 && n_x >= 1 && n_x <= 8) {
+    switch (n_x) {
+      case 1: e = APMM_K1_ONE(-1, 1); break;
+      case 2: e = APMM_K1_ONE(-1, 2); break;
+      case 3: e = APMM_K1_ONE(-1, 3); break;
+      case 4: e = APMM_K1_ONE(-1, 4); break;
+      case 5: e = APMM_K1_ONE(-1, 5); break;
+      case 6: e = APMM_K1_ONE(-1, 6); break;
+      case 7: e = APMM_K1_ONE(-1, 7); break;
+      default: e = APMM_K1_ONE(-1, 8); break;
+    }
+  } else {
+    e = APMM_K1_ONE(0, 0);
+  }
+#undef APMM_K1_ONE
   return e != cudaSuccess ? e : cudaGetLastError();
 }
 
