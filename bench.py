@@ -394,6 +394,8 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     ctx = ap.Context(local_rank)
+    if args.early_features:  # documented opt-in: this bench's features are static inputs
+        ctx.set_early_feature_read(True)
     stream = torch.cuda.Stream(device=dev)  # every launch of the timed region goes here
     torch.cuda.set_stream(stream)
     full_gemms = workload_gemms(args.workload)
@@ -752,6 +754,9 @@ def run_ours(args, rank, world, local_rank):
         "config": bench_config(args.workload, world),
         "per_rank_shapes": [list(g) for g in gemms],
         "launch": "eager" if graph is None else "one cuda graph of the K timed steps",
+        "pdl_feature_reads": ("early (--early-features: features are static inputs here)"
+                              if args.early_features else
+                              "after the previous kernel (safe default; features may be its output)"),
         "l2": ("no flush: per-step packed inputs %.0f MB + outputs %.0f MB > 2 x 126 MB L2" % (
             sum(packed_bytes(g[0], g[2], g[3]) + packed_bytes(g[1], g[2], g[4]) for g in gemms) / 1e6,
             sum(4 * g[0] * g[1] for g in gemms) / 1e6) if nrot == 1 else
@@ -821,6 +826,9 @@ def main():
                      help="skip the post-timing sampled-row parity check (dev only)")
     ap_.add_argument("--no-graph", action="store_true",
                      help="time eager launches instead of replaying the step as a CUDA graph")
+    ap_.add_argument("--early-features", action="store_true",
+                     help="APMM_OPT_EARLY_FEATURE_READ: let the next call read its (static) "
+                          "features while the previous GEMM drains (not the default)")
     ap_.add_argument("--profile", action="store_true",
                      help="for ncu: no heat phase, no e2e, no CPU baseline (numbers invalid)")
     args = ap_.parse_args()
