@@ -63,7 +63,7 @@ __host__ __device__ constexpr int raw_plane(int nw) { return kHalf * 16 * raw_rb
 __host__ __device__ constexpr int raw_bytes(int nw) { return nw * raw_plane(nw); }
 constexpr int kOpStageBytes = 2 * kAS;
 __host__ __device__ constexpr int op_stages(int nw) { return nw <= 2 ? 5 : 4; }
-constexpr int kSmemCap = 232448 - 1024 - 1024 - 2048;  // 227 KB minus alignment slack, barriers and the static rowsum buffers
+constexpr int kSmemCap = 232448 - 1024 - 1024 - 2048 - 4096;  // + 4 KB epilogue column terms  // 227 KB minus alignment slack, barriers and the static rowsum buffers
 __host__ __device__ constexpr int raw_stages(int nw) {
   return (kSmemCap - op_stages(nw) * kOpStageBytes - 4 * 2 * kEpiBuf) / raw_bytes(nw) > 16
              ? 16
@@ -100,6 +100,7 @@ struct Params {
   unsigned long long* dbg;  // APMM_DEBUG_WAITS=1: wait-cycle counters per role, else null
   unsigned long long* ts;   // dev launch trace (APMM_TRACE): [0] start [1] pdl_wait [4] end
   uint32_t early_w;         // PDL: weight-plane loads + transforms before the previous kernel ends
+  uint32_t ts_clock;        // dev (APMM_TRACE_CLOCK): clock64 stamps inside the epilogue chunk loop
   // In-kernel feature prep (split mode; replaces the K1x launch): after griddepcontrol.wait
   // the epilogue warps of all CTAs expand X planes -> u8 codes + rowsum(U_x) (the layout K1
   // writes, read back by the B operand's TMA) and zero Y, then meet at a grid-wide barrier
@@ -280,11 +281,12 @@ __global__ void __maxnreg__(kXformWarpsCfg == 4 ? 136 : 108)
   __shared__ int32_t rsw_s[2][kHalf];
   __shared__ __align__(8) uint64_t rsw_full[2], rsw_empty[2];
   __shared__ __align__(8) uint64_t x_ready;  // xprep: the grid-wide feature prep is done
+  __shared__ __align__(16) uint32_t xterm_s[4][kPairN];  // epilogue: per-warp column terms
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
   auto stamp = [&](int k) {
-    if (p.ts && threadIdx.x == 0) {
+    if (p.ts && !p.ts_clock && threadIdx.x == 0) {
       unsigned long long t;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
       p.ts[blockIdx.x * 8 + k] = t;
@@ -388,7 +390,7 @@ __global__ void __maxnreg__(kXformWarpsCfg == 4 ? 136 : 108)
           // proxy before arriving. The cluster-scope form invalidated L1 (CCTL.IVALL) on every
           // poll (ncu source view, profiles/r02_ncu_mid_wplanes.txt).
           mbar_wait_b(&full_bar[stage], phase, 3, af);
-          if (p.ts && t == cluster && kb == un.kb0) {  // first operand stage ready
+          if (p.ts && !p.ts_clock && t == cluster && kb == un.kb0) {  // first operand stage ready
             unsigned long long tt;
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt));
             p.ts[blockIdx.x * 8 + 2] = tt;
@@ -405,7 +407,7 @@ __global__ void __maxnreg__(kXformWarpsCfg == 4 ? 136 : 108)
           if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
         mma_commit_pair_mc(&tmem_full[acc], 0x3);
-        if (p.ts) {  // last write = the last unit's MMAs issued
+        if (p.ts && !p.ts_clock) {  // last write = the last unit's MMAs issued
           unsigned long long tt;
           asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt));
           p.ts[blockIdx.x * 8 + 3] = tt;
@@ -647,46 +649,56 @@ __global__ void __maxnreg__(kXformWarpsCfg == 4 ? 136 : 108)
       double swv = 0.0;
       if (p.yf) swv = p.gran_w ? (row_ok ? p.s_w[row] : 0.0) : p.s_w[0];
 
-      // this tile's rowsum(U_x) into registers BEFORE waiting for the accumulator (lane l
-      // holds columns 8l..8l+7; chunk c's column j is a shuffle from lane 4c + j/8): the
-      // per-chunk global loads were serialised L2 round trips (~0.8 us each) exposed on a
-      // CTA's last tile (APMM_PAIR_TS timeline)
-      int4 rsx_lo = make_int4(0, 0, 0, 0), rsx_hi = make_int4(0, 0, 0, 0);
-      if (8u * lane < ti.ncols) {
-        const int4* src = reinterpret_cast<const int4*>(p.rowsum_x + ti.col0 + 8u * lane);
-        // written by this grid's feature prep (xprep): coherent L2 loads, never the
-        // read-only path (ld.global.nc may serve data cached before the grid barrier)
-        rsx_lo = p.xprep ? __ldcg(src) : __ldg(src);
-        rsx_hi = p.xprep ? __ldcg(src + 1) : __ldg(src + 1);
+      // this unit's column terms coef_x * rowsum(U_x) into the warp's shared row BEFORE
+      // waiting for the accumulator; each chunk then reads its 32 terms as 8 broadcast
+      // 128-bit loads (a shuffle per column cost ~450 cycles per chunk, dev cycle trace)
+      {
+        uint4 lo = make_uint4(0, 0, 0, 0), hi = make_uint4(0, 0, 0, 0);
+        if (8u * lane < ti.ncols) {
+          const int4* src = reinterpret_cast<const int4*>(p.rowsum_x + ti.col0 + 8u * lane);
+          // written by this grid's feature prep (xprep): coherent L2 loads, never the
+          // read-only path (ld.global.nc may serve data cached before the grid barrier)
+          const int4 a = p.xprep ? __ldcg(src) : __ldg(src);
+          const int4 b = p.xprep ? __ldcg(src + 1) : __ldg(src + 1);
+          lo = make_uint4(coef_x * uint32_t(a.x), coef_x * uint32_t(a.y), coef_x * uint32_t(a.z),
+                          coef_x * uint32_t(a.w));
+          hi = make_uint4(coef_x * uint32_t(b.x), coef_x * uint32_t(b.y), coef_x * uint32_t(b.z),
+                          coef_x * uint32_t(b.w));
+        }
+        __syncwarp();  // the previous unit's reads of this row are done
+        reinterpret_cast<uint4*>(&xterm_s[wq][0])[2 * lane] = lo;
+        reinterpret_cast<uint4*>(&xterm_s[wq][0])[2 * lane + 1] = hi;
+        __syncwarp();
       }
       mbar_wait_b(&tmem_full[acc], acc_phase, 5);
       tc_fence_after();
-      if (p.ts && lane == 0 && warp == 4) {  // accumulator ready (last write = last unit)
+      if (p.ts && !p.ts_clock && lane == 0 && warp == 4) {  // accumulator ready (last write = last unit)
         unsigned long long tt;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt));
         p.ts[blockIdx.x * 8 + 6] = tt;
       }
       const uint32_t t_addr = tmem_base + ((wq * 32u) << 16) + acc * kPairN;
+      // dev fine trace: cycles of the first two chunks of the CTA's last unit (warp 4, lane 0)
+      const bool fine = p.ts && p.ts_clock && lane == 0 && warp == 4 && t + nclusters >= num_tiles;
+      long long f0 = fine ? clock64() : 0;
+      auto fstamp = [&](int k) {
+        if (fine) p.ts[blockIdx.x * 8 + k] = static_cast<unsigned long long>(clock64() - f0);
+      };
 #pragma unroll 1
       for (uint32_t c = 0; c < ti.ncols / 32; ++c) {
         uint32_t r[32];
         tmem_ld_32x32b_x32(t_addr + c * 32, r);
         tmem_ld_wait();
+        if (c < 2) fstamp(1 + 3 * c);  // [1] / [4]: accumulator chunk in registers
         const uint32_t col0 = ti.col0 + c * 32;
+        const uint4* xt = reinterpret_cast<const uint4*>(&xterm_s[wq][c * 32]);
 #pragma unroll
         for (int j4 = 0; j4 < 8; ++j4) {
-          // columns 4 j4 .. 4 j4 + 3 of the chunk: lane 4c + j4/2, half (j4 & 1)
-          const uint32_t src_lane = 4u * c + (j4 >> 1);
-          const int4 mine = (j4 & 1) ? rsx_hi : rsx_lo;
-          int4 rs;
-          rs.x = __shfl_sync(0xffffffffu, mine.x, src_lane);
-          rs.y = __shfl_sync(0xffffffffu, mine.y, src_lane);
-          rs.z = __shfl_sync(0xffffffffu, mine.z, src_lane);
-          rs.w = __shfl_sync(0xffffffffu, mine.w, src_lane);
-          r[4 * j4 + 0] = 4u * r[4 * j4 + 0] + row_term - coef_x * uint32_t(rs.x);
-          r[4 * j4 + 1] = 4u * r[4 * j4 + 1] + row_term - coef_x * uint32_t(rs.y);
-          r[4 * j4 + 2] = 4u * r[4 * j4 + 2] + row_term - coef_x * uint32_t(rs.z);
-          r[4 * j4 + 3] = 4u * r[4 * j4 + 3] + row_term - coef_x * uint32_t(rs.w);
+          const uint4 v = xt[j4];  // same address in every lane: one broadcast wavefront
+          r[4 * j4 + 0] = 4u * r[4 * j4 + 0] + row_term - v.x;
+          r[4 * j4 + 1] = 4u * r[4 * j4 + 1] + row_term - v.y;
+          r[4 * j4 + 2] = 4u * r[4 * j4 + 2] + row_term - v.z;
+          r[4 * j4 + 3] = 4u * r[4 * j4 + 3] + row_term - v.w;
         }
         if (p.yf) {
           if (p.gran_x) {
@@ -701,6 +713,7 @@ __global__ void __maxnreg__(kXformWarpsCfg == 4 ? 136 : 108)
             for (int j = 0; j < 32; ++j) r[j] = dequant_bits(r[j], swv, sx);
           }
         }
+        if (c < 2) fstamp(2 + 3 * c);  // [2] / [5]: recovery math done
         if (p.tma_store) {
           uint8_t* buf = staging + (wq * 2 + nbuf) * kEpiBuf;
           nbuf ^= 1;
@@ -722,6 +735,7 @@ __global__ void __maxnreg__(kXformWarpsCfg == 4 ? 136 : 108)
             }
             bulk_commit();
           }
+          if (c < 2) fstamp(3 + 3 * c);  // [3] / [6]: staged, fenced, bulk op issued
         } else if (row_ok && col0 < p.rows_x) {
           uint32_t* dst = (p.y ? reinterpret_cast<uint32_t*>(p.y) : reinterpret_cast<uint32_t*>(p.yf)) +
                           uint64_t(row) * p.rows_x + col0;
@@ -732,11 +746,12 @@ __global__ void __maxnreg__(kXformWarpsCfg == 4 ? 136 : 108)
         }
         __syncwarp();
       }
+      fstamp(7);  // [7]: every chunk of the unit issued
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(mapa(smem_u32(&tmem_empty[acc]), lead_rank));
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
-      if (p.ts && lane == 0 && warp == 4) {  // chunks issued (last write = last unit)
+      if (p.ts && !p.ts_clock && lane == 0 && warp == 4) {  // chunks issued (last write = last unit)
         unsigned long long tt;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt));
         p.ts[blockIdx.x * 8 + 7] = tt;
@@ -745,7 +760,7 @@ __global__ void __maxnreg__(kXformWarpsCfg == 4 ? 136 : 108)
     // the staging buffers must have been read before the CTA exits; the stores themselves
     // complete with the grid (as CUTLASS's tma_store_wait), so no write round trip here
     if (lane == 0) bulk_wait_read<0>();
-    if (p.ts && lane == 0 && warp == 4) {  // epilogue drained
+    if (p.ts && !p.ts_clock && lane == 0 && warp == 4) {  // epilogue drained
       unsigned long long tt;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt));
       p.ts[blockIdx.x * 8 + 5] = tt;
@@ -888,6 +903,8 @@ cudaError_t launch_gemm_pair_wplanes(const GemmArgs& a, const uint32_t* w_planes
   p.tail_mask = tail ? ((1u << tail) - 1u) : 0xffffffffu;
   p.dbg = a.dbg;
   p.ts = a.trace;
+  static const bool ts_clock = APMM_DEV_ENV("APMM_TRACE_CLOCK") != nullptr;
+  p.ts_clock = ts_clock ? 1u : 0u;
   p.early_w = a.early_w ? 1u : 0u;
   if (a.xprep_planes) {
     p.xprep = 1u;
