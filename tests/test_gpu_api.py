@@ -226,3 +226,44 @@ def test_early_read_options_are_bit_identical(gpu, oracle):
         ctx.set_early_feature_read(False)
         torch.cuda.synchronize()
         assert torch.equal(y1, y2) and torch.equal(y1, y3)
+
+
+def test_graph_replays_of_every_route(gpu):
+    """Back-to-back calls captured once and replayed several times (the serving pattern):
+    the PDL chain between calls, the ping-pong workspace halves and the mid route's in-kernel
+    grid barrier (count + generation, reused across replays) give the eager results on every
+    replay."""
+    import torch
+    ap, _ = gpu
+    dev = torch.device("cuda", 0)
+    s = torch.cuda.Stream()
+    shapes = [(4096, 8, 4096, 3, 8), (4096, 128, 4096, 2, 4), (2304, 2560, 4096, 2, 4),
+              (4096, 512, 4096, 2, 4)]
+    for (n_out, m, k, nw, nx) in shapes:
+        ctx = ap.Context(0)
+        ctx.set_stream(s)
+        ctx.reserve(n_out, m, k, nw)
+        wpr = k // 32
+        ws = [torch.randint(-2**31, 2**31 - 1, (nw * n_out * wpr,), dtype=torch.int32, device=dev)
+              for _ in range(3)]
+        xs = [torch.randint(-2**31, 2**31 - 1, (nx * m * wpr,), dtype=torch.int32, device=dev)
+              for _ in range(3)]
+        ys = [torch.empty((n_out, m), dtype=torch.int32, device=dev) for _ in range(3)]
+        want = []
+        ref_ctx = ap.Context(0)
+        for i in range(3):
+            y = torch.empty_like(ys[i])
+            ap.cu_matmul_ap(ws[i], n_out, nw, xs[i], m, nx, k, y, ref_ctx)
+            want.append(y)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            for i in range(3):
+                ap.cu_matmul_ap(ws[i], n_out, nw, xs[i], m, nx, k, ys[i], ctx, stream=s)
+        for rep in range(3):
+            for y in ys:
+                y.fill_(-1)
+            g.replay()
+            torch.cuda.synchronize()
+            for i in range(3):
+                assert torch.equal(ys[i], want[i]), (n_out, m, k, rep, i)
