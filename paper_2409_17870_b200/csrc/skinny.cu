@@ -69,9 +69,13 @@ __host__ __device__ constexpr int sk_ctas_per_sm(int, int) { return 1; }
 __host__ __device__ constexpr uint32_t sk_smem_budget(int n, int nt) {
   return kSkSmemSM / sk_ctas_per_sm(n, nt);
 }
-// Per-warp TMA ring: a slot holds one work item, n planes x 16 rows x 64 B = n KB. The
-// depth (2..kMaxStages) is chosen at launch from the shared memory the X slice leaves.
-constexpr int kMaxStages = 16;
+// Per-warp TMA ring: a slot holds one work item, n planes x 16 rows x 64 B = n KB. Two slots
+// per warp: with deeper rings every warp requests its whole share at once, HBM serves the
+// requests in arbitrary order and warps wait for their first item while later items arrive
+// (8192^2 W3A8 M=1: 9.4 us at depth 2, 10.1 at 3, 10.8 at 4 or 8,
+// profiles/r02/r2_sk_stages.txt, profiles/r02/r2_decode_xfirst.txt); 16 warps x 2 slots keep
+// ~100 KB per SM in flight.
+constexpr uint32_t kStages = 2;
 constexpr int kXPieces = 16;  // X slice copy pieces (barriers)
 __host__ __device__ constexpr uint32_t slot_bytes(int n) { return static_cast<uint32_t>(n) * 1024u; }
 // Shared-memory X layout per 512-column chunk, real feature rows only (M = rows_x):
@@ -91,12 +95,16 @@ struct SkinnyParams {
   const uint8_t* xfrag;      // prep output: [chunks_total][chunk_bytes_m(frag_rows(rows_x))]
   const uint32_t* x_planes;  // inprep: reference layout [n_x][rows_x][wpr]
   uint32_t inprep;           // 1: this kernel builds its X slice itself (no prep kernel)
-  uint32_t prefetch;         // L2 prefetch distance in ring items (0: off)
   uint32_t n_x, k_logical;
+  // work split, precomputed on the host so that the prologue has no division: a CTA's first
+  // TMA issue is on the critical path of every call
+  uint32_t log2_wk;          // warps_k = WARPS >> log2(R), a power of two
+  uint32_t gs, cpw, xpc;     // CTAs per slice, chunks per warp per tile, chunks per X piece
+  uint64_t inv_slices, inv_gs;  // ceil(2^32 / d) for d = S, gs
+  uint64_t inv_sw, inv_sw_last;  // the same for the slice words (full slices, the last slice)
   const int32_t* rsx;        // prep output: rowsum(U_x) parts [rows_x][rsx_parts]
   uint32_t rsx_parts;
   uint32_t rows_w, rows_x, wpr, n_planes;
-  uint32_t stages;           // per-warp ring depth (2..kMaxStages)
   uint32_t chunks_total;     // ceil(wpr / 16)
   uint32_t slices, slice_chunks;
   uint32_t rgroups;          // R: 16-row groups per tile (warps_k = warps / R)
@@ -112,17 +120,40 @@ struct SkinnyParams {
   uint32_t coef_w, coef_x, c0;
   // multipliers kept in the parameter bank so ptxas emits IMAD (FMA pipe), not SHF/IADD
   uint32_t m2, m4, m16, neg1;
-  unsigned long long* ts;    // APMM_SKINNY_TS=1 (dev only): per-CTA phase timestamps, else null
+  unsigned long long* ts;    // dev builds only: per-CTA phase stamps [grid][8], else null
   uint32_t early_w;          // PDL: weight loads may start before the previous kernel completes
-  uint32_t ts_clock;         // dev: stamps are the SM's clock64 (cycle resolution, per CTA) instead
-  uint32_t l2_prefetch;      // 1: L2-prefetch each warp's next item ahead of its TMA load
+  uint32_t ts_clock;         // dev: stamps are the SM's clock64 (cycles, per CTA), else globaltimer
 };
 
+// floor(n / d) for n, d < 2^16 from inv = ceil(2^32 / d): exact (the error n * (inv * d - 2^32)
+// / 2^32 stays below 1 / d)
+APMM_DEV uint32_t div_small(uint32_t n, uint64_t inv) {
+  return static_cast<uint32_t>((static_cast<uint64_t>(n) * inv) >> 32);
+}
+inline uint64_t inv_small(uint32_t d) { return ((uint64_t(1) << 32) + d - 1) / d; }
+
+// dev builds: per-CTA phase stamps (0 start, 1 pdl_wait, 2 x_ready, 3 item0, 4 tile0, 5 end,
+// 6 inited, 7 issued); compiled out of the release library
+#ifdef APMM_DEVTOOLS
+#define SK_STAMP(k)                                                                         \
+  do {                                                                                      \
+    if (p.ts && tid == 0)                                                                   \
+      p.ts[blockIdx.x * 8 + (k)] =                                                          \
+          p.ts_clock ? static_cast<unsigned long long>(clock64()) : gtime_ns();             \
+  } while (0)
+#else
+#define SK_STAMP(k) \
+  do {              \
+  } while (0)
+#endif
+
+#ifdef APMM_DEVTOOLS
 APMM_DEV unsigned long long gtime_ns() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
+#endif
 
 APMM_DEV void mma_u8(uint32_t (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
                      uint32_t b0, uint32_t b1) {
@@ -140,13 +171,6 @@ APMM_DEV void tma_load_3d(uint32_t dst, const void* tmap, uint32_t bar, int32_t 
       " [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(dst),
       "l"(reinterpret_cast<uint64_t>(tmap)), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "l"(hint)
       : "memory");
-}
-// Prefetch one weight tile into L2 (no shared memory, no completion).
-APMM_DEV void tma_prefetch_l2_3d(const void* tmap, int32_t c0, int32_t c1, int32_t c2) {
-  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global [%0, {%1, %2, %3}];" ::"l"(
-                   reinterpret_cast<uint64_t>(tmap)),
-               "r"(c0), "r"(c1), "r"(c2)
-               : "memory");
 }
 // One bulk (non-tensor) TMA copy global -> this CTA's shared memory, completing on `bar`.
 APMM_DEV void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
@@ -295,73 +319,36 @@ __global__ void __launch_bounds__(sk_threads(N, NT), sk_ctas_per_sm(N, NT))
   constexpr uint32_t M_PAD = NT * 8u;
   constexpr uint32_t ONES = M_PAD - 1u;  // the all-ones feature column -> rowsum(U_w)
   extern __shared__ __align__(128) uint8_t smem[];
-  __shared__ __align__(8) uint64_t full_bar[WARPS * kMaxStages];
+  __shared__ __align__(8) uint64_t full_bar[WARPS * kStages];
   __shared__ __align__(8) uint64_t xbars[kXPieces];  // X slice arrival, per piece of chunks
   __shared__ uint32_t rsx_s[M_PAD];
   __shared__ uint32_t s_last;
 
   const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t g = lane >> 2, t = lane & 3;
-  if (p.ts && tid == 0) p.ts[blockIdx.x * 8 + 0] = (p.ts_clock ? static_cast<unsigned long long>(clock64()) : gtime_ns());
-  // dev (APMM_TRACE_CLOCK): cycle stamps of the individual prologue steps, thread 0 only
-  auto fine = [&](int k) {
-    if (p.ts && p.ts_clock && tid == 0) p.ts[blockIdx.x * 8 + k] = clock64();
-  };
-  const uint32_t warps_k = WARPS / p.rgroups;
-  const uint32_t wr = warp / warps_k, wk = warp % warps_k;
-  const uint32_t tile_rows = 16u * p.rgroups;
+  SK_STAMP(0);
+  const uint32_t warps_k = 1u << p.log2_wk;
+  const uint32_t wr = warp >> p.log2_wk, wk = warp & (warps_k - 1u);
+  const uint32_t tile_rows = (WARPS >> p.log2_wk) * 16u;
 
   // persistent CTA: slice = blockIdx.x % S, tiles j0, j0 + gs, ... (gs CTAs per slice)
-  const uint32_t slice = blockIdx.x % p.slices;
-  const uint32_t j0 = blockIdx.x / p.slices, gs = gridDim.x / p.slices;
+  const uint32_t j0 = div_small(blockIdx.x, p.inv_slices);
+  const uint32_t slice = blockIdx.x - j0 * p.slices;
+  const uint32_t gs = p.gs, cpw = p.cpw;  // chunks per warp per tile
   const uint32_t s_begin = slice * p.slice_chunks;
   const uint32_t s_end = min(s_begin + p.slice_chunks, p.chunks_total);
-  const uint32_t cpw = (p.slice_chunks + warps_k - 1) / warps_k;  // chunks per warp per tile
-  const uint32_t my_tiles = j0 < p.n_tiles ? (p.n_tiles - j0 + gs - 1) / gs : 0u;
+  const uint32_t my_tiles = j0 < p.n_tiles ? div_small(p.n_tiles - j0 + gs - 1u, p.inv_gs) : 0u;
 
   uint8_t* xs = smem;
-  const uint32_t stages = p.stages;
-  const uint32_t ring = apmm_ptx::smem_u32(smem + p.ring_off) + warp * (stages * SLOT);
+  const uint32_t ring = apmm_ptx::smem_u32(smem + p.ring_off) + warp * (kStages * SLOT);
   uint32_t* red = reinterpret_cast<uint32_t*>(smem + p.red_off);  // [tile_rows][M_PAD]
-  uint64_t* bars = full_bar + warp * kMaxStages;
+  uint64_t* bars = full_bar + warp * kStages;
   const uint32_t xchunk_bytes = chunk_bytes_m(frag_rows(p.rows_x));
 
-  if (lane == 0) {
-    for (uint32_t s = 0; s < stages; ++s) apmm_ptx::mbar_init(&bars[s], 1);
-    if (warp == 0) {
-      for (int i = 0; i < kXPieces; ++i) apmm_ptx::mbar_init(&xbars[i], 1);
-    }
-    fine(1);
-    // mbarrier inits -> visible to the TMA unit (async proxy). A non-cluster launch needs
-    // no cluster-scope release (fence.mbarrier_init.release.cluster cost ~0.8 us per CTA at
-    // kernel start, profiles/r01b_skinny_phase_ts2.txt).
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    fine(2);
-    apmm_ptx::tma_prefetch_desc(&tmap_w);
-    fine(3);
-  }
-  __syncwarp();
-  const uint64_t hint = apmm_ptx::policy_evict_first();  // weights are read exactly once
-  fine(4);
-
   // ---- per-warp TMA ring: item cursor (tile index, chunk step) ----
-  // L2 prefetch cursor, kPrefetch items ahead of the ring: the weight stream runs at HBM
-  // rate from the kernel's first microsecond (through the start-up and in whatever order
-  // HBM serves it) while the shallow shared-memory ring refills from L2.
-  uint32_t pf_tile = 0, pf_c = 0;
-  auto prefetch_next = [&]() {
-    if (p.l2_prefetch && pf_tile < my_tiles) {
-      const uint32_t chunk = s_begin + pf_c * warps_k + wk;
-      if (chunk < s_end && lane == 0) {
-        const uint32_t row0 = (j0 + pf_tile * gs) * tile_rows + wr * 16u;
-        tma_prefetch_l2_3d(&tmap_w, int32_t(chunk * kChunkWords), int32_t(row0), 0);
-      }
-      if (++pf_c == cpw) { pf_c = 0; ++pf_tile; }
-    }
-  };
   uint32_t is_tile = 0, is_c = 0, is_slot = 0;
+  uint64_t hint = 0;
   auto issue = [&]() {
-    prefetch_next();
     if (is_tile < my_tiles) {
       const uint32_t chunk = s_begin + is_c * warps_k + wk;
       if (chunk < s_end && lane == 0) {
@@ -372,23 +359,34 @@ __global__ void __launch_bounds__(sk_threads(N, NT), sk_ctas_per_sm(N, NT))
       }
       if (++is_c == cpw) { is_c = 0; ++is_tile; }
     }
-    if (++is_slot == stages) is_slot = 0;
+    is_slot ^= 1u;
   };
 
-  // The weight planes are inputs of this call, so their loads may overlap the prep kernel
-  // still running ahead of us (PDL); X, the workspace and Y only after pdl_wait.
-  if (p.ts && !p.ts_clock && tid == 0) p.ts[blockIdx.x * 8 + 6] = gtime_ns();
+  // Each warp initialises its own ring barriers and issues its first weight load at once:
+  // the weight planes are inputs of this call, so their loads may overlap the kernel still
+  // running ahead of us (PDL); X, the workspace and Y only after pdl_wait.
+  if (lane == 0) {
+    apmm_ptx::mbar_init(&bars[0], 1);
+    apmm_ptx::mbar_init(&bars[1], 1);
+    if (warp == 0) {
+#pragma unroll
+      for (int i = 0; i < kXPieces; ++i) apmm_ptx::mbar_init(&xbars[i], 1);
+    }
+    // mbarrier inits -> visible to the TMA unit (async proxy). A non-cluster launch needs
+    // no cluster-scope release (fence.mbarrier_init.release.cluster cost ~0.8 us per CTA at
+    // kernel start, profiles/r01b_skinny_phase_ts2.txt).
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  __syncwarp();
+  SK_STAMP(6);
+  hint = apmm_ptx::policy_evict_first();  // weights are read exactly once
   if (!p.early_w) apmm_ptx::pdl_wait();  // weights may be produced by the previous kernel
-  for (uint32_t i = 0; i < stages - 1 + p.prefetch; ++i) prefetch_next();
-  fine(5);
-  for (uint32_t s = 0; s + 1 < stages; ++s) issue();
-  fine(6);
-  if (p.ts && !p.ts_clock && tid == 0) p.ts[blockIdx.x * 8 + 7] = gtime_ns();
+  issue();
+  SK_STAMP(7);
   apmm_ptx::pdl_wait();
-  fine(7);
-  if (p.ts && !p.ts_clock && tid == 0) p.ts[blockIdx.x * 8 + 1] = gtime_ns();
+  SK_STAMP(1);
   __syncthreads();  // xbars initialised
-  const uint32_t xpc = (p.slice_chunks + kXPieces - 1) / kXPieces;  // chunks per X piece
+  const uint32_t xpc = p.xpc;  // chunks per X piece
   if (p.inprep) {
     // Feature prep in the prologue (few feature rows): this CTA's K slice of X planes ->
     // fragment-order codes in shared memory, its rowsum(U_x) share, and the zero / ones
@@ -400,7 +398,8 @@ __global__ void __launch_bounds__(sk_threads(N, NT), sk_ctas_per_sm(N, NT))
     const uint32_t xr = frag_rows(p.rows_x);
     const uint64_t pstride = uint64_t(p.rows_x) * p.wpr;
     for (uint32_t idx = tid; idx < xr * slice_words; idx += THREADS) {
-      const uint32_t tok = idx / slice_words, wl = idx - tok * slice_words;
+      const uint32_t tok = div_small(idx, slice + 1u == p.slices ? p.inv_sw_last : p.inv_sw);
+      const uint32_t wl = idx - tok * slice_words;
       const uint32_t W = s_begin * kChunkWords + wl;
       const bool real = tok < p.rows_x;
       uint32_t v[8];
@@ -447,7 +446,7 @@ __global__ void __launch_bounds__(sk_threads(N, NT), sk_ctas_per_sm(N, NT))
     for (uint32_t q = tid; q < tile_rows * M_PAD; q += THREADS) red[q] = 0u;
     __syncthreads();
   }
-  if (p.ts && !p.ts_clock && tid == 0) p.ts[blockIdx.x * 8 + 2] = gtime_ns();
+  SK_STAMP(2);
   // The terms are linear in K: with the prep kernel, slice 0 adds the X term and the whole
   // constant; with in-kernel prep every slice adds its own X term and K_slice * A * B.
   uint32_t cterm = slice == 0 ? p.c0 : 0u;
@@ -490,7 +489,7 @@ __global__ void __launch_bounds__(sk_threads(N, NT), sk_ctas_per_sm(N, NT))
         apmm_ptx::mbar_wait(&bars[cs_slot], (phase_bits >> cs_slot) & 1u);
         phase_bits ^= 1u << cs_slot;
         // slot layout (TMA box {16 words, 16 rows, planes}): [plane][row][16 words]
-        const uint8_t* slot = smem + p.ring_off + (warp * stages + cs_slot) * SLOT + g * 64u + t * 16u;
+        const uint8_t* slot = smem + p.ring_off + (warp * kStages + cs_slot) * SLOT + g * 64u + t * 16u;
         uint4 wa[N], wb[N];
 #pragma unroll
         for (int pl = 0; pl < N; ++pl) {
@@ -539,10 +538,10 @@ __global__ void __launch_bounds__(sk_threads(N, NT), sk_ctas_per_sm(N, NT))
           }
         }
       }
-      if (++cs_slot == stages) cs_slot = 0;
-      if (p.ts && !p.ts_clock && tid == 0 && ti == 0 && c == 0) p.ts[blockIdx.x * 8 + 3] = gtime_ns();
+      cs_slot ^= 1u;
+      if (ti == 0 && c == 0) SK_STAMP(3);
     }
-    if (p.ts && !p.ts_clock && tid == 0 && ti == 0) p.ts[blockIdx.x * 8 + 4] = gtime_ns();
+    if (ti == 0) SK_STAMP(4);
 
     // ---------------- end of tile: combine the K groups, epilogue ----------------
     if (ti + 1 == my_tiles) apmm_ptx::pdl_trigger();  // last tile: the next call may start
@@ -615,7 +614,7 @@ __global__ void __launch_bounds__(sk_threads(N, NT), sk_ctas_per_sm(N, NT))
     // s_last is next written after the next tile's first barrier
   }
   if (my_tiles == 0) apmm_ptx::pdl_trigger();
-  if (p.ts && !p.ts_clock && tid == 0) p.ts[blockIdx.x * 8 + 5] = gtime_ns();
+  SK_STAMP(5);
 }
 
 template <int N, int NT, bool SPLIT>
@@ -664,21 +663,16 @@ cudaError_t dispatch_n(int n_w, bool split, const CUtensorMap& tm, const SkinnyP
                   : launch_t<8, NT, false>(tm, p, grid, smem, s);
 }
 
-// Work plan: R (16-row groups per tile), S (K slices), grid. Minimises the per-warp
-// critical path in 512-column chunk steps, ceil(tiles / CTAs per slice) *
-// (ceil(slice_chunks / warps_k) + per-tile epilogue cost), plus a charge for the split-K
-// atomics, subject to the X slice fitting shared memory.
 struct Plan {
-  uint32_t r, s, slice_chunks, n_tiles, grid, smem, ring_off, red_off, stages;
+  uint32_t r, s, slice_chunks, n_tiles, grid, smem, ring_off, red_off;
 };
 
-// Work plan: R (16-row groups per tile), S (K slices), ring depth, grid. The cost counts a
-// warp's critical path in item steps (one item = 16 rows x 512 columns): the compute,
+// Work plan: R (16-row groups per tile), S (K slices), grid. The cost counts a warp's
+// critical path in item steps (one item = 16 rows x 512 columns): the compute,
 // ceil(tiles / CTAs per slice) * (ceil(slice_chunks / warps_k) + epilogue), plus memory
-// round trips, ceil(items / items in flight) * ~3 steps, plus the split-K atomics. The X
+// round trips, ~3 steps per item beyond the one in flight, plus the split-K atomics. The X
 // slice, the ring and the reduction buffer share the CTA's shared memory.
-Plan plan_for(uint64_t rows_w, uint64_t rows_x, uint32_t chunks, int n, int nt, int num_sms,
-              int stage_cap = 0) {
+Plan plan_for(uint64_t rows_w, uint64_t rows_x, uint32_t chunks, int n, int nt, int num_sms) {
   const uint32_t warps = static_cast<uint32_t>(sk_threads(n, nt) / 32);
   const uint32_t stage_all = warps * slot_bytes(n);  // one ring stage of every warp
   const uint32_t budget = sk_smem_budget(n, nt);
@@ -692,19 +686,15 @@ Plan plan_for(uint64_t rows_w, uint64_t rows_x, uint32_t chunks, int n, int nt, 
       const uint32_t sc = (chunks + s - 1) / s;
       if ((chunks + sc - 1) / sc != s) continue;  // same plan as a smaller s
       const uint32_t used = sc * chunk_bytes_m(frag_rows(static_cast<uint32_t>(rows_x))) + red_bytes(nt, r);
-      if (used + 2 * stage_all + 1024u > budget) continue;  // 1 KB: ring alignment
-      uint32_t stages = (budget - used - 1024u) / stage_all;
-      if (stages > kMaxStages) stages = kMaxStages;
-      if (stage_cap >= 2 && stages > static_cast<uint32_t>(stage_cap)) stages = stage_cap;
+      if (used + kStages * stage_all + 1024u > budget) continue;  // 1 KB: ring alignment
       const uint32_t per_slice = ctas / s;
       if (per_slice == 0) break;
       const uint64_t gs = n_tiles < per_slice ? n_tiles : per_slice;
       const uint64_t rounds = (n_tiles + gs - 1) / gs;
       const uint32_t cpw = (sc + warps_k - 1) / warps_k;
-      const double items = static_cast<double>(rounds * cpw);
-      const double trips = static_cast<double>((rounds * cpw + stages - 2) / (stages - 1));
+      const double trips = static_cast<double>(rounds * cpw);
       const double cost = static_cast<double>(rounds) * (cpw + 0.6) + 3.0 * trips +
-                          (s > 1 ? 0.25 * rounds + 1.0 : 0.0) + 0.0 * items;
+                          (s > 1 ? 0.25 * rounds + 1.0 : 0.0);
       if (cost < best_cost - 1e-9) {
         best_cost = cost;
         best.r = r;
@@ -712,13 +702,12 @@ Plan plan_for(uint64_t rows_w, uint64_t rows_x, uint32_t chunks, int n, int nt, 
         best.slice_chunks = sc;
         best.n_tiles = static_cast<uint32_t>(n_tiles);
         best.grid = static_cast<uint32_t>(gs * s);
-        best.stages = stages;
       }
     }
   }
   best.ring_off = best.slice_chunks * chunk_bytes_m(frag_rows(static_cast<uint32_t>(rows_x)));
   best.ring_off = (best.ring_off + 1023u) & ~1023u;
-  best.red_off = best.ring_off + best.stages * stage_all;
+  best.red_off = best.ring_off + kStages * stage_all;
   best.smem = best.red_off + red_bytes(nt, best.r);
   return best;
 }
@@ -766,21 +755,11 @@ cudaError_t launch_skinny(const SkinnyArgs& a, cudaStream_t s) {
   const bool ext_shape = a.n_w <= 2 && nt <= 2;
   const bool split = a.n_w <= 4 && kab < (ext_shape ? 67108864.0 : 268435456.0);
   const int kn = kernel_n(a.n_w, split);
-  // Ring depth 2 per warp: with deeper rings every warp requests its whole share at once,
-  // HBM serves the requests in arbitrary order and warps wait for their first item while
-  // later items arrive (8192^2 W3A8 M=1: 9.7 us at depth 4, 8.4 us at depth 2,
-  // profiles/r01b_skinny_stage_sweep.txt). 16 warps x 2 slots still keep ~100 KB per SM in
-  // flight, above what HBM latency x bandwidth needs. APMM_SK_STAGES overrides (dev).
-  static const int stage_cap = [] {
-    const char* e = APMM_DEV_ENV("APMM_SK_STAGES");
-    return e ? std::atoi(e) : 2;
-  }();
   static const int inprep_env = [] {
     const char* e = APMM_DEV_ENV("APMM_SK_INPREP");
     return e ? std::atoi(e) : -1;
   }();
-  const Plan pl = plan_for(a.rows_w, a.rows_x, p.chunks_total, kn, static_cast<int>(nt), a.num_sms,
-                           stage_cap);
+  const Plan pl = plan_for(a.rows_w, a.rows_x, p.chunks_total, kn, static_cast<int>(nt), a.num_sms);
   // In-kernel feature prep pays only for a single feature row (saves the prep launch and its
   // PDL round trip; for more rows the redundant per-CTA transposes cost more).
   const bool inprep = inprep_env >= 0 ? inprep_env != 0 : a.rows_x <= 1;
@@ -819,9 +798,9 @@ cudaError_t launch_skinny(const SkinnyArgs& a, cudaStream_t s) {
   }
   if (show) {
     std::fprintf(stderr, "[apmm skinny] %llux%llux%llu W%dA%d: R=%u S=%u slice_chunks=%u tiles=%u "
-                 "grid=%u smem=%u stages=%u split=%d repack=%d\n", (unsigned long long)a.rows_w,
+                 "grid=%u smem=%u split=%d repack=%d\n", (unsigned long long)a.rows_w,
                  (unsigned long long)a.rows_x, (unsigned long long)a.k, a.n_w, a.n_x, pl.r, pl.s,
-                 pl.slice_chunks, pl.n_tiles, pl.grid, pl.smem, pl.stages, int(split),
+                 pl.slice_chunks, pl.n_tiles, pl.grid, pl.smem, int(split),
                  int(needs_repack(a.k, a.w_planes)));
   }
   const uint64_t rows_pad = uint64_t(pl.n_tiles) * 16u * pl.r;
@@ -831,18 +810,27 @@ cudaError_t launch_skinny(const SkinnyArgs& a, cudaStream_t s) {
   p.x_planes = a.x_planes;
   p.inprep = inprep ? 1u : 0u;
   p.early_w = a.early_w ? 1u : 0u;
-  static const uint32_t prefetch = [] {
-    const char* e = APMM_DEV_ENV("APMM_SK_PREFETCH");
-    return e ? static_cast<uint32_t>(std::atoi(e)) : 0u;  // measured no gain (r01b_skinny_prefetch_sweep.txt)
-  }();
-  p.prefetch = prefetch;
   p.n_x = static_cast<uint32_t>(a.n_x);
   p.k_logical = static_cast<uint32_t>(a.k);
   p.rsx = rsx;
   p.rsx_parts = prep_blocks;
   p.rgroups = pl.r;
-  p.stages = pl.stages;
   p.slices = pl.s;
+  {
+    const uint32_t warps = static_cast<uint32_t>(sk_threads(kn, static_cast<int>(nt)) / 32);
+    uint32_t l = 0;
+    while ((1u << (l + 1)) <= pl.r) ++l;  // R is a power of two
+    const uint32_t warps_k = warps >> l;
+    p.log2_wk = 0;
+    while ((1u << (p.log2_wk + 1)) <= warps_k) ++p.log2_wk;
+    p.gs = pl.grid / pl.s;
+    p.cpw = (pl.slice_chunks + warps_k - 1) / warps_k;
+    p.xpc = (pl.slice_chunks + kXPieces - 1) / kXPieces;
+    p.inv_slices = inv_small(pl.s);
+    p.inv_gs = inv_small(p.gs);
+    p.inv_sw = inv_small(pl.slice_chunks * kChunkWords);
+    p.inv_sw_last = inv_small((p.chunks_total - (pl.s - 1) * pl.slice_chunks) * kChunkWords);
+  }
   p.slice_chunks = pl.slice_chunks;
   p.n_tiles = pl.n_tiles;
   p.ring_off = pl.ring_off;
@@ -860,24 +848,9 @@ cudaError_t launch_skinny(const SkinnyArgs& a, cudaStream_t s) {
   p.m4 = 4u;
   p.m16 = 16u;
   p.neg1 = 0xFFFFFFFFu;
-  static const bool want_ts = APMM_DEV_ENV("APMM_SKINNY_TS") != nullptr;
-  static unsigned long long* ts_buf = nullptr;
-  if (want_ts) {
-    if (!ts_buf) cudaMalloc(&ts_buf, 1024 * 8 * sizeof(unsigned long long));
-    cudaMemsetAsync(ts_buf, 0, 1024 * 8 * sizeof(unsigned long long), s);
-    p.ts = ts_buf;
-  }
   if (a.trace) p.ts = a.trace;  // dev launch trace (APMM_TRACE)
   static const bool ts_clock = APMM_DEV_ENV("APMM_TRACE_CLOCK") != nullptr;
   p.ts_clock = ts_clock ? 1u : 0u;
-  // Off: the L2 prefetch ahead of each TMA load doubled the TMA instructions a warp issues
-  // at kernel start (~1000 cycles of the prologue, cycle trace) and the stream gained nothing:
-  // 8192^2 W3A8 M=1 9.67 -> 9.15 us, 4096x1x11008 W2A4 7.54 -> 7.00 us (r02/r2_sk_l2pf.txt).
-  static const int l2pf = [] {  // dev A/B (APMM_SK_L2PF=0/1)
-    const char* e = APMM_DEV_ENV("APMM_SK_L2PF");
-    return e ? std::atoi(e) : 0;
-  }();
-  p.l2_prefetch = l2pf ? 1u : 0u;
 
   if (!inprep) {  // feature prep (same shared-memory carveout as the streaming kernel: no reconfig)
     static DeviceBits carve_set;
@@ -913,28 +886,6 @@ cudaError_t launch_skinny(const SkinnyArgs& a, cudaStream_t s) {
     default: res = dispatch_n<8>(a.n_w, split, tm, p, pl.grid, pl.smem, s); break;
   }
   if (a.ev_stop) cudaEventRecordWithFlags(a.ev_stop, s, a.ev_flags);
-  if (want_ts && res == cudaSuccess) {  // dev only: per-phase CTA timeline (us from first start)
-    unsigned long long h[1024 * 8];
-    cudaStreamSynchronize(s);
-    cudaMemcpy(h, ts_buf, pl.grid * 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
-    unsigned long long t0 = ~0ull;
-    for (uint32_t b = 0; b < pl.grid; ++b) t0 = h[b * 8] && h[b * 8] < t0 ? h[b * 8] : t0;
-    const char* names[8] = {"start", "pdl_wait", "x_ready", "item0", "tile0", "end", "inited", "issued"};
-    for (int k = 0; k < 8; ++k) {
-      double mn = 1e30, mx = 0, sum = 0;
-      uint32_t cnt = 0;
-      for (uint32_t b = 0; b < pl.grid; ++b) {
-        if (!h[b * 8 + k]) continue;
-        const double v = (h[b * 8 + k] - t0) * 1e-3;
-        mn = v < mn ? v : mn;
-        mx = v > mx ? v : mx;
-        sum += v;
-        ++cnt;
-      }
-      std::fprintf(stderr, "[apmm skinny ts] %-8s min %7.2f avg %7.2f max %7.2f us (%u CTAs)\n",
-                   names[k], cnt ? mn : 0.0, cnt ? sum / cnt : 0.0, mx, cnt);
-    }
-  }
   return res;
 }
 

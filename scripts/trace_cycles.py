@@ -40,9 +40,8 @@ g.replay()
 torch.cuda.synchronize()
 fn(ctx.h, buf.ctypes.data, kinds.ctypes.data)
 t = buf.reshape(slots, 1024, 8).astype(np.int64)
-names = ["start", "mbar_init", "fence_proxy", "prefetch_desc", "createpolicy", "prefetch_next",
-         "issue", "pdl_wait"]
-order = [1, 2, 3, 4, 5, 6, 7]
+names = ["start", "pdl_wait", "x_ready", "item0", "tile0", "end", "inited", "issued"]
+order = [6, 7, 1, 2, 3, 4, 5]
 print(f"{n_out}x{m}x{k} W{nw}A{nx}: cycles from each CTA's own start (median / p90 over CTAs)")
 for i in range(slots):
     if kinds[i] != 5:
