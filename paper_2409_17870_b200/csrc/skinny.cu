@@ -50,6 +50,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 
 #include "internal.h"
 #include "ptx.cuh"
@@ -75,7 +76,11 @@ __host__ __device__ constexpr uint32_t sk_smem_budget(int n, int nt) {
 // (8192^2 W3A8 M=1: 9.4 us at depth 2, 10.1 at 3, 10.8 at 4 or 8,
 // profiles/r02/r2_sk_stages.txt, profiles/r02/r2_decode_xfirst.txt); 16 warps x 2 slots keep
 // ~100 KB per SM in flight.
+#ifndef APMM_SK_STAGES_DEV
 constexpr uint32_t kStages = 2;
+#else
+constexpr uint32_t kStages = APMM_SK_STAGES_DEV;  // dev A/B builds only
+#endif
 constexpr int kXPieces = 16;  // X slice copy pieces (barriers)
 __host__ __device__ constexpr uint32_t slot_bytes(int n) { return static_cast<uint32_t>(n) * 1024u; }
 // Shared-memory X layout per 512-column chunk, real feature rows only (M = rows_x):
@@ -100,7 +105,7 @@ struct SkinnyParams {
   // TMA issue is on the critical path of every call
   uint32_t log2_wk;          // warps_k = WARPS >> log2(R), a power of two
   uint32_t gs, cpw, xpc;     // CTAs per slice, chunks per warp per tile, chunks per X piece
-  uint64_t inv_slices, inv_gs;  // ceil(2^32 / d) for d = S, gs
+  uint64_t inv_slices, inv_gs, inv_xpc;  // ceil(2^32 / d) for d = S, gs, xpc
   uint64_t inv_sw, inv_sw_last;  // the same for the slice words (full slices, the last slice)
   const int32_t* rsx;        // prep output: rowsum(U_x) parts [rows_x][rsx_parts]
   uint32_t rsx_parts;
@@ -123,6 +128,8 @@ struct SkinnyParams {
   unsigned long long* ts;    // dev builds only: per-CTA phase stamps [grid][8], else null
   uint32_t early_w;          // PDL: weight loads may start before the previous kernel completes
   uint32_t ts_clock;         // dev: stamps are the SM's clock64 (cycles, per CTA), else globaltimer
+  uint32_t x_first;          // dev A/B (APMM_SK_XFIRST): in-kernel prep issues its feature loads
+                             // before the first weight load (which then waits for pdl_wait)
 };
 
 // floor(n / d) for n, d < 2^16 from inv = ceil(2^32 / d): exact (the error n * (inv * d - 2^32)
@@ -359,15 +366,15 @@ __global__ void __launch_bounds__(sk_threads(N, NT), sk_ctas_per_sm(N, NT))
       }
       if (++is_c == cpw) { is_c = 0; ++is_tile; }
     }
-    is_slot ^= 1u;
+    is_slot = is_slot + 1u == kStages ? 0u : is_slot + 1u;
   };
 
   // Each warp initialises its own ring barriers and issues its first weight load at once:
   // the weight planes are inputs of this call, so their loads may overlap the kernel still
   // running ahead of us (PDL); X, the workspace and Y only after pdl_wait.
   if (lane == 0) {
-    apmm_ptx::mbar_init(&bars[0], 1);
-    apmm_ptx::mbar_init(&bars[1], 1);
+#pragma unroll
+    for (uint32_t q = 0; q < kStages; ++q) apmm_ptx::mbar_init(&bars[q], 1);
     if (warp == 0) {
 #pragma unroll
       for (int i = 0; i < kXPieces; ++i) apmm_ptx::mbar_init(&xbars[i], 1);
@@ -381,7 +388,10 @@ __global__ void __launch_bounds__(sk_threads(N, NT), sk_ctas_per_sm(N, NT))
   SK_STAMP(6);
   hint = apmm_ptx::policy_evict_first();  // weights are read exactly once
   if (!p.early_w) apmm_ptx::pdl_wait();  // weights may be produced by the previous kernel
-  issue();
+  const bool x_first = p.x_first && p.inprep;
+  if (!x_first)
+#pragma unroll
+    for (uint32_t q = 0; q + 1 < kStages; ++q) issue();
   SK_STAMP(7);
   apmm_ptx::pdl_wait();
   SK_STAMP(1);
@@ -390,33 +400,55 @@ __global__ void __launch_bounds__(sk_threads(N, NT), sk_ctas_per_sm(N, NT))
   if (p.inprep) {
     // Feature prep in the prologue (few feature rows): this CTA's K slice of X planes ->
     // fragment-order codes in shared memory, its rowsum(U_x) share, and the zero / ones
-    // rows. One thread per (fragment row, 32-column word): n_x words -> 8x8 transpose.
-    for (uint32_t q = tid; q < M_PAD; q += THREADS) rsx_s[q] = 0u;
-    for (uint32_t q = tid; q < tile_rows * M_PAD; q += THREADS) red[q] = 0u;
-    __syncthreads();
+    // rows. One thread per (feature row, 32-column word): n_x words -> 8x8 transpose. Every
+    // thread's first loads are issued before anything else, so the whole slice of a single
+    // feature row costs one round trip; the constant rows need no loads.
     const uint32_t slice_words = (s_end > s_begin ? s_end - s_begin : 0u) * kChunkWords;
     const uint32_t xr = frag_rows(p.rows_x);
+    const uint32_t real_words = p.rows_x * slice_words;
     const uint64_t pstride = uint64_t(p.rows_x) * p.wpr;
-    for (uint32_t idx = tid; idx < xr * slice_words; idx += THREADS) {
-      const uint32_t tok = div_small(idx, slice + 1u == p.slices ? p.inv_sw_last : p.inv_sw);
-      const uint32_t wl = idx - tok * slice_words;
+    const uint64_t inv_sw = slice + 1u == p.slices ? p.inv_sw_last : p.inv_sw;
+    auto xload = [&](uint32_t idx, uint32_t (&v)[8]) {
+      const uint32_t tok = div_small(idx, inv_sw), wl = idx - tok * slice_words;
       const uint32_t W = s_begin * kChunkWords + wl;
-      const bool real = tok < p.rows_x;
-      uint32_t v[8];
-      uint32_t rs = 0;
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        v[i] = (real && uint32_t(i) < p.n_x && W < p.wpr)
-                   ? __ldg(p.x_planes + i * pstride + uint64_t(tok) * p.wpr + W)
-                   : (tok == p.rows_x + 1u ? 0x01010101u : 0u);
-        if (real) rs += uint32_t(__popc(v[i])) << i;
-      }
-      if (real) transpose8(v);
+      for (int i = 0; i < 8; ++i)
+        v[i] = (uint32_t(i) < p.n_x && W < p.wpr)
+                   ? __ldg(p.x_planes + i * pstride + uint64_t(tok) * p.wpr + W) : 0u;
+    };
+    auto xstore = [&](uint32_t tok, uint32_t wl, const uint32_t (&v)[8]) {
       const uint32_t cl = wl / kChunkWords, t4 = (wl % kChunkWords) >> 2, w = wl & 3u;
       uint4* dst = reinterpret_cast<uint4*>(xs + cl * xchunk_bytes) + ((w * 2u) * xr + tok) * 4u + t4;
       dst[0] = make_uint4(v[0], v[1], v[2], v[3]);
       dst[xr * 4u] = make_uint4(v[4], v[5], v[6], v[7]);
+    };
+    auto xprocess = [&](uint32_t idx, uint32_t (&v)[8]) {
+      const uint32_t tok = div_small(idx, inv_sw), wl = idx - tok * slice_words;
+      uint32_t rs = 0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) rs += uint32_t(__popc(v[i])) << i;
+      transpose8(v);
+      xstore(tok, wl, v);
       if (rs) atomicAdd(&rsx_s[tok], rs);
+    };
+    uint32_t v0[8];
+    if (tid < real_words) xload(tid, v0);
+    if (x_first)
+#pragma unroll
+      for (uint32_t q = 0; q + 1 < kStages; ++q) issue();
+    for (uint32_t q = tid; q < M_PAD; q += THREADS) rsx_s[q] = 0u;
+    for (uint32_t q = tid; q < tile_rows * M_PAD; q += THREADS) red[q] = 0u;
+    for (uint32_t q = tid; q < 2u * slice_words; q += THREADS) {  // the zero and all-ones rows
+      const uint32_t hi = q >= slice_words ? 1u : 0u, c = hi ? 0x01010101u : 0u;
+      const uint32_t v[8] = {c, c, c, c, c, c, c, c};
+      xstore(p.rows_x + hi, q - hi * slice_words, v);
+    }
+    __syncthreads();  // rsx_s zeroed
+    if (tid < real_words) xprocess(tid, v0);
+    for (uint32_t idx = tid + THREADS; idx < real_words; idx += THREADS) {
+      uint32_t v[8];
+      xload(idx, v);
+      xprocess(idx, v);
     }
     __syncthreads();
   } else {
@@ -485,9 +517,10 @@ __global__ void __launch_bounds__(sk_threads(N, NT), sk_ctas_per_sm(N, NT))
       issue();
       const uint32_t chunk = s_begin + c * warps_k + wk;
       if (chunk < s_end) {
-        if (!p.inprep) apmm_ptx::mbar_wait(&xbars[(chunk - s_begin) / xpc], 0);
+        if (!p.inprep) apmm_ptx::mbar_wait(&xbars[div_small(chunk - s_begin, p.inv_xpc)], 0);
         apmm_ptx::mbar_wait(&bars[cs_slot], (phase_bits >> cs_slot) & 1u);
         phase_bits ^= 1u << cs_slot;
+        if (ti == 0 && c == 0) SK_STAMP(3);  // the first item's weights are in
         // slot layout (TMA box {16 words, 16 rows, planes}): [plane][row][16 words]
         const uint8_t* slot = smem + p.ring_off + (warp * kStages + cs_slot) * SLOT + g * 64u + t * 16u;
         uint4 wa[N], wb[N];
@@ -538,8 +571,7 @@ __global__ void __launch_bounds__(sk_threads(N, NT), sk_ctas_per_sm(N, NT))
           }
         }
       }
-      cs_slot ^= 1u;
-      if (ti == 0 && c == 0) SK_STAMP(3);
+      cs_slot = cs_slot + 1u == kStages ? 0u : cs_slot + 1u;
     }
     if (ti == 0) SK_STAMP(4);
 
@@ -679,12 +711,23 @@ Plan plan_for(uint64_t rows_w, uint64_t rows_x, uint32_t chunks, int n, int nt, 
   const uint32_t ctas = static_cast<uint32_t>(num_sms * sk_ctas_per_sm(n, nt));
   Plan best{};
   double best_cost = 1e30;
+  static const int force_r = [] {  // dev: APMM_SK_RS="R,S" pins the plan (A/B of the cost model)
+    const char* e = APMM_DEV_ENV("APMM_SK_RS");
+    return e ? std::atoi(e) : 0;
+  }();
+  static const int force_s = [] {
+    const char* e = APMM_DEV_ENV("APMM_SK_RS");
+    const char* c = e ? std::strchr(e, ',') : nullptr;
+    return c ? std::atoi(c + 1) : 0;
+  }();
   for (uint32_t r = 1; r <= 8 && r <= warps; r <<= 1) {
+    if (force_r && r != static_cast<uint32_t>(force_r)) continue;
     const uint32_t warps_k = warps / r;
     const uint64_t n_tiles = (rows_w + 16 * r - 1) / (16 * r);
     for (uint32_t s = 1; s <= chunks; ++s) {
       const uint32_t sc = (chunks + s - 1) / s;
       if ((chunks + sc - 1) / sc != s) continue;  // same plan as a smaller s
+      if (force_s && s != static_cast<uint32_t>(force_s)) continue;
       const uint32_t used = sc * chunk_bytes_m(frag_rows(static_cast<uint32_t>(rows_x))) + red_bytes(nt, r);
       if (used + kStages * stage_all + 1024u > budget) continue;  // 1 KB: ring alignment
       const uint32_t per_slice = ctas / s;
@@ -828,6 +871,7 @@ cudaError_t launch_skinny(const SkinnyArgs& a, cudaStream_t s) {
     p.xpc = (pl.slice_chunks + kXPieces - 1) / kXPieces;
     p.inv_slices = inv_small(pl.s);
     p.inv_gs = inv_small(p.gs);
+    p.inv_xpc = inv_small(p.xpc);
     p.inv_sw = inv_small(pl.slice_chunks * kChunkWords);
     p.inv_sw_last = inv_small((p.chunks_total - (pl.s - 1) * pl.slice_chunks) * kChunkWords);
   }
@@ -851,6 +895,8 @@ cudaError_t launch_skinny(const SkinnyArgs& a, cudaStream_t s) {
   if (a.trace) p.ts = a.trace;  // dev launch trace (APMM_TRACE)
   static const bool ts_clock = APMM_DEV_ENV("APMM_TRACE_CLOCK") != nullptr;
   p.ts_clock = ts_clock ? 1u : 0u;
+  static const uint32_t x_first = APMM_DEV_ENV("APMM_SK_XFIRST") != nullptr ? 1u : 0u;
+  p.x_first = x_first;
 
   if (!inprep) {  // feature prep (same shared-memory carveout as the streaming kernel: no reconfig)
     static DeviceBits carve_set;

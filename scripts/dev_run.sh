@@ -1,5 +1,3 @@
-# dev A/B run for the decode kernel; outputs under gpurun_out/abl
 mkdir -p gpurun_out/abl
 export PYTHONUNBUFFERED=1
-timeout 600 python -m pytest tests -q -x -m gpu > gpurun_out/abl/pytest_gpu.txt 2>&1
-for ip in -1 1; do echo "== inprep $ip"; APMM_LIB=$PWD/abtest/libapmm_b200_dev.so APMM_SK_INPREP=$ip timeout 120 python scripts/decode_bench.py 30; done > gpurun_out/abl/decode_inprep.txt 2>&1
+for v in "" _s3 _s4; do echo "== stages lib$v"; APMM_LIB=$PWD/abtest/libapmm_b200_dev$v.so timeout 120 python scripts/decode_bench.py 30 8192x1,8192x8,8192x16,4096x1,11008x1,4096x1x11008,4096x16; done > gpurun_out/abl/decode_stages.txt 2>&1
