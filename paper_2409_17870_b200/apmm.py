@@ -200,6 +200,7 @@ class Route(enum.IntEnum):
     PAIR_SPLITK = 5
     SINGLE_SM = 6
     TENSOR_CORE = 7
+    STREAM_TC = 8
 
 
 OPT_ROUTE, OPT_EARLY_WEIGHT_READ, OPT_EARLY_FEATURE_READ = 1, 2, 3

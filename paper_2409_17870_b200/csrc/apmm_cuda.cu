@@ -45,6 +45,8 @@ struct apmm_ctx {
   size_t sk_ws_bytes = 0;
   void* sk_scratch = nullptr;  // K5 feature fragments (ping-pong halves) + weight repack
   size_t sk_scratch_bytes = 0;
+  void* tc_ws = nullptr;  // K6 feature codes + rowsum parts
+  size_t tc_ws_bytes = 0;
   bool dbg_waits = false;  // APMM_DEBUG_WAITS=1: MMA-issuer wait-cycle counters (dev only)
   void* dbg = nullptr;  // APMM_DEBUG_WAITS counters (dev only)
   int* flags = nullptr;  // device error flags (recover: 2 ints; quantize / requant: 1)
@@ -226,7 +228,7 @@ struct TimedLaunch {
 };
 
 // Kernel routes (apmm_cuda.h APMM_ROUTE_*). Every route computes the same bits.
-enum class Route { Skinny, Mid, Pair, PairW, PairSplit, Single };
+enum class Route { Skinny, Mid, Pair, PairW, PairSplit, Single, StreamTc };
 
 const char* route_name(Route r) {
   switch (r) {
@@ -235,22 +237,24 @@ const char* route_name(Route r) {
     case Route::Pair: return "pair (K1 + K3)";
     case Route::PairW: return "pair weight-planes (K3f)";
     case Route::PairSplit: return "pair split-K (K1 + K3)";
+    case Route::StreamTc: return "stream tensor-memory (K6)";
     default: return "single-SM (K1 + K3')";
   }
 }
 
 // Which routes can serve a call (their layout / output constraints).
 struct RouteCaps {
-  bool skinny, mid, pair_w, pair_split;
+  bool skinny, mid, pair_w, pair_split, stream_tc;
 };
-RouteCaps caps_of(const uint32_t* w, uint64_t rows_x, uint64_t k, const void* y, bool dequant,
-                  bool x_ready) {
+RouteCaps caps_of(const uint32_t* w, uint64_t rows_w, int n_w, uint64_t rows_x, uint64_t k,
+                  const void* y, bool dequant, bool x_ready) {
   const bool splitk_out = !dequant && rows_x % 4 == 0 && reinterpret_cast<uintptr_t>(y) % 16 == 0;
   RouteCaps c;
   c.skinny = rows_x <= kSkinnyMaxRowsX && !x_ready;
   c.mid = splitk_out && gemm_wplanes_addressable(w, k);
   c.pair_w = gemm_wplanes_addressable(w, k);
   c.pair_split = splitk_out;
+  c.stream_tc = !dequant && !x_ready && stream_tc_supported(w, rows_w, rows_x, k, n_w, y);
   return c;
 }
 
@@ -283,6 +287,7 @@ int pick_route(const apmm_ctx* ctx, const RouteCaps& c, uint64_t rows_w, uint64_
     case APMM_ROUTE_PAIR_WPLANES: return forced(c.pair_w, Route::PairW);
     case APMM_ROUTE_PAIR_SPLITK: return forced(c.pair_split, Route::PairSplit);
     case APMM_ROUTE_SINGLE_SM: return forced(true, Route::Single);
+    case APMM_ROUTE_STREAM_TC: return forced(c.stream_tc, Route::StreamTc);
     default: break;
   }
   const bool allow_skinny = ctx->route != APMM_ROUTE_TENSOR_CORE;
@@ -336,8 +341,8 @@ int run_matmul(apmm_ctx* ctx, const uint32_t* w, uint64_t rows_w, int n_w, const
                int gran_x, uint64_t k, int32_t* y, float* yf, cudaStream_t stream,
                bool x_ready = false, unsigned* colmax = nullptr, bool colmax_global = false) {
   CU(cudaSetDevice(ctx->device));
-  const RouteCaps caps = caps_of(w, rows_x, k, yf ? static_cast<const void*>(yf) : y, yf != nullptr,
-                                 x_ready);
+  const RouteCaps caps = caps_of(w, rows_w, n_w, rows_x, k, yf ? static_cast<const void*>(yf) : y,
+                                 yf != nullptr, x_ready);
   Route route;
   int st = pick_route(ctx, caps, rows_w, rows_x, &route);
   if (st) return st;
@@ -380,6 +385,35 @@ int run_matmul(apmm_ctx* ctx, const uint32_t* w, uint64_t rows_w, int n_w, const
       CU(launch_colmax(yf, rows_w, rows_x, colmax, colmax_global, ctx->num_sms, stream));
       ctx->launches += 1;
     }
+    return APMM_OK;
+  }
+  if (route == Route::StreamTc) {
+    // feature prep (codes + rowsum, Y zeroed) + K6, the weight planes streamed once into TMEM
+    if ((st = ensure(&ctx->tc_ws, &ctx->tc_ws_bytes, stream_tc_ws_bytes(rows_x, k), ctx->device,
+                     stream))) {
+      return st;
+    }
+    StreamTcArgs s{};
+    s.w_planes = w;
+    s.x_planes = x;
+    s.rows_w = rows_w;
+    s.rows_x = rows_x;
+    s.k = k;
+    s.n_w = n_w;
+    s.n_x = n_x;
+    s.y = y;
+    s.num_sms = ctx->num_sms;
+    s.ws = ctx->tc_ws;
+    s.early_w = ctx->early_w;
+    s.early_x = ctx->early_w && ctx->early_x;
+    {
+      TimedLaunch t(ctx, 0, stream, /*record=*/false);
+      s.ev_start = t.ev.first;
+      s.ev_stop = t.ev.second;
+      s.ev_flags = t.flags;
+      CU(launch_stream_tc(s, stream));
+    }
+    ctx->launches += 2;  // feature prep + K6
     return APMM_OK;
   }
   if ((st = ensure(&ctx->ws, &ctx->ws_bytes, matmul_ws_bytes(rows_w, rows_x, k), ctx->device,
@@ -654,6 +688,7 @@ int apmm_ctx_destroy(apmm_ctx* ctx) {
   if (ctx->ws) cudaFree(ctx->ws);
   if (ctx->sk_ws) cudaFree(ctx->sk_ws);
   if (ctx->sk_scratch) cudaFree(ctx->sk_scratch);
+  if (ctx->tc_ws) cudaFree(ctx->tc_ws);
   if (ctx->io) cudaFree(ctx->io);
   if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
   if (ctx->s_in) cudaStreamDestroy(ctx->s_in);
@@ -689,7 +724,7 @@ int apmm_ctx_set_option(apmm_ctx* ctx, int option, int value) {
   if (!ctx) return fail(APMM_E_INVALID_ARGUMENT, "null context");
   switch (option) {
     case APMM_OPT_ROUTE:
-      if (value < APMM_ROUTE_AUTO || value > APMM_ROUTE_TENSOR_CORE) {
+      if (value < APMM_ROUTE_AUTO || value > APMM_ROUTE_STREAM_TC) {
         return fail(APMM_E_INVALID_ARGUMENT, "unknown route %d", value);
       }
       ctx->route = value;
@@ -724,6 +759,9 @@ int apmm_ctx_reserve(apmm_ctx* ctx, uint64_t rows_w, uint64_t rows_x, uint64_t k
   }
   const cudaStream_t s = ctx->bound ? ctx->bound_stream : ctx->stream;
   if ((st = ensure(&ctx->ws, &ctx->ws_bytes, matmul_ws_bytes(rows_w, rows_x, k), ctx->device, s))) {
+    return st;
+  }
+  if ((st = ensure(&ctx->tc_ws, &ctx->tc_ws_bytes, stream_tc_ws_bytes(rows_x, k), ctx->device, s))) {
     return st;
   }
   if (rows_x <= kSkinnyMaxRowsX) {

@@ -196,6 +196,28 @@ size_t skinny_scratch_bytes(uint64_t rows_w, uint64_t rows_x, uint64_t k, int n_
                             const void* w_planes);
 cudaError_t launch_skinny(const SkinnyArgs& a, cudaStream_t s);
 
+// K6 (stream_tc.cu): weight planes streamed per warp, expanded in registers into TMEM (the
+// MMA's A operand), features as u8 codes in shared memory (B), tcgen05 kind::i8, K split
+// over every SM with int32 partials TMA reduce-added into a Y zeroed by the feature prep.
+struct StreamTcArgs {
+  const uint32_t* w_planes;  // reference layout [n_w][rows_w][ceil(k/32)]
+  const uint32_t* x_planes;  // reference layout [n_x][rows_x][ceil(k/32)]
+  uint64_t rows_w, rows_x, k;
+  int n_w, n_x;
+  int32_t* y;                // [rows_w][rows_x] int32
+  int num_sms;
+  void* ws;                  // stream_tc_ws_bytes(): feature codes + rowsum parts
+  bool early_w = true;       // PDL: weight loads may start before the previous kernel completes
+  bool early_x = false;      // PDL: the feature prep may read X before it
+  cudaEvent_t ev_start = nullptr, ev_stop = nullptr;  // measurement: around the GEMM launch
+  unsigned ev_flags = 0;
+};
+// Whether K6 can serve a call (shape, alignment and shared-memory budget).
+bool stream_tc_supported(const uint32_t* w, uint64_t rows_w, uint64_t rows_x, uint64_t k, int n_w,
+                         const void* y);
+size_t stream_tc_ws_bytes(uint64_t rows_x, uint64_t k);
+cudaError_t launch_stream_tc(const StreamTcArgs& a, cudaStream_t s);
+
 // Tensor-map encoder obtained from the driver through the runtime (no -lcuda).
 // 2-D row-major tensor [outer x inner] with `stride_bytes` between rows, 128B swizzle.
 CUresult encode_tmap_2d(CUtensorMap* map, CUtensorMapDataType dtype, uint32_t elem_bytes,
@@ -204,6 +226,7 @@ CUresult encode_tmap_2d(CUtensorMap* map, CUtensorMapDataType dtype, uint32_t el
 // 3-D u32 tensor, no swizzle, zero OOB fill: dims {inner, mid, outer}, byte strides of the
 // mid and outer dimensions (multiples of 16).
 CUresult encode_tmap_3d_u32(CUtensorMap* map, const void* base, const uint64_t (&dims)[3],
-                            const uint64_t (&stride_bytes)[2], const uint32_t (&box)[3]);
+                            const uint64_t (&stride_bytes)[2], const uint32_t (&box)[3],
+                            int swizzle_bytes = 0);  // 0: none, 64: SWIZZLE_64B
 
 }  // namespace apmm_b200

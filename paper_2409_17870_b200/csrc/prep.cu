@@ -700,7 +700,8 @@ CUresult encode_tmap_2d(CUtensorMap* map, CUtensorMapDataType dtype, uint32_t /*
 }
 
 CUresult encode_tmap_3d_u32(CUtensorMap* map, const void* base, const uint64_t (&dims)[3],
-                            const uint64_t (&stride_bytes)[2], const uint32_t (&box)[3]) {
+                            const uint64_t (&stride_bytes)[2], const uint32_t (&box)[3],
+                            int swizzle_bytes) {
   auto encode = tmap_encoder();
   if (!encode) return CUDA_ERROR_NOT_FOUND;
   const cuuint64_t d[3] = {dims[0], dims[1], dims[2]};
@@ -708,7 +709,8 @@ CUresult encode_tmap_3d_u32(CUtensorMap* map, const void* base, const uint64_t (
   const cuuint32_t b[3] = {box[0], box[1], box[2]};
   const cuuint32_t es[3] = {1, 1, 1};
   return encode(map, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, const_cast<void*>(base), d, st, b, es,
-                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                CU_TENSOR_MAP_INTERLEAVE_NONE,
+                swizzle_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_NONE,
                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
 }
 

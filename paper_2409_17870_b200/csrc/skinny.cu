@@ -615,6 +615,7 @@ __global__ void __launch_bounds__(sk_threads(N, NT), sk_ctas_per_sm(N, NT))
         p.y[o] = static_cast<int32_t>(v);
       }
     }
+    if (p.slices == 1 && ti + 1 == my_tiles) break;  // last tile: red is not reused
     __syncthreads();  // every reader of red is done
     for (uint32_t e = tid; e < elems; e += THREADS) red[e] = 0u;
     if (p.slices > 1 && tid == 0) {

@@ -1,0 +1,593 @@
+// stream_tc.cu -- K6: the WnAm bipolar-INT GEMM for small and mid token counts (8 <= M_tok
+// <= 64): the packed weight planes are streamed from HBM once, expanded to u8 codes in
+// registers and written straight into TENSOR MEMORY, where tcgen05.mma reads them as its A
+// operand (kind::i8, A from TMEM, B from shared memory). No code byte of W touches shared
+// memory or HBM, and the features are read by the tensor core from shared memory instead of
+// being re-loaded into registers for every weight tile (the mma.sync kernel K5 spends most of
+// its shared-memory bandwidth on those feature fragments once M_tok > 8).
+//
+// The algebra is the one of every route (reference kernel.cpp:187-254):
+//   Y = 4 * sum_k u_w u_x - 2B * rowsum(U_w) - 2A * rowsum(U_x) + K*A*B   (mod 2^32).
+// rowsum(U_w) comes out of the MMA: the feature operand carries an all-ones token row (column
+// M_tok of D). Both K-linear terms are formed per K segment, the X term and the constant by the
+// segment that holds K step 0, so K may be split anywhere.
+//
+// Work: the output is cut into tiles of 128 weight rows (the UMMA M) and K into steps of 512
+// columns; the tile-steps (tile-major) are dealt to one persistent CTA per SM as contiguous
+// ranges (stream-K). A CTA's run of steps of one tile accumulates in TMEM; at its end the
+// partial tile is TMA reduce-added (exact wrapping u32 add) into Y, which the feature-prep
+// launch zeroed.
+//
+// CTA: 8 transform warps in two warpgroups + 1 MMA warp. Warpgroup g expands the CTA's steps
+// g, g+2, ... into its own 128-column A buffer: warp q of the group owns TMEM lanes 32q..32q+31
+// = weight rows 32q.. of the tile, one row per thread. Per step a warp streams one TMA box
+// {16 words, 32 rows, n_w planes} through its own ring (64-byte rows, 64-byte swizzle: the
+// per-thread row reads are bank-conflict free), turns each 32-column word into 8 registers of
+// u8 codes (register r, byte b = column 8b + r: the K order of the feature codes, DESIGN.md
+// "Data layout") and stores them with tcgen05.st. The MMA warp streams the feature tile of the
+// step (K1-order u8 codes, 128B swizzle) and issues 16 MMAs of K = 32.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "internal.h"
+#include "ptx.cuh"
+
+namespace apmm_b200 {
+namespace {
+
+using namespace apmm_ptx;
+
+constexpr int kTfWarps = 8;                     // two warpgroups of transform warps
+constexpr int kMmaWarp = kTfWarps;
+constexpr int kThreads = (kTfWarps + 1) * 32;
+constexpr uint32_t kStepWords = 16;             // plane words (512 columns) per step
+constexpr uint32_t kStepBytes = kStepWords * 32;  // feature code bytes per step and token
+constexpr uint32_t kTileRows = 128;
+constexpr uint32_t kBStages = 3;                // feature-code tiles in flight
+constexpr uint32_t kTmemCols = 512;
+constexpr uint32_t kColD = 256;                 // A buffers at columns 0 and 128, D from 256
+constexpr uint32_t kStageBytes = 32u * 128u;    // per-warp epilogue staging: 32 rows x 32 int32
+constexpr uint32_t kSmemCap = 232448u - 2048u;  // opt-in maximum minus static + alignment
+constexpr uint32_t kMaxRowsX = 64;
+constexpr uint32_t kPrepThreads = 256;
+
+__host__ __device__ constexpr uint32_t n_mma_of(uint32_t rows_x) {
+  return rows_x + 1 <= 16 ? 16u : (rows_x + 1 + 15) / 16 * 16;  // + the all-ones token row
+}
+__host__ __device__ constexpr uint32_t wslot_bytes(int n) { return 32u * 64u * static_cast<uint32_t>(n); }
+__host__ __device__ constexpr uint32_t b_stage_bytes(uint32_t n_mma) { return n_mma * kStepBytes; }
+
+struct TcParams {
+  const int32_t* rsx_part;   // feature prep: rowsum(U_x) parts [n_mma][parts]
+  uint32_t parts;
+  uint32_t rows_x, n_mma;
+  uint32_t n_w;
+  uint32_t steps_per_tile;   // K steps per tile
+  uint32_t q_steps, r_steps;  // total tile-steps = q * grid + r (CTA c gets q + (c < r))
+  uint64_t inv_spt;           // ceil(2^32 / steps_per_tile)
+  uint32_t wst;               // per-warp weight ring slots (1 or 2)
+  uint32_t w_off, st_off;     // shared-memory carve-up: B ring at 0, W rings, staging
+  uint32_t coef_w, coef_x, c0;
+  uint32_t early_w;
+};
+
+// floor(n / d) for n, d < 2^16 from inv = ceil(2^32 / d)
+APMM_DEV uint32_t div_small(uint32_t n, uint64_t inv) {
+  return static_cast<uint32_t>((static_cast<uint64_t>(n) * inv) >> 32);
+}
+
+template <uint32_t M>
+APMM_DEV uint32_t sel(uint32_t a, uint32_t b) {
+  uint32_t r;
+  asm("lop3.b32 %0, %1, %2, %3, 0xD8;" : "=r"(r) : "r"(a), "r"(b), "n"(M));
+  return r;
+}
+// delta swap with both shifts on the FMA pipe (IMAD / IMAD.HI), the selects as LOP3
+template <int S>
+APMM_DEV void swap_sel(uint32_t& a, uint32_t& b) {
+  const uint32_t bs = b * (1u << S);
+  const uint32_t as = __umulhi(a, 1u << (32 - S));
+  const uint32_t na = S == 1 ? sel<0xAAAAAAAAu>(a, bs) : S == 2 ? sel<0xCCCCCCCCu>(a, bs)
+                                                               : sel<0xF0F0F0F0u>(a, bs);
+  b = S == 1 ? sel<0x55555555u>(b, as) : S == 2 ? sel<0x33333333u>(b, as) : sel<0x0F0F0F0Fu>(b, as);
+  a = na;
+}
+
+// u8 codes of one 32-column word (x[i] = plane i's word, zero for i >= N): o[r] byte b = code
+// of column 8b + r. N <= 4: two swap stages leave nibble pairs (column 8b+r low, 8b+4+r high).
+template <int N>
+APMM_DEV void codes_of_word(uint32_t (&x)[8], uint32_t* o) {
+  if (N <= 4) {
+    swap_sel<2>(x[0], x[2]);
+    swap_sel<2>(x[1], x[3]);
+    swap_sel<1>(x[0], x[1]);
+    swap_sel<1>(x[2], x[3]);
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      o[r] = x[r] & 0x0F0F0F0Fu;
+      o[4 + r] = __umulhi(x[r], 1u << 28) & 0x0F0F0F0Fu;  // x >> 4 on the FMA pipe
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) swap_sel<4>(x[i], x[i + 4]);
+#pragma unroll
+    for (int i = 0; i < 8; i += 4) {
+      swap_sel<2>(x[i], x[i + 2]);
+      swap_sel<2>(x[i + 1], x[i + 3]);
+    }
+#pragma unroll
+    for (int i = 0; i < 8; i += 2) swap_sel<1>(x[i], x[i + 1]);
+#pragma unroll
+    for (int r = 0; r < 8; ++r) o[r] = x[r];
+  }
+}
+
+APMM_DEV void tma_load_3d(uint32_t dst, const void* tmap, uint32_t bar, int32_t c0, int32_t c1,
+                          int32_t c2, uint64_t hint) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "l"(hint)
+      : "memory");
+}
+APMM_DEV void tma_reduce_add_2d(const void* tmap, const void* smem_src, int32_t c0, int32_t c1) {
+  asm volatile(
+      "cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+          reinterpret_cast<uint64_t>(tmap)),
+      "r"(smem_u32(smem_src)), "r"(c0), "r"(c1)
+      : "memory");
+}
+// D[tmem] (+)= A[tmem] * B[smem]^T (kind::i8, u8 x u8 -> s32)
+APMM_DEV void mma_i8_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
+                        uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+APMM_DEV void tmem_st_32x32b_x32(uint32_t taddr, const uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+      "{%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16, "
+      "%17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+      "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]),
+      "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]),
+      "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]),
+      "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
+}
+APMM_DEV void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+APMM_DEV uint32_t tmem_ld_32x32b_x1(uint32_t taddr) {
+  uint32_t v;
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(v) : "r"(taddr));
+  return v;
+}
+
+template <int N>
+__global__ void __launch_bounds__(kThreads, 1)
+    stream_tc_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_x,
+                     const __grid_constant__ CUtensorMap tm_y, const TcParams p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  __shared__ __align__(8) uint64_t wfull[kTfWarps * 2];
+  __shared__ __align__(8) uint64_t bfull[kBStages], bempty[kBStages];
+  __shared__ __align__(8) uint64_t afull[2], aempty[2], dfull, dempty;
+  __shared__ uint32_t tmem_base_s;
+  __shared__ int32_t rsx_s[kMaxRowsX];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+
+  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // this CTA's tile-steps [a, b)
+  const uint32_t a = blockIdx.x * p.q_steps + min(blockIdx.x, p.r_steps);
+  const uint32_t n_steps = p.q_steps + (blockIdx.x < p.r_steps ? 1u : 0u);
+  const uint32_t b = a + n_steps;
+  const uint32_t spt = p.steps_per_tile;
+
+  if (tid == 0) {
+    for (int i = 0; i < kTfWarps * 2; ++i) mbar_init(&wfull[i], 1);
+    for (uint32_t i = 0; i < kBStages; ++i) {
+      mbar_init(&bfull[i], 1);
+      mbar_init(&bempty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&afull[i], 4);  // one arrive per warp of the group
+      mbar_init(&aempty[i], 1);
+    }
+    mbar_init(&dfull, 1);
+    mbar_init(&dempty, kTfWarps);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (warp == kMmaWarp) tmem_alloc<kTmemCols>(&tmem_base_s);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_base_s;
+  const uint32_t sbase = smem_u32(smem);
+
+  if (warp < kTfWarps) {
+    // ---------------- transform warps ----------------
+    const uint32_t wg = warp >> 2, q = warp & 3;
+    const uint32_t wslot0 = sbase + p.w_off + warp * p.wst * wslot_bytes(N);
+    uint64_t* wbar = wfull + warp * 2;
+    const uint64_t hint = policy_evict_first();  // weights are read exactly once
+    // this warp's items: steps a + wg, a + wg + 2, ...
+    uint32_t is_j = a + wg, is_slot = 0;
+    auto issue = [&]() {
+      if (is_j < b && lane == 0) {
+        const uint32_t tile = div_small(is_j, p.inv_spt), s = is_j - tile * spt;
+        mbar_arrive_expect_tx(&wbar[is_slot], wslot_bytes(N));
+        tma_load_3d(wslot0 + is_slot * wslot_bytes(N), &tm_w, smem_u32(&wbar[is_slot]),
+                    int32_t(s * kStepWords), int32_t(tile * kTileRows + q * 32u), 0, hint);
+      }
+      is_j += 2;
+      if (++is_slot == p.wst) is_slot = 0;
+    };
+    if (!p.early_w) pdl_wait();
+    for (uint32_t i = 0; i < p.wst; ++i) issue();
+    pdl_wait();  // features' rowsum parts and Y only after the previous kernel
+    for (uint32_t c = lane; c < p.rows_x; c += 32) {
+      if (wg == 0 && q == 0) {
+        int32_t sum = 0;
+        for (uint32_t i = 0; i < p.parts; ++i) sum += __ldg(p.rsx_part + c * p.parts + i);
+        rsx_s[c] = sum;
+      }
+    }
+    asm volatile("bar.sync 1, %0;" ::"n"(kTfWarps * 32));  // rsx_s visible to the 8 warps
+    uint8_t* stage = smem + p.st_off + warp * kStageBytes;
+    const uint32_t my_lane_addr = (q * 32u) << 16;
+    uint32_t cs_slot = 0, wphase = 0, uses = 0, segs = 0;
+    uint32_t seg_first_s = 0;  // K step at which the current segment started
+    for (uint32_t j = a; j < b; ++j) {
+      const uint32_t tile = div_small(j, p.inv_spt), s = j - tile * spt;
+      if (j == a || s == 0) seg_first_s = s;
+      if (((j - a) & 1u) == wg) {
+        // the MMAs that read this A buffer two steps ago are done
+        if (uses > 0) mbar_wait(&aempty[wg], (uses - 1) & 1u);
+        tc_fence_after();
+        mbar_wait(&wbar[cs_slot], (wphase >> cs_slot) & 1u);
+        wphase ^= 1u << cs_slot;
+        // the warp's 32 rows x 16 words x N planes, one row per thread (swizzled 16-B chunks)
+        uint4 wv[N][4];
+        const uint32_t rowb = wslot0 + cs_slot * wslot_bytes(N) + lane * 64u;
+        const uint32_t sw = (lane >> 1) & 3u;
+#pragma unroll
+        for (int pl = 0; pl < N; ++pl)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const uint32_t addr = rowb + pl * 2048u + ((c ^ sw) << 4);
+            asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(wv[pl][c].x), "=r"(wv[pl][c].y), "=r"(wv[pl][c].z), "=r"(wv[pl][c].w)
+                         : "r"(addr));
+          }
+        __syncwarp();
+        if (++cs_slot == p.wst) cs_slot = 0;
+        issue();  // the slot is free again: the item after next of this warp
+        const uint32_t acol = tmem + my_lane_addr + wg * 128u;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          uint32_t o[32];
+#pragma unroll
+          for (int wd = 0; wd < 4; ++wd) {
+            uint32_t x[8];
+#pragma unroll
+            for (int pl = 0; pl < 8; ++pl) {
+              const uint4& v = wv[pl < N ? pl : 0][c];
+              x[pl] = pl < N ? (wd == 0 ? v.x : wd == 1 ? v.y : wd == 2 ? v.z : v.w) : 0u;
+            }
+            codes_of_word<N>(x, o + wd * 8);
+          }
+          tmem_st_32x32b_x32(acol + c * 32u, o);
+        }
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&afull[wg]);
+        ++uses;
+      }
+      if (s + 1 == spt || j + 1 == b) {
+        // ---------------- segment end: partial tile -> reduce-add into Y ----------------
+        mbar_wait(&dfull, segs & 1u);
+        tc_fence_after();
+        const uint32_t dcol = tmem + my_lane_addr + kColD;
+        const uint32_t rsw = tmem_ld_32x32b_x1(dcol + p.rows_x);
+        tmem_ld_wait();
+        const bool first = seg_first_s == 0;  // this segment holds K step 0: X term + constant
+        const uint32_t chunks = (p.rows_x + 31) / 32;
+        for (uint32_t cc = wg; cc < chunks; cc += 2) {
+          uint32_t d[32];
+          tmem_ld_32x32b_x32(dcol + cc * 32u, d);
+          tmem_ld_wait();
+          if (lane == 0) bulk_wait_read<0>();  // the staging buffer's previous reduce-add read it
+          __syncwarp();
+#pragma unroll
+          for (int c4 = 0; c4 < 8; ++c4) {
+            uint32_t v[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const uint32_t col = cc * 32u + c4 * 4u + e;
+              uint32_t t = 4u * d[c4 * 4 + e] - p.coef_w * rsw;
+              if (first && col < p.rows_x) t += p.c0 - p.coef_x * static_cast<uint32_t>(rsx_s[col]);
+              v[e] = t;
+            }
+            st_shared_v4(smem_u32(stage) + lane * 128u + ((c4 ^ (lane & 7u)) << 4), v[0], v[1], v[2], v[3]);
+          }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_reduce_add_2d(&tm_y, stage, int32_t(cc * 32u), int32_t(tile * kTileRows + q * 32u));
+            bulk_commit();
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&dempty);
+        ++segs;
+      }
+    }
+    if (lane == 0) bulk_wait<0>();
+  } else {
+    // ---------------- MMA warp: feature tiles + tcgen05.mma ----------------
+    if (lane == 0) {
+      const uint32_t idesc = idesc_i8_u8u8(kTileRows, p.n_mma);
+      const uint64_t hint = policy_evict_last();  // the feature codes are re-read by every CTA
+      auto load_b = [&](uint32_t i) {  // feature codes of step a + i into stage i % kBStages
+        const uint32_t j = a + i;
+        const uint32_t tile = div_small(j, p.inv_spt), s = j - tile * spt;
+        const uint32_t st = i % kBStages;
+        uint8_t* dst = smem + st * b_stage_bytes(p.n_mma);
+        mbar_arrive_expect_tx(&bfull[st], b_stage_bytes(p.n_mma));
+#pragma unroll
+        for (int kg = 0; kg < 4; ++kg)
+          tma_load_2d(dst + kg * p.n_mma * 128u, &tm_x, &bfull[st], int32_t(s * kStepBytes + kg * 128u), 0, hint);
+      };
+      pdl_wait();  // the feature codes are written by the prep launch right before us
+      for (uint32_t i = 0; i < kBStages && i < n_steps; ++i) load_b(i);
+      uint32_t segs = 0;
+      bool seg_open = false;
+      for (uint32_t i = 0; i < n_steps; ++i) {
+        const uint32_t j = a + i, wg = i & 1u;
+        const uint32_t tile = div_small(j, p.inv_spt), s = j - tile * spt;
+        const uint32_t st = i % kBStages;
+        mbar_wait(&bfull[st], (i / kBStages) & 1u);
+        mbar_wait(&afull[wg], (i >> 1) & 1u);
+        if (!seg_open && segs > 0) mbar_wait(&dempty, (segs - 1) & 1u);  // epilogue read D
+        tc_fence_after();
+        const uint32_t bstage = sbase + st * b_stage_bytes(p.n_mma);
+#pragma unroll
+        for (uint32_t k = 0; k < 16; ++k) {
+          const uint64_t bdesc = umma_desc_sw128(bstage + (k >> 2) * p.n_mma * 128u + (k & 3u) * 32u);
+          mma_i8_ts(tmem + kColD, tmem + wg * 128u + k * 8u, bdesc, idesc, (seg_open || k > 0) ? 1u : 0u);
+        }
+        seg_open = true;
+        mma_commit(&aempty[wg]);
+        mma_commit(&bempty[st]);
+        if (s + 1 == spt || j + 1 == b) {
+          mma_commit(&dfull);
+          seg_open = false;
+          ++segs;
+        }
+        // refill the stage of step i - 1 (its MMAs were issued a step ago) with step i + 2
+        if (i >= 1 && i + kBStages - 1 < n_steps) {
+          const uint32_t pst = (i - 1) % kBStages;
+          mbar_wait(&bempty[pst], ((i - 1) / kBStages) & 1u);
+          load_b(i + kBStages - 1);
+        }
+      }
+    }
+    __syncwarp();
+  }
+  pdl_trigger();
+  tc_fence_before();
+  __syncthreads();
+  if (warp == kMmaWarp) {
+    tc_fence_after();
+    tmem_dealloc<kTmemCols>(tmem);
+  }
+}
+
+// Feature prep: X planes -> u8 codes [n_mma][kpad] in the K1 order (rows >= rows_x: the
+// all-ones row at rows_x, zeros after), rowsum(U_x) parts, and Y zeroed for the reduce-adds.
+// thread = (code row, 32-column word). PDL: triggers at once; reads X and writes its outputs
+// only after griddepcontrol.wait (X may be the previous kernel's output, and the previous
+// call's GEMM may still read the codes) unless early_x.
+__global__ void __launch_bounds__(kPrepThreads) stream_tc_prep_kernel(
+    const uint32_t* __restrict__ x, uint32_t rows_x, uint32_t wpr, int n_x, uint32_t kwords,
+    uint8_t* __restrict__ codes, int32_t* __restrict__ rsx_part, uint4* __restrict__ y_zero,
+    uint64_t y_vec4, uint32_t early_x) {
+  pdl_trigger();
+  if (!early_x) pdl_wait();
+  const uint32_t row = blockIdx.y, W = blockIdx.x * kPrepThreads + threadIdx.x;
+  uint32_t v[8];
+  int32_t rs = 0;
+  const bool real = row < rows_x;
+  const uint64_t pstride = uint64_t(rows_x) * wpr;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    v[i] = (real && i < n_x && W < wpr) ? __ldg(x + i * pstride + uint64_t(row) * wpr + W) : 0u;
+    rs += __popc(v[i]) << i;
+  }
+  if (early_x) pdl_wait();
+  if (real) {
+    // 8x8 transpose in all four byte lanes: register r, byte b <- column 8b + r
+    auto sw = [](uint32_t& a, uint32_t& b, int s, uint32_t m) {
+      const uint32_t na = (a & ~(m << s)) | ((b << s) & (m << s));
+      b = (b & ~m) | ((a >> s) & m);
+      a = na;
+    };
+#pragma unroll
+    for (int i = 0; i < 4; ++i) sw(v[i], v[i + 4], 4, 0x0F0F0F0Fu);
+#pragma unroll
+    for (int i = 0; i < 8; i += 4) {
+      sw(v[i], v[i + 2], 2, 0x33333333u);
+      sw(v[i + 1], v[i + 3], 2, 0x33333333u);
+    }
+#pragma unroll
+    for (int i = 0; i < 8; i += 2) sw(v[i], v[i + 1], 1, 0x55555555u);
+  } else {
+    const uint32_t c = row == rows_x ? 0x01010101u : 0u;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = c;
+  }
+  if (W < kwords) {
+    uint4* dst = reinterpret_cast<uint4*>(codes + uint64_t(row) * kwords * 32u + uint64_t(W) * 32u);
+    dst[0] = make_uint4(v[0], v[1], v[2], v[3]);
+    dst[1] = make_uint4(v[4], v[5], v[6], v[7]);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) rs += __shfl_xor_sync(0xffffffffu, rs, o);
+  __shared__ int32_t part[kPrepThreads / 32];
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = rs;
+  __syncthreads();
+  if (threadIdx.x == 0 && real) {
+    int32_t s = 0;
+    for (int i = 0; i < kPrepThreads / 32; ++i) s += part[i];
+    rsx_part[uint64_t(row) * gridDim.x + blockIdx.x] = s;
+  }
+  // zero Y (grid-stride over the whole launch)
+  const uint64_t nthreads = uint64_t(gridDim.x) * gridDim.y * kPrepThreads;
+  const uint64_t gtid = (uint64_t(blockIdx.y) * gridDim.x + blockIdx.x) * kPrepThreads + threadIdx.x;
+  for (uint64_t i = gtid; i < y_vec4; i += nthreads) y_zero[i] = make_uint4(0, 0, 0, 0);
+}
+
+struct Layout {
+  uint32_t n_mma, wst, w_off, st_off, smem;
+};
+Layout layout_of(uint64_t rows_x, int n_w) {
+  Layout l{};
+  l.n_mma = n_mma_of(static_cast<uint32_t>(rows_x));
+  l.w_off = kBStages * b_stage_bytes(l.n_mma);
+  for (uint32_t wst = 2; wst >= 1; --wst) {
+    l.wst = wst;
+    l.st_off = l.w_off + kTfWarps * wst * wslot_bytes(n_w);
+    l.smem = l.st_off + kTfWarps * kStageBytes + 1024u;  // + alignment slack
+    if (l.smem <= kSmemCap) return l;
+  }
+  l.smem = 0;
+  return l;
+}
+uint32_t kwords_of(uint64_t k) { return static_cast<uint32_t>((k + kStepBytes - 1) / kStepBytes * kStepWords); }
+uint32_t prep_blocks_of(uint64_t k) { return (kwords_of(k) + kPrepThreads - 1) / kPrepThreads; }
+
+template <int N>
+cudaError_t launch_n(const CUtensorMap& tw, const CUtensorMap& tx, const CUtensorMap& ty, const TcParams& p,
+                     unsigned grid, uint32_t smem, cudaStream_t s) {
+  auto kern = stream_tc_kernel<N>;
+  static DeviceBits attr_set;
+  const int dev = current_device();
+  if (!attr_set.test(dev)) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(kSmemCap));
+    if (e != cudaSuccess) return e;
+    attr_set.set(dev);
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, tw, tx, ty, p);
+  return e != cudaSuccess ? e : cudaGetLastError();
+}
+
+}  // namespace
+
+bool stream_tc_supported(const uint32_t* w, uint64_t rows_w, uint64_t rows_x, uint64_t k, int n_w,
+                         const void* y) {
+  const uint64_t wpr = (k + 31) / 32;
+  const uint64_t tiles = (rows_w + kTileRows - 1) / kTileRows;
+  const uint64_t steps = (wpr + kStepWords - 1) / kStepWords;
+  return rows_x >= 1 && rows_x <= kMaxRowsX && rows_x % 4 == 0 && n_w <= 4 && wpr % 4 == 0 &&
+         reinterpret_cast<uintptr_t>(w) % 16 == 0 && reinterpret_cast<uintptr_t>(y) % 16 == 0 &&
+         tiles * steps < 65536 && layout_of(rows_x, n_w).smem != 0;
+}
+
+size_t stream_tc_ws_bytes(uint64_t rows_x, uint64_t k) {
+  const uint64_t n_mma = n_mma_of(static_cast<uint32_t>(rows_x));
+  return round_up(n_mma * kwords_of(k) * 32u, 256) + round_up(n_mma * prep_blocks_of(k) * 4u, 256);
+}
+
+cudaError_t launch_stream_tc(const StreamTcArgs& a, cudaStream_t s) {
+  const Layout l = layout_of(a.rows_x, a.n_w);
+  if (!l.smem) return cudaErrorInvalidConfiguration;
+  const uint32_t wpr = static_cast<uint32_t>((a.k + 31) / 32);
+  const uint32_t kwords = kwords_of(a.k);
+  const uint32_t spt = kwords / kStepWords;
+  const uint32_t tiles = static_cast<uint32_t>((a.rows_w + kTileRows - 1) / kTileRows);
+  const uint32_t total = tiles * spt;
+  const uint32_t grid = total < static_cast<uint32_t>(a.num_sms) ? total : static_cast<uint32_t>(a.num_sms);
+  uint8_t* codes = static_cast<uint8_t*>(a.ws);
+  int32_t* rsx_part = reinterpret_cast<int32_t*>(codes + round_up(uint64_t(l.n_mma) * kwords * 32u, 256));
+  const uint32_t parts = prep_blocks_of(a.k);
+
+  // feature prep (+ Y zeroing)
+  {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(parts, l.n_mma);
+    cfg.blockDim = dim3(kPrepThreads);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const uint64_t y_vec4 = a.rows_w * a.rows_x / 4;  // rows_x % 4 == 0
+    cudaError_t e = cudaLaunchKernelEx(&cfg, stream_tc_prep_kernel, a.x_planes,
+                                       static_cast<uint32_t>(a.rows_x), wpr, a.n_x, kwords, codes,
+                                       rsx_part, reinterpret_cast<uint4*>(a.y), y_vec4,
+                                       a.early_x ? 1u : 0u);
+    if (e != cudaSuccess) return e;
+  }
+  CUtensorMap tw, tx, ty;
+  {
+    const uint64_t dims[3] = {wpr, a.rows_w, static_cast<uint64_t>(a.n_w)};
+    const uint64_t strides[2] = {uint64_t(wpr) * 4, uint64_t(wpr) * 4 * a.rows_w};
+    const uint32_t box[3] = {kStepWords, 32u, static_cast<uint32_t>(a.n_w)};
+    if (encode_tmap_3d_u32(&tw, a.w_planes, dims, strides, box, 64) != CUDA_SUCCESS) return cudaErrorInvalidValue;
+  }
+  if (encode_tmap_2d(&tx, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, codes, uint64_t(kwords) * 32u, l.n_mma,
+                     uint64_t(kwords) * 32u, 128u, l.n_mma) != CUDA_SUCCESS) {
+    return cudaErrorInvalidValue;
+  }
+  if (encode_tmap_2d(&ty, CU_TENSOR_MAP_DATA_TYPE_INT32, 4, a.y, a.rows_x, a.rows_w, a.rows_x * 4,
+                     32u, 32u) != CUDA_SUCCESS) {
+    return cudaErrorInvalidValue;
+  }
+  TcParams p{};
+  p.rsx_part = rsx_part;
+  p.parts = parts;
+  p.rows_x = static_cast<uint32_t>(a.rows_x);
+  p.n_mma = l.n_mma;
+  p.n_w = static_cast<uint32_t>(a.n_w);
+  p.steps_per_tile = spt;
+  p.q_steps = total / grid;
+  p.r_steps = total % grid;
+  p.inv_spt = ((uint64_t(1) << 32) + spt - 1) / spt;
+  p.wst = l.wst;
+  p.w_off = l.w_off;
+  p.st_off = l.st_off;
+  const uint32_t A = (1u << a.n_w) - 1u, B = (1u << a.n_x) - 1u;
+  p.coef_w = 2u * B;
+  p.coef_x = 2u * A;
+  p.c0 = static_cast<uint32_t>(a.k) * A * B;
+  p.early_w = a.early_w ? 1u : 0u;
+  if (a.ev_start) cudaEventRecordWithFlags(a.ev_start, s, a.ev_flags);
+  cudaError_t e;
+  switch (a.n_w) {
+    case 1: e = launch_n<1>(tw, tx, ty, p, grid, l.smem, s); break;
+    case 2: e = launch_n<2>(tw, tx, ty, p, grid, l.smem, s); break;
+    case 3: e = launch_n<3>(tw, tx, ty, p, grid, l.smem, s); break;
+    default: e = launch_n<4>(tw, tx, ty, p, grid, l.smem, s); break;
+  }
+  if (a.ev_stop) cudaEventRecordWithFlags(a.ev_stop, s, a.ev_flags);
+  return e;
+}
+
+}  // namespace apmm_b200

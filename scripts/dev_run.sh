@@ -1,3 +1,6 @@
 mkdir -p gpurun_out/abl
 export PYTHONUNBUFFERED=1
-for v in "" _s3 _s4; do echo "== stages lib$v"; APMM_LIB=$PWD/abtest/libapmm_b200_dev$v.so timeout 120 python scripts/decode_bench.py 30 8192x1,8192x8,8192x16,4096x1,11008x1,4096x1x11008,4096x16; done > gpurun_out/abl/decode_stages.txt 2>&1
+timeout 300 python -m pytest tests/test_gpu_parity.py -q -x -k "stream_tensor" > gpurun_out/abl/k6_tests.txt 2>&1
+echo rc=$? >> gpurun_out/abl/k6_tests.txt
+( timeout 200 python scripts/route_sweep.py 8192 8192 3 8 8,16,32,48,64
+  timeout 200 python scripts/route_sweep.py 4096 4096 2 4 8,16,32,64 ) > gpurun_out/abl/route_sweep_k6.txt 2>&1

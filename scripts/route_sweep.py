@@ -18,7 +18,7 @@ torch.cuda.set_stream(s)  # graph replays and the timing events run on s
 wpr = (k + 31) // 32
 ws = [torch.randint(-2**31, 2**31 - 1, (nw * n_out * wpr,), dtype=torch.int32, device=dev)
       for _ in range(max(2, int(300e6 // (4 * nw * n_out * wpr)) + 1))]
-routes = [ap.Route.AUTO, ap.Route.SKINNY, ap.Route.MID_SPLITK, ap.Route.SINGLE_SM,
+routes = [ap.Route.AUTO, ap.Route.SKINNY, ap.Route.STREAM_TC, ap.Route.MID_SPLITK, ap.Route.SINGLE_SM,
           ap.Route.PAIR_SPLITK, ap.Route.PAIR, ap.Route.PAIR_WPLANES]
 print(f"{n_out} x M x {k} W{nw}A{nx}: us per call (graph replay); roofline = max(bytes/6544 GB/s, ops/3219 TOPS)")
 print("     M  roofline " + " ".join(f"{r.name:>12s}" for r in routes))
