@@ -266,6 +266,12 @@ RouteCaps caps_of(const uint32_t* w, uint64_t rows_w, int n_w, uint64_t rows_x, 
 // kSkinnyPreferRows stay on K5 (faster there: 4096x40x4096 8.6 vs 12.6 us,
 // profiles/r01b_skinny_mid_boundary.txt), and K5 takes up to 63 rows when the split-K path
 // cannot (int32 output with a TMA-storable Y only). TENSOR_CORE = the same without K5.
+// K6 (weight planes streamed into TMEM, tcgen05) from 12 feature rows on (when it can serve:
+// int32 output, rows_x % 4 == 0, <= 64 rows, n_w <= 4): 8192^2 W3A8 M = 16 / 32 / 64: 15.3 /
+// 15.0 / 15.9 us vs 16.3 (K5) / 24.9 (K5) / 31.0 (K3f split-K); 4096^2 W2A4 M = 64: 8.8 vs
+// 11.8 us (profiles/r02/r2_route_sweep_k6.txt). K5 stays faster below (M = 8: 12.2 vs 15.3 us).
+constexpr uint64_t kStreamTcMinRows = 12;
+
 int pick_route(const apmm_ctx* ctx, const RouteCaps& c, uint64_t rows_w, uint64_t rows_x,
                Route* out) {
   const uint64_t pair_tiles = ((rows_w + 255) / 256) * ((rows_x + kPairN - 1) / kPairN);
@@ -291,7 +297,9 @@ int pick_route(const apmm_ctx* ctx, const RouteCaps& c, uint64_t rows_w, uint64_
     default: break;
   }
   const bool allow_skinny = ctx->route != APMM_ROUTE_TENSOR_CORE;
-  if (allow_skinny && c.skinny && (rows_x <= kSkinnyPreferRows || !mid)) {
+  if (c.stream_tc && rows_x >= kStreamTcMinRows) {
+    *out = Route::StreamTc;
+  } else if (allow_skinny && c.skinny && (rows_x <= kSkinnyPreferRows || !mid)) {
     *out = Route::Skinny;
   } else if (pair) {
     *out = Route::Pair;
@@ -406,6 +414,8 @@ int run_matmul(apmm_ctx* ctx, const uint32_t* w, uint64_t rows_w, int n_w, const
     s.ws = ctx->tc_ws;
     s.early_w = ctx->early_w;
     s.early_x = ctx->early_w && ctx->early_x;
+    s.trace_prep = trace_slot(ctx, 7);
+    s.trace = trace_slot(ctx, 6);
     {
       TimedLaunch t(ctx, 0, stream, /*record=*/false);
       s.ev_start = t.ev.first;

@@ -209,6 +209,8 @@ struct StreamTcArgs {
   void* ws;                  // stream_tc_ws_bytes(): feature codes + rowsum parts
   bool early_w = true;       // PDL: weight loads may start before the previous kernel completes
   bool early_x = false;      // PDL: the feature prep may read X before it
+  unsigned long long* trace = nullptr;       // dev (APMM_TRACE): K6 per-CTA stamps [grid][8]
+  unsigned long long* trace_prep = nullptr;  // dev (APMM_TRACE): prep per-block stamps
   cudaEvent_t ev_start = nullptr, ev_stop = nullptr;  // measurement: around the GEMM launch
   unsigned ev_flags = 0;
 };
@@ -227,6 +229,6 @@ CUresult encode_tmap_2d(CUtensorMap* map, CUtensorMapDataType dtype, uint32_t el
 // mid and outer dimensions (multiples of 16).
 CUresult encode_tmap_3d_u32(CUtensorMap* map, const void* base, const uint64_t (&dims)[3],
                             const uint64_t (&stride_bytes)[2], const uint32_t (&box)[3],
-                            int swizzle_bytes = 0);  // 0: none, 64: SWIZZLE_64B
+                            int swizzle_bytes = 0);  // 0: none, 32 / 64: SWIZZLE_32B / 64B
 
 }  // namespace apmm_b200

@@ -710,7 +710,9 @@ CUresult encode_tmap_3d_u32(CUtensorMap* map, const void* base, const uint64_t (
   const cuuint32_t es[3] = {1, 1, 1};
   return encode(map, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, const_cast<void*>(base), d, st, b, es,
                 CU_TENSOR_MAP_INTERLEAVE_NONE,
-                swizzle_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                swizzle_bytes == 64   ? CU_TENSOR_MAP_SWIZZLE_64B
+                : swizzle_bytes == 32 ? CU_TENSOR_MAP_SWIZZLE_32B
+                                      : CU_TENSOR_MAP_SWIZZLE_NONE,
                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
 }
 

@@ -30,6 +30,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "internal.h"
 #include "ptx.cuh"
@@ -39,15 +40,20 @@ namespace {
 
 using namespace apmm_ptx;
 
-constexpr int kTfWarps = 8;                     // two warpgroups of transform warps
+constexpr int kGroups = 2;                      // A buffers = steps in flight
+constexpr int kTfWarps = 16;                    // 8 row groups of 16 rows x kGroups steps
 constexpr int kMmaWarp = kTfWarps;
 constexpr int kThreads = (kTfWarps + 1) * 32;
-constexpr uint32_t kStepWords = 16;             // plane words (512 columns) per step
+constexpr uint32_t kStepWords = 16;             // plane words per step (512 columns)
 constexpr uint32_t kStepBytes = kStepWords * 32;  // feature code bytes per step and token
+constexpr uint32_t kAcols = kStepWords * 8;     // TMEM columns of one A buffer (4 codes each)
+constexpr uint32_t kRowBytes = kStepWords * 4;  // bytes of one weight row of one plane per step
+constexpr uint32_t kItemRows = 16;              // weight rows per warp item
+constexpr int kEpiWarps = 8;                    // warps with an epilogue staging buffer
 constexpr uint32_t kTileRows = 128;
 constexpr uint32_t kBStages = 3;                // feature-code tiles in flight
 constexpr uint32_t kTmemCols = 512;
-constexpr uint32_t kColD = 256;                 // A buffers at columns 0 and 128, D from 256
+constexpr uint32_t kColD = kGroups * kAcols;   // A buffers at columns 0, 64, 128, 192; D from 256
 constexpr uint32_t kStageBytes = 32u * 128u;    // per-warp epilogue staging: 32 rows x 32 int32
 constexpr uint32_t kSmemCap = 232448u - 2048u;  // opt-in maximum minus static + alignment
 constexpr uint32_t kMaxRowsX = 64;
@@ -56,7 +62,7 @@ constexpr uint32_t kPrepThreads = 256;
 __host__ __device__ constexpr uint32_t n_mma_of(uint32_t rows_x) {
   return rows_x + 1 <= 16 ? 16u : (rows_x + 1 + 15) / 16 * 16;  // + the all-ones token row
 }
-__host__ __device__ constexpr uint32_t wslot_bytes(int n) { return 32u * 64u * static_cast<uint32_t>(n); }
+__host__ __device__ constexpr uint32_t wslot_bytes(int n) { return kItemRows * kRowBytes * static_cast<uint32_t>(n); }
 __host__ __device__ constexpr uint32_t b_stage_bytes(uint32_t n_mma) { return n_mma * kStepBytes; }
 
 struct TcParams {
@@ -71,7 +77,26 @@ struct TcParams {
   uint32_t w_off, st_off;     // shared-memory carve-up: B ring at 0, W rings, staging
   uint32_t coef_w, coef_x, c0;
   uint32_t early_w;
+  unsigned long long* ts;     // dev builds: per-CTA globaltimer stamps [grid][8], else null
+  uint32_t ts_mode;           // dev: 0 phases, 1 MMA warp: step i ready (slot i + 1), 2 warp 0:
+                              // its item u landed (slot u + 1), 3 warp 0: item u stored
 };
+
+#ifdef APMM_DEVTOOLS
+APMM_DEV unsigned long long gtime_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define TC_STAMP(ts, slot, k) \
+  do {                        \
+    if (ts) (ts)[(slot) * 8 + (k)] = gtime_ns(); \
+  } while (0)
+#else
+#define TC_STAMP(ts, slot, k) \
+  do {                        \
+  } while (0)
+#endif
 
 // floor(n / d) for n, d < 2^16 from inv = ceil(2^32 / d)
 APMM_DEV uint32_t div_small(uint32_t n, uint64_t inv) {
@@ -148,9 +173,9 @@ APMM_DEV void mma_i8_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32
       "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
       "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
-APMM_DEV void tmem_st_32x32b_x32(uint32_t taddr, const uint32_t (&r)[32]) {
+APMM_DEV void tmem_st_16x256b_x8(uint32_t taddr, const uint32_t (&r)[32]) {
   asm volatile(
-      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+      "tcgen05.st.sync.aligned.16x256b.x8.b32 [%0], "
       "{%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16, "
       "%17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32};" ::"r"(taddr),
       "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
@@ -174,12 +199,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t wfull[kTfWarps * 2];
   __shared__ __align__(8) uint64_t bfull[kBStages], bempty[kBStages];
-  __shared__ __align__(8) uint64_t afull[2], aempty[2], dfull, dempty;
+  __shared__ __align__(8) uint64_t afull[kGroups], aempty[kGroups], dfull, dempty;
   __shared__ uint32_t tmem_base_s;
   __shared__ int32_t rsx_s[kMaxRowsX];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
 
   const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) TC_STAMP(p.ts, blockIdx.x, 0);
   // this CTA's tile-steps [a, b)
   const uint32_t a = blockIdx.x * p.q_steps + min(blockIdx.x, p.r_steps);
   const uint32_t n_steps = p.q_steps + (blockIdx.x < p.r_steps ? 1u : 0u);
@@ -192,8 +218,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&bfull[i], 1);
       mbar_init(&bempty[i], 1);
     }
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&afull[i], 4);  // one arrive per warp of the group
+    for (int i = 0; i < kGroups; ++i) {
+      mbar_init(&afull[i], kTfWarps / kGroups);  // one arrive per warp filling the buffer
       mbar_init(&aempty[i], 1);
     }
     mbar_init(&dfull, 1);
@@ -209,94 +235,122 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp < kTfWarps) {
     // ---------------- transform warps ----------------
-    const uint32_t wg = warp >> 2, q = warp & 3;
+    // warp (q = warp % 4, h = warp / 4): TMEM lane quarter q, row group rg = 2q + (h & 1) of the
+    // tile (16 rows = lanes 16 rg ..), A buffer wg = h / 2 (the CTA's steps of that parity)
+    const uint32_t q = warp & 3, h = warp >> 2;
+    const uint32_t rg = 2u * q + (h & 1u), wg = h >> 1;
+    const uint32_t g = lane >> 2, t = lane & 3;
     const uint32_t wslot0 = sbase + p.w_off + warp * p.wst * wslot_bytes(N);
     uint64_t* wbar = wfull + warp * 2;
     const uint64_t hint = policy_evict_first();  // weights are read exactly once
-    // this warp's items: steps a + wg, a + wg + 2, ...
+    // this warp's items: steps a + wg, a + wg + kGroups, ...
     uint32_t is_j = a + wg, is_slot = 0;
     auto issue = [&]() {
       if (is_j < b && lane == 0) {
         const uint32_t tile = div_small(is_j, p.inv_spt), s = is_j - tile * spt;
         mbar_arrive_expect_tx(&wbar[is_slot], wslot_bytes(N));
         tma_load_3d(wslot0 + is_slot * wslot_bytes(N), &tm_w, smem_u32(&wbar[is_slot]),
-                    int32_t(s * kStepWords), int32_t(tile * kTileRows + q * 32u), 0, hint);
+                    int32_t(s * kStepWords), int32_t(tile * kTileRows + rg * kItemRows), 0, hint);
       }
-      is_j += 2;
+      is_j += kGroups;
       if (++is_slot == p.wst) is_slot = 0;
     };
     if (!p.early_w) pdl_wait();
     for (uint32_t i = 0; i < p.wst; ++i) issue();
     pdl_wait();  // features' rowsum parts and Y only after the previous kernel
+    if (tid == 0 && p.ts_mode == 0) TC_STAMP(p.ts, blockIdx.x, 1);
     for (uint32_t c = lane; c < p.rows_x; c += 32) {
-      if (wg == 0 && q == 0) {
+      if (warp == 0) {
         int32_t sum = 0;
         for (uint32_t i = 0; i < p.parts; ++i) sum += __ldg(p.rsx_part + c * p.parts + i);
         rsx_s[c] = sum;
       }
     }
-    asm volatile("bar.sync 1, %0;" ::"n"(kTfWarps * 32));  // rsx_s visible to the 8 warps
-    uint8_t* stage = smem + p.st_off + warp * kStageBytes;
-    const uint32_t my_lane_addr = (q * 32u) << 16;
+    asm volatile("bar.sync 1, %0;" ::"n"(kTfWarps * 32));  // rsx_s visible to the transform warps
+    uint8_t* stage = smem + p.st_off + (warp % kEpiWarps) * kStageBytes;
+    const uint32_t my_lane_addr = (q * 32u) << 16;          // epilogue: 32x32b over the quarter
+    const uint32_t st_lane_addr = (rg * kItemRows) << 16;   // transform: 16x256b, 16 lanes
     uint32_t cs_slot = 0, wphase = 0, uses = 0, segs = 0;
     uint32_t seg_first_s = 0;  // K step at which the current segment started
     for (uint32_t j = a; j < b; ++j) {
       const uint32_t tile = div_small(j, p.inv_spt), s = j - tile * spt;
       if (j == a || s == 0) seg_first_s = s;
-      if (((j - a) & 1u) == wg) {
-        // the MMAs that read this A buffer two steps ago are done
+      if (((j - a) & (kGroups - 1u)) == wg) {
+        // the MMAs that read this A buffer kGroups steps ago are done
         if (uses > 0) mbar_wait(&aempty[wg], (uses - 1) & 1u);
         tc_fence_after();
         mbar_wait(&wbar[cs_slot], (wphase >> cs_slot) & 1u);
         wphase ^= 1u << cs_slot;
-        // the warp's 32 rows x 16 words x N planes, one row per thread (swizzled 16-B chunks)
-        uint4 wv[N][4];
-        const uint32_t rowb = wslot0 + cs_slot * wslot_bytes(N) + lane * 64u;
-        const uint32_t sw = (lane >> 1) & 3u;
+        if (tid == 0 && uses == 0 && p.ts_mode == 0) TC_STAMP(p.ts, blockIdx.x, 2);
+        if (tid == 0 && uses < 6 && p.ts_mode == 2) TC_STAMP(p.ts, blockIdx.x, uses + 1);
+        // slot layout (TMA box {16 words, 16 rows, planes}): [plane][row][16 words]; thread
+        // (g, t) takes words 4t..4t+3 of rows g and g + 8 (conflict-free 16-byte reads)
+        uint4 wa[N], wb[N];
+        const uint32_t rowb = wslot0 + cs_slot * wslot_bytes(N) + g * kRowBytes + t * 16u;
 #pragma unroll
-        for (int pl = 0; pl < N; ++pl)
-#pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            const uint32_t addr = rowb + pl * 2048u + ((c ^ sw) << 4);
-            asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
-                         : "=r"(wv[pl][c].x), "=r"(wv[pl][c].y), "=r"(wv[pl][c].z), "=r"(wv[pl][c].w)
-                         : "r"(addr));
-          }
+        for (int pl = 0; pl < N; ++pl) {
+          const uint32_t addr = rowb + pl * kItemRows * kRowBytes;
+          asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                       : "=r"(wa[pl].x), "=r"(wa[pl].y), "=r"(wa[pl].z), "=r"(wa[pl].w) : "r"(addr));
+          asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                       : "=r"(wb[pl].x), "=r"(wb[pl].y), "=r"(wb[pl].z), "=r"(wb[pl].w)
+                       : "r"(addr + 8u * kRowBytes));
+        }
         __syncwarp();
         if (++cs_slot == p.wst) cs_slot = 0;
         issue();  // the slot is free again: the item after next of this warp
-        const uint32_t acol = tmem + my_lane_addr + wg * 128u;
+        // tcgen05.st.16x256b: register 4jj + e of thread (g, t) -> lane g + 8 (e >> 1), column
+        // 8jj + 2t + (e & 1) (profiles/r02/r2_tmem_layout.txt). Word 4t + w of the step, code
+        // register r -> column 32 w + 8 (r >> 1) + 2t + (r & 1): the feature prep writes X in the
+        // same permuted K order (stream_tc_prep_kernel).
+        const uint32_t acol = tmem + st_lane_addr + wg * kAcols;
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          uint32_t o[32];
+        for (int half = 0; half < 2; ++half) {
+          uint32_t oa[2][8], ob[2][8];
 #pragma unroll
-          for (int wd = 0; wd < 4; ++wd) {
-            uint32_t x[8];
+          for (int w2 = 0; w2 < 2; ++w2) {
+            const int wd = half * 2 + w2;
+            uint32_t xa[8], xb[8];
 #pragma unroll
             for (int pl = 0; pl < 8; ++pl) {
-              const uint4& v = wv[pl < N ? pl : 0][c];
-              x[pl] = pl < N ? (wd == 0 ? v.x : wd == 1 ? v.y : wd == 2 ? v.z : v.w) : 0u;
+              const uint4& va = wa[pl < N ? pl : 0];
+              const uint4& vb = wb[pl < N ? pl : 0];
+              xa[pl] = pl < N ? (wd == 0 ? va.x : wd == 1 ? va.y : wd == 2 ? va.z : va.w) : 0u;
+              xb[pl] = pl < N ? (wd == 0 ? vb.x : wd == 1 ? vb.y : wd == 2 ? vb.z : vb.w) : 0u;
             }
-            codes_of_word<N>(x, o + wd * 8);
+            codes_of_word<N>(xa, oa[w2]);
+            codes_of_word<N>(xb, ob[w2]);
           }
-          tmem_st_32x32b_x32(acol + c * 32u, o);
+          uint32_t o[32];
+#pragma unroll
+          for (int jj = 0; jj < 8; ++jj) {
+            const int w2 = jj >> 2, r0 = 2 * (jj & 3);
+            o[4 * jj + 0] = oa[w2][r0];
+            o[4 * jj + 1] = oa[w2][r0 + 1];
+            o[4 * jj + 2] = ob[w2][r0];
+            o[4 * jj + 3] = ob[w2][r0 + 1];
+          }
+          tmem_st_16x256b_x8(acol + half * 64u, o);
         }
         tmem_st_wait();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&afull[wg]);
+        if (tid == 0 && uses == 0 && p.ts_mode == 0) TC_STAMP(p.ts, blockIdx.x, 3);
+        if (tid == 0 && uses < 6 && p.ts_mode == 3) TC_STAMP(p.ts, blockIdx.x, uses + 1);
         ++uses;
       }
       if (s + 1 == spt || j + 1 == b) {
         // ---------------- segment end: partial tile -> reduce-add into Y ----------------
         mbar_wait(&dfull, segs & 1u);
         tc_fence_after();
+        if (tid == 0 && segs == 0 && p.ts_mode == 0) TC_STAMP(p.ts, blockIdx.x, 6);
         const uint32_t dcol = tmem + my_lane_addr + kColD;
         const uint32_t rsw = tmem_ld_32x32b_x1(dcol + p.rows_x);
         tmem_ld_wait();
         const bool first = seg_first_s == 0;  // this segment holds K step 0: X term + constant
         const uint32_t chunks = (p.rows_x + 31) / 32;
-        for (uint32_t cc = wg; cc < chunks; cc += 2) {
+        for (uint32_t cc = h; cc < chunks && warp < kEpiWarps; cc += 2) {
           uint32_t d[32];
           tmem_ld_32x32b_x32(dcol + cc * 32u, d);
           tmem_ld_wait();
@@ -340,7 +394,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint8_t* dst = smem + st * b_stage_bytes(p.n_mma);
         mbar_arrive_expect_tx(&bfull[st], b_stage_bytes(p.n_mma));
 #pragma unroll
-        for (int kg = 0; kg < 4; ++kg)
+        for (int kg = 0; kg < int(kStepBytes / 128); ++kg)
           tma_load_2d(dst + kg * p.n_mma * 128u, &tm_x, &bfull[st], int32_t(s * kStepBytes + kg * 128u), 0, hint);
       };
       pdl_wait();  // the feature codes are written by the prep launch right before us
@@ -348,20 +402,23 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t segs = 0;
       bool seg_open = false;
       for (uint32_t i = 0; i < n_steps; ++i) {
-        const uint32_t j = a + i, wg = i & 1u;
+        const uint32_t j = a + i, wg = i & (kGroups - 1u);
         const uint32_t tile = div_small(j, p.inv_spt), s = j - tile * spt;
         const uint32_t st = i % kBStages;
         mbar_wait(&bfull[st], (i / kBStages) & 1u);
-        mbar_wait(&afull[wg], (i >> 1) & 1u);
+        mbar_wait(&afull[wg], (i / kGroups) & 1u);
         if (!seg_open && segs > 0) mbar_wait(&dempty, (segs - 1) & 1u);  // epilogue read D
         tc_fence_after();
         const uint32_t bstage = sbase + st * b_stage_bytes(p.n_mma);
 #pragma unroll
-        for (uint32_t k = 0; k < 16; ++k) {
+        for (uint32_t k = 0; k < kStepBytes / 32; ++k) {
           const uint64_t bdesc = umma_desc_sw128(bstage + (k >> 2) * p.n_mma * 128u + (k & 3u) * 32u);
-          mma_i8_ts(tmem + kColD, tmem + wg * 128u + k * 8u, bdesc, idesc, (seg_open || k > 0) ? 1u : 0u);
+          mma_i8_ts(tmem + kColD, tmem + wg * kAcols + k * 8u, bdesc, idesc, (seg_open || k > 0) ? 1u : 0u);
         }
         seg_open = true;
+        if (i == 0 && p.ts_mode == 0) TC_STAMP(p.ts, blockIdx.x, 4);
+        if (i + 1 == n_steps && p.ts_mode == 0) TC_STAMP(p.ts, blockIdx.x, 5);
+        if (i < 6 && p.ts_mode == 1) TC_STAMP(p.ts, blockIdx.x, i + 1);
         mma_commit(&aempty[wg]);
         mma_commit(&bempty[st]);
         if (s + 1 == spt || j + 1 == b) {
@@ -382,6 +439,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   pdl_trigger();
   tc_fence_before();
   __syncthreads();
+  if (tid == 0) TC_STAMP(p.ts, blockIdx.x, 7);
   if (warp == kMmaWarp) {
     tc_fence_after();
     tmem_dealloc<kTmemCols>(tmem);
@@ -396,9 +454,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 __global__ void __launch_bounds__(kPrepThreads) stream_tc_prep_kernel(
     const uint32_t* __restrict__ x, uint32_t rows_x, uint32_t wpr, int n_x, uint32_t kwords,
     uint8_t* __restrict__ codes, int32_t* __restrict__ rsx_part, uint4* __restrict__ y_zero,
-    uint64_t y_vec4, uint32_t early_x) {
+    uint64_t y_vec4, uint32_t early_x, unsigned long long* ts) {
+  const uint32_t bslot = blockIdx.y * gridDim.x + blockIdx.x;
+  if (threadIdx.x == 0 && bslot < 1024) TC_STAMP(ts, bslot, 0);
   pdl_trigger();
   if (!early_x) pdl_wait();
+  if (threadIdx.x == 0 && bslot < 1024) TC_STAMP(ts, bslot, 1);
   const uint32_t row = blockIdx.y, W = blockIdx.x * kPrepThreads + threadIdx.x;
   uint32_t v[8];
   int32_t rs = 0;
@@ -432,9 +493,15 @@ __global__ void __launch_bounds__(kPrepThreads) stream_tc_prep_kernel(
     for (int i = 0; i < 8; ++i) v[i] = c;
   }
   if (W < kwords) {
-    uint4* dst = reinterpret_cast<uint4*>(codes + uint64_t(row) * kwords * 32u + uint64_t(W) * 32u);
-    dst[0] = make_uint4(v[0], v[1], v[2], v[3]);
-    dst[1] = make_uint4(v[4], v[5], v[6], v[7]);
+    // K order of the A operand (see the transform warps): within a 512-column step, word
+    // 4t + w, code register r -> 32-bit column 32 w + 8 (r >> 1) + 2t + (r & 1)
+    const uint32_t wl = W % kStepWords, t = wl >> 2, w = wl & 3u;
+    uint32_t* dst = reinterpret_cast<uint32_t*>(codes + uint64_t(row) * kwords * 32u +
+                                                uint64_t(W / kStepWords) * kStepBytes) +
+                    32u * w + 2u * t;
+#pragma unroll
+    for (int r = 0; r < 8; r += 2)
+      *reinterpret_cast<uint2*>(dst + 8 * (r >> 1)) = make_uint2(v[r], v[r + 1]);
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) rs += __shfl_xor_sync(0xffffffffu, rs, o);
@@ -450,6 +517,7 @@ __global__ void __launch_bounds__(kPrepThreads) stream_tc_prep_kernel(
   const uint64_t nthreads = uint64_t(gridDim.x) * gridDim.y * kPrepThreads;
   const uint64_t gtid = (uint64_t(blockIdx.y) * gridDim.x + blockIdx.x) * kPrepThreads + threadIdx.x;
   for (uint64_t i = gtid; i < y_vec4; i += nthreads) y_zero[i] = make_uint4(0, 0, 0, 0);
+  if (threadIdx.x == 0 && bslot < 1024) TC_STAMP(ts, bslot, 2);
 }
 
 struct Layout {
@@ -462,7 +530,7 @@ Layout layout_of(uint64_t rows_x, int n_w) {
   for (uint32_t wst = 2; wst >= 1; --wst) {
     l.wst = wst;
     l.st_off = l.w_off + kTfWarps * wst * wslot_bytes(n_w);
-    l.smem = l.st_off + kTfWarps * kStageBytes + 1024u;  // + alignment slack
+    l.smem = l.st_off + kEpiWarps * kStageBytes + 1024u;  // + alignment slack
     if (l.smem <= kSmemCap) return l;
   }
   l.smem = 0;
@@ -542,15 +610,17 @@ cudaError_t launch_stream_tc(const StreamTcArgs& a, cudaStream_t s) {
     cudaError_t e = cudaLaunchKernelEx(&cfg, stream_tc_prep_kernel, a.x_planes,
                                        static_cast<uint32_t>(a.rows_x), wpr, a.n_x, kwords, codes,
                                        rsx_part, reinterpret_cast<uint4*>(a.y), y_vec4,
-                                       a.early_x ? 1u : 0u);
+                                       a.early_x ? 1u : 0u, a.trace_prep);
     if (e != cudaSuccess) return e;
   }
   CUtensorMap tw, tx, ty;
   {
     const uint64_t dims[3] = {wpr, a.rows_w, static_cast<uint64_t>(a.n_w)};
     const uint64_t strides[2] = {uint64_t(wpr) * 4, uint64_t(wpr) * 4 * a.rows_w};
-    const uint32_t box[3] = {kStepWords, 32u, static_cast<uint32_t>(a.n_w)};
-    if (encode_tmap_3d_u32(&tw, a.w_planes, dims, strides, box, 64) != CUDA_SUCCESS) return cudaErrorInvalidValue;
+    const uint32_t box[3] = {kStepWords, kItemRows, static_cast<uint32_t>(a.n_w)};
+    if (encode_tmap_3d_u32(&tw, a.w_planes, dims, strides, box) != CUDA_SUCCESS) {
+      return cudaErrorInvalidValue;
+    }
   }
   if (encode_tmap_2d(&tx, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, codes, uint64_t(kwords) * 32u, l.n_mma,
                      uint64_t(kwords) * 32u, 128u, l.n_mma) != CUDA_SUCCESS) {
@@ -578,6 +648,12 @@ cudaError_t launch_stream_tc(const StreamTcArgs& a, cudaStream_t s) {
   p.coef_x = 2u * A;
   p.c0 = static_cast<uint32_t>(a.k) * A * B;
   p.early_w = a.early_w ? 1u : 0u;
+  p.ts = a.trace;
+  static const uint32_t ts_mode = [] {
+    const char* e = APMM_DEV_ENV("APMM_TC_TS_MODE");
+    return e ? static_cast<uint32_t>(std::atoi(e)) : 0u;
+  }();
+  p.ts_mode = ts_mode;
   if (a.ev_start) cudaEventRecordWithFlags(a.ev_start, s, a.ev_flags);
   cudaError_t e;
   switch (a.n_w) {

@@ -19,6 +19,8 @@ slots = int(os.environ.get("APMM_TRACE", "0"))
 assert slots >= 2 * calls, "run with APMM_TRACE >= 2 x calls and the dev library"
 dev = torch.device("cuda", 0)
 ctx = ap.Context(0)
+if os.environ.get("ROUTE"):  # e.g. ROUTE=STREAM_TC
+    ctx.set_route(ap.Route[os.environ["ROUTE"]])
 lib = ctx.lib
 fn = lib.apmm_dev_trace_read
 fn.restype, fn.argtypes = C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]
@@ -52,7 +54,9 @@ names = {1: ("expand", ["start", "w_done", "waited", "end"]),
          2: ("pair", ["start", "pdl_wait", "first_full", "last_issue", "end"]),
          3: ("wplanes", ["start", "pdl_wait", "first_full", "last_issue", "end", "epi_done",
                          "acc_ready", "chunks_out"]),
-         5: ("skinny", ["start", "pdl_wait", "x_ready", "item0", "tile0", "end", "inited", "issued"])}
+         5: ("skinny", ["start", "pdl_wait", "x_ready", "item0", "tile0", "end", "inited", "issued"]),
+         6: ("stream_tc", ["start", "pdl_wait", "w0_in", "a0_st", "mma0", "mma_last", "epi0", "end"]),
+         7: ("tc_prep", ["start", "pdl_wait", "end"])}
 t0 = min(t[i][t[i] > 0].min() for i in range(slots) if (t[i] > 0).any())
 print(f"{n_out}x{m}x{k} W{nw}A{nx}: {calls} calls, {1e3 * e0.elapsed_time(e1) / calls:.2f} us/call (graph)")
 for i in range(slots):
