@@ -40,8 +40,13 @@ namespace {
 
 using namespace apmm_ptx;
 
-constexpr int kGroups = 2;                      // A buffers = steps in flight
-constexpr int kTfWarps = 16;                    // 8 row groups of 16 rows x kGroups steps
+constexpr int kGroups = 2;                      // warp sets: the CTA's even / odd steps
+#ifndef APMM_TC_BUFS_AB
+constexpr int kBufs = 2;                        // A buffers in TMEM (step i -> buffer i % kBufs)
+#else
+constexpr int kBufs = APMM_TC_BUFS_AB;          // A/B builds only
+#endif
+constexpr int kTfWarps = 16;                    // 8 row groups of 16 rows x kGroups sets
 constexpr int kMmaWarp = kTfWarps;
 constexpr int kThreads = (kTfWarps + 1) * 32;
 constexpr uint32_t kStepWords = 16;             // plane words per step (512 columns)
@@ -50,10 +55,20 @@ constexpr uint32_t kAcols = kStepWords * 8;     // TMEM columns of one A buffer 
 constexpr uint32_t kRowBytes = kStepWords * 4;  // bytes of one weight row of one plane per step
 constexpr uint32_t kItemRows = 16;              // weight rows per warp item
 constexpr int kEpiWarps = 8;                    // warps with an epilogue staging buffer
+// Weight ring slots per warp. Deeper rings measured slower (8192 x 16 x 8192 W3A8: 15.2 /
+// 15.8 / 18.6 / 18.6 us at 1 / 2 / 3 / 4 slots, profiles/r02/r2_k6_wst.txt; 8192 x 32: 15.9 vs
+// 18.3 us at 1 vs 2, r2_k6_ab.txt): the item is copied to registers at once, so one slot
+// already overlaps the next item's load with this one's transform.
+constexpr uint32_t kMaxWst = 1;
+#ifdef APMM_DEVTOOLS
+constexpr bool kDevAblate = true;
+#else
+constexpr bool kDevAblate = false;
+#endif
 constexpr uint32_t kTileRows = 128;
 constexpr uint32_t kBStages = 3;                // feature-code tiles in flight
 constexpr uint32_t kTmemCols = 512;
-constexpr uint32_t kColD = kGroups * kAcols;   // A buffers at columns 0, 64, 128, 192; D from 256
+constexpr uint32_t kColD = kBufs * kAcols;     // A buffers at columns 0 and 128; D from 256
 constexpr uint32_t kStageBytes = 32u * 128u;    // per-warp epilogue staging: 32 rows x 32 int32
 constexpr uint32_t kSmemCap = 232448u - 2048u;  // opt-in maximum minus static + alignment
 constexpr uint32_t kMaxRowsX = 64;
@@ -73,13 +88,14 @@ struct TcParams {
   uint32_t steps_per_tile;   // K steps per tile
   uint32_t q_steps, r_steps;  // total tile-steps = q * grid + r (CTA c gets q + (c < r))
   uint64_t inv_spt;           // ceil(2^32 / steps_per_tile)
-  uint32_t wst;               // per-warp weight ring slots (1 or 2)
+  uint32_t wst;               // per-warp weight ring slots (1..kMaxWst)
   uint32_t w_off, st_off;     // shared-memory carve-up: B ring at 0, W rings, staging
   uint32_t coef_w, coef_x, c0;
   uint32_t early_w;
   unsigned long long* ts;     // dev builds: per-CTA globaltimer stamps [grid][8], else null
   uint32_t ts_mode;           // dev: 0 phases, 1 MMA warp: step i ready (slot i + 1), 2 warp 0:
                               // its item u landed (slot u + 1), 3 warp 0: item u stored
+  uint32_t ablate;            // dev only (APMM_TC_ABLATE, results wrong): 1 no MMAs, 2 no transposes
 };
 
 #ifdef APMM_DEVTOOLS
@@ -197,9 +213,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     stream_tc_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_x,
                      const __grid_constant__ CUtensorMap tm_y, const TcParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  __shared__ __align__(8) uint64_t wfull[kTfWarps * 2];
+  __shared__ __align__(8) uint64_t wfull[kTfWarps * kMaxWst];
   __shared__ __align__(8) uint64_t bfull[kBStages], bempty[kBStages];
-  __shared__ __align__(8) uint64_t afull[kGroups], aempty[kGroups], dfull, dempty;
+  __shared__ __align__(8) uint64_t afull[kBufs], aempty[kBufs], dfull, dempty;
   __shared__ uint32_t tmem_base_s;
   __shared__ int32_t rsx_s[kMaxRowsX];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -213,12 +229,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t spt = p.steps_per_tile;
 
   if (tid == 0) {
-    for (int i = 0; i < kTfWarps * 2; ++i) mbar_init(&wfull[i], 1);
+    for (int i = 0; i < kTfWarps * kMaxWst; ++i) mbar_init(&wfull[i], 1);
     for (uint32_t i = 0; i < kBStages; ++i) {
       mbar_init(&bfull[i], 1);
       mbar_init(&bempty[i], 1);
     }
-    for (int i = 0; i < kGroups; ++i) {
+    for (int i = 0; i < kBufs; ++i) {
       mbar_init(&afull[i], kTfWarps / kGroups);  // one arrive per warp filling the buffer
       mbar_init(&aempty[i], 1);
     }
@@ -241,7 +257,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t rg = 2u * q + (h & 1u), wg = h >> 1;
     const uint32_t g = lane >> 2, t = lane & 3;
     const uint32_t wslot0 = sbase + p.w_off + warp * p.wst * wslot_bytes(N);
-    uint64_t* wbar = wfull + warp * 2;
+    uint64_t* wbar = wfull + warp * kMaxWst;
     const uint64_t hint = policy_evict_first();  // weights are read exactly once
     // this warp's items: steps a + wg, a + wg + kGroups, ...
     uint32_t is_j = a + wg, is_slot = 0;
@@ -271,13 +287,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t my_lane_addr = (q * 32u) << 16;          // epilogue: 32x32b over the quarter
     const uint32_t st_lane_addr = (rg * kItemRows) << 16;   // transform: 16x256b, 16 lanes
     uint32_t cs_slot = 0, wphase = 0, uses = 0, segs = 0;
+    uint32_t bi = 0, ui = 0;  // step j - a = 3 ui + bi: A buffer bi, its use ui
     uint32_t seg_first_s = 0;  // K step at which the current segment started
     for (uint32_t j = a; j < b; ++j) {
       const uint32_t tile = div_small(j, p.inv_spt), s = j - tile * spt;
       if (j == a || s == 0) seg_first_s = s;
       if (((j - a) & (kGroups - 1u)) == wg) {
-        // the MMAs that read this A buffer kGroups steps ago are done
-        if (uses > 0) mbar_wait(&aempty[wg], (uses - 1) & 1u);
+        // the MMAs that read this A buffer three steps ago (the other warp set's) are done
+        if (ui > 0) mbar_wait(&aempty[bi], (ui - 1) & 1u);
+        if (tid == 0 && uses == 1 && p.ts_mode == 4) TC_STAMP(p.ts, blockIdx.x, 6);
         tc_fence_after();
         mbar_wait(&wbar[cs_slot], (wphase >> cs_slot) & 1u);
         wphase ^= 1u << cs_slot;
@@ -303,7 +321,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // 8jj + 2t + (e & 1) (profiles/r02/r2_tmem_layout.txt). Word 4t + w of the step, code
         // register r -> column 32 w + 8 (r >> 1) + 2t + (r & 1): the feature prep writes X in the
         // same permuted K order (stream_tc_prep_kernel).
-        const uint32_t acol = tmem + st_lane_addr + wg * kAcols;
+        const uint32_t acol = tmem + st_lane_addr + bi * kAcols;
 #pragma unroll
         for (int half = 0; half < 2; ++half) {
           uint32_t oa[2][8], ob[2][8];
@@ -318,8 +336,16 @@ __global__ void __launch_bounds__(kThreads, 1)
               xa[pl] = pl < N ? (wd == 0 ? va.x : wd == 1 ? va.y : wd == 2 ? va.z : va.w) : 0u;
               xb[pl] = pl < N ? (wd == 0 ? vb.x : wd == 1 ? vb.y : wd == 2 ? vb.z : vb.w) : 0u;
             }
-            codes_of_word<N>(xa, oa[w2]);
-            codes_of_word<N>(xb, ob[w2]);
+            if (kDevAblate && (p.ablate & 2u)) {
+#pragma unroll
+              for (int r = 0; r < 8; ++r) {
+                oa[w2][r] = xa[r & (N - 1)];
+                ob[w2][r] = xb[r & (N - 1)];
+              }
+            } else {
+              codes_of_word<N>(xa, oa[w2]);
+              codes_of_word<N>(xb, ob[w2]);
+            }
           }
           uint32_t o[32];
 #pragma unroll
@@ -335,10 +361,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         tmem_st_wait();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&afull[wg]);
+        if (lane == 0) mbar_arrive(&afull[bi]);
         if (tid == 0 && uses == 0 && p.ts_mode == 0) TC_STAMP(p.ts, blockIdx.x, 3);
         if (tid == 0 && uses < 6 && p.ts_mode == 3) TC_STAMP(p.ts, blockIdx.x, uses + 1);
         ++uses;
+      }
+      if (++bi == kBufs) {
+        bi = 0;
+        ++ui;
       }
       if (s + 1 == spt || j + 1 == b) {
         // ---------------- segment end: partial tile -> reduce-add into Y ----------------
@@ -402,24 +432,26 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t segs = 0;
       bool seg_open = false;
       for (uint32_t i = 0; i < n_steps; ++i) {
-        const uint32_t j = a + i, wg = i & (kGroups - 1u);
+        const uint32_t j = a + i, ab = i % kBufs;
         const uint32_t tile = div_small(j, p.inv_spt), s = j - tile * spt;
         const uint32_t st = i % kBStages;
         mbar_wait(&bfull[st], (i / kBStages) & 1u);
-        mbar_wait(&afull[wg], (i / kGroups) & 1u);
+        mbar_wait(&afull[ab], (i / kBufs) & 1u);
         if (!seg_open && segs > 0) mbar_wait(&dempty, (segs - 1) & 1u);  // epilogue read D
         tc_fence_after();
         const uint32_t bstage = sbase + st * b_stage_bytes(p.n_mma);
+        if (i < 3 && p.ts_mode == 4) TC_STAMP(p.ts, blockIdx.x, 2 * i + 1);
 #pragma unroll
-        for (uint32_t k = 0; k < kStepBytes / 32; ++k) {
+        for (uint32_t k = 0; k < ((kDevAblate && (p.ablate & 1u)) ? 1u : kStepBytes / 32); ++k) {
           const uint64_t bdesc = umma_desc_sw128(bstage + (k >> 2) * p.n_mma * 128u + (k & 3u) * 32u);
-          mma_i8_ts(tmem + kColD, tmem + wg * kAcols + k * 8u, bdesc, idesc, (seg_open || k > 0) ? 1u : 0u);
+          mma_i8_ts(tmem + kColD, tmem + ab * kAcols + k * 8u, bdesc, idesc, (seg_open || k > 0) ? 1u : 0u);
         }
         seg_open = true;
+        if (i < 2 && p.ts_mode == 4) TC_STAMP(p.ts, blockIdx.x, 2 * i + 2);
         if (i == 0 && p.ts_mode == 0) TC_STAMP(p.ts, blockIdx.x, 4);
         if (i + 1 == n_steps && p.ts_mode == 0) TC_STAMP(p.ts, blockIdx.x, 5);
         if (i < 6 && p.ts_mode == 1) TC_STAMP(p.ts, blockIdx.x, i + 1);
-        mma_commit(&aempty[wg]);
+        mma_commit(&aempty[ab]);
         mma_commit(&bempty[st]);
         if (s + 1 == spt || j + 1 == b) {
           mma_commit(&dfull);
@@ -523,11 +555,11 @@ __global__ void __launch_bounds__(kPrepThreads) stream_tc_prep_kernel(
 struct Layout {
   uint32_t n_mma, wst, w_off, st_off, smem;
 };
-Layout layout_of(uint64_t rows_x, int n_w) {
+Layout layout_of(uint64_t rows_x, int n_w, uint32_t wst_cap = kMaxWst) {
   Layout l{};
   l.n_mma = n_mma_of(static_cast<uint32_t>(rows_x));
   l.w_off = kBStages * b_stage_bytes(l.n_mma);
-  for (uint32_t wst = 2; wst >= 1; --wst) {
+  for (uint32_t wst = wst_cap; wst >= 1; --wst) {
     l.wst = wst;
     l.st_off = l.w_off + kTfWarps * wst * wslot_bytes(n_w);
     l.smem = l.st_off + kEpiWarps * kStageBytes + 1024u;  // + alignment slack
@@ -583,7 +615,11 @@ size_t stream_tc_ws_bytes(uint64_t rows_x, uint64_t k) {
 }
 
 cudaError_t launch_stream_tc(const StreamTcArgs& a, cudaStream_t s) {
-  const Layout l = layout_of(a.rows_x, a.n_w);
+  static const uint32_t wst_cap = [] {  // dev A/B: APMM_TC_WST caps the weight ring depth
+    const char* e = APMM_DEV_ENV("APMM_TC_WST");
+    return e ? static_cast<uint32_t>(std::atoi(e)) : kMaxWst;
+  }();
+  const Layout l = layout_of(a.rows_x, a.n_w, wst_cap);
   if (!l.smem) return cudaErrorInvalidConfiguration;
   const uint32_t wpr = static_cast<uint32_t>((a.k + 31) / 32);
   const uint32_t kwords = kwords_of(a.k);
@@ -654,6 +690,11 @@ cudaError_t launch_stream_tc(const StreamTcArgs& a, cudaStream_t s) {
     return e ? static_cast<uint32_t>(std::atoi(e)) : 0u;
   }();
   p.ts_mode = ts_mode;
+  static const uint32_t ablate = [] {
+    const char* e = APMM_DEV_ENV("APMM_TC_ABLATE");
+    return e ? static_cast<uint32_t>(std::atoi(e)) : 0u;
+  }();
+  p.ablate = ablate;
   if (a.ev_start) cudaEventRecordWithFlags(a.ev_start, s, a.ev_flags);
   cudaError_t e;
   switch (a.n_w) {
