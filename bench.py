@@ -724,10 +724,12 @@ def run_ours(args, rank, world, local_rank):
     bytes_step = sum(algorithmic_bytes(g) for g in gemms)
     # which roofline bounds the dominant kernel: compare the two ideal times per step
     hbm_bound = bytes_step / (hbm_peak * 1e9) > ops_step / (i8_peak * 1e12)
-    skinny = all(g[1] <= 40 for g in gemms)
-    kname = ("skinny_kernel (weight planes -> mma.sync u8 fragments)" if skinny else
-             "gemm_u8_pair_kernel / gemm_u8_tc_kernel / gemm_pair_wplanes_kernel "
-             "(tcgen05.mma kind::i8)")
+    small = [g[1] for g in gemms]
+    kname = ("skinny_kernel (weight planes -> mma.sync u8 fragments)" if max(small) <= 8 else
+             "skinny_kernel (M_tok <= 8) / stream_tc_kernel (12 <= M_tok <= 64: weight planes "
+             "expanded into TMEM, tcgen05.mma kind::i8 A-from-TMEM)" if max(small) <= 64 else
+             "gemm_u8_pair_kernel / gemm_u8_tc_kernel / gemm_pair_wplanes_kernel / "
+             "stream_tc_kernel (tcgen05.mma kind::i8)")
     per_rank_step_s = ms_max * 1e-3 / args.steps
     if hbm_bound:
         achieved = (args.steps * bytes_step / max(gemm_n, 1)) / (gemm_avg_ms * 1e-3) / 1e9

@@ -387,7 +387,7 @@ int run_matmul(apmm_ctx* ctx, const uint32_t* w, uint64_t rows_w, int n_w, const
       s.ev_flags = t.flags;
       CU(launch_skinny(s, stream));
     }
-    ctx->launches += rows_x <= 1 ? 1 : 2;  // (feature prep +) streaming kernel
+    ctx->launches += skinny_launches(rows_x);  // (feature prep +) streaming kernel
     if (colmax) {  // K5's epilogue does not form the column absmax: one pass over yf
       CU(cudaMemsetAsync(colmax, 0, colmax_bytes(rows_x), stream));
       CU(launch_colmax(yf, rows_w, rows_x, colmax, colmax_global, ctx->num_sms, stream));

@@ -195,6 +195,7 @@ size_t skinny_acc_bytes(uint64_t rows_w, uint64_t rows_x);
 size_t skinny_scratch_bytes(uint64_t rows_w, uint64_t rows_x, uint64_t k, int n_w,
                             const void* w_planes);
 cudaError_t launch_skinny(const SkinnyArgs& a, cudaStream_t s);
+int skinny_launches(uint64_t rows_x);  // kernels launch_skinny issues (feature prep + K5, or K5)
 
 // K6 (stream_tc.cu): weight planes streamed per warp, expanded in registers into TMEM (the
 // MMA's A operand), features as u8 codes in shared memory (B), tcgen05 kind::i8, K split

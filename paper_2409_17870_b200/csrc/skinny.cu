@@ -61,6 +61,7 @@ namespace {
 constexpr int kChunkWords = 16;  // 512 columns per warp step
 constexpr uint32_t kSkSmemSM = 224u * 1024u;  // dynamic budget per SM (227 KB max minus static)
 constexpr int kPrepThreads = 256;
+constexpr uint64_t kInprepMaxRows = 8;  // feature rows staged by the streaming kernel itself
 
 // One persistent CTA per SM: 16 warps where registers allow, else 8. (Two smaller CTAs per
 // SM were measured slower: the halved shared memory forces more K slices, and the split-K
@@ -431,8 +432,9 @@ __global__ void __launch_bounds__(sk_threads(N, NT), sk_ctas_per_sm(N, NT))
       xstore(tok, wl, v);
       if (rs) atomicAdd(&rsx_s[tok], rs);
     };
-    uint32_t v0[8];
+    uint32_t v0[8], v1[8];
     if (tid < real_words) xload(tid, v0);
+    if (tid + THREADS < real_words) xload(tid + THREADS, v1);
     if (x_first)
 #pragma unroll
       for (uint32_t q = 0; q + 1 < kStages; ++q) issue();
@@ -445,10 +447,14 @@ __global__ void __launch_bounds__(sk_threads(N, NT), sk_ctas_per_sm(N, NT))
     }
     __syncthreads();  // rsx_s zeroed
     if (tid < real_words) xprocess(tid, v0);
-    for (uint32_t idx = tid + THREADS; idx < real_words; idx += THREADS) {
-      uint32_t v[8];
+    if (tid + THREADS < real_words) xprocess(tid + THREADS, v1);
+    for (uint32_t idx = tid + 2 * THREADS; idx < real_words; idx += 2 * THREADS) {
+      uint32_t v[8], v2[8];
+      const bool two = idx + THREADS < real_words;
       xload(idx, v);
+      if (two) xload(idx + THREADS, v2);
       xprocess(idx, v);
+      if (two) xprocess(idx + THREADS, v2);
     }
     __syncthreads();
   } else {
@@ -770,6 +776,8 @@ uint64_t frag_half_bytes(uint64_t rows_x, uint64_t k) {
 
 }  // namespace
 
+int skinny_launches(uint64_t rows_x) { return rows_x <= kInprepMaxRows ? 1 : 2; }
+
 size_t skinny_acc_bytes(uint64_t rows_w, uint64_t rows_x) {
   // tiles of 16R rows, R <= 8: rows padded to 128 cover every plan; + tile counters
   const uint64_t rows = (rows_w + 127) / 128 * 128;
@@ -804,9 +812,11 @@ cudaError_t launch_skinny(const SkinnyArgs& a, cudaStream_t s) {
     return e ? std::atoi(e) : -1;
   }();
   const Plan pl = plan_for(a.rows_w, a.rows_x, p.chunks_total, kn, static_cast<int>(nt), a.num_sms);
-  // In-kernel feature prep pays only for a single feature row (saves the prep launch and its
-  // PDL round trip; for more rows the redundant per-CTA transposes cost more).
-  const bool inprep = inprep_env >= 0 ? inprep_env != 0 : a.rows_x <= 1;
+  // In-kernel feature prep up to 8 feature rows (two batched load rounds per thread): saves the
+  // prep launch and its PDL round trip; 8192^2 W3A8 M=8 12.25 -> 11.78 us, 4096^2 W2A4 M=8
+  // 6.17 -> 5.08 us (profiles/r02/r2_k5_inprep2.txt). Beyond that the redundant per-CTA
+  // transposes cost more (and rows_x >= 12 goes to K6 when it can).
+  const bool inprep = inprep_env >= 0 ? inprep_env != 0 : a.rows_x <= kInprepMaxRows;
   if (pl.grid == 0) return cudaErrorInvalidConfiguration;
   static const bool show = APMM_DEV_ENV("APMM_DEBUG_PLAN") != nullptr;
 

@@ -1,13 +1,17 @@
-# round-end evidence: tests, every bench workload, reference arm, ncu launch list + full captures
-mkdir -p gpurun_out/fin
+# round-end evidence: tests, every bench workload, reference arm, ncu launch lists + full captures
+O=gpurun_out/fin
+mkdir -p $O
 export PYTHONUNBUFFERED=1
-nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,driver_version --format=csv > gpurun_out/fin/smi.txt
-timeout 600 python -m pytest tests -m gpu -x -q > gpurun_out/fin/pytest_gpu.log 2>&1; echo rc=$? >> gpurun_out/fin/pytest_gpu.log
-timeout 100 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/fin/smoke.log 2>&1
-for w in sweep4096 llama7b decode llama7b_small ffn70b; do timeout 300 python bench.py --workload $w > gpurun_out/fin/bench_$w.log 2>&1; done
-timeout 300 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/fin/bench_ref.log 2>&1
-timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/fin/launches_sweep.csv python bench.py --steps 2 --warmup 3 --profile --no-graph --no-cpu-baseline > gpurun_out/fin/ncu_launch.log 2>&1
-timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/fin/launches_decode.csv python bench.py --workload decode --steps 2 --warmup 3 --profile --no-graph --no-cpu-baseline > gpurun_out/fin/ncu_launch_dec.log 2>&1
-timeout 300 ncu --set full --import-source on --clock-control none -k regex:gemm_u8_pair --launch-skip 5 -c 1 -o gpurun_out/fin/pair_w2a4 python scripts/skinny_probe.py 4096 4096 4096 2 4 10 > gpurun_out/fin/ncu_pair.log 2>&1
-timeout 300 ncu --set full --import-source on --clock-control none -k regex:skinny --launch-skip 10 -c 1 -o gpurun_out/fin/skinny_m1 python scripts/skinny_probe.py 8192 1 8192 3 8 20 > gpurun_out/fin/ncu_sk1.log 2>&1
-timeout 300 ncu --set full --import-source on --clock-control none -k regex:skinny --launch-skip 10 -c 1 -o gpurun_out/fin/skinny_m16 python scripts/skinny_probe.py 8192 16 8192 3 8 20 > gpurun_out/fin/ncu_sk16.log 2>&1
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,driver_version --format=csv > $O/smi.txt
+timeout 600 python -m pytest tests -m gpu -x -q > $O/pytest_gpu.log 2>&1; echo rc=$? >> $O/pytest_gpu.log
+timeout 100 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1
+for w in ffn70b sweep4096 llama7b decode llama7b_small llama7b_mid; do timeout 300 python bench.py --workload $w > $O/bench_$w.log 2>&1; done
+timeout 300 python bench.py --impl reference --steps 3 --warmup 3 > $O/bench_ref.log 2>&1
+timeout 200 python scripts/decode_bench.py 30 > $O/decode_bench.txt 2>&1
+( timeout 200 python scripts/route_sweep.py 8192 8192 3 8 1,8,16,32,64
+  timeout 200 python scripts/route_sweep.py 4096 4096 2 4 8,16,32,64,128,256,512 ) > $O/route_sweep.txt 2>&1
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/launches_decode.csv python bench.py --workload decode --steps 2 --warmup 3 --profile --no-graph --no-cpu-baseline > $O/ncu_launch_dec.log 2>&1
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file $O/launches_mid.csv python bench.py --workload llama7b_mid --steps 2 --warmup 3 --profile --no-graph --no-cpu-baseline > $O/ncu_launch_mid.log 2>&1
+timeout 300 ncu --set full --import-source on --clock-control none -k regex:skinny_kernel --launch-skip 10 -c 1 -o $O/skinny_m1 python scripts/skinny_probe.py 8192 1 8192 3 8 20 > $O/ncu_sk1.log 2>&1
+timeout 300 ncu --set full --import-source on --clock-control none -k regex:stream_tc_kernel --launch-skip 10 -c 1 -o $O/stream_tc_m16 python scripts/skinny_probe.py 8192 16 8192 3 8 20 > $O/ncu_tc16.log 2>&1
+timeout 300 ncu --set full --import-source on --clock-control none -k regex:stream_tc_kernel --launch-skip 10 -c 1 -o $O/stream_tc_m64 python scripts/skinny_probe.py 4096 64 4096 2 4 20 > $O/ncu_tc64.log 2>&1
