@@ -127,7 +127,7 @@ enum {
   APMM_ROUTE_PAIR_SPLITK = 5,  /* K1 + K3 with K split over the pairs */
   APMM_ROUTE_SINGLE_SM = 6,    /* K1 + K3': 1-SM 128x256 tiles */
   APMM_ROUTE_TENSOR_CORE = 7,  /* AUTO without K5 (tcgen05 routes only) */
-  APMM_ROUTE_STREAM_TC = 8     /* K6: weight planes streamed into TMEM (A operand), 4 <= rows_x <= 64 */
+  APMM_ROUTE_STREAM_TC = 8     /* K6: weight planes streamed into TMEM (A operand), rows_x <= 128, rows_x % 4 == 0 */
 };
 APMM_API int apmm_ctx_set_option(apmm_ctx* ctx, int option, int value);
 APMM_API int apmm_ctx_get_option(const apmm_ctx* ctx, int option, int* value);

@@ -266,11 +266,14 @@ RouteCaps caps_of(const uint32_t* w, uint64_t rows_w, int n_w, uint64_t rows_x, 
 // kSkinnyPreferRows stay on K5 (faster there: 4096x40x4096 8.6 vs 12.6 us,
 // profiles/r01b_skinny_mid_boundary.txt), and K5 takes up to 63 rows when the split-K path
 // cannot (int32 output with a TMA-storable Y only). TENSOR_CORE = the same without K5.
-// K6 (weight planes streamed into TMEM, tcgen05) from 12 feature rows on (when it can serve:
-// int32 output, rows_x % 4 == 0, <= 64 rows, n_w <= 4): 8192^2 W3A8 M = 16 / 32 / 64: 15.3 /
-// 15.0 / 15.9 us vs 16.3 (K5) / 24.9 (K5) / 31.0 (K3f split-K); 4096^2 W2A4 M = 64: 8.8 vs
-// 11.8 us (profiles/r02/r2_route_sweep_k6.txt). K5 stays faster below (M = 8: 12.2 vs 15.3 us).
+// K6 (weight planes streamed into TMEM, tcgen05) for 12..128 feature rows (when it can serve:
+// int32 output, rows_x % 4 == 0, n_w <= 4): 8192^2 W3A8 M = 16 / 32 / 64: 14.3 / 14.6 / 15.9 us
+// vs 16.3 (K5) / 24.8 (K5) / 30.9 (K3f split-K); Llama-2-7B W2A4 M = 128: 4096x4096 12.3 vs
+// 12.8, 11008x4096 17.7 vs 29.0, 4096x11008 17.7 vs 24.0 us (K3f)
+// (profiles/r02/final/route_sweep.txt, profiles/r02/r2_k6_m128.txt). K5 stays faster below
+// (M = 8: 11.5 vs 14.2 us).
 constexpr uint64_t kStreamTcMinRows = 12;
+constexpr uint64_t kStreamTcMaxRows = 128;
 
 int pick_route(const apmm_ctx* ctx, const RouteCaps& c, uint64_t rows_w, uint64_t rows_x,
                Route* out) {
@@ -297,7 +300,7 @@ int pick_route(const apmm_ctx* ctx, const RouteCaps& c, uint64_t rows_w, uint64_
     default: break;
   }
   const bool allow_skinny = ctx->route != APMM_ROUTE_TENSOR_CORE;
-  if (c.stream_tc && rows_x >= kStreamTcMinRows) {
+  if (c.stream_tc && rows_x >= kStreamTcMinRows && rows_x <= kStreamTcMaxRows) {
     *out = Route::StreamTc;
   } else if (allow_skinny && c.skinny && (rows_x <= kSkinnyPreferRows || !mid)) {
     *out = Route::Skinny;

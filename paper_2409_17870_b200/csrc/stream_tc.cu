@@ -1,5 +1,5 @@
-// stream_tc.cu -- K6: the WnAm bipolar-INT GEMM for small and mid token counts (8 <= M_tok
-// <= 64): the packed weight planes are streamed from HBM once, expanded to u8 codes in
+// stream_tc.cu -- K6: the WnAm bipolar-INT GEMM for small and mid token counts (12 <= M_tok
+// <= 128 by AUTO): the packed weight planes are streamed from HBM once, expanded to u8 codes in
 // registers and written straight into TENSOR MEMORY, where tcgen05.mma reads them as its A
 // operand (kind::i8, A from TMEM, B from shared memory). No code byte of W touches shared
 // memory or HBM, and the features are read by the tensor core from shared memory instead of
@@ -66,12 +66,12 @@ constexpr bool kDevAblate = true;
 constexpr bool kDevAblate = false;
 #endif
 constexpr uint32_t kTileRows = 128;
-constexpr uint32_t kBStages = 3;                // feature-code tiles in flight
+constexpr uint32_t kBStages = 3;                // feature-code tiles in flight (2 for n_mma > 80)
 constexpr uint32_t kTmemCols = 512;
 constexpr uint32_t kColD = kBufs * kAcols;     // A buffers at columns 0 and 128; D from 256
 constexpr uint32_t kStageBytes = 32u * 128u;    // per-warp epilogue staging: 32 rows x 32 int32
 constexpr uint32_t kSmemCap = 232448u - 2048u;  // opt-in maximum minus static + alignment
-constexpr uint32_t kMaxRowsX = 64;
+constexpr uint32_t kMaxRowsX = 128;
 constexpr uint32_t kPrepThreads = 256;
 
 __host__ __device__ constexpr uint32_t n_mma_of(uint32_t rows_x) {
@@ -89,6 +89,7 @@ struct TcParams {
   uint32_t q_steps, r_steps;  // total tile-steps = q * grid + r (CTA c gets q + (c < r))
   uint64_t inv_spt;           // ceil(2^32 / steps_per_tile)
   uint32_t wst;               // per-warp weight ring slots (1..kMaxWst)
+  uint32_t bst;               // feature-code ring stages (2..kBStages)
   uint32_t w_off, st_off;     // shared-memory carve-up: B ring at 0, W rings, staging
   uint32_t coef_w, coef_x, c0;
   uint32_t early_w;
@@ -417,10 +418,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       const uint32_t idesc = idesc_i8_u8u8(kTileRows, p.n_mma);
       const uint64_t hint = policy_evict_last();  // the feature codes are re-read by every CTA
-      auto load_b = [&](uint32_t i) {  // feature codes of step a + i into stage i % kBStages
+      const uint32_t bst = p.bst;
+      auto load_b = [&](uint32_t i) {  // feature codes of step a + i into stage i % bst
         const uint32_t j = a + i;
         const uint32_t tile = div_small(j, p.inv_spt), s = j - tile * spt;
-        const uint32_t st = i % kBStages;
+        const uint32_t st = i % bst;
         uint8_t* dst = smem + st * b_stage_bytes(p.n_mma);
         mbar_arrive_expect_tx(&bfull[st], b_stage_bytes(p.n_mma));
 #pragma unroll
@@ -428,14 +430,14 @@ __global__ void __launch_bounds__(kThreads, 1)
           tma_load_2d(dst + kg * p.n_mma * 128u, &tm_x, &bfull[st], int32_t(s * kStepBytes + kg * 128u), 0, hint);
       };
       pdl_wait();  // the feature codes are written by the prep launch right before us
-      for (uint32_t i = 0; i < kBStages && i < n_steps; ++i) load_b(i);
+      for (uint32_t i = 0; i < bst && i < n_steps; ++i) load_b(i);
       uint32_t segs = 0;
       bool seg_open = false;
       for (uint32_t i = 0; i < n_steps; ++i) {
         const uint32_t j = a + i, ab = i % kBufs;
         const uint32_t tile = div_small(j, p.inv_spt), s = j - tile * spt;
-        const uint32_t st = i % kBStages;
-        mbar_wait(&bfull[st], (i / kBStages) & 1u);
+        const uint32_t st = i % bst;
+        mbar_wait(&bfull[st], (i / bst) & 1u);
         mbar_wait(&afull[ab], (i / kBufs) & 1u);
         if (!seg_open && segs > 0) mbar_wait(&dempty, (segs - 1) & 1u);  // epilogue read D
         tc_fence_after();
@@ -459,10 +461,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           ++segs;
         }
         // refill the stage of step i - 1 (its MMAs were issued a step ago) with step i + 2
-        if (i >= 1 && i + kBStages - 1 < n_steps) {
-          const uint32_t pst = (i - 1) % kBStages;
-          mbar_wait(&bempty[pst], ((i - 1) / kBStages) & 1u);
-          load_b(i + kBStages - 1);
+        if (i >= 1 && i + bst - 1 < n_steps) {
+          const uint32_t pst = (i - 1) % bst;
+          mbar_wait(&bempty[pst], ((i - 1) / bst) & 1u);
+          load_b(i + bst - 1);
         }
       }
     }
@@ -553,17 +555,20 @@ __global__ void __launch_bounds__(kPrepThreads) stream_tc_prep_kernel(
 }
 
 struct Layout {
-  uint32_t n_mma, wst, w_off, st_off, smem;
+  uint32_t n_mma, wst, bst, w_off, st_off, smem;
 };
 Layout layout_of(uint64_t rows_x, int n_w, uint32_t wst_cap = kMaxWst) {
   Layout l{};
   l.n_mma = n_mma_of(static_cast<uint32_t>(rows_x));
-  l.w_off = kBStages * b_stage_bytes(l.n_mma);
-  for (uint32_t wst = wst_cap; wst >= 1; --wst) {
-    l.wst = wst;
-    l.st_off = l.w_off + kTfWarps * wst * wslot_bytes(n_w);
-    l.smem = l.st_off + kEpiWarps * kStageBytes + 1024u;  // + alignment slack
-    if (l.smem <= kSmemCap) return l;
+  for (uint32_t bst = kBStages; bst >= 2; --bst) {
+    l.bst = bst;
+    l.w_off = bst * b_stage_bytes(l.n_mma);
+    for (uint32_t wst = wst_cap; wst >= 1; --wst) {
+      l.wst = wst;
+      l.st_off = l.w_off + kTfWarps * wst * wslot_bytes(n_w);
+      l.smem = l.st_off + kEpiWarps * kStageBytes + 1024u;  // + alignment slack
+      if (l.smem <= kSmemCap) return l;
+    }
   }
   l.smem = 0;
   return l;
@@ -677,6 +682,7 @@ cudaError_t launch_stream_tc(const StreamTcArgs& a, cudaStream_t s) {
   p.r_steps = total % grid;
   p.inv_spt = ((uint64_t(1) << 32) + spt - 1) / spt;
   p.wst = l.wst;
+  p.bst = l.bst;
   p.w_off = l.w_off;
   p.st_off = l.st_off;
   const uint32_t A = (1u << a.n_w) - 1u, B = (1u << a.n_x) - 1u;
