@@ -274,16 +274,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     };
     if (!p.early_w) pdl_wait();
     for (uint32_t i = 0; i < p.wst; ++i) issue();
-    pdl_wait();  // features' rowsum parts and Y only after the previous kernel
-    if (tid == 0 && p.ts_mode == 0) TC_STAMP(p.ts, blockIdx.x, 1);
-    for (uint32_t c = lane; c < p.rows_x; c += 32) {
-      if (warp == 0) {
-        int32_t sum = 0;
-        for (uint32_t i = 0; i < p.parts; ++i) sum += __ldg(p.rsx_part + c * p.parts + i);
-        rsx_s[c] = sum;
-      }
-    }
-    asm volatile("bar.sync 1, %0;" ::"n"(kTfWarps * 32));  // rsx_s visible to the transform warps
+    // The transform warps touch only the weight planes (call inputs), tensor memory and shared
+    // memory until their first epilogue: they expand the first steps while the feature prep
+    // still runs; griddepcontrol.wait (features' rowsum, Y) comes at the first segment end.
+    // rowsum(U_x) is needed only by the first epilogue: loaded there, off the path to the
+    // first MMA
     uint8_t* stage = smem + p.st_off + (warp % kEpiWarps) * kStageBytes;
     const uint32_t my_lane_addr = (q * 32u) << 16;          // epilogue: 32x32b over the quarter
     const uint32_t st_lane_addr = (rg * kItemRows) << 16;   // transform: 16x256b, 16 lanes
@@ -373,6 +368,18 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       if (s + 1 == spt || j + 1 == b) {
         // ---------------- segment end: partial tile -> reduce-add into Y ----------------
+        if (segs == 0) {
+          pdl_wait();  // rowsum(U_x) parts and Y only after the prep launch completed
+          if (tid == 0 && p.ts_mode == 0) TC_STAMP(p.ts, blockIdx.x, 1);
+          if (warp == 0) {
+            for (uint32_t c = lane; c < p.rows_x; c += 32) {
+              int32_t sum = 0;
+              for (uint32_t i = 0; i < p.parts; ++i) sum += __ldg(p.rsx_part + c * p.parts + i);
+              rsx_s[c] = sum;
+            }
+          }
+          asm volatile("bar.sync 1, %0;" ::"n"(kTfWarps * 32));  // rsx_s visible to the transform warps
+        }
         mbar_wait(&dfull, segs & 1u);
         tc_fence_after();
         if (tid == 0 && segs == 0 && p.ts_mode == 0) TC_STAMP(p.ts, blockIdx.x, 6);
