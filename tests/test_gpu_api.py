@@ -230,15 +230,15 @@ def test_early_read_options_are_bit_identical(gpu, oracle):
 
 def test_graph_replays_of_every_route(gpu):
     """Back-to-back calls captured once and replayed several times (the serving pattern):
-    the PDL chain between calls, the ping-pong workspace halves and the mid route's in-kernel
-    grid barrier (count + generation, reused across replays) give the eager results on every
-    replay."""
+    the PDL chain between calls, the ping-pong workspace halves, K6's feature prep + stream-K
+    reduce-adds (M = 16, 128) and the mid route's in-kernel grid barrier (count + generation,
+    reused across replays; M = 256) give the eager results on every replay."""
     import torch
     ap, _ = gpu
     dev = torch.device("cuda", 0)
     s = torch.cuda.Stream()
     shapes = [(4096, 8, 4096, 3, 8), (4096, 128, 4096, 2, 4), (2304, 2560, 4096, 2, 4),
-              (4096, 512, 4096, 2, 4)]
+              (4096, 512, 4096, 2, 4), (8192, 16, 8192, 3, 8), (4096, 256, 4096, 2, 4)]
     for (n_out, m, k, nw, nx) in shapes:
         ctx = ap.Context(0)
         ctx.set_stream(s)
