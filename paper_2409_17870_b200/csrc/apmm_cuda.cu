@@ -266,13 +266,13 @@ RouteCaps caps_of(const uint32_t* w, uint64_t rows_w, int n_w, uint64_t rows_x, 
 // kSkinnyPreferRows stay on K5 (faster there: 4096x40x4096 8.6 vs 12.6 us,
 // profiles/r01b_skinny_mid_boundary.txt), and K5 takes up to 63 rows when the split-K path
 // cannot (int32 output with a TMA-storable Y only). TENSOR_CORE = the same without K5.
-// K6 (weight planes streamed into TMEM, tcgen05) for 12..128 feature rows (when it can serve:
+// K6 (weight planes streamed into TMEM, tcgen05) for 16..128 feature rows (when it can serve:
 // int32 output, rows_x % 4 == 0, n_w <= 4): 8192^2 W3A8 M = 16 / 32 / 64: 14.3 / 14.6 / 15.9 us
 // vs 16.3 (K5) / 24.8 (K5) / 30.9 (K3f split-K); Llama-2-7B W2A4 M = 128: 4096x4096 12.3 vs
 // 12.8, 11008x4096 17.7 vs 29.0, 4096x11008 17.7 vs 24.0 us (K3f)
 // (profiles/r02/final/route_sweep.txt, profiles/r02/r2_k6_m128.txt). K5 stays faster below
-// (M = 8: 11.5 vs 14.2 us).
-constexpr uint64_t kStreamTcMinRows = 12;
+// (M = 8: 11.5 vs 14.2 us; up to 15 rows K5 keeps two 8-column n-tiles).
+constexpr uint64_t kStreamTcMinRows = 16;
 constexpr uint64_t kStreamTcMaxRows = 128;
 
 int pick_route(const apmm_ctx* ctx, const RouteCaps& c, uint64_t rows_w, uint64_t rows_x,
