@@ -66,7 +66,13 @@ constexpr bool kDevAblate = true;
 constexpr bool kDevAblate = false;
 #endif
 constexpr uint32_t kTileRows = 128;
-constexpr uint32_t kBStages = 3;                // feature-code tiles in flight (2 for n_mma > 80)
+#ifndef APMM_TC_BST_AB
+// feature-code tiles in flight: up to 6 as shared memory allows (3 at 64 rows, 2 above 80);
+// 8192 x 16 x 8192 W3A8 14.95 -> 14.53 us at 6 vs 3 (profiles/r02/r2_k6_bst.txt)
+constexpr uint32_t kBStages = 6;
+#else
+constexpr uint32_t kBStages = APMM_TC_BST_AB;   // A/B builds only
+#endif
 constexpr uint32_t kTmemCols = 512;
 constexpr uint32_t kColD = kBufs * kAcols;     // A buffers at columns 0 and 128; D from 256
 constexpr uint32_t kStageBytes = 32u * 128u;    // per-warp epilogue staging: 32 rows x 32 int32
