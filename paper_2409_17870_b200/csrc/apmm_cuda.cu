@@ -279,7 +279,10 @@ int pick_route(const apmm_ctx* ctx, const RouteCaps& c, uint64_t rows_w, uint64_
                Route* out) {
   const uint64_t pair_tiles = ((rows_w + 255) / 256) * ((rows_x + kPairN - 1) / kPairN);
   const bool pair = pair_tiles >= static_cast<uint64_t>(ctx->num_sms / 2);
-  const bool mid = c.mid && !pair && rows_x <= 256;
+  // K3f split-K up to 512 feature rows when the pair tiles cannot fill the machine:
+  // 4096 x 384 / 512 x 4096 W2A4 21.0 / 21.8 us vs 23.5 / 22.3 (1-SM), 4096 x 384 / 512 x 11008
+  // 44.0 / 44.9 vs 50.2 / 49.2 (profiles/r02/r2_route_sweep_m192_512.txt)
+  const bool mid = c.mid && !pair && rows_x <= 512;
   auto forced = [&](bool ok, Route r) {
     if (!ok) {
       return fail(APMM_E_INVALID_ARGUMENT, "forced route %s cannot serve this call "
