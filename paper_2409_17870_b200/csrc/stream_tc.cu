@@ -59,8 +59,12 @@ constexpr int kEpiWarps = 8;                    // warps with an epilogue stagin
 // 15.8 / 18.6 / 18.6 us at 1 / 2 / 3 / 4 slots, profiles/r02/r2_k6_wst.txt; 8192 x 32: 15.9 vs
 // 18.3 us at 1 vs 2, r2_k6_ab.txt): the item is copied to registers at once, so one slot
 // already overlaps the next item's load with this one's transform.
+#ifndef APMM_TC_WST_AB
 constexpr uint32_t kMaxWst = 1;
-#ifdef APMM_DEVTOOLS
+#else
+constexpr uint32_t kMaxWst = APMM_TC_WST_AB;  // A/B builds only
+#endif
+#if defined(APMM_DEVTOOLS) && defined(APMM_TC_DEV_ABLATE)
 constexpr bool kDevAblate = true;
 #else
 constexpr bool kDevAblate = false;

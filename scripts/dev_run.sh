@@ -1,4 +1,3 @@
 mkdir -p gpurun_out/abl
 export PYTHONUNBUFFERED=1
-timeout 600 python -m pytest tests -q -x -m gpu > gpurun_out/abl/pytest_gpu.txt 2>&1; echo rc=$? >> gpurun_out/abl/pytest_gpu.txt
-timeout 300 python bench.py --workload llama7b_mid > gpurun_out/abl/bench_mid.log 2>&1
+for v in rel w2b3 w2b2 w1b3 w3b3; do echo "== $v"; APMM_LIB=$PWD/abtest/lib_$v.so timeout 100 python scripts/decode_bench.py 40 8192x16,8192x32,4096x16,11008x16,4096x16x11008; done > gpurun_out/abl/k6_wb.txt 2>&1
