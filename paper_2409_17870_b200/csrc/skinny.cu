@@ -318,18 +318,21 @@ __global__ void __launch_bounds__(kPrepThreads) prep_x_kernel(const uint32_t* __
   }
 }
 
-template <int N, int NT, bool SPLIT>
+// PR: rowsum(U_w) from popcounts of the weight planes instead of an all-ones feature column
+// (used when the feature rows fill their n-tiles exactly: M_tok = 8 needs one n-tile, not two)
+template <int N, int NT, bool SPLIT, bool PR>
 __global__ void __launch_bounds__(sk_threads(N, NT), sk_ctas_per_sm(N, NT))
     skinny_kernel(const __grid_constant__ CUtensorMap tmap_w, const SkinnyParams p) {
   constexpr int THREADS = sk_threads(N, NT);
   constexpr int WARPS = THREADS / 32;
   constexpr uint32_t SLOT = slot_bytes(N);
   constexpr uint32_t M_PAD = NT * 8u;
-  constexpr uint32_t ONES = M_PAD - 1u;  // the all-ones feature column -> rowsum(U_w)
+  constexpr uint32_t ONES = PR ? 0xFFFFFFFFu : M_PAD - 1u;  // the all-ones column -> rowsum(U_w)
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ __align__(8) uint64_t full_bar[WARPS * kStages];
   __shared__ __align__(8) uint64_t xbars[kXPieces];  // X slice arrival, per piece of chunks
   __shared__ uint32_t rsx_s[M_PAD];
+  __shared__ uint32_t rsw_s[PR ? 128 : 1];  // PR: rowsum(U_w) of the tile's rows
   __shared__ uint32_t s_last;
 
   const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -440,6 +443,7 @@ __global__ void __launch_bounds__(sk_threads(N, NT), sk_ctas_per_sm(N, NT))
       for (uint32_t q = 0; q + 1 < kStages; ++q) issue();
     for (uint32_t q = tid; q < M_PAD; q += THREADS) rsx_s[q] = 0u;
     for (uint32_t q = tid; q < tile_rows * M_PAD; q += THREADS) red[q] = 0u;
+    if (PR) for (uint32_t q = tid; q < tile_rows; q += THREADS) rsw_s[q] = 0u;
     for (uint32_t q = tid; q < 2u * slice_words; q += THREADS) {  // the zero and all-ones rows
       const uint32_t hi = q >= slice_words ? 1u : 0u, c = hi ? 0x01010101u : 0u;
       const uint32_t v[8] = {c, c, c, c, c, c, c, c};
@@ -482,6 +486,7 @@ __global__ void __launch_bounds__(sk_threads(N, NT), sk_ctas_per_sm(N, NT))
       rsx_s[q] = static_cast<uint32_t>(s);
     }
     for (uint32_t q = tid; q < tile_rows * M_PAD; q += THREADS) red[q] = 0u;
+    if (PR) for (uint32_t q = tid; q < tile_rows; q += THREADS) rsw_s[q] = 0u;
     __syncthreads();
   }
   SK_STAMP(2);
@@ -516,6 +521,7 @@ __global__ void __launch_bounds__(sk_threads(N, NT), sk_ctas_per_sm(N, NT))
     xrow[nt] = tok < p.rows_x ? tok : (tok == ONES ? p.rows_x + 1u : p.rows_x);
   }
   uint32_t cs_slot = 0, phase_bits = 0;
+  uint32_t rsa = 0, rsb = 0;  // PR: this thread's share of rowsum(U_w) of rows g, g + 8
   for (uint32_t ti = 0; ti < my_tiles; ++ti) {
     const uint32_t tile = j0 + ti * gs;
     for (uint32_t c = 0; c < cpw; ++c) {
@@ -535,6 +541,13 @@ __global__ void __launch_bounds__(sk_threads(N, NT), sk_ctas_per_sm(N, NT))
           const bool live = SPLIT || uint32_t(pl) < p.n_planes;
           wa[pl] = live ? *reinterpret_cast<const uint4*>(slot + pl * 1024) : make_uint4(0, 0, 0, 0);
           wb[pl] = live ? *reinterpret_cast<const uint4*>(slot + pl * 1024 + 512) : make_uint4(0, 0, 0, 0);
+        }
+        if (PR) {
+#pragma unroll
+          for (int pl = 0; pl < N; ++pl) {
+            rsa += (__popc(wa[pl].x) + __popc(wa[pl].y) + __popc(wa[pl].z) + __popc(wa[pl].w)) << pl;
+            rsb += (__popc(wb[pl].x) + __popc(wb[pl].y) + __popc(wb[pl].z) + __popc(wb[pl].w)) << pl;
+          }
         }
         const uint4* xchunk = reinterpret_cast<const uint4*>(xs + (chunk - s_begin) * xchunk_bytes);
         const uint32_t m4 = frag_rows(p.rows_x) * 4u;
@@ -599,6 +612,17 @@ __global__ void __launch_bounds__(sk_threads(N, NT), sk_ctas_per_sm(N, NT))
           lo[nt][e] = hi[nt][e] = 0u;
         }
       }
+      if (PR) {  // the four t lanes of a row hold different words of it
+        rsa += __shfl_xor_sync(0xffffffffu, rsa, 1);
+        rsa += __shfl_xor_sync(0xffffffffu, rsa, 2);
+        rsb += __shfl_xor_sync(0xffffffffu, rsb, 1);
+        rsb += __shfl_xor_sync(0xffffffffu, rsb, 2);
+        if (t == 0) {
+          atomicAdd(&rsw_s[wr * 16u + g], rsa);
+          atomicAdd(&rsw_s[wr * 16u + g + 8u], rsb);
+        }
+        rsa = rsb = 0u;
+      }
     }
     __syncthreads();
     const uint32_t elems = tile_rows * M_PAD;
@@ -606,8 +630,8 @@ __global__ void __launch_bounds__(sk_threads(N, NT), sk_ctas_per_sm(N, NT))
       const uint32_t rl = e / M_PAD, tok = e % M_PAD;
       const uint32_t row = tile * tile_rows + rl;
       if (row >= p.rows_w || tok >= p.rows_x) continue;
-      const uint32_t v = 4u * red[e] - p.coef_w * red[rl * M_PAD + ONES] -
-                         p.coef_x * rsx_s[tok] + cterm;
+      const uint32_t rsw = PR ? rsw_s[rl] : red[rl * M_PAD + (PR ? 0u : ONES)];
+      const uint32_t v = 4u * red[e] - p.coef_w * rsw - p.coef_x * rsx_s[tok] + cterm;
       if (p.slices > 1) {
         atomicAdd(p.acc + (uint64_t(tile) * tile_rows + rl) * M_PAD + tok, v);
         continue;
@@ -624,6 +648,7 @@ __global__ void __launch_bounds__(sk_threads(N, NT), sk_ctas_per_sm(N, NT))
     if (p.slices == 1 && ti + 1 == my_tiles) break;  // last tile: red is not reused
     __syncthreads();  // every reader of red is done
     for (uint32_t e = tid; e < elems; e += THREADS) red[e] = 0u;
+    if (PR) for (uint32_t q = tid; q < tile_rows; q += THREADS) rsw_s[q] = 0u;
     if (p.slices > 1 && tid == 0) {
       __threadfence();
       const uint32_t prev = atomicAdd(p.counters + tile, 1u);
@@ -656,10 +681,10 @@ __global__ void __launch_bounds__(sk_threads(N, NT), sk_ctas_per_sm(N, NT))
   SK_STAMP(5);
 }
 
-template <int N, int NT, bool SPLIT>
+template <int N, int NT, bool SPLIT, bool PR>
 cudaError_t launch_t(const CUtensorMap& tm, const SkinnyParams& p, unsigned grid, uint32_t smem,
                      cudaStream_t s) {
-  auto kern = skinny_kernel<N, NT, SPLIT>;
+  auto kern = skinny_kernel<N, NT, SPLIT, PR>;
   static DeviceBits attr_set;  // one per instantiation
   const int dev = current_device();
   cudaError_t e;
@@ -687,19 +712,27 @@ cudaError_t launch_t(const CUtensorMap& tm, const SkinnyParams& p, unsigned grid
 // N = 4 (n_w <= 4) or N = 8 (n_w 5..8), unused planes masked at run time.
 int kernel_n(int n_w, bool split) { return split ? n_w : (n_w <= 4 ? 4 : 8); }
 
-template <int NT>
-cudaError_t dispatch_n(int n_w, bool split, const CUtensorMap& tm, const SkinnyParams& p,
-                       unsigned grid, uint32_t smem, cudaStream_t s) {
+template <int NT, bool PR>
+cudaError_t dispatch_np(int n_w, bool split, const CUtensorMap& tm, const SkinnyParams& p,
+                        unsigned grid, uint32_t smem, cudaStream_t s) {
   if (split) {
     switch (n_w) {
-      case 1: return launch_t<1, NT, true>(tm, p, grid, smem, s);
-      case 2: return launch_t<2, NT, true>(tm, p, grid, smem, s);
-      case 3: return launch_t<3, NT, true>(tm, p, grid, smem, s);
-      default: return launch_t<4, NT, true>(tm, p, grid, smem, s);
+      case 1: return launch_t<1, NT, true, PR>(tm, p, grid, smem, s);
+      case 2: return launch_t<2, NT, true, PR>(tm, p, grid, smem, s);
+      case 3: return launch_t<3, NT, true, PR>(tm, p, grid, smem, s);
+      default: return launch_t<4, NT, true, PR>(tm, p, grid, smem, s);
     }
   }
-  return n_w <= 4 ? launch_t<4, NT, false>(tm, p, grid, smem, s)
-                  : launch_t<8, NT, false>(tm, p, grid, smem, s);
+  return n_w <= 4 ? launch_t<4, NT, false, PR>(tm, p, grid, smem, s)
+                  : launch_t<8, NT, false, PR>(tm, p, grid, smem, s);
+}
+template <int NT>
+cudaError_t dispatch_n(int n_w, bool split, bool pr, const CUtensorMap& tm, const SkinnyParams& p,
+                       unsigned grid, uint32_t smem, cudaStream_t s) {
+  if constexpr (NT <= 2) {
+    if (pr) return dispatch_np<NT, true>(n_w, split, tm, p, grid, smem, s);
+  }
+  return dispatch_np<NT, false>(n_w, split, tm, p, grid, smem, s);
 }
 
 struct Plan {
@@ -762,7 +795,12 @@ Plan plan_for(uint64_t rows_w, uint64_t rows_x, uint32_t chunks, int n, int nt, 
   return best;
 }
 
-uint32_t nt_of(uint64_t rows_x) { return static_cast<uint32_t>(rows_x / 8 + 1); }  // + ones column
+// rowsum(U_w) by popcount when the feature rows fill whole n-tiles (8 or 16 rows); otherwise
+// through the all-ones feature column
+bool popc_rowsum(uint64_t rows_x) { return rows_x % 8 == 0 && rows_x <= 16; }
+uint32_t nt_of(uint64_t rows_x) {
+  return static_cast<uint32_t>(popc_rowsum(rows_x) ? rows_x / 8 : rows_x / 8 + 1);  // + ones column
+}
 bool needs_repack(uint64_t k, const void* w) {
   return ((k + 31) / 32) % 4 != 0 || reinterpret_cast<uintptr_t>(w) % 16 != 0;
 }
@@ -807,6 +845,7 @@ cudaError_t launch_skinny(const SkinnyArgs& a, cudaStream_t s) {
   const bool ext_shape = a.n_w <= 2 && nt <= 2;
   const bool split = a.n_w <= 4 && kab < (ext_shape ? 67108864.0 : 268435456.0);
   const int kn = kernel_n(a.n_w, split);
+  const bool pr = popc_rowsum(a.rows_x);
   static const int inprep_env = [] {
     const char* e = APMM_DEV_ENV("APMM_SK_INPREP");
     return e ? std::atoi(e) : -1;
@@ -933,14 +972,14 @@ cudaError_t launch_skinny(const SkinnyArgs& a, cudaStream_t s) {
   if (a.ev_start) cudaEventRecordWithFlags(a.ev_start, s, a.ev_flags);
   cudaError_t res;
   switch (nt) {
-    case 1: res = dispatch_n<1>(a.n_w, split, tm, p, pl.grid, pl.smem, s); break;
-    case 2: res = dispatch_n<2>(a.n_w, split, tm, p, pl.grid, pl.smem, s); break;
-    case 3: res = dispatch_n<3>(a.n_w, split, tm, p, pl.grid, pl.smem, s); break;
-    case 4: res = dispatch_n<4>(a.n_w, split, tm, p, pl.grid, pl.smem, s); break;
-    case 5: res = dispatch_n<5>(a.n_w, split, tm, p, pl.grid, pl.smem, s); break;
-    case 6: res = dispatch_n<6>(a.n_w, split, tm, p, pl.grid, pl.smem, s); break;
-    case 7: res = dispatch_n<7>(a.n_w, split, tm, p, pl.grid, pl.smem, s); break;
-    default: res = dispatch_n<8>(a.n_w, split, tm, p, pl.grid, pl.smem, s); break;
+    case 1: res = dispatch_n<1>(a.n_w, split, pr, tm, p, pl.grid, pl.smem, s); break;
+    case 2: res = dispatch_n<2>(a.n_w, split, pr, tm, p, pl.grid, pl.smem, s); break;
+    case 3: res = dispatch_n<3>(a.n_w, split, pr, tm, p, pl.grid, pl.smem, s); break;
+    case 4: res = dispatch_n<4>(a.n_w, split, pr, tm, p, pl.grid, pl.smem, s); break;
+    case 5: res = dispatch_n<5>(a.n_w, split, pr, tm, p, pl.grid, pl.smem, s); break;
+    case 6: res = dispatch_n<6>(a.n_w, split, pr, tm, p, pl.grid, pl.smem, s); break;
+    case 7: res = dispatch_n<7>(a.n_w, split, pr, tm, p, pl.grid, pl.smem, s); break;
+    default: res = dispatch_n<8>(a.n_w, split, pr, tm, p, pl.grid, pl.smem, s); break;
   }
   if (a.ev_stop) cudaEventRecordWithFlags(a.ev_stop, s, a.ev_flags);
   return res;
