@@ -346,7 +346,7 @@ def test_mid_size_split_k_path(gpu, oracle, n_out, m_tok, k, nw, nx):
     (4096, 64, 4096, 2, 4), (8192, 16, 8192, 3, 8), (4096, 8, 4096, 2, 4), (11008, 32, 4096, 4, 4),
     (4096, 64, 11008, 1, 2), (1000, 4, 4224, 3, 5), (2305, 60, 4200, 2, 8), (300, 12, 128, 4, 1),
     (8192, 48, 8192, 3, 8), (129, 64, 640, 2, 3), (4096, 128, 4096, 2, 4), (1000, 100, 4224, 4, 8),
-    (4096, 96, 11008, 3, 4)])
+    (4096, 96, 11008, 3, 4), (2048, 124, 4096, 4, 8), (2051, 128, 1152, 1, 1)])
 def test_stream_tensor_memory_path(gpu, oracle, n_out, m_tok, k, nw, nx):
     """K6 (APMM_ROUTE_STREAM_TC): weight planes streamed per warp, expanded in registers into
     TMEM as the MMA's A operand, K split over every SM (stream-K ranges, partial tiles TMA
