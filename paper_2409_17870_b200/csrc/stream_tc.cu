@@ -1,4 +1,4 @@
-// stream_tc.cu -- K6: the WnAm bipolar-INT GEMM for small and mid token counts (12 <= M_tok
+// stream_tc.cu -- K6: the WnAm bipolar-INT GEMM for small and mid token counts (16 <= M_tok
 // <= 128 by AUTO): the packed weight planes are streamed from HBM once, expanded to u8 codes in
 // registers and written straight into TENSOR MEMORY, where tcgen05.mma reads them as its A
 // operand (kind::i8, A from TMEM, B from shared memory). No code byte of W touches shared
@@ -16,16 +16,19 @@
 // columns; the tile-steps (tile-major) are dealt to one persistent CTA per SM as contiguous
 // ranges (stream-K). A CTA's run of steps of one tile accumulates in TMEM; at its end the
 // partial tile is TMA reduce-added (exact wrapping u32 add) into Y, which the feature-prep
-// launch zeroed.
+// launch (stream_tc_prep_kernel, the call's first launch) zeroed.
 //
-// CTA: 8 transform warps in two warpgroups + 1 MMA warp. Warpgroup g expands the CTA's steps
-// g, g+2, ... into its own 128-column A buffer: warp q of the group owns TMEM lanes 32q..32q+31
-// = weight rows 32q.. of the tile, one row per thread. Per step a warp streams one TMA box
-// {16 words, 32 rows, n_w planes} through its own ring (64-byte rows, 64-byte swizzle: the
-// per-thread row reads are bank-conflict free), turns each 32-column word into 8 registers of
-// u8 codes (register r, byte b = column 8b + r: the K order of the feature codes, DESIGN.md
-// "Data layout") and stores them with tcgen05.st. The MMA warp streams the feature tile of the
-// step (K1-order u8 codes, 128B swizzle) and issues 16 MMAs of K = 32.
+// CTA: 16 transform warps + 1 MMA warp. Transform warp (q = warp % 4, h = warp / 4) owns the
+// 16-row group rg = 2q + (h & 1) of the tile (TMEM lanes 16 rg.., inside its lane quarter q)
+// and the CTA's steps of parity h / 2, each written into that parity's 128-column A buffer.
+// Per step a warp streams K5's item -- TMA box {16 words, 16 rows, n_w planes}, 64-byte rows,
+// conflict-free 16-byte reads with thread (g, t) on words 4t.. of rows g and g + 8 -- through
+// its one-slot ring, copies it to registers (the slot is re-issued at once), turns each
+// 32-column word into 8 registers of u8 codes with K5's transposes and stores them with
+// tcgen05.st.16x256b; the features are written by the prep in the matching permuted K order.
+// The MMA warp streams the feature tile of the step (128B swizzle, up to 6 stages) and issues
+// 16 MMAs of K = 32 per step. Measured limits: an M=128, K=32 i8 MMA costs
+// >= 56 cycles with A in TMEM for N <= 64 (A-operand read, scripts/mma_rate_probe.cu).
 #include <cuda.h>
 #include <cuda_runtime.h>
 

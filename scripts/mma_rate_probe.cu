@@ -24,7 +24,7 @@ __host__ __device__ constexpr uint32_t idesc(uint32_t M, uint32_t N) {
   return (2u << 4) | ((N >> 3) << 17) | ((M >> 4) << 24);
 }
 
-template <int N, bool TS>
+template <int N, bool TS, bool STORE = false, int ND = 1>
 __global__ void probe(unsigned long long* out, int iters) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint32_t tbase;
@@ -48,27 +48,45 @@ __global__ void probe(unsigned long long* out, int iters) {
       const uint64_t bd = desc_sw128(b_smem + k * 32);
       if (TS) {
         asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-                     "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}" ::"r"(t + 256),
-                     "r"(t + (i & 15) * 8), "l"(bd), "r"(idesc(128, N)), "r"(i > 0 ? 1 : 0));
+                     "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}" ::"r"(t + 256 + (i % ND) * 64),
+                     "r"(t + (i & 15) * 8), "l"(bd), "r"(idesc(128, N)), "r"(i >= ND ? 1 : 0));
       } else {
         const uint64_t ad = desc_sw128(a_smem + k * 32);
         asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-                     "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(t + 256),
-                     "l"(ad), "l"(bd), "r"(idesc(128, N)), "r"(i > 0 ? 1 : 0));
+                     "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(t + 256 + (i % ND) * 64),
+                     "l"(ad), "l"(bd), "r"(idesc(128, N)), "r"(i >= ND ? 1 : 0));
       }
     }
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(&bar)) : "memory");
     asm volatile("{\n\t.reg .pred P1;\nW:\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%0], 0;\n\t@!P1 bra W;\n\t}" ::"r"(su32(&bar)) : "memory");
     out[blockIdx.x] = clock64() - t0;
+  } else if (STORE && threadIdx.x >= 32) {
+    // warps 1..3: tcgen05.st 32x32b.x32 into their lane quarter, columns 384.., for as long as
+    // the MMAs run (the K6 transform warps' traffic next to the MMA's A-operand reads)
+    const uint32_t w = threadIdx.x >> 5;
+    uint32_t r[32];
+    for (int i = 0; i < 32; ++i) r[i] = threadIdx.x * 33u + i;
+    const uint32_t addr = t + ((32u * w) << 16) + 384u;
+    for (int it = 0; it < iters / 4; ++it) {
+      asm volatile(
+          "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, "
+          "%13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32};" ::"r"(addr),
+          "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+          "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]),
+          "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]),
+          "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+          : "memory");
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   if (threadIdx.x < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(t));
 }
 
-template <int N, bool TS>
+template <int N, bool TS, bool STORE = false, int ND = 1>
 void run(unsigned long long* d, int sms) {
-  auto k = probe<N, TS>;
+  auto k = probe<N, TS, STORE, ND>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
   const int iters = 4096;
   k<<<sms, 128, 100 * 1024>>>(d, iters);
@@ -77,7 +95,8 @@ void run(unsigned long long* d, int sms) {
   cudaMemcpy(h, d, sms * 8, cudaMemcpyDeviceToHost);
   double s = 0;
   for (int i = 0; i < sms; ++i) s += h[i];
-  std::printf("%s N=%3d: %6.1f cycles per MMA (M=128 K=32; all %d SMs busy) err=%s\n", TS ? "TS" : "SS", N,
+  std::printf("%s%s N=%3d, %d accumulators: %6.1f cycles per MMA (M=128 K=32; all %d SMs busy) err=%s\n",
+              TS ? "TS" : "SS", STORE ? " + concurrent tcgen05.st (3 warps)" : "", N, ND,
               s / sms / iters, sms, cudaGetErrorString(cudaGetLastError()));
 }
 
@@ -96,5 +115,12 @@ int main() {
   run<64, false>(d, sms);
   run<128, false>(d, sms);
   run<256, false>(d, sms);
+  run<32, true, true>(d, sms);
+  run<64, true, true>(d, sms);
+  run<32, false, true>(d, sms);
+  run<32, true, false, 2>(d, sms);
+  run<32, true, false, 4>(d, sms);
+  run<32, false, false, 2>(d, sms);
+  run<64, true, false, 2>(d, sms);
   return 0;
 }
