@@ -603,7 +603,7 @@ def run_ours(args, rank, world, local_rank):
             gather_only()
         cg_ms = timed(compute_gather)
         recv_bytes = (world - 1) * ms_blk * m_full * 4
-        gather = {"format": "int32 Y row blocks", "collective": "all_gather_into_tensor (NCCL)",
+        gather = {"format": "int32 Y row blocks", "collective": f"all_gather_into_tensor ({dist.get_backend()})",
                   "ms_per_step": g_ms, "recv_bytes_per_rank": recv_bytes,
                   "algbw_GBps": recv_bytes / (g_ms * 1e-3) / 1e9,
                   "compute_plus_gather_ms_per_step": cg_ms,
