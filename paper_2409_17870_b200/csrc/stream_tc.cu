@@ -122,7 +122,16 @@ APMM_DEV unsigned long long gtime_ns() {
   do {                        \
     if (ts) (ts)[(slot) * 8 + (k)] = gtime_ns(); \
   } while (0)
+// ts_mode 5: per-step clock64 events of one CTA in 4 pages of 8 (slot blockIdx.x + 256 page)
+#define TC_CLK(pg, k)                                                                       \
+  do {                                                                                      \
+    if (p.ts && p.ts_mode == 5)                                                             \
+      p.ts[(blockIdx.x + 256u * (pg)) * 8u + (k)] = static_cast<unsigned long long>(clock64()); \
+  } while (0)
 #else
+#define TC_CLK(pg, k) \
+  do {                \
+  } while (0)
 #define TC_STAMP(ts, slot, k) \
   do {                        \
   } while (0)
@@ -236,6 +245,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid == 0) TC_STAMP(p.ts, blockIdx.x, 0);
+  if (tid == 0) TC_CLK(3, 0);
   // this CTA's tile-steps [a, b)
   const uint32_t a = blockIdx.x * p.q_steps + min(blockIdx.x, p.r_steps);
   const uint32_t n_steps = p.q_steps + (blockIdx.x < p.r_steps ? 1u : 0u);
@@ -304,10 +314,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (((j - a) & (kGroups - 1u)) == wg) {
         // the MMAs that read this A buffer three steps ago (the other warp set's) are done
         if (ui > 0) mbar_wait(&aempty[bi], (ui - 1) & 1u);
+        const uint32_t si = j - a;  // this CTA's step index
+        if ((warp == 0 || warp == 8) && lane == 0 && si < 4) TC_CLK(0, si);
         if (tid == 0 && uses == 1 && p.ts_mode == 4) TC_STAMP(p.ts, blockIdx.x, 6);
         tc_fence_after();
         mbar_wait(&wbar[cs_slot], (wphase >> cs_slot) & 1u);
         wphase ^= 1u << cs_slot;
+        if ((warp == 0 || warp == 8) && lane == 0 && si < 4) TC_CLK(0, 4 + si);
         if (tid == 0 && uses == 0 && p.ts_mode == 0) TC_STAMP(p.ts, blockIdx.x, 2);
         if (tid == 0 && uses < 6 && p.ts_mode == 2) TC_STAMP(p.ts, blockIdx.x, uses + 1);
         // slot layout (TMA box {16 words, 16 rows, planes}): [plane][row][16 words]; thread
@@ -371,6 +384,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&afull[bi]);
+        if ((warp == 0 || warp == 8) && lane == 0 && j - a < 4) TC_CLK(1, j - a);
         if (tid == 0 && uses == 0 && p.ts_mode == 0) TC_STAMP(p.ts, blockIdx.x, 3);
         if (tid == 0 && uses < 6 && p.ts_mode == 3) TC_STAMP(p.ts, blockIdx.x, uses + 1);
         ++uses;
@@ -395,6 +409,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         mbar_wait(&dfull, segs & 1u);
         tc_fence_after();
+        if (tid == 0 && segs == 0) TC_CLK(3, 1);
         if (tid == 0 && segs == 0 && p.ts_mode == 0) TC_STAMP(p.ts, blockIdx.x, 6);
         const uint32_t dcol = tmem + my_lane_addr + kColD;
         const uint32_t rsw = tmem_ld_32x32b_x1(dcol + p.rows_x);
@@ -462,6 +477,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (!seg_open && segs > 0) mbar_wait(&dempty, (segs - 1) & 1u);  // epilogue read D
         tc_fence_after();
         const uint32_t bstage = sbase + st * b_stage_bytes(p.n_mma);
+        if (i < 4) TC_CLK(1, 4 + i);
         if (i < 3 && p.ts_mode == 4) TC_STAMP(p.ts, blockIdx.x, 2 * i + 1);
 #pragma unroll
         for (uint32_t k = 0; k < ((kDevAblate && (p.ablate & 1u)) ? 1u : kStepBytes / 32); ++k) {
@@ -469,6 +485,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           mma_i8_ts(tmem + kColD, tmem + ab * kAcols + k * 8u, bdesc, idesc, (seg_open || k > 0) ? 1u : 0u);
         }
         seg_open = true;
+        if (i < 4) TC_CLK(2, i);
         if (i < 2 && p.ts_mode == 4) TC_STAMP(p.ts, blockIdx.x, 2 * i + 2);
         if (i == 0 && p.ts_mode == 0) TC_STAMP(p.ts, blockIdx.x, 4);
         if (i + 1 == n_steps && p.ts_mode == 0) TC_STAMP(p.ts, blockIdx.x, 5);
@@ -484,6 +501,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (i >= 1 && i + bst - 1 < n_steps) {
           const uint32_t pst = (i - 1) % bst;
           mbar_wait(&bempty[pst], ((i - 1) / bst) & 1u);
+          if (i < 4) TC_CLK(2, 4 + i);
           load_b(i + bst - 1);
         }
       }
