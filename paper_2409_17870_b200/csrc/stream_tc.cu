@@ -90,7 +90,17 @@ constexpr uint32_t kPrepThreads = 256;
 __host__ __device__ constexpr uint32_t n_mma_of(uint32_t rows_x) {
   return rows_x + 1 <= 16 ? 16u : (rows_x + 1 + 15) / 16 * 16;  // + the all-ones token row
 }
-__host__ __device__ constexpr uint32_t wslot_bytes(int n) { return kItemRows * kRowBytes * static_cast<uint32_t>(n); }
+#ifndef APMM_TC_SHAREDW_AB
+constexpr bool kSharedW = false;
+#else
+constexpr bool kSharedW = APMM_TC_SHAREDW_AB != 0;  // A/B builds only
+#endif
+// kSharedW: one TMA box per step {16 words, 128 rows, n_w planes} shared by the 8 warps that fill
+// the step's A buffer (the whole step's weights arrive together) instead of one 16-row box per
+// warp (the MMA waits for the latest of 8 independent arrivals)
+__host__ __device__ constexpr uint32_t wslot_bytes(int n) {
+  return (kSharedW ? kTileRows : kItemRows) * kRowBytes * static_cast<uint32_t>(n);
+}
 __host__ __device__ constexpr uint32_t b_stage_bytes(uint32_t n_mma) { return n_mma * kStepBytes; }
 
 struct TcParams {
@@ -237,6 +247,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                      const __grid_constant__ CUtensorMap tm_y, const TcParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t wfull[kTfWarps * kMaxWst];
+  __shared__ __align__(8) uint64_t wempty[kGroups * 4];  // kSharedW: the set's warps are done
   __shared__ __align__(8) uint64_t bfull[kBStages], bempty[kBStages];
   __shared__ __align__(8) uint64_t afull[kBufs], aempty[kBufs], dfull, dempty;
   __shared__ uint32_t tmem_base_s;
@@ -254,6 +265,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (tid == 0) {
     for (int i = 0; i < kTfWarps * kMaxWst; ++i) mbar_init(&wfull[i], 1);
+    for (int i = 0; i < kGroups * 4; ++i) mbar_init(&wempty[i], kTfWarps / kGroups);
     for (uint32_t i = 0; i < kBStages; ++i) {
       mbar_init(&bfull[i], 1);
       mbar_init(&bempty[i], 1);
@@ -280,21 +292,26 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t q = warp & 3, h = warp >> 2;
     const uint32_t rg = 2u * q + (h & 1u), wg = h >> 1;
     const uint32_t g = lane >> 2, t = lane & 3;
-    const uint32_t wslot0 = sbase + p.w_off + warp * p.wst * wslot_bytes(N);
-    uint64_t* wbar = wfull + warp * kMaxWst;
+    // kSharedW: the set's slots (issued by the set's first warp), else this warp's own
+    const uint32_t wslot0 = sbase + p.w_off + (kSharedW ? wg : warp) * p.wst * wslot_bytes(N);
+    uint64_t* wbar = wfull + (kSharedW ? wg : warp) * kMaxWst;
+    uint64_t* webar = wempty + wg * 4;
+    const bool producer = !kSharedW || (warp & 7u) == 0u;
     const uint64_t hint = policy_evict_first();  // weights are read exactly once
     // this warp's items: steps a + wg, a + wg + kGroups, ...
     uint32_t is_j = a + wg, is_slot = 0;
     auto issue = [&]() {
-      if (is_j < b && lane == 0) {
+      if (is_j < b && lane == 0 && producer) {
         const uint32_t tile = div_small(is_j, p.inv_spt), s = is_j - tile * spt;
         mbar_arrive_expect_tx(&wbar[is_slot], wslot_bytes(N));
         tma_load_3d(wslot0 + is_slot * wslot_bytes(N), &tm_w, smem_u32(&wbar[is_slot]),
-                    int32_t(s * kStepWords), int32_t(tile * kTileRows + rg * kItemRows), 0, hint);
+                    int32_t(s * kStepWords),
+                    int32_t(tile * kTileRows + (kSharedW ? 0u : rg * kItemRows)), 0, hint);
       }
       is_j += kGroups;
       if (++is_slot == p.wst) is_slot = 0;
     };
+    uint32_t we_phase = 0;  // kSharedW: per-slot parity of wempty
     if (!p.early_w) pdl_wait();
     for (uint32_t i = 0; i < p.wst; ++i) issue();
     // The transform warps touch only the weight planes (call inputs), tensor memory and shared
@@ -326,10 +343,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         // slot layout (TMA box {16 words, 16 rows, planes}): [plane][row][16 words]; thread
         // (g, t) takes words 4t..4t+3 of rows g and g + 8 (conflict-free 16-byte reads)
         uint4 wa[N], wb[N];
-        const uint32_t rowb = wslot0 + cs_slot * wslot_bytes(N) + g * kRowBytes + t * 16u;
+        const uint32_t rowb = wslot0 + cs_slot * wslot_bytes(N) + g * kRowBytes + t * 16u +
+                              (kSharedW ? rg * kItemRows * kRowBytes : 0u);
 #pragma unroll
         for (int pl = 0; pl < N; ++pl) {
-          const uint32_t addr = rowb + pl * kItemRows * kRowBytes;
+          const uint32_t addr = rowb + pl * (kSharedW ? kTileRows : kItemRows) * kRowBytes;
           asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
                        : "=r"(wa[pl].x), "=r"(wa[pl].y), "=r"(wa[pl].z), "=r"(wa[pl].w) : "r"(addr));
           asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
@@ -337,6 +355,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                        : "r"(addr + 8u * kRowBytes));
         }
         __syncwarp();
+        if (kSharedW) {
+          if (lane == 0) mbar_arrive(&webar[cs_slot]);
+          if (producer && is_j < b) {  // every warp of the set has read the slot: refill it
+            mbar_wait(&webar[cs_slot], (we_phase >> cs_slot) & 1u);
+          }
+          we_phase ^= 1u << cs_slot;
+          __syncwarp();
+        }
         if (++cs_slot == p.wst) cs_slot = 0;
         issue();  // the slot is free again: the item after next of this warp
         // tcgen05.st.16x256b: register 4jj + e of thread (g, t) -> lane g + 8 (e >> 1), column
@@ -603,7 +629,7 @@ Layout layout_of(uint64_t rows_x, int n_w, uint32_t wst_cap = kMaxWst) {
     l.w_off = bst * b_stage_bytes(l.n_mma);
     for (uint32_t wst = wst_cap; wst >= 1; --wst) {
       l.wst = wst;
-      l.st_off = l.w_off + kTfWarps * wst * wslot_bytes(n_w);
+      l.st_off = l.w_off + (kSharedW ? kGroups : kTfWarps) * wst * wslot_bytes(n_w);
       l.smem = l.st_off + kEpiWarps * kStageBytes + 1024u;  // + alignment slack
       if (l.smem <= kSmemCap) return l;
     }
@@ -696,7 +722,7 @@ cudaError_t launch_stream_tc(const StreamTcArgs& a, cudaStream_t s) {
   {
     const uint64_t dims[3] = {wpr, a.rows_w, static_cast<uint64_t>(a.n_w)};
     const uint64_t strides[2] = {uint64_t(wpr) * 4, uint64_t(wpr) * 4 * a.rows_w};
-    const uint32_t box[3] = {kStepWords, kItemRows, static_cast<uint32_t>(a.n_w)};
+    const uint32_t box[3] = {kStepWords, kSharedW ? kTileRows : kItemRows, static_cast<uint32_t>(a.n_w)};
     if (encode_tmap_3d_u32(&tw, a.w_planes, dims, strides, box) != CUDA_SUCCESS) {
       return cudaErrorInvalidValue;
     }
