@@ -522,8 +522,10 @@ def test_dequant_epilogue(gpu, oracle):
     north-star tolerance 1e-3 relative; the device does the same fp64 ops, so it is exact."""
     ap, ctx = gpu
     rng = np.random.default_rng(11)
+    # (n = 8 and 16 feature rows take K5's popcount-rowsum variant)
     for (m, n, k, nw, nx, gw, gx) in [(1, 1, 2, 2, 2, 0, 0), (64, 48, 300, 2, 4, 1, 1),
-                                      (300, 257, 1000, 3, 8, 1, 0), (129, 1, 4096, 4, 8, 0, 1)]:
+                                      (300, 257, 1000, 3, 8, 1, 0), (129, 1, 4096, 4, 8, 0, 1),
+                                      (500, 8, 4096, 3, 8, 1, 1), (257, 16, 2048, 2, 4, 0, 1)]:
         wv, xv = rng.uniform(-1, 1, (m, k)), rng.uniform(-1, 1, (n, k))
         wc, ws = oracle.quantize(wv, nw, gw)
         xc, xs = oracle.quantize(xv, nx, gx)
