@@ -90,17 +90,13 @@ constexpr uint32_t kPrepThreads = 256;
 __host__ __device__ constexpr uint32_t n_mma_of(uint32_t rows_x) {
   return rows_x + 1 <= 16 ? 16u : (rows_x + 1 + 15) / 16 * 16;  // + the all-ones token row
 }
-#ifndef APMM_TC_SHAREDW_AB
-constexpr bool kSharedW = false;
-#else
-constexpr bool kSharedW = APMM_TC_SHAREDW_AB != 0;  // A/B builds only
-#endif
-// kSharedW: one TMA box per step {16 words, 128 rows, n_w planes} shared by the 8 warps that fill
-// the step's A buffer (the whole step's weights arrive together) instead of one 16-row box per
-// warp (the MMA waits for the latest of 8 independent arrivals)
-__host__ __device__ constexpr uint32_t wslot_bytes(int n) {
-  return (kSharedW ? kTileRows : kItemRows) * kRowBytes * static_cast<uint32_t>(n);
-}
+// Per-warp weight item: 16 rows x 16 words x n planes (one step). PW ("pair" layout): the two
+// warps of a row group (one per step parity) share one TMA box of 16 rows x 32 words x n planes
+// covering a step pair -- 128-byte row segments instead of 64: K6's stream pattern alone runs
+// 25.2 MB in 3.9 instead of 5.9 us (scripts/k6_stream_probe.cu, profiles/r02/r2_k6_stream_probe.txt)
+__host__ __device__ constexpr uint32_t wslot_bytes(int n) { return kItemRows * kRowBytes * static_cast<uint32_t>(n); }
+__host__ __device__ constexpr uint32_t pslot_bytes(int n) { return 2u * wslot_bytes(n); }
+constexpr uint32_t kPairSlots = 2;  // pair boxes in flight per row group
 __host__ __device__ constexpr uint32_t b_stage_bytes(uint32_t n_mma) { return n_mma * kStepBytes; }
 
 struct TcParams {
@@ -241,13 +237,13 @@ APMM_DEV uint32_t tmem_ld_32x32b_x1(uint32_t taddr) {
   return v;
 }
 
-template <int N>
+template <int N, bool PW>
 __global__ void __launch_bounds__(kThreads, 1)
     stream_tc_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_x,
                      const __grid_constant__ CUtensorMap tm_y, const TcParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t wfull[kTfWarps * kMaxWst];
-  __shared__ __align__(8) uint64_t wempty[kGroups * 4];  // kSharedW: the set's warps are done
+  __shared__ __align__(8) uint64_t wempty[8 * kPairSlots];  // PW: both warps of the row group read it
   __shared__ __align__(8) uint64_t bfull[kBStages], bempty[kBStages];
   __shared__ __align__(8) uint64_t afull[kBufs], aempty[kBufs], dfull, dempty;
   __shared__ uint32_t tmem_base_s;
@@ -257,15 +253,16 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid == 0) TC_STAMP(p.ts, blockIdx.x, 0);
   if (tid == 0) TC_CLK(3, 0);
-  // this CTA's tile-steps [a, b)
-  const uint32_t a = blockIdx.x * p.q_steps + min(blockIdx.x, p.r_steps);
-  const uint32_t n_steps = p.q_steps + (blockIdx.x < p.r_steps ? 1u : 0u);
+  // this CTA's tile-steps [a, b) (PW: q / r count step pairs)
+  constexpr uint32_t unit = PW ? 2u : 1u;
+  const uint32_t a = unit * (blockIdx.x * p.q_steps + min(blockIdx.x, p.r_steps));
+  const uint32_t n_steps = unit * (p.q_steps + (blockIdx.x < p.r_steps ? 1u : 0u));
   const uint32_t b = a + n_steps;
   const uint32_t spt = p.steps_per_tile;
 
   if (tid == 0) {
     for (int i = 0; i < kTfWarps * kMaxWst; ++i) mbar_init(&wfull[i], 1);
-    for (int i = 0; i < kGroups * 4; ++i) mbar_init(&wempty[i], kTfWarps / kGroups);
+    for (uint32_t i = 0; i < 8 * kPairSlots; ++i) mbar_init(&wempty[i], 2);
     for (uint32_t i = 0; i < kBStages; ++i) {
       mbar_init(&bfull[i], 1);
       mbar_init(&bempty[i], 1);
@@ -292,28 +289,42 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t q = warp & 3, h = warp >> 2;
     const uint32_t rg = 2u * q + (h & 1u), wg = h >> 1;
     const uint32_t g = lane >> 2, t = lane & 3;
-    // kSharedW: the set's slots (issued by the set's first warp), else this warp's own
-    const uint32_t wslot0 = sbase + p.w_off + (kSharedW ? wg : warp) * p.wst * wslot_bytes(N);
-    uint64_t* wbar = wfull + (kSharedW ? wg : warp) * kMaxWst;
-    uint64_t* webar = wempty + wg * 4;
-    const bool producer = !kSharedW || (warp & 7u) == 0u;
+    // PW: the row group's pair slots (issued by its even-step warp), else this warp's own ring
+    const uint32_t wslot0 = sbase + p.w_off + (PW ? rg * kPairSlots * pslot_bytes(N) : warp * p.wst * wslot_bytes(N));
+    uint64_t* wbar = wfull + (PW ? rg * kPairSlots : warp * kMaxWst);
+    uint64_t* webar = wempty + rg * kPairSlots;
+    const bool producer = !PW || wg == 0u;
     const uint64_t hint = policy_evict_first();  // weights are read exactly once
     // this warp's items: steps a + wg, a + wg + kGroups, ...
     uint32_t is_j = a + wg, is_slot = 0;
     auto issue = [&]() {
-      if (is_j < b && lane == 0 && producer) {
+      if (PW) return;
+      if (is_j < b && lane == 0) {
         const uint32_t tile = div_small(is_j, p.inv_spt), s = is_j - tile * spt;
         mbar_arrive_expect_tx(&wbar[is_slot], wslot_bytes(N));
         tma_load_3d(wslot0 + is_slot * wslot_bytes(N), &tm_w, smem_u32(&wbar[is_slot]),
-                    int32_t(s * kStepWords),
-                    int32_t(tile * kTileRows + (kSharedW ? 0u : rg * kItemRows)), 0, hint);
+                    int32_t(s * kStepWords), int32_t(tile * kTileRows + rg * kItemRows), 0, hint);
       }
       is_j += kGroups;
       if (++is_slot == p.wst) is_slot = 0;
     };
-    uint32_t we_phase = 0;  // kSharedW: per-slot parity of wempty
+    // PW: pair k = CTA steps (2k, 2k + 1), one box {32 words, 16 rows, n} into slot k % 2
+    auto issue_pair = [&](uint32_t k) {
+      if (PW && producer && lane == 0 && 2u * k < n_steps) {
+        const uint32_t j = a + 2u * k;
+        const uint32_t tile = div_small(j, p.inv_spt), s = j - tile * spt;
+        const uint32_t sl = k % kPairSlots;
+        mbar_arrive_expect_tx(&wbar[sl], pslot_bytes(N));
+        tma_load_3d(wslot0 + sl * pslot_bytes(N), &tm_w, smem_u32(&wbar[sl]),
+                    int32_t(s * kStepWords), int32_t(tile * kTileRows + rg * kItemRows), 0, hint);
+      }
+    };
     if (!p.early_w) pdl_wait();
-    for (uint32_t i = 0; i < p.wst; ++i) issue();
+    if (PW) {
+      for (uint32_t k = 0; k < kPairSlots; ++k) issue_pair(k);
+    } else {
+      for (uint32_t i = 0; i < p.wst; ++i) issue();
+    }
     // The transform warps touch only the weight planes (call inputs), tensor memory and shared
     // memory until their first epilogue: they expand the first steps while the feature prep
     // still runs; griddepcontrol.wait (features' rowsum, Y) comes at the first segment end.
@@ -335,36 +346,46 @@ __global__ void __launch_bounds__(kThreads, 1)
         if ((warp == 0 || warp == 8) && lane == 0 && si < 4) TC_CLK(0, si);
         if (tid == 0 && uses == 1 && p.ts_mode == 4) TC_STAMP(p.ts, blockIdx.x, 6);
         tc_fence_after();
-        mbar_wait(&wbar[cs_slot], (wphase >> cs_slot) & 1u);
-        wphase ^= 1u << cs_slot;
+        const uint32_t pk = si >> 1;  // PW: this step's pair
+        if (PW) {
+          mbar_wait(&wbar[pk % kPairSlots], (pk / kPairSlots) & 1u);
+        } else {
+          mbar_wait(&wbar[cs_slot], (wphase >> cs_slot) & 1u);
+          wphase ^= 1u << cs_slot;
+        }
         if ((warp == 0 || warp == 8) && lane == 0 && si < 4) TC_CLK(0, 4 + si);
         if (tid == 0 && uses == 0 && p.ts_mode == 0) TC_STAMP(p.ts, blockIdx.x, 2);
         if (tid == 0 && uses < 6 && p.ts_mode == 2) TC_STAMP(p.ts, blockIdx.x, uses + 1);
         // slot layout (TMA box {16 words, 16 rows, planes}): [plane][row][16 words]; thread
         // (g, t) takes words 4t..4t+3 of rows g and g + 8 (conflict-free 16-byte reads)
         uint4 wa[N], wb[N];
-        const uint32_t rowb = wslot0 + cs_slot * wslot_bytes(N) + g * kRowBytes + t * 16u +
-                              (kSharedW ? rg * kItemRows * kRowBytes : 0u);
+        // PW slot: [plane][16 rows][32 words] (128-byte rows), this warp's half = its step's
+        // 16 words; else [plane][16 rows][16 words]
+        constexpr uint32_t rbytes = PW ? 2u * kRowBytes : kRowBytes;
+        const uint32_t rowb = (PW ? wslot0 + (pk % kPairSlots) * pslot_bytes(N) + wg * kRowBytes
+                                  : wslot0 + cs_slot * wslot_bytes(N)) + g * rbytes + t * 16u;
 #pragma unroll
         for (int pl = 0; pl < N; ++pl) {
-          const uint32_t addr = rowb + pl * (kSharedW ? kTileRows : kItemRows) * kRowBytes;
+          const uint32_t addr = rowb + pl * kItemRows * rbytes;
           asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
                        : "=r"(wa[pl].x), "=r"(wa[pl].y), "=r"(wa[pl].z), "=r"(wa[pl].w) : "r"(addr));
           asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
                        : "=r"(wb[pl].x), "=r"(wb[pl].y), "=r"(wb[pl].z), "=r"(wb[pl].w)
-                       : "r"(addr + 8u * kRowBytes));
+                       : "r"(addr + 8u * rbytes));
         }
         __syncwarp();
-        if (kSharedW) {
-          if (lane == 0) mbar_arrive(&webar[cs_slot]);
-          if (producer && is_j < b) {  // every warp of the set has read the slot: refill it
-            mbar_wait(&webar[cs_slot], (we_phase >> cs_slot) & 1u);
+        if (PW) {
+          if (lane == 0) mbar_arrive(&webar[pk % kPairSlots]);
+          // the even-step warp refills the previous pair's slot (both halves read) with pair pk + 1
+          if (producer && pk >= 1) {
+            if (lane == 0) mbar_wait(&webar[(pk - 1) % kPairSlots], ((pk - 1) / kPairSlots) & 1u);
+            issue_pair(pk + 1);
           }
-          we_phase ^= 1u << cs_slot;
           __syncwarp();
+        } else {
+          if (++cs_slot == p.wst) cs_slot = 0;
+          issue();  // the slot is free again: the item after next of this warp
         }
-        if (++cs_slot == p.wst) cs_slot = 0;
-        issue();  // the slot is free again: the item after next of this warp
         // tcgen05.st.16x256b: register 4jj + e of thread (g, t) -> lane g + 8 (e >> 1), column
         // 8jj + 2t + (e & 1) (profiles/r02/r2_tmem_layout.txt). Word 4t + w of the step, code
         // register r -> column 32 w + 8 (r >> 1) + 2t + (r & 1): the feature prep writes X in the
@@ -620,30 +641,40 @@ __global__ void __launch_bounds__(kPrepThreads) stream_tc_prep_kernel(
 
 struct Layout {
   uint32_t n_mma, wst, bst, w_off, st_off, smem;
+  bool pw;  // pair-box weight layout
 };
-Layout layout_of(uint64_t rows_x, int n_w, uint32_t wst_cap = kMaxWst) {
+// The pair-box layout (two step boxes in flight per row group) where shared memory allows it,
+// else one 16-row box per warp.
+Layout layout_of(uint64_t rows_x, int n_w, uint32_t wst_cap = kMaxWst, bool allow_pw = true) {
   Layout l{};
   l.n_mma = n_mma_of(static_cast<uint32_t>(rows_x));
-  for (uint32_t bst = kBStages; bst >= 2; --bst) {
-    l.bst = bst;
-    l.w_off = bst * b_stage_bytes(l.n_mma);
-    for (uint32_t wst = wst_cap; wst >= 1; --wst) {
-      l.wst = wst;
-      l.st_off = l.w_off + (kSharedW ? kGroups : kTfWarps) * wst * wslot_bytes(n_w);
-      l.smem = l.st_off + kEpiWarps * kStageBytes + 1024u;  // + alignment slack
-      if (l.smem <= kSmemCap) return l;
+  for (int pw = allow_pw ? 1 : 0; pw >= 0; --pw) {
+    l.pw = pw != 0;
+    for (uint32_t bst = kBStages; bst >= 2; --bst) {
+      l.bst = bst;
+      l.w_off = bst * b_stage_bytes(l.n_mma);
+      for (uint32_t wst = pw ? 1u : wst_cap; wst >= 1; --wst) {
+        l.wst = wst;
+        l.st_off = l.w_off + (pw ? 8u * kPairSlots * pslot_bytes(n_w) : kTfWarps * wst * wslot_bytes(n_w));
+        l.smem = l.st_off + kEpiWarps * kStageBytes + 1024u;  // + alignment slack
+        if (l.smem <= kSmemCap) return l;
+      }
     }
   }
   l.smem = 0;
   return l;
 }
-uint32_t kwords_of(uint64_t k) { return static_cast<uint32_t>((k + kStepBytes - 1) / kStepBytes * kStepWords); }
+// feature code words: whole steps, whole step pairs for the pair layout
+uint32_t kwords_of(uint64_t k, bool pw = true) {
+  const uint64_t unit = (pw ? 2u : 1u) * kStepBytes;
+  return static_cast<uint32_t>((k + unit - 1) / unit * (unit / 32u));
+}
 uint32_t prep_blocks_of(uint64_t k) { return (kwords_of(k) + kPrepThreads - 1) / kPrepThreads; }
 
-template <int N>
+template <int N, bool PW>
 cudaError_t launch_n(const CUtensorMap& tw, const CUtensorMap& tx, const CUtensorMap& ty, const TcParams& p,
                      unsigned grid, uint32_t smem, cudaStream_t s) {
-  auto kern = stream_tc_kernel<N>;
+  auto kern = stream_tc_kernel<N, PW>;
   static DeviceBits attr_set;
   const int dev = current_device();
   if (!attr_set.test(dev)) {
@@ -688,13 +719,22 @@ cudaError_t launch_stream_tc(const StreamTcArgs& a, cudaStream_t s) {
     const char* e = APMM_DEV_ENV("APMM_TC_WST");
     return e ? static_cast<uint32_t>(std::atoi(e)) : kMaxWst;
   }();
-  const Layout l = layout_of(a.rows_x, a.n_w, wst_cap);
+  static const bool allow_pw = APMM_DEV_ENV("APMM_TC_NOPAIR") == nullptr;  // dev A/B
+  Layout l = layout_of(a.rows_x, a.n_w, wst_cap, allow_pw);
   if (!l.smem) return cudaErrorInvalidConfiguration;
   const uint32_t wpr = static_cast<uint32_t>((a.k + 31) / 32);
-  const uint32_t kwords = kwords_of(a.k);
+  if (l.pw) {
+    // stream-K over step pairs is coarser: keep the pair layout only where it does not lengthen
+    // the busiest CTA's step count (11008 x 16 x 4096: 6 steps vs 5 measured 12% slower)
+    const uint64_t tl = (a.rows_w + kTileRows - 1) / kTileRows, sms = static_cast<uint64_t>(a.num_sms);
+    const uint64_t n1 = tl * (kwords_of(a.k, false) / kStepWords), n2 = tl * (kwords_of(a.k, true) / kStepWords) / 2;
+    const uint64_t max1 = (n1 + sms - 1) / sms, max2 = 2 * ((n2 + sms - 1) / sms);
+    if (max2 > max1) l = layout_of(a.rows_x, a.n_w, wst_cap, false);
+  }
+  const uint32_t kwords = kwords_of(a.k, l.pw);
   const uint32_t spt = kwords / kStepWords;
   const uint32_t tiles = static_cast<uint32_t>((a.rows_w + kTileRows - 1) / kTileRows);
-  const uint32_t total = tiles * spt;
+  const uint32_t total = tiles * spt / (l.pw ? 2u : 1u);  // work units: steps or step pairs
   const uint32_t grid = total < static_cast<uint32_t>(a.num_sms) ? total : static_cast<uint32_t>(a.num_sms);
   uint8_t* codes = static_cast<uint8_t*>(a.ws);
   int32_t* rsx_part = reinterpret_cast<int32_t*>(codes + round_up(uint64_t(l.n_mma) * kwords * 32u, 256));
@@ -722,7 +762,7 @@ cudaError_t launch_stream_tc(const StreamTcArgs& a, cudaStream_t s) {
   {
     const uint64_t dims[3] = {wpr, a.rows_w, static_cast<uint64_t>(a.n_w)};
     const uint64_t strides[2] = {uint64_t(wpr) * 4, uint64_t(wpr) * 4 * a.rows_w};
-    const uint32_t box[3] = {kStepWords, kSharedW ? kTileRows : kItemRows, static_cast<uint32_t>(a.n_w)};
+    const uint32_t box[3] = {(l.pw ? 2u : 1u) * kStepWords, kItemRows, static_cast<uint32_t>(a.n_w)};
     if (encode_tmap_3d_u32(&tw, a.w_planes, dims, strides, box) != CUDA_SUCCESS) {
       return cudaErrorInvalidValue;
     }
@@ -768,10 +808,10 @@ cudaError_t launch_stream_tc(const StreamTcArgs& a, cudaStream_t s) {
   if (a.ev_start) cudaEventRecordWithFlags(a.ev_start, s, a.ev_flags);
   cudaError_t e;
   switch (a.n_w) {
-    case 1: e = launch_n<1>(tw, tx, ty, p, grid, l.smem, s); break;
-    case 2: e = launch_n<2>(tw, tx, ty, p, grid, l.smem, s); break;
-    case 3: e = launch_n<3>(tw, tx, ty, p, grid, l.smem, s); break;
-    default: e = launch_n<4>(tw, tx, ty, p, grid, l.smem, s); break;
+    case 1: e = l.pw ? launch_n<1, true>(tw, tx, ty, p, grid, l.smem, s) : launch_n<1, false>(tw, tx, ty, p, grid, l.smem, s); break;
+    case 2: e = l.pw ? launch_n<2, true>(tw, tx, ty, p, grid, l.smem, s) : launch_n<2, false>(tw, tx, ty, p, grid, l.smem, s); break;
+    case 3: e = l.pw ? launch_n<3, true>(tw, tx, ty, p, grid, l.smem, s) : launch_n<3, false>(tw, tx, ty, p, grid, l.smem, s); break;
+    default: e = l.pw ? launch_n<4, true>(tw, tx, ty, p, grid, l.smem, s) : launch_n<4, false>(tw, tx, ty, p, grid, l.smem, s); break;
   }
   if (a.ev_stop) cudaEventRecordWithFlags(a.ev_stop, s, a.ev_flags);
   return e;
