@@ -274,11 +274,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_init(&dfull, 1);
     mbar_init(&dempty, kTfWarps);
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    TC_CLK(3, 2);
   }
   if (warp == kMmaWarp) tmem_alloc<kTmemCols>(&tmem_base_s);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  if (tid == 0) TC_CLK(3, 3);
   const uint32_t tmem = tmem_base_s;
   const uint32_t sbase = smem_u32(smem);
 
@@ -325,6 +327,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     } else {
       for (uint32_t i = 0; i < p.wst; ++i) issue();
     }
+    if (tid == 0) TC_CLK(3, 4);
     // The transform warps touch only the weight planes (call inputs), tensor memory and shared
     // memory until their first epilogue: they expand the first steps while the feature prep
     // still runs; griddepcontrol.wait (features' rowsum, Y) comes at the first segment end.

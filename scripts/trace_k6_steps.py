@@ -54,7 +54,9 @@ for si in range(slots):
     ok = start > 0
     if not ok.any():
         continue
-    print(f" slot {si}: CTAs {grid}, first dfull {int(np.median(tt[768:768 + grid, 1][ok] - start[ok]))}")
+    pro = [int(np.median(tt[768:768 + grid, c][ok] - start[ok])) for c in (2, 3, 4, 1)]
+    print(f" slot {si}: CTAs {grid}, barriers init {pro[0]}, TMEM alloc + sync {pro[1]}, "
+          f"first W issued {pro[2]}, first dfull {pro[3]}")
     for nm, pg, k0 in names:
         vals = []
         for st in range(4):
