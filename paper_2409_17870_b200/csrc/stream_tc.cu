@@ -116,6 +116,7 @@ struct TcParams {
   uint32_t ts_mode;           // dev: 0 phases, 1 MMA warp: step i ready (slot i + 1), 2 warp 0:
                               // its item u landed (slot u + 1), 3 warp 0: item u stored
   uint32_t ablate;            // dev only (APMM_TC_ABLATE, results wrong): 1 no MMAs, 2 no transposes
+  uint32_t nd, dstride;       // D accumulators (1 or 2, alternating per segment), columns apart
 };
 
 #ifdef APMM_DEVTOOLS
@@ -245,7 +246,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __shared__ __align__(8) uint64_t wfull[kTfWarps * kMaxWst];
   __shared__ __align__(8) uint64_t wempty[8 * kPairSlots];  // PW: both warps of the row group read it
   __shared__ __align__(8) uint64_t bfull[kBStages], bempty[kBStages];
-  __shared__ __align__(8) uint64_t afull[kBufs], aempty[kBufs], dfull, dempty;
+  __shared__ __align__(8) uint64_t afull[kBufs], aempty[kBufs], dfull[2], dempty[2];
   __shared__ uint32_t tmem_base_s;
   __shared__ int32_t rsx_s[kMaxRowsX];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -271,8 +272,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&afull[i], kTfWarps / kGroups);  // one arrive per warp filling the buffer
       mbar_init(&aempty[i], 1);
     }
-    mbar_init(&dfull, 1);
-    mbar_init(&dempty, kTfWarps);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&dfull[i], 1);
+      mbar_init(&dempty[i], kTfWarps);
+    }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     TC_CLK(3, 2);
   }
@@ -339,6 +342,62 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t cs_slot = 0, wphase = 0, uses = 0, segs = 0;
     uint32_t bi = 0, ui = 0;  // step j - a = 3 ui + bi: A buffer bi, its use ui
     uint32_t seg_first_s = 0;  // K step at which the current segment started
+    // ---------------- segment epilogue: partial tile -> reduce-add into Y ----------------
+    // first: the segment holds K step 0 (X term + constant)
+    uint32_t pend_tile = ~0u;
+    bool pend_first = false;
+    auto epilogue = [&](uint32_t tile, bool first) {
+      if (segs == 0) {
+        pdl_wait();  // rowsum(U_x) parts and Y only after the prep launch completed
+        if (tid == 0 && p.ts_mode == 0) TC_STAMP(p.ts, blockIdx.x, 1);
+        if (warp == 0) {
+          for (uint32_t c = lane; c < p.rows_x; c += 32) {
+            int32_t sum = 0;
+            for (uint32_t i = 0; i < p.parts; ++i) sum += __ldg(p.rsx_part + c * p.parts + i);
+            rsx_s[c] = sum;
+          }
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(kTfWarps * 32));  // rsx_s visible to the transform warps
+      }
+      const uint32_t db = p.nd == 2 ? (segs & 1u) : 0u;  // this segment's D buffer
+      mbar_wait(&dfull[db], (p.nd == 2 ? segs >> 1 : segs) & 1u);
+      tc_fence_after();
+      if (tid == 0 && segs == 0) TC_CLK(3, 1);
+      if (tid == 0 && segs == 0 && p.ts_mode == 0) TC_STAMP(p.ts, blockIdx.x, 6);
+      const uint32_t dcol = tmem + my_lane_addr + kColD + db * p.dstride;
+      const uint32_t rsw = tmem_ld_32x32b_x1(dcol + p.rows_x);
+      tmem_ld_wait();
+      const uint32_t chunks = (p.rows_x + 31) / 32;
+      for (uint32_t cc = h; cc < chunks && warp < kEpiWarps; cc += 2) {
+        uint32_t d[32];
+        tmem_ld_32x32b_x32(dcol + cc * 32u, d);
+        tmem_ld_wait();
+        if (lane == 0) bulk_wait_read<0>();  // the staging buffer's previous reduce-add read it
+        __syncwarp();
+  #pragma unroll
+        for (int c4 = 0; c4 < 8; ++c4) {
+          uint32_t v[4];
+  #pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const uint32_t col = cc * 32u + c4 * 4u + e;
+            uint32_t t = 4u * d[c4 * 4 + e] - p.coef_w * rsw;
+            if (first && col < p.rows_x) t += p.c0 - p.coef_x * static_cast<uint32_t>(rsx_s[col]);
+            v[e] = t;
+          }
+          st_shared_v4(smem_u32(stage) + lane * 128u + ((c4 ^ (lane & 7u)) << 4), v[0], v[1], v[2], v[3]);
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          tma_reduce_add_2d(&tm_y, stage, int32_t(cc * 32u), int32_t(tile * kTileRows + q * 32u));
+          bulk_commit();
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&dempty[db]);
+      ++segs;
+    };
     for (uint32_t j = a; j < b; ++j) {
       const uint32_t tile = div_small(j, p.inv_spt), s = j - tile * spt;
       if (j == a || s == 0) seg_first_s = s;
@@ -444,59 +503,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         ++ui;
       }
       if (s + 1 == spt || j + 1 == b) {
-        // ---------------- segment end: partial tile -> reduce-add into Y ----------------
-        if (segs == 0) {
-          pdl_wait();  // rowsum(U_x) parts and Y only after the prep launch completed
-          if (tid == 0 && p.ts_mode == 0) TC_STAMP(p.ts, blockIdx.x, 1);
-          if (warp == 0) {
-            for (uint32_t c = lane; c < p.rows_x; c += 32) {
-              int32_t sum = 0;
-              for (uint32_t i = 0; i < p.parts; ++i) sum += __ldg(p.rsx_part + c * p.parts + i);
-              rsx_s[c] = sum;
-            }
-          }
-          asm volatile("bar.sync 1, %0;" ::"n"(kTfWarps * 32));  // rsx_s visible to the transform warps
+        // segment end: with two D buffers the epilogue of a segment runs at the end of the
+        // next one (its MMAs drain meanwhile and the transform warps go on to the next
+        // segment's steps), else at once
+        if (p.nd == 2) {
+          if (pend_tile != ~0u) epilogue(pend_tile, pend_first);
+          pend_tile = tile;
+          pend_first = seg_first_s == 0;
+        } else {
+          epilogue(tile, seg_first_s == 0);
         }
-        mbar_wait(&dfull, segs & 1u);
-        tc_fence_after();
-        if (tid == 0 && segs == 0) TC_CLK(3, 1);
-        if (tid == 0 && segs == 0 && p.ts_mode == 0) TC_STAMP(p.ts, blockIdx.x, 6);
-        const uint32_t dcol = tmem + my_lane_addr + kColD;
-        const uint32_t rsw = tmem_ld_32x32b_x1(dcol + p.rows_x);
-        tmem_ld_wait();
-        const bool first = seg_first_s == 0;  // this segment holds K step 0: X term + constant
-        const uint32_t chunks = (p.rows_x + 31) / 32;
-        for (uint32_t cc = h; cc < chunks && warp < kEpiWarps; cc += 2) {
-          uint32_t d[32];
-          tmem_ld_32x32b_x32(dcol + cc * 32u, d);
-          tmem_ld_wait();
-          if (lane == 0) bulk_wait_read<0>();  // the staging buffer's previous reduce-add read it
-          __syncwarp();
-#pragma unroll
-          for (int c4 = 0; c4 < 8; ++c4) {
-            uint32_t v[4];
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const uint32_t col = cc * 32u + c4 * 4u + e;
-              uint32_t t = 4u * d[c4 * 4 + e] - p.coef_w * rsw;
-              if (first && col < p.rows_x) t += p.c0 - p.coef_x * static_cast<uint32_t>(rsx_s[col]);
-              v[e] = t;
-            }
-            st_shared_v4(smem_u32(stage) + lane * 128u + ((c4 ^ (lane & 7u)) << 4), v[0], v[1], v[2], v[3]);
-          }
-          fence_proxy_async_smem();
-          __syncwarp();
-          if (lane == 0) {
-            tma_reduce_add_2d(&tm_y, stage, int32_t(cc * 32u), int32_t(tile * kTileRows + q * 32u));
-            bulk_commit();
-          }
-        }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&dempty);
-        ++segs;
       }
     }
+    if (pend_tile != ~0u) epilogue(pend_tile, pend_first);
     if (lane == 0) bulk_wait<0>();
   } else {
     // ---------------- MMA warp: feature tiles + tcgen05.mma ----------------
@@ -524,7 +543,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t st = i % bst;
         mbar_wait(&bfull[st], (i / bst) & 1u);
         mbar_wait(&afull[ab], (i / kBufs) & 1u);
-        if (!seg_open && segs > 0) mbar_wait(&dempty, (segs - 1) & 1u);  // epilogue read D
+        const uint32_t db = p.nd == 2 ? (segs & 1u) : 0u, ds = p.nd == 2 ? segs >> 1 : segs;
+        if (!seg_open && ds > 0) mbar_wait(&dempty[db], (ds - 1) & 1u);  // epilogue read this D
         tc_fence_after();
         const uint32_t bstage = sbase + st * b_stage_bytes(p.n_mma);
         if (i < 4) TC_CLK(1, 4 + i);
@@ -532,7 +552,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (uint32_t k = 0; k < ((kDevAblate && (p.ablate & 1u)) ? 1u : kStepBytes / 32); ++k) {
           const uint64_t bdesc = umma_desc_sw128(bstage + (k >> 2) * p.n_mma * 128u + (k & 3u) * 32u);
-          mma_i8_ts(tmem + kColD, tmem + ab * kAcols + k * 8u, bdesc, idesc, (seg_open || k > 0) ? 1u : 0u);
+          mma_i8_ts(tmem + kColD + db * p.dstride, tmem + ab * kAcols + k * 8u, bdesc, idesc, (seg_open || k > 0) ? 1u : 0u);
         }
         seg_open = true;
         if (i < 4) TC_CLK(2, i);
@@ -543,7 +563,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         mma_commit(&aempty[ab]);
         mma_commit(&bempty[st]);
         if (s + 1 == spt || j + 1 == b) {
-          mma_commit(&dfull);
+          mma_commit(&dfull[db]);
           seg_open = false;
           ++segs;
         }
@@ -798,6 +818,12 @@ cudaError_t launch_stream_tc(const StreamTcArgs& a, cudaStream_t s) {
   p.c0 = static_cast<uint32_t>(a.k) * A * B;
   p.early_w = a.early_w ? 1u : 0u;
   p.ts = a.trace;
+  // two D accumulators where tensor memory holds them (A buffers at 0..255): the epilogue of a
+  // segment then overlaps the next segment's MMAs
+  static const bool nd1 = APMM_DEV_ENV("APMM_TC_ND1") != nullptr;  // dev A/B
+  p.dstride = (l.n_mma + 31u) / 32u * 32u;
+  const uint32_t dread = ((static_cast<uint32_t>(a.rows_x) + 31u) / 32u) * 32u;
+  p.nd = !nd1 && kColD + p.dstride + (dread > l.n_mma ? dread : l.n_mma) <= kTmemCols ? 2u : 1u;
   static const uint32_t ts_mode = [] {
     const char* e = APMM_DEV_ENV("APMM_TC_TS_MODE");
     return e ? static_cast<uint32_t>(std::atoi(e)) : 0u;
