@@ -338,6 +338,7 @@ __global__ void __launch_bounds__(sk_threads(N, NT), sk_ctas_per_sm(N, NT))
   const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t g = lane >> 2, t = lane & 3;
   SK_STAMP(0);
+  if (tid == 0) apmm_ptx::tma_prefetch_desc(&tmap_w);  // the descriptor fetch off every warp's first load
   const uint32_t warps_k = 1u << p.log2_wk;
   const uint32_t wr = warp >> p.log2_wk, wk = warp & (warps_k - 1u);
   const uint32_t tile_rows = (WARPS >> p.log2_wk) * 16u;

@@ -254,6 +254,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid == 0) TC_STAMP(p.ts, blockIdx.x, 0);
   if (tid == 0) TC_CLK(3, 0);
+  if (tid == 32) {  // descriptor fetches off the first loads (warp 0 initialises the barriers)
+    tma_prefetch_desc(&tm_w);
+    tma_prefetch_desc(&tm_x);
+    tma_prefetch_desc(&tm_y);
+  }
   // this CTA's tile-steps [a, b) (PW: q / r count step pairs)
   constexpr uint32_t unit = PW ? 2u : 1u;
   const uint32_t a = unit * (blockIdx.x * p.q_steps + min(blockIdx.x, p.r_steps));
