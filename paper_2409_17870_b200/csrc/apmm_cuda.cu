@@ -403,7 +403,8 @@ int run_matmul(apmm_ctx* ctx, const uint32_t* w, uint64_t rows_w, int n_w, const
   }
   if (route == Route::StreamTc) {
     // feature prep (codes + rowsum, Y zeroed) + K6, the weight planes streamed once into TMEM
-    if ((st = ensure(&ctx->tc_ws, &ctx->tc_ws_bytes, stream_tc_ws_bytes(rows_x, k), ctx->device,
+    if ((st = ensure(&ctx->tc_ws, &ctx->tc_ws_bytes,
+                     stream_tc_ws_bytes(rows_x, k, rows_w, stream_tc_padded(rows_x, y)), ctx->device,
                      stream))) {
       return st;
     }
@@ -429,7 +430,7 @@ int run_matmul(apmm_ctx* ctx, const uint32_t* w, uint64_t rows_w, int n_w, const
       s.ev_flags = t.flags;
       CU(launch_stream_tc(s, stream));
     }
-    ctx->launches += 2;  // feature prep + K6
+    ctx->launches += stream_tc_padded(rows_x, y) ? 3 : 2;  // feature prep + K6 (+ unpad copy)
     return APMM_OK;
   }
   if ((st = ensure(&ctx->ws, &ctx->ws_bytes, matmul_ws_bytes(rows_w, rows_x, k), ctx->device,
@@ -777,7 +778,8 @@ int apmm_ctx_reserve(apmm_ctx* ctx, uint64_t rows_w, uint64_t rows_x, uint64_t k
   if ((st = ensure(&ctx->ws, &ctx->ws_bytes, matmul_ws_bytes(rows_w, rows_x, k), ctx->device, s))) {
     return st;
   }
-  if ((st = ensure(&ctx->tc_ws, &ctx->tc_ws_bytes, stream_tc_ws_bytes(rows_x, k), ctx->device, s))) {
+  if ((st = ensure(&ctx->tc_ws, &ctx->tc_ws_bytes,
+                   stream_tc_ws_bytes(rows_x, k, rows_w, rows_x <= kStreamTcMaxRows), ctx->device, s))) {
     return st;
   }
   if (rows_x <= kSkinnyMaxRowsX) {

@@ -207,7 +207,7 @@ struct StreamTcArgs {
   int n_w, n_x;
   int32_t* y;                // [rows_w][rows_x] int32
   int num_sms;
-  void* ws;                  // stream_tc_ws_bytes(): feature codes + rowsum parts
+  void* ws;                  // stream_tc_ws_bytes(): feature codes + rowsum parts (+ padded Y)
   bool early_w = true;       // PDL: weight loads may start before the previous kernel completes
   bool early_x = false;      // PDL: the feature prep may read X before it
   unsigned long long* trace = nullptr;       // dev (APMM_TRACE): K6 per-CTA stamps [grid][8]
@@ -218,7 +218,10 @@ struct StreamTcArgs {
 // Whether K6 can serve a call (shape, alignment and shared-memory budget).
 bool stream_tc_supported(const uint32_t* w, uint64_t rows_w, uint64_t rows_x, uint64_t k, int n_w,
                          const void* y);
-size_t stream_tc_ws_bytes(uint64_t rows_x, uint64_t k);
+// Whether a call writes a padded Y in the workspace first (rows_x % 4 != 0 or Y not 16-byte
+// aligned: the TMA reduce-adds need 16-byte rows) and copies it out.
+bool stream_tc_padded(uint64_t rows_x, const void* y);
+size_t stream_tc_ws_bytes(uint64_t rows_x, uint64_t k, uint64_t rows_w, bool padded);
 cudaError_t launch_stream_tc(const StreamTcArgs& a, cudaStream_t s);
 
 // Tensor-map encoder obtained from the driver through the runtime (no -lcuda).

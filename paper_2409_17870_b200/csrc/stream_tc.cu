@@ -599,7 +599,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 // only after griddepcontrol.wait (X may be the previous kernel's output, and the previous
 // call's GEMM may still read the codes) unless early_x.
 __global__ void __launch_bounds__(kPrepThreads) stream_tc_prep_kernel(
-    const uint32_t* __restrict__ x, uint32_t rows_x, uint32_t wpr, int n_x, uint32_t kwords,
+    const uint32_t* __restrict__ x, uint32_t rows_x, uint32_t x_rows, uint32_t wpr, int n_x, uint32_t kwords,
     uint8_t* __restrict__ codes, int32_t* __restrict__ rsx_part, uint4* __restrict__ y_zero,
     uint64_t y_vec4, uint32_t early_x, unsigned long long* ts) {
   const uint32_t bslot = blockIdx.y * gridDim.x + blockIdx.x;
@@ -610,8 +610,9 @@ __global__ void __launch_bounds__(kPrepThreads) stream_tc_prep_kernel(
   const uint32_t row = blockIdx.y, W = blockIdx.x * kPrepThreads + threadIdx.x;
   uint32_t v[8];
   int32_t rs = 0;
-  const bool real = row < rows_x;
-  const uint64_t pstride = uint64_t(rows_x) * wpr;
+  // rows_x: the (4-aligned) code rows before the all-ones row; x_rows <= rows_x of them are X's
+  const bool real = row < x_rows;
+  const uint64_t pstride = uint64_t(x_rows) * wpr;
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
     v[i] = (real && i < n_x && W < wpr) ? __ldg(x + i * pstride + uint64_t(row) * wpr + W) : 0u;
@@ -655,7 +656,7 @@ __global__ void __launch_bounds__(kPrepThreads) stream_tc_prep_kernel(
   __shared__ int32_t part[kPrepThreads / 32];
   if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = rs;
   __syncthreads();
-  if (threadIdx.x == 0 && real) {
+  if (threadIdx.x == 0 && row < rows_x) {  // (padding rows: zero codes, zero rowsum)
     int32_t s = 0;
     for (int i = 0; i < kPrepThreads / 32; ++i) s += part[i];
     rsx_part[uint64_t(row) * gridDim.x + blockIdx.x] = s;
@@ -665,6 +666,18 @@ __global__ void __launch_bounds__(kPrepThreads) stream_tc_prep_kernel(
   const uint64_t gtid = (uint64_t(blockIdx.y) * gridDim.x + blockIdx.x) * kPrepThreads + threadIdx.x;
   for (uint64_t i = gtid; i < y_vec4; i += nthreads) y_zero[i] = make_uint4(0, 0, 0, 0);
   if (threadIdx.x == 0 && bslot < 1024) TC_STAMP(ts, bslot, 2);
+}
+
+// Ragged feature counts: K6 wrote Y padded to rx columns; copy the first rows_x of each row.
+__global__ void __launch_bounds__(256) stream_tc_unpad_kernel(const int32_t* __restrict__ src,
+                                                              int32_t* __restrict__ dst, uint32_t rx,
+                                                              uint32_t rows_x, uint64_t n) {
+  pdl_trigger();
+  pdl_wait();
+  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t r = i / rows_x;
+    dst[i] = src[r * rx + (i - r * rows_x)];
+  }
 }
 
 struct Layout {
@@ -732,14 +745,21 @@ bool stream_tc_supported(const uint32_t* w, uint64_t rows_w, uint64_t rows_x, ui
   const uint64_t wpr = (k + 31) / 32;
   const uint64_t tiles = (rows_w + kTileRows - 1) / kTileRows;
   const uint64_t steps = (wpr + kStepWords - 1) / kStepWords;
-  return rows_x >= 1 && rows_x <= kMaxRowsX && rows_x % 4 == 0 && n_w <= 4 && wpr % 4 == 0 &&
-         reinterpret_cast<uintptr_t>(w) % 16 == 0 && reinterpret_cast<uintptr_t>(y) % 16 == 0 &&
-         tiles * steps < 65536 && layout_of(rows_x, n_w).smem != 0;
+  const uint64_t rx4 = (rows_x + 3) / 4 * 4;
+  return rows_x >= 1 && rx4 <= kMaxRowsX && n_w <= 4 && wpr % 4 == 0 &&
+         reinterpret_cast<uintptr_t>(w) % 16 == 0 && reinterpret_cast<uintptr_t>(y) % 4 == 0 &&
+         tiles * steps < 65536 && layout_of(rx4, n_w).smem != 0;
 }
 
-size_t stream_tc_ws_bytes(uint64_t rows_x, uint64_t k) {
-  const uint64_t n_mma = n_mma_of(static_cast<uint32_t>(rows_x));
-  return round_up(n_mma * kwords_of(k) * 32u, 256) + round_up(n_mma * prep_blocks_of(k) * 4u, 256);
+bool stream_tc_padded(uint64_t rows_x, const void* y) {
+  return rows_x % 4 != 0 || reinterpret_cast<uintptr_t>(y) % 16 != 0;
+}
+
+size_t stream_tc_ws_bytes(uint64_t rows_x, uint64_t k, uint64_t rows_w, bool padded) {
+  const uint64_t rx4 = (rows_x + 3) / 4 * 4;
+  const uint64_t n_mma = n_mma_of(static_cast<uint32_t>(rx4));
+  return round_up(n_mma * kwords_of(k) * 32u, 256) + round_up(n_mma * prep_blocks_of(k) * 4u, 256) +
+         (padded ? round_up(rows_w * rx4 * 4u, 256) : 0);
 }
 
 cudaError_t launch_stream_tc(const StreamTcArgs& a, cudaStream_t s) {
@@ -748,7 +768,10 @@ cudaError_t launch_stream_tc(const StreamTcArgs& a, cudaStream_t s) {
     return e ? static_cast<uint32_t>(std::atoi(e)) : kMaxWst;
   }();
   static const bool allow_pw = APMM_DEV_ENV("APMM_TC_NOPAIR") == nullptr;  // dev A/B
-  Layout l = layout_of(a.rows_x, a.n_w, wst_cap, allow_pw);
+  // ragged feature counts run on a 4-aligned row count into a padded Y in the workspace
+  const bool padded = stream_tc_padded(a.rows_x, a.y);
+  const uint64_t rx = (a.rows_x + 3) / 4 * 4;
+  Layout l = layout_of(rx, a.n_w, wst_cap, allow_pw);
   if (!l.smem) return cudaErrorInvalidConfiguration;
   const uint32_t wpr = static_cast<uint32_t>((a.k + 31) / 32);
   if (l.pw) {
@@ -757,7 +780,7 @@ cudaError_t launch_stream_tc(const StreamTcArgs& a, cudaStream_t s) {
     const uint64_t tl = (a.rows_w + kTileRows - 1) / kTileRows, sms = static_cast<uint64_t>(a.num_sms);
     const uint64_t n1 = tl * (kwords_of(a.k, false) / kStepWords), n2 = tl * (kwords_of(a.k, true) / kStepWords) / 2;
     const uint64_t max1 = (n1 + sms - 1) / sms, max2 = 2 * ((n2 + sms - 1) / sms);
-    if (max2 > max1) l = layout_of(a.rows_x, a.n_w, wst_cap, false);
+    if (max2 > max1) l = layout_of(rx, a.n_w, wst_cap, false);
   }
   const uint32_t kwords = kwords_of(a.k, l.pw);
   const uint32_t spt = kwords / kStepWords;
@@ -767,6 +790,9 @@ cudaError_t launch_stream_tc(const StreamTcArgs& a, cudaStream_t s) {
   uint8_t* codes = static_cast<uint8_t*>(a.ws);
   int32_t* rsx_part = reinterpret_cast<int32_t*>(codes + round_up(uint64_t(l.n_mma) * kwords * 32u, 256));
   const uint32_t parts = prep_blocks_of(a.k);
+  int32_t* ydst = padded ? reinterpret_cast<int32_t*>(reinterpret_cast<uint8_t*>(rsx_part) +
+                                                       round_up(uint64_t(l.n_mma) * parts * 4u, 256))
+                         : a.y;
 
   // feature prep (+ Y zeroing)
   {
@@ -779,10 +805,10 @@ cudaError_t launch_stream_tc(const StreamTcArgs& a, cudaStream_t s) {
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    const uint64_t y_vec4 = a.rows_w * a.rows_x / 4;  // rows_x % 4 == 0
+    const uint64_t y_vec4 = a.rows_w * rx / 4;
     cudaError_t e = cudaLaunchKernelEx(&cfg, stream_tc_prep_kernel, a.x_planes,
-                                       static_cast<uint32_t>(a.rows_x), wpr, a.n_x, kwords, codes,
-                                       rsx_part, reinterpret_cast<uint4*>(a.y), y_vec4,
+                                       static_cast<uint32_t>(rx), static_cast<uint32_t>(a.rows_x), wpr,
+                                       a.n_x, kwords, codes, rsx_part, reinterpret_cast<uint4*>(ydst), y_vec4,
                                        a.early_x ? 1u : 0u, a.trace_prep);
     if (e != cudaSuccess) return e;
   }
@@ -799,14 +825,14 @@ cudaError_t launch_stream_tc(const StreamTcArgs& a, cudaStream_t s) {
                      uint64_t(kwords) * 32u, 128u, l.n_mma) != CUDA_SUCCESS) {
     return cudaErrorInvalidValue;
   }
-  if (encode_tmap_2d(&ty, CU_TENSOR_MAP_DATA_TYPE_INT32, 4, a.y, a.rows_x, a.rows_w, a.rows_x * 4,
+  if (encode_tmap_2d(&ty, CU_TENSOR_MAP_DATA_TYPE_INT32, 4, ydst, rx, a.rows_w, rx * 4,
                      32u, 32u) != CUDA_SUCCESS) {
     return cudaErrorInvalidValue;
   }
   TcParams p{};
   p.rsx_part = rsx_part;
   p.parts = parts;
-  p.rows_x = static_cast<uint32_t>(a.rows_x);
+  p.rows_x = static_cast<uint32_t>(rx);
   p.n_mma = l.n_mma;
   p.n_w = static_cast<uint32_t>(a.n_w);
   p.steps_per_tile = spt;
@@ -827,7 +853,7 @@ cudaError_t launch_stream_tc(const StreamTcArgs& a, cudaStream_t s) {
   // segment then overlaps the next segment's MMAs
   static const bool nd1 = APMM_DEV_ENV("APMM_TC_ND1") != nullptr;  // dev A/B
   p.dstride = (l.n_mma + 31u) / 32u * 32u;
-  const uint32_t dread = ((static_cast<uint32_t>(a.rows_x) + 31u) / 32u) * 32u;
+  const uint32_t dread = ((static_cast<uint32_t>(rx) + 31u) / 32u) * 32u;
   p.nd = !nd1 && kColD + p.dstride + (dread > l.n_mma ? dread : l.n_mma) <= kTmemCols ? 2u : 1u;
   static const uint32_t ts_mode = [] {
     const char* e = APMM_DEV_ENV("APMM_TC_TS_MODE");
@@ -846,6 +872,21 @@ cudaError_t launch_stream_tc(const StreamTcArgs& a, cudaStream_t s) {
     case 2: e = l.pw ? launch_n<2, true>(tw, tx, ty, p, grid, l.smem, s) : launch_n<2, false>(tw, tx, ty, p, grid, l.smem, s); break;
     case 3: e = l.pw ? launch_n<3, true>(tw, tx, ty, p, grid, l.smem, s) : launch_n<3, false>(tw, tx, ty, p, grid, l.smem, s); break;
     default: e = l.pw ? launch_n<4, true>(tw, tx, ty, p, grid, l.smem, s) : launch_n<4, false>(tw, tx, ty, p, grid, l.smem, s); break;
+  }
+  if (e == cudaSuccess && padded) {
+    // padded Y -> the caller's [rows_w][rows_x] (PDL: waits for K6 inside)
+    cudaLaunchConfig_t cfg{};
+    const uint64_t n = a.rows_w * a.rows_x;
+    cfg.gridDim = dim3(static_cast<unsigned>(std::min<uint64_t>((n + 255) / 256, 4u * a.num_sms)));
+    cfg.blockDim = dim3(256);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, stream_tc_unpad_kernel, static_cast<const int32_t*>(ydst), a.y,
+                           static_cast<uint32_t>(rx), static_cast<uint32_t>(a.rows_x), n);
   }
   if (a.ev_stop) cudaEventRecordWithFlags(a.ev_stop, s, a.ev_flags);
   return e;

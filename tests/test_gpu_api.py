@@ -238,7 +238,8 @@ def test_graph_replays_of_every_route(gpu):
     dev = torch.device("cuda", 0)
     s = torch.cuda.Stream()
     shapes = [(4096, 8, 4096, 3, 8), (4096, 128, 4096, 2, 4), (2304, 2560, 4096, 2, 4),
-              (4096, 512, 4096, 2, 4), (8192, 16, 8192, 3, 8), (4096, 256, 4096, 2, 4)]
+              (4096, 512, 4096, 2, 4), (8192, 16, 8192, 3, 8), (4096, 256, 4096, 2, 4),
+              (8192, 63, 8192, 3, 8)]
     for (n_out, m, k, nw, nx) in shapes:
         ctx = ap.Context(0)
         ctx.set_stream(s)

@@ -346,13 +346,15 @@ def test_mid_size_split_k_path(gpu, oracle, n_out, m_tok, k, nw, nx):
     (4096, 64, 4096, 2, 4), (8192, 16, 8192, 3, 8), (4096, 8, 4096, 2, 4), (11008, 32, 4096, 4, 4),
     (4096, 64, 11008, 1, 2), (1000, 4, 4224, 3, 5), (2305, 60, 4200, 2, 8), (300, 12, 128, 4, 1),
     (8192, 48, 8192, 3, 8), (129, 64, 640, 2, 3), (4096, 128, 4096, 2, 4), (1000, 100, 4224, 4, 8),
-    (4096, 96, 11008, 3, 4), (2048, 124, 4096, 4, 8), (2051, 128, 1152, 1, 1)])
+    (4096, 96, 11008, 3, 4), (2048, 124, 4096, 4, 8), (2051, 128, 1152, 1, 1),
+    (8192, 63, 8192, 3, 8), (1000, 17, 4224, 2, 4), (2051, 125, 1152, 1, 1), (300, 30, 640, 4, 2)])
 def test_stream_tensor_memory_path(gpu, oracle, n_out, m_tok, k, nw, nx):
     """K6 (APMM_ROUTE_STREAM_TC): weight planes streamed per warp, expanded in registers into
     TMEM as the MMA's A operand, K split over every SM (stream-K ranges, partial tiles TMA
     reduce-added into a Y zeroed by the feature prep), rowsum(U_w) from an all-ones feature row.
     Against the oracle on sampled rows and bit-equal to the 1-SM route on every entry; ragged
-    row tiles, a tail word (K % 32 != 0), one-step K and segments that start mid-tile."""
+    row tiles, a tail word (K % 32 != 0), one-step K, segments that start mid-tile, and feature
+    counts that are not a multiple of 4 (a padded Y in the workspace, then an unpad copy)."""
     ap, ctx = gpu
     _route_vs_route(ap, ctx, oracle, n_out, m_tok, k, nw, nx, n_out * 3 + m_tok,
                     ap.Route.STREAM_TC, ap.Route.SINGLE_SM)
