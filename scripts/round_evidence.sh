@@ -15,3 +15,5 @@ timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --c
 timeout 300 ncu --set full --import-source on --clock-control none -k regex:skinny_kernel --launch-skip 10 -c 1 -o $O/skinny_m1 python scripts/skinny_probe.py 8192 1 8192 3 8 20 > $O/ncu_sk1.log 2>&1
 timeout 300 ncu --set full --import-source on --clock-control none -k regex:stream_tc_kernel --launch-skip 10 -c 1 -o $O/stream_tc_m16 python scripts/skinny_probe.py 8192 16 8192 3 8 20 > $O/ncu_tc16.log 2>&1
 timeout 300 ncu --set full --import-source on --clock-control none -k regex:stream_tc_kernel --launch-skip 10 -c 1 -o $O/stream_tc_m64 python scripts/skinny_probe.py 4096 64 4096 2 4 20 > $O/ncu_tc64.log 2>&1
+timeout 300 ncu --set full --import-source on --clock-control none -k regex:gemm_pair_wplanes_kernel --launch-skip 10 -c 1 -o $O/k3f_m256 python scripts/skinny_probe.py 4096 256 4096 2 4 20 > $O/ncu_k3f256.log 2>&1
+timeout 300 ncu --set full --import-source on --clock-control none -k regex:gemm_pair_wplanes_kernel --launch-skip 10 -c 1 -o $O/k3f_m512 python scripts/skinny_probe.py 4096 512 4096 2 4 20 > $O/ncu_k3f512.log 2>&1
