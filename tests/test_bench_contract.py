@@ -51,3 +51,30 @@ def test_reference_arm_under_torchrun_prints_once():
                 "--warmup", "3"])
     lines = _lines(out)
     assert len(lines) == 1 and lines[0]["n_gpus"] == 2 and lines[0]["impl"] == "reference"
+
+
+@pytest.mark.gpu
+def test_gpu_arm_line():
+    """The GPU arm on a small workload: same metric/unit as the reference arm, parity checked,
+    roofline / e2e / launch-count fields present."""
+    out = _run_gpu([sys.executable, "bench.py", "--workload", "llama7b_small", "--steps", "3",
+                    "--warmup", "3", "--no-cpu-baseline"])
+    lines = _lines(out)
+    assert len(lines) == 1
+    d = lines[0]
+    sys.path.insert(0, ROOT)
+    import bench
+    assert d["metric"] == bench.METRIC and d["unit"] == bench.UNIT and d["n_gpus"] == 1
+    assert d["value"] > 0 and d["parity"].startswith("ok")
+    assert d["gpu_launches"] > 0
+    assert d["e2e"]["value"] > 0 and d["e2e"]["h2d_bytes_per_step"] > 0
+    assert d["e2e"]["d2h_bytes_per_step"] > 0
+    r = d["roofline"]
+    assert r["bound"] in ("hbm", "tensor") and r["peak"] > 0
+    assert r["frac"] == pytest.approx(r["achieved"] / r["peak"])
+
+
+def _run_gpu(cmd, timeout=600):
+    p = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=timeout)
+    assert p.returncode == 0, p.stderr[-2000:]
+    return p.stdout
